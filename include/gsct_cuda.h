@@ -1,0 +1,214 @@
+/* gsct_cuda.h — C ABI of the B200-native FaCT-GS hot paths (libgsct_b200.so).
+ *
+ * Plain C: pointers, sizes and POD structs only; no C++ or torch types cross this
+ * boundary. Every entry point replaces one reference operator of the header-only C++
+ * library `gsct` (reference paths below are relative to /root/reference):
+ *
+ *   gsct_rasterize_fwd  <- gsct::rasterize_view      proj/include/gsct/projector.hpp:308-360
+ *   gsct_rasterize_bwd  <- gsct::rasterize_backward  proj/include/gsct/projector.hpp:371-482
+ *                          (+ ParamGradients::add over views, proj/include/gsct/core.hpp:152-162)
+ *   gsct_voxelize_fwd   <- gsct::voxelize / voxelize_full  proj/include/gsct/voxelizer.hpp:162-206
+ *   gsct_voxelize_bwd   <- gsct::voxelize_backward    proj/include/gsct/voxelizer.hpp:214-263
+ *   gsct_debug_project  <- gsct::project_cloud        proj/include/gsct/projector.hpp:292-303
+ *   gsct_debug_tile_pairs <- gsct::bin_tiles          proj/include/gsct/projector.hpp:266-286
+ *   gsct_debug_voxel_boxes <- detail::prepare_voxel_splats proj/include/gsct/voxelizer.hpp:145-155
+ *   gsct_host_*         <- harness/utility functions (rng.hpp, bench.hpp, synthetic.hpp,
+ *                          voxelizer.hpp:76-93 sample_subvolume, projector.hpp:29-43 view_frame)
+ *
+ * Semantics follow the reference: per pixel / voxel, splats accumulate in ascending splat
+ * index (projector.hpp:305-307, voxelizer.hpp:159-161); backward gradients are owned per
+ * splat and reduced in a fixed order, so every result is bit-stable run to run; culled and
+ * degenerate splats are counted, not errors. Invalid input returns GSCT_ERR_CONTRACT with
+ * the reference's message (gsct::contract_error, common.hpp:15-31), naming the lowest
+ * offending splat index for non-finite parameters or zero quaternions (core.hpp:86-90).
+ *
+ * Numerics: per-splat set-up (activation, covariance, projection, line-integral factor,
+ * dilation, conic, integer bounding boxes, tile/brick keys, chain rule) runs in fp64 in the
+ * reference's operation order, so boxes and keys are bit-exact; per-pair work (exp of the
+ * quadratic form, accumulation) is fp32. Images and volumes are fp32; gradients fp64.
+ *
+ * Layouts: cloud arrays are the reference's AoS doubles (GaussianCloud vectors):
+ *   pos[3N], log_scale[3N], quat[4N] (w,x,y,z), raw_density[N].
+ * Images: [n_views][n_v][n_u] (u fastest, core.hpp:237). Volumes: x fastest, then y, z
+ * (core.hpp:300-302). Pointers flagged GSCT_HOST are copied through the context's pinned
+ * staging; GSCT_DEVICE pointers are used in place (device-resident fast path).
+ */
+#ifndef GSCT_CUDA_H
+#define GSCT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSCT_ABI_VERSION 1
+
+enum gsct_status {
+  GSCT_OK = 0,
+  GSCT_ERR_CONTRACT = 1, /* maps to gsct::contract_error */
+  GSCT_ERR_CUDA = 2,
+  GSCT_ERR_OOM = 3
+};
+
+enum gsct_location { GSCT_HOST = 0, GSCT_DEVICE = 1 };
+
+typedef struct gsct_ctx_s* gsct_ctx;
+
+/* ScanGeometry minus the angle list (core.hpp:203-222). */
+typedef struct {
+  int cone; /* 0 parallel, 1 cone (BeamMode) */
+  int n_u, n_v;
+  double s_u, s_v;
+  double source_to_origin, origin_to_detector;
+} gsct_geometry;
+
+/* RasterSettings (projector.hpp:64-71). bounding: 0 rect_density_aware, 1 square. */
+typedef struct {
+  double tau_cut, sigma_cap, dilation_px2;
+  int tile_size, dilate, bounding;
+} gsct_raster_settings;
+
+/* VoxelSettings (voxelizer.hpp:99-102). */
+typedef struct {
+  double tau_cut, sigma_cap;
+} gsct_voxel_settings;
+
+/* The grid bounding boxes are computed in: a GridRegion's dims/spacing/origin
+ * (voxelizer.hpp:43-71; origin = world centre of voxel (0,0,0)). */
+typedef struct {
+  int dims[3];
+  double spacing;
+  double origin[3];
+} gsct_grid;
+
+/* Sub-box [lo, hi) of the grid that a call produces (z-slab sharding). NULL = whole grid.
+ * Boxes stay in grid coordinates and are clipped, so slabs tile the full-grid result. */
+typedef struct {
+  int lo[3], hi[3];
+} gsct_window;
+
+/* RenderStats (projector.hpp:73-80); accumulated with += like the reference. */
+typedef struct {
+  int64_t culled, degenerate, tile_pairs, pixel_pairs;
+  double forward_ms, backward_ms;
+} gsct_stats;
+
+typedef struct {
+  int64_t n;
+  const double* pos;
+  const double* log_scale;
+  const double* quat;
+  const double* raw_density;
+  int location; /* gsct_location */
+} gsct_cloud;
+
+/* ParamGradients (core.hpp:135-150): overwritten (not accumulated) by the call. */
+typedef struct {
+  double* pos;           /* 3N */
+  double* log_scale;     /* 3N */
+  double* quat;          /* 4N */
+  double* raw_density;   /* N */
+  double* pos_grad_norm; /* N */
+  uint8_t* visible;      /* N */
+  int location;
+} gsct_grads;
+
+/* ---- context ---------------------------------------------------------------- */
+int gsct_ctx_create(int device, gsct_ctx* out);
+void gsct_ctx_destroy(gsct_ctx ctx);
+const char* gsct_ctx_last_error(gsct_ctx ctx);
+/* Run on an external CUDA stream (cudaStream_t as void*), e.g. torch's current stream. */
+int gsct_ctx_set_stream(gsct_ctx ctx, void* stream);
+void* gsct_ctx_stream(gsct_ctx ctx);
+/* async != 0: calls only enqueue work (no host sync, no *_ms timing); device-side
+ * stats/errors are collected by gsct_ctx_synchronize. Default: synchronous (reference). */
+int gsct_ctx_set_async(gsct_ctx ctx, int async);
+int gsct_ctx_synchronize(gsct_ctx ctx, gsct_stats* stats_accum);
+/* Bytes of device workspace currently held (grow-only arena). */
+size_t gsct_ctx_workspace_bytes(gsct_ctx ctx);
+/* Number of kernels this context has launched (for the bench's gpu_launches claim). */
+int64_t gsct_ctx_launch_count(gsct_ctx ctx);
+int gsct_abi_version(void);
+
+/* ---- rasterizer ---------------------------------------------------------------- */
+/* Forward projection of n_views views (angles: host array, radians) into
+ * images[n_views][n_v][n_u] (fp32). One call == n_views calls of rasterize_view. */
+int gsct_rasterize_fwd(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_geometry* geom,
+                       const double* angles, int n_views, const gsct_raster_settings* rs,
+                       float* images, int images_location, gsct_stats* stats);
+
+/* Backward of the same views: grads = sum over views (ascending view order, fp64) of
+ * rasterize_backward(view, grad_images[view]); pos_grad_norm sums the per-view |dL/dmean2d|,
+ * visible ORs (exactly ParamGradients::add over the per-view results). */
+int gsct_rasterize_bwd(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_geometry* geom,
+                       const double* angles, int n_views, const gsct_raster_settings* rs,
+                       const float* grad_images, int grad_location, gsct_grads* out,
+                       gsct_stats* stats);
+
+/* ---- voxelizer ----------------------------------------------------------------- */
+/* volume: window dims (x fastest), fp32. */
+int gsct_voxelize_fwd(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_grid* grid,
+                      const gsct_window* window, const gsct_voxel_settings* vs, float* volume,
+                      int volume_location, gsct_stats* stats);
+
+int gsct_voxelize_bwd(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_grid* grid,
+                      const gsct_window* window, const gsct_voxel_settings* vs,
+                      const float* grad_volume, int grad_location, gsct_grads* out,
+                      gsct_stats* stats);
+
+/* Split backward for z-slab sharding: per-splat partial sums over the window
+ * (moments: device fp32 [10][N]: sum t, sum t*d (3), sum t*d_i*d_j (6; xx,yy,zz,xy,xz,yz),
+ * t = exp(-q/2) * w, d in world units), reduced across ranks by the caller (NCCL
+ * all-reduce sum), then finished per splat in fp64. */
+int gsct_voxelize_bwd_moments(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_grid* grid,
+                              const gsct_window* window, const gsct_voxel_settings* vs,
+                              const float* grad_volume, int grad_location, float* moments_dev);
+int gsct_voxelize_bwd_finish(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_grid* grid,
+                             const gsct_voxel_settings* vs, const float* moments_dev,
+                             gsct_grads* out);
+
+/* ---- parity hooks (bit-exactness checks against the CPU oracle) ------------------ */
+/* Per splat for one view: rect[4N] (u_min,u_max,v_min,v_max), flags[N] (bit0 culled,
+ * bit1 degenerate), mean2d[2N], conic[4N] (row-major), amplitude[N]; host outputs. */
+int gsct_debug_project(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_geometry* geom,
+                       double angle, const gsct_raster_settings* rs, int32_t* rect,
+                       uint8_t* flags, double* mean2d, double* conic, double* amplitude);
+/* Sorted (key, value) pairs of the binning of n_views views: key = view*n_tiles + tile,
+ * value = splat; *n_pairs is set; arrays written only if capacity suffices. */
+int gsct_debug_tile_pairs(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_geometry* geom,
+                          const double* angles, int n_views, const gsct_raster_settings* rs,
+                          uint32_t* keys, uint32_t* values, int64_t capacity, int64_t* n_pairs);
+/* lo[3N], hi[3N] inclusive grid indices (clipped to the window), skip[N]. */
+int gsct_debug_voxel_boxes(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_grid* grid,
+                           const gsct_window* window, const gsct_voxel_settings* vs,
+                           int32_t* lo, int32_t* hi, uint8_t* skip);
+
+/* ---- host-side harness (no GPU needed) ------------------------------------------ */
+/* view_frame (projector.hpp:29-43): u[3], v[3], d[3], detector_center[3], source[3], focal. */
+void gsct_host_view_frame(const gsct_geometry* geom, double angle, double frame[16]);
+/* default_angles / default_geometry (synthetic.hpp:236-271). */
+void gsct_host_default_geometry(const int dims[3], double spacing, int n_views, int cone,
+                                int n_u, int n_v, gsct_geometry* out, double* angles);
+/* Rng (rng.hpp:18-69): mt19937_64 with the reference's uniform/normal mappings. */
+void* gsct_host_rng_create(uint64_t seed);
+void gsct_host_rng_destroy(void* rng);
+double gsct_host_rng_uniform(void* rng, double lo, double hi);
+double gsct_host_rng_normal(void* rng);
+int64_t gsct_host_rng_uniform_int(void* rng, int64_t n);
+/* sample_subvolume (voxelizer.hpp:76-93): writes offset[3], dims[3]; returns 0 or 1 (error). */
+int gsct_host_sample_subvolume(const int parent_dims[3], const int sub_dims[3], void* rng,
+                               int offset[3], int dims[3]);
+/* Seeded clouds written into caller arrays (pos, log_scale, quat, raw):
+ *   kind 0: synthetic_cloud (bench.hpp:33-52): p0=half_extent p1=scale p2=anisotropy p3=density
+ *   kind 1: random_cloud (tests/oracles.hpp:168-184): p0=pos_range p1=scale_lo p2=scale_hi
+ *   kind 2: modified 3D Shepp-Logan phantom cloud: p0=grid side (voxels),
+ *           p1=spacing; positions uniform in the outer ellipsoid, 1-NN-like scales. */
+int gsct_host_make_cloud(int kind, int64_t count, uint64_t seed, const double* params,
+                         double* pos, double* log_scale, double* quat, double* raw);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSCT_CUDA_H */

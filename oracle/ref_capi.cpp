@@ -1,0 +1,295 @@
+// TEST INFRASTRUCTURE ONLY. A thin extern "C" wrapper that calls the UNCHANGED reference
+// implementation (/root/reference/proj/include/gsct/*.hpp, compiled here with the
+// Eigen-subset shim) so Python tests and bench.py's reference arm can call it through
+// ctypes. Built by oracle/Makefile into oracle/_ref/libgsct_ref.so (git-ignored, travels
+// to the GPU box prebuilt). Array layouts match oracle/gsct_oracle.h.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "gsct/bench.hpp"
+#include "gsct/core.hpp"
+#include "gsct/parallel.hpp"
+#include "gsct/projector.hpp"
+#include "gsct/synthetic.hpp"
+#include "gsct/voxelizer.hpp"
+#include "oracles.hpp"
+
+using namespace gsct;
+
+namespace {
+std::string g_err;
+
+struct Geo {
+  int cone, n_u, n_v;
+  double s_u, s_v, source_to_origin, origin_to_detector;
+};
+struct RS {
+  double tau_cut, sigma_cap, dilation_px2;
+  int tile_size, dilate, bounding;
+};
+struct VS {
+  double tau_cut, sigma_cap;
+};
+struct Region {
+  int dims[3];
+  double spacing;
+  double origin[3];
+};
+struct Stats {
+  int64_t culled, degenerate, tile_pairs, pixel_pairs;
+};
+
+ScanGeometry to_geom(const Geo* g, const double* angles, int n_angles) {
+  ScanGeometry geom;
+  geom.mode = g->cone ? BeamMode::cone : BeamMode::parallel;
+  geom.n_u = g->n_u;
+  geom.n_v = g->n_v;
+  geom.s_u = g->s_u;
+  geom.s_v = g->s_v;
+  geom.source_to_origin = g->source_to_origin;
+  geom.origin_to_detector = g->origin_to_detector;
+  geom.angles.assign(angles, angles + n_angles);
+  return geom;
+}
+RasterSettings to_rs(const RS* r) {
+  RasterSettings s;
+  s.tau_cut = r->tau_cut;
+  s.sigma_cap = r->sigma_cap;
+  s.dilation_px2 = r->dilation_px2;
+  s.tile_size = r->tile_size;
+  s.dilate = r->dilate != 0;
+  s.bounding = r->bounding ? BoundingMode::square_circumscribed : BoundingMode::rect_density_aware;
+  return s;
+}
+VoxelSettings to_vs(const VS* v) {
+  VoxelSettings s;
+  s.tau_cut = v->tau_cut;
+  s.sigma_cap = v->sigma_cap;
+  return s;
+}
+GridRegion to_region(const Region* r) {
+  GridRegion g;
+  g.dims = {r->dims[0], r->dims[1], r->dims[2]};
+  g.spacing = r->spacing;
+  g.origin = Vec3(r->origin[0], r->origin[1], r->origin[2]);
+  return g;
+}
+void put_stats(const RenderStats& s, Stats* out, double* ms) {
+  if (out) {
+    out->culled += s.culled;
+    out->degenerate += s.degenerate;
+    out->tile_pairs += s.tile_pairs;
+    out->pixel_pairs += s.pixel_pairs;
+  }
+  if (ms) {
+    ms[0] += s.forward_ms;
+    ms[1] += s.backward_ms;
+  }
+}
+void put_grads(const ParamGradients& g, double* gp, double* gl, double* gq, double* gr,
+               double* pgn, uint8_t* vis) {
+  const std::size_t n = g.positions.size();
+  for (std::size_t i = 0; i < n; ++i) {
+    for (int k = 0; k < 3; ++k) {
+      gp[3 * i + k] = g.positions[i][k];
+      gl[3 * i + k] = g.log_scales[i][k];
+    }
+    for (int k = 0; k < 4; ++k) gq[4 * i + k] = g.rotations[i][k];
+    gr[i] = g.raw_densities[i];
+    pgn[i] = g.pos_grad_norm[i];
+    vis[i] = g.visible[i];
+  }
+}
+}  // namespace
+
+#define GUARD(body)                      \
+  try {                                  \
+    body;                                \
+    return 0;                            \
+  } catch (const contract_error& e) {    \
+    g_err = e.what();                    \
+    return 1;                            \
+  } catch (const std::exception& e) {    \
+    g_err = e.what();                    \
+    return 2;                            \
+  }
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+void ref_set_threads(int n) { set_thread_count(n); }
+int ref_thread_count() { return thread_count(); }
+
+void* ref_cloud_create(int64_t n, const double* pos, const double* ls, const double* q,
+                       const double* raw) {
+  auto* c = new GaussianCloud();
+  c->reserve(static_cast<std::size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    c->push_back(Vec3(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]),
+                 Vec3(ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]),
+                 Vec4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]), raw[i]);
+  }
+  return c;
+}
+void ref_cloud_destroy(void* c) { delete static_cast<GaussianCloud*>(c); }
+
+int ref_rasterize_view(void* cloud, const Geo* g, const double* angles, int n_angles, int view,
+                       const RS* rs, double* image, Stats* stats, double* ms) {
+  GUARD({
+    RenderStats s;
+    const Image img = rasterize_view(*static_cast<GaussianCloud*>(cloud), to_geom(g, angles, n_angles),
+                                     static_cast<std::size_t>(view), to_rs(rs), &s);
+    std::memcpy(image, img.values.data(), img.values.size() * sizeof(double));
+    put_stats(s, stats, ms);
+  })
+}
+
+int ref_rasterize_backward(void* cloud, const Geo* g, const double* angles, int n_angles, int view,
+                           const double* grad_image, const RS* rs, double* gp, double* gl,
+                           double* gq, double* gr, double* pgn, uint8_t* vis, double* ms) {
+  GUARD({
+    const ScanGeometry geom = to_geom(g, angles, n_angles);
+    Image gi = Image::zeros(geom.n_u, geom.n_v);
+    std::memcpy(gi.values.data(), grad_image, gi.values.size() * sizeof(double));
+    RenderStats s;
+    const ParamGradients pg = rasterize_backward(*static_cast<GaussianCloud*>(cloud), geom,
+                                                 static_cast<std::size_t>(view), gi, to_rs(rs), &s);
+    put_grads(pg, gp, gl, gq, gr, pgn, vis);
+    put_stats(s, nullptr, ms);
+  })
+}
+
+// project_cloud + bin_tiles for one view: per-splat bbox/flags and the CSR tile lists.
+int ref_project_and_bin(void* cloud, const Geo* g, const double* angles, int n_angles, int view,
+                        const RS* rs, int32_t* rect /*4N*/, uint8_t* culled, uint8_t* degenerate,
+                        double* mean2d /*2N*/, double* conic /*4N*/, double* amplitude,
+                        int64_t* tile_offsets, int32_t* tile_splats, int64_t* n_pairs) {
+  GUARD({
+    const GaussianCloud& c = *static_cast<GaussianCloud*>(cloud);
+    const ScanGeometry geom = to_geom(g, angles, n_angles);
+    const ViewFrame frame = view_frame(geom, static_cast<std::size_t>(view));
+    const RasterSettings settings = to_rs(rs);
+    const std::vector<Splat2D> splats = project_cloud(c, frame, geom, settings);
+    for (std::size_t i = 0; i < splats.size(); ++i) {
+      const Splat2D& s = splats[i];
+      rect[4 * i] = s.u_min;
+      rect[4 * i + 1] = s.u_max;
+      rect[4 * i + 2] = s.v_min;
+      rect[4 * i + 3] = s.v_max;
+      culled[i] = s.culled;
+      degenerate[i] = s.degenerate;
+      mean2d[2 * i] = s.mean2d[0];
+      mean2d[2 * i + 1] = s.mean2d[1];
+      for (int k = 0; k < 4; ++k) conic[4 * i + k] = s.conic(k / 2, k % 2);
+      amplitude[i] = s.amplitude;
+    }
+    const TileBins bins = bin_tiles(splats, geom.n_u, geom.n_v, settings.tile_size);
+    int64_t acc = 0;
+    for (std::size_t t = 0; t < bins.bins.size(); ++t) {
+      if (tile_offsets) tile_offsets[t] = acc;
+      for (const int32_t idx : bins.bins[t]) {
+        if (tile_splats) tile_splats[acc] = idx;
+        ++acc;
+      }
+    }
+    if (tile_offsets) tile_offsets[bins.bins.size()] = acc;
+    *n_pairs = acc;
+  })
+}
+
+int ref_voxelize(void* cloud, const Region* r, const VS* vs, double* volume, Stats* stats,
+                 double* ms) {
+  GUARD({
+    RenderStats s;
+    const Volume v = voxelize(*static_cast<GaussianCloud*>(cloud), to_region(r), to_vs(vs), &s);
+    std::memcpy(volume, v.values.data(), v.values.size() * sizeof(double));
+    put_stats(s, stats, ms);
+  })
+}
+
+int ref_voxelize_backward(void* cloud, const Region* r, const double* grad_volume, const VS* vs,
+                          double* gp, double* gl, double* gq, double* gr, double* pgn,
+                          uint8_t* vis, double* ms) {
+  GUARD({
+    const GridRegion region = to_region(r);
+    Volume gvol = Volume::zeros(region.dims, region.spacing, region.origin);
+    std::memcpy(gvol.values.data(), grad_volume, gvol.values.size() * sizeof(double));
+    RenderStats s;
+    const ParamGradients pg =
+        voxelize_backward(*static_cast<GaussianCloud*>(cloud), region, gvol, to_vs(vs), &s);
+    put_grads(pg, gp, gl, gq, gr, pgn, vis);
+    put_stats(s, nullptr, ms);
+  })
+}
+
+int ref_prepare_voxel_splats(void* cloud, const Region* r, const VS* vs, int32_t* lo, int32_t* hi,
+                             uint8_t* skip) {
+  GUARD({
+    const std::vector<detail::VoxelSplat> sp =
+        detail::prepare_voxel_splats(*static_cast<GaussianCloud*>(cloud), to_region(r), to_vs(vs));
+    for (std::size_t i = 0; i < sp.size(); ++i) {
+      for (int k = 0; k < 3; ++k) {
+        lo[3 * i + k] = sp[i].lo[k];
+        hi[3 * i + k] = sp[i].hi[k];
+      }
+      skip[i] = sp[i].skip;
+    }
+  })
+}
+
+// Harness generators from the reference (bench.hpp:33-52, synthetic.hpp:246-271).
+int64_t ref_synthetic_cloud(int64_t count, double half_extent, double scale, double anisotropy,
+                            double density, uint64_t seed, double* pos, double* ls, double* q,
+                            double* raw) {
+  SyntheticCloudConfig cfg;
+  cfg.count = count;
+  cfg.half_extent = half_extent;
+  cfg.scale = scale;
+  cfg.anisotropy = anisotropy;
+  cfg.density = density;
+  cfg.seed = seed;
+  const GaussianCloud c = synthetic_cloud(cfg);
+  for (std::size_t i = 0; i < c.size(); ++i) {
+    for (int k = 0; k < 3; ++k) {
+      pos[3 * i + k] = c.positions[i][k];
+      ls[3 * i + k] = c.log_scales[i][k];
+    }
+    for (int k = 0; k < 4; ++k) q[4 * i + k] = c.rotations[i][k];
+    raw[i] = c.raw_densities[i];
+  }
+  return static_cast<int64_t>(c.size());
+}
+
+// oracles::random_cloud (tests/oracles.hpp:168-184), the reference tests' fixture cloud.
+int64_t ref_random_cloud(uint64_t seed, int count, double pos_range, double scale_lo,
+                         double scale_hi, double* pos, double* ls, double* q, double* raw) {
+  const GaussianCloud c = oracles::random_cloud(seed, count, pos_range, scale_lo, scale_hi);
+  for (std::size_t i = 0; i < c.size(); ++i) {
+    for (int k = 0; k < 3; ++k) {
+      pos[3 * i + k] = c.positions[i][k];
+      ls[3 * i + k] = c.log_scales[i][k];
+    }
+    for (int k = 0; k < 4; ++k) q[4 * i + k] = c.rotations[i][k];
+    raw[i] = c.raw_densities[i];
+  }
+  return static_cast<int64_t>(c.size());
+}
+
+void ref_default_geometry(int nx, int ny, int nz, double spacing, int n_views, int cone, int n_u,
+                          int n_v, Geo* out, double* angles) {
+  const Volume vol = Volume::zeros({nx, ny, nz}, spacing, Vec3::Zero());
+  const ScanGeometry g = default_geometry(vol, static_cast<std::size_t>(n_views),
+                                          cone ? BeamMode::cone : BeamMode::parallel, n_u, n_v);
+  out->cone = cone;
+  out->n_u = g.n_u;
+  out->n_v = g.n_v;
+  out->s_u = g.s_u;
+  out->s_v = g.s_v;
+  out->source_to_origin = g.source_to_origin;
+  out->origin_to_detector = g.origin_to_detector;
+  for (int i = 0; i < n_views; ++i) angles[i] = g.angles[static_cast<std::size_t>(i)];
+}
+
+}  // extern "C"

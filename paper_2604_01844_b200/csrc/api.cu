@@ -1,0 +1,777 @@
+// C-ABI implementation (include/gsct_cuda.h): device context, grow-only workspace,
+// host<->device staging, per-call orchestration of the set-up / sort / pair / tail kernels,
+// error mapping to the reference's contract_error messages, and RenderStats.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <string>
+#include <vector>
+
+#include "../../include/gsct_cuda.h"
+#include "gsct_internal.cuh"
+
+using namespace gsct_dev;
+
+namespace gsct_dev {
+thread_local int64_t* g_launch_counter = nullptr;
+}
+
+namespace {
+
+enum Slot {
+  S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
+  S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
+  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_COUNT_SLOTS
+};
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct CallError {
+  int code;
+  std::string msg;
+};
+
+}  // namespace
+
+struct gsct_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool async = false;
+  std::string err;
+  int64_t launches = 0;
+  Buf bufs[S_COUNT_SLOTS];
+  DevStats* dstats = nullptr;   // device
+  DevStats* hstats = nullptr;   // pinned host mirror
+  uint32_t* hscratch = nullptr; // pinned 2 x u32 for scan totals
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  gsct_stats pending{};          // async-mode stats accumulated at synchronize
+};
+
+namespace {
+
+void throw_cuda(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw CallError{GSCT_ERR_OOM, std::string(what) + ": out of device memory"};
+  }
+  throw CallError{GSCT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+#define CK(call)                              \
+  do {                                        \
+    cudaError_t e_ = (call);                  \
+    if (e_ != cudaSuccess) throw_cuda(e_, #call); \
+  } while (0)
+
+void contract(bool ok, const std::string& msg) {
+  if (!ok) throw CallError{GSCT_ERR_CONTRACT, msg};
+}
+
+template <class T>
+T* ws(gsct_ctx c, Slot s, size_t count) {
+  Buf& b = c->bufs[s];
+  const size_t bytes = count * sizeof(T) + 16;
+  if (b.cap < bytes) {
+    if (b.p) CK(cudaFreeAsync(b.p, c->stream));
+    b.p = nullptr;
+    b.cap = 0;
+    size_t want = bytes + bytes / 4;
+    CK(cudaMallocAsync(&b.p, want, c->stream));
+    b.cap = want;
+  }
+  return static_cast<T*>(b.p);
+}
+
+struct Guard {  // sets the launch counter for the duration of an API call
+  explicit Guard(gsct_ctx c) {
+    g_launch_counter = &c->launches;
+    cudaSetDevice(c->device);
+  }
+  ~Guard() { g_launch_counter = nullptr; }
+};
+
+template <class F>
+int run(gsct_ctx c, F&& f) {
+  if (!c) return GSCT_ERR_CONTRACT;
+  Guard guard(c);
+  try {
+    f();
+    c->err.clear();
+    return GSCT_OK;
+  } catch (const CallError& e) {
+    c->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return GSCT_ERR_CUDA;
+  }
+}
+
+void validate_geometry(const gsct_geometry* g, const double* angles, int n_views) {
+  contract(g != nullptr, "ScanGeometry: null geometry");
+  contract(g->n_u >= 1 && g->n_v >= 1, "ScanGeometry: detector must be at least 1x1");
+  contract(g->s_u > 0.0 && g->s_v > 0.0, "ScanGeometry: pixel spacing must be positive");
+  contract(n_views >= 0, "ScanGeometry: negative view count");
+  for (int i = 0; i < n_views; ++i) contract(std::isfinite(angles[i]), "ScanGeometry: non-finite angle");
+  if (g->cone)
+    contract(g->source_to_origin > 0.0 && g->origin_to_detector > 0.0,
+             "ScanGeometry: cone distances must be positive");
+  contract(g->n_u <= 65535 && g->n_v <= 65535, "ScanGeometry: detector side above 65535 unsupported");
+}
+
+Frame make_frame(const gsct_geometry* g, double angle) {
+  double f[16];
+  gsct_host_view_frame(g, angle, f);
+  Frame fr;
+  for (int k = 0; k < 3; ++k) {
+    fr.u[k] = f[k];
+    fr.v[k] = f[3 + k];
+    fr.d[k] = f[6 + k];
+    fr.dc[k] = f[9 + k];
+    fr.src[k] = f[12 + k];
+  }
+  fr.focal = f[15];
+  return fr;
+}
+
+Geo make_geo(const gsct_geometry* g) { return Geo{g->cone, g->n_u, g->n_v, g->s_u, g->s_v}; }
+
+RSet make_rs(const gsct_raster_settings* r) {
+  return RSet{r->tau_cut, r->sigma_cap, r->dilation_px2, r->tile_size, r->dilate, r->bounding};
+}
+
+Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl) {
+  contract(cl != nullptr && cl->n >= 0, "GaussianCloud: invalid cloud");
+  contract(cl->n < (int64_t(1) << 31), "GaussianCloud: more than 2^31 splats unsupported");
+  Cloud d{cl->n, cl->pos, cl->log_scale, cl->quat, cl->raw_density};
+  if (cl->n == 0) return d;
+  contract(cl->pos && cl->log_scale && cl->quat && cl->raw_density,
+           "GaussianCloud: parameter arrays out of lockstep");
+  if (cl->location == GSCT_HOST) {
+    const size_t n = static_cast<size_t>(cl->n);
+    double* p = ws<double>(c, S_POS, 3 * n);
+    double* l = ws<double>(c, S_LS, 3 * n);
+    double* q = ws<double>(c, S_Q, 4 * n);
+    double* r = ws<double>(c, S_RAW, n);
+    CK(cudaMemcpyAsync(p, cl->pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(l, cl->log_scale, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(q, cl->quat, 4 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(r, cl->raw_density, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    d.pos = p;
+    d.ls = l;
+    d.q = q;
+    d.raw = r;
+  }
+  return d;
+}
+
+void reset_stats(gsct_ctx c) {
+  if (c->async) return;  // async: accumulate until gsct_ctx_synchronize
+  DevStats z{0, 0, 0, 0, ~0ull};
+  CK(cudaMemcpyAsync(c->dstats, &z, sizeof z, cudaMemcpyHostToDevice, c->stream));
+}
+
+// Reads device stats, maps device-side contract errors, accumulates RenderStats.
+void finish_sync(gsct_ctx c, gsct_stats* stats, bool counters, double* ms_slot) {
+  if (c->async) return;
+  CK(cudaMemcpyAsync(c->hstats, c->dstats, sizeof(DevStats), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaEventRecord(c->ev1, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaGetLastError());
+  const DevStats& h = *c->hstats;
+  if (h.error_key != ~0ull) {
+    const unsigned long long idx = h.error_key >> 2;
+    const int code = static_cast<int>(h.error_key & 3);
+    throw CallError{GSCT_ERR_CONTRACT, std::string(code == 1 ? "activate: non-finite parameter in splat "
+                                                             : "activate: zero quaternion in splat ") +
+                                           std::to_string(idx)};
+  }
+  if (stats) {
+    if (counters) {
+      stats->culled += static_cast<int64_t>(h.culled);
+      stats->degenerate += static_cast<int64_t>(h.degenerate);
+      stats->tile_pairs += static_cast<int64_t>(h.tile_pairs);
+      stats->pixel_pairs += static_cast<int64_t>(h.pixel_pairs);
+    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    if (ms_slot == &stats->forward_ms) stats->forward_ms += ms;
+    if (ms_slot == &stats->backward_ms) stats->backward_ms += ms;
+  }
+}
+
+uint32_t read_scan_total(gsct_ctx c, const uint32_t* offsets, const uint32_t* counts, int64_t n) {
+  CK(cudaMemcpyAsync(c->hscratch, offsets + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hscratch + 1, counts + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return c->hscratch[0] + c->hscratch[1];
+}
+
+int bits_for(uint64_t n_keys) {
+  int b = 1;
+  while ((uint64_t(1) << b) < n_keys) ++b;
+  return b;
+}
+
+// Exclusive scan of counts + pair emission + stable radix sort by key + key ranges.
+// Returns the number of pairs; sorted values end up in *vals_out, start/end per key.
+template <class Emit>
+int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32_t n_keys,
+                     Emit&& emit, uint32_t** keys_out, uint32_t** vals_out, uint32_t** start,
+                     uint32_t** end) {
+  uint32_t* offsets = ws<uint32_t>(c, S_OFFSET, static_cast<size_t>(n_items));
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
+  void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
+  const uint32_t total = read_scan_total(c, offsets, counts, n_items);
+  *start = ws<uint32_t>(c, S_START, n_keys);
+  *end = ws<uint32_t>(c, S_END, n_keys);
+  CK(cudaMemsetAsync(*start, 0, n_keys * sizeof(uint32_t), c->stream));
+  CK(cudaMemsetAsync(*end, 0, n_keys * sizeof(uint32_t), c->stream));
+  if (total == 0) {
+    *keys_out = *vals_out = nullptr;
+    return 0;
+  }
+  uint32_t* k1 = ws<uint32_t>(c, S_KEYS, total);
+  uint32_t* v1 = ws<uint32_t>(c, S_VALS, total);
+  uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, total);
+  uint32_t* v2 = ws<uint32_t>(c, S_VALS2, total);
+  emit(offsets, k1, v1);
+  cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
+  const int end_bit = bits_for(n_keys);
+  tmp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(total), 0, end_bit, c->stream));
+  tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(total), 0, end_bit, c->stream));
+  *keys_out = kb.Current();
+  *vals_out = vb.Current();
+  launch_ranges(*keys_out, total, *start, *end, c->stream);
+  return total;
+}
+
+int views_per_chunk(int64_t n, int n_views) {
+  const int64_t budget = int64_t(1) << 25;  // (view, splat) items per chunk
+  int64_t v = n > 0 ? budget / n : n_views;
+  if (v < 1) v = 1;
+  if (v > n_views) v = n_views;
+  return static_cast<int>(v);
+}
+
+}  // namespace
+
+extern "C" {
+
+int gsct_abi_version(void) { return GSCT_ABI_VERSION; }
+
+int gsct_ctx_create(int device, gsct_ctx* out) {
+  if (!out) return GSCT_ERR_CONTRACT;
+  *out = nullptr;
+  int n_dev = 0;
+  if (cudaGetDeviceCount(&n_dev) != cudaSuccess || device < 0 || device >= n_dev) {
+    cudaGetLastError();
+    return GSCT_ERR_CUDA;
+  }
+  auto* c = new gsct_ctx_s();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&c->dstats, sizeof(DevStats)) != cudaSuccess ||
+      cudaMallocHost(&c->hstats, sizeof(DevStats)) != cudaSuccess ||
+      cudaMallocHost(&c->hscratch, 4 * sizeof(uint32_t)) != cudaSuccess ||
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return GSCT_ERR_CUDA;
+  }
+  c->own_stream = true;
+  DevStats z{0, 0, 0, 0, ~0ull};
+  cudaMemcpy(c->dstats, &z, sizeof z, cudaMemcpyHostToDevice);
+  *out = c;
+  return GSCT_OK;
+}
+
+void gsct_ctx_destroy(gsct_ctx c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (Buf& b : c->bufs)
+    if (b.p) cudaFreeAsync(b.p, c->stream);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->dstats);
+  cudaFreeHost(c->hstats);
+  cudaFreeHost(c->hscratch);
+  cudaEventDestroy(c->ev0);
+  cudaEventDestroy(c->ev1);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* gsct_ctx_last_error(gsct_ctx c) { return c ? c->err.c_str() : "null context"; }
+
+int gsct_ctx_set_stream(gsct_ctx c, void* stream) {
+  return run(c, [&] {
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->own_stream) CK(cudaStreamDestroy(c->stream));
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+      c->own_stream = false;
+    } else {
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+  });
+}
+
+void* gsct_ctx_stream(gsct_ctx c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int gsct_ctx_set_async(gsct_ctx c, int async) {
+  return run(c, [&] {
+    CK(cudaStreamSynchronize(c->stream));
+    c->async = async != 0;
+    DevStats z{0, 0, 0, 0, ~0ull};
+    CK(cudaMemcpyAsync(c->dstats, &z, sizeof z, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int gsct_ctx_synchronize(gsct_ctx c, gsct_stats* stats_accum) {
+  return run(c, [&] {
+    CK(cudaMemcpyAsync(c->hstats, c->dstats, sizeof(DevStats), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaGetLastError());
+    const DevStats h = *c->hstats;
+    DevStats z{0, 0, 0, 0, ~0ull};
+    CK(cudaMemcpyAsync(c->dstats, &z, sizeof z, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (stats_accum) {
+      stats_accum->culled += static_cast<int64_t>(h.culled);
+      stats_accum->degenerate += static_cast<int64_t>(h.degenerate);
+      stats_accum->tile_pairs += static_cast<int64_t>(h.tile_pairs);
+      stats_accum->pixel_pairs += static_cast<int64_t>(h.pixel_pairs);
+    }
+    if (h.error_key != ~0ull) {
+      const unsigned long long idx = h.error_key >> 2;
+      const int code = static_cast<int>(h.error_key & 3);
+      throw CallError{GSCT_ERR_CONTRACT, std::string(code == 1 ? "activate: non-finite parameter in splat "
+                                                               : "activate: zero quaternion in splat ") +
+                                             std::to_string(idx)};
+    }
+  });
+}
+
+size_t gsct_ctx_workspace_bytes(gsct_ctx c) {
+  if (!c) return 0;
+  size_t s = 0;
+  for (const Buf& b : c->bufs) s += b.cap;
+  return s;
+}
+
+int64_t gsct_ctx_launch_count(gsct_ctx c) { return c ? c->launches : 0; }
+
+// ---------------------------------------------------------------------------------------
+// Rasterizer
+// ---------------------------------------------------------------------------------------
+
+int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry* geom,
+                       const double* angles, int n_views, const gsct_raster_settings* rs,
+                       float* images, int images_location, gsct_stats* stats) {
+  return run(c, [&] {
+    validate_geometry(geom, angles, n_views);
+    contract(rs != nullptr, "RasterSettings: null");
+    contract(rs->tile_size >= 1, "bin_tiles: tile size must be at least 1");
+    contract(images != nullptr || n_views == 0, "rasterize: null image buffer");
+    if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    const int64_t n = d.n;
+    const int64_t npx = static_cast<int64_t>(geom->n_u) * geom->n_v;
+    const int tiles_u = (geom->n_u + kTile - 1) / kTile, tiles_v = (geom->n_v + kTile - 1) / kTile;
+    const int n_tiles = tiles_u * tiles_v;
+    std::vector<Frame> frames(static_cast<size_t>(n_views));
+    for (int v = 0; v < n_views; ++v) frames[static_cast<size_t>(v)] = make_frame(geom, angles[v]);
+    Frame* dframes = ws<Frame>(c, S_FRAMES, frames.size() + 1);
+    if (n_views)
+      CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
+    float* out = images;
+    if (images_location == GSCT_HOST && n_views) out = ws<float>(c, S_IMAGES, static_cast<size_t>(npx) * n_views);
+    const Geo g = make_geo(geom);
+    const RSet r = make_rs(rs);
+    int chunk = views_per_chunk(n, n_views);
+    for (int v0 = 0; v0 < n_views; v0 += chunk) {
+      const int cv = std::min(chunk, n_views - v0);
+      float* img = out + static_cast<int64_t>(v0) * npx;
+      if (n == 0) {
+        CK(cudaMemsetAsync(img, 0, static_cast<size_t>(npx) * cv * sizeof(float), c->stream));
+        continue;
+      }
+      RasterRec* rec = ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * cv);
+      uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * cv);
+      launch_raster_preprocess(d, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
+      CK(cudaGetLastError());
+      uint32_t *keys, *vals, *start, *end;
+      const uint32_t n_keys = static_cast<uint32_t>(cv) * static_cast<uint32_t>(n_tiles);
+      bin_and_sort(
+          c, cnt, n * cv, n_keys,
+          [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
+            launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kTile, tiles_u, n_tiles, k, v, c->stream);
+          },
+          &keys, &vals, &start, &end);
+      launch_raster_fwd(rec, vals, start, end, n, cv, geom->n_u, geom->n_v, tiles_u, tiles_v, img, c->stream);
+      CK(cudaGetLastError());
+    }
+    if (images_location == GSCT_HOST && n_views)
+      CK(cudaMemcpyAsync(images, out, static_cast<size_t>(npx) * n_views * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
+  });
+}
+
+int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry* geom,
+                       const double* angles, int n_views, const gsct_raster_settings* rs,
+                       const float* grad_images, int grad_location, gsct_grads* out,
+                       gsct_stats* stats) {
+  return run(c, [&] {
+    validate_geometry(geom, angles, n_views);
+    contract(rs != nullptr, "RasterSettings: null");
+    contract(rs->tile_size >= 1, "bin_tiles: tile size must be at least 1");
+    contract(out != nullptr, "rasterize_backward: null gradient output");
+    contract(grad_images != nullptr || n_views == 0, "rasterize_backward: grad image dims must match detector");
+    if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    const int64_t n = d.n;
+    const size_t un = static_cast<size_t>(n);
+    const int64_t npx = static_cast<int64_t>(geom->n_u) * geom->n_v;
+    double *gp = out->pos, *gl = out->log_scale, *gq = out->quat, *gr = out->raw_density, *gn = out->pos_grad_norm;
+    uint8_t* gv = out->visible;
+    if (out->location == GSCT_HOST) {
+      gp = ws<double>(c, S_GPOS, 3 * un);
+      gl = ws<double>(c, S_GLS, 3 * un);
+      gq = ws<double>(c, S_GQ, 4 * un);
+      gr = ws<double>(c, S_GRAW, un);
+      gn = ws<double>(c, S_GPGN, un);
+      gv = ws<uint8_t>(c, S_GVIS, un);
+    }
+    if (n > 0 && n_views == 0) {
+      CK(cudaMemsetAsync(gp, 0, 3 * un * sizeof(double), c->stream));
+      CK(cudaMemsetAsync(gl, 0, 3 * un * sizeof(double), c->stream));
+      CK(cudaMemsetAsync(gq, 0, 4 * un * sizeof(double), c->stream));
+      CK(cudaMemsetAsync(gr, 0, un * sizeof(double), c->stream));
+      CK(cudaMemsetAsync(gn, 0, un * sizeof(double), c->stream));
+      CK(cudaMemsetAsync(gv, 0, un, c->stream));
+    }
+    std::vector<Frame> frames(static_cast<size_t>(n_views));
+    for (int v = 0; v < n_views; ++v) frames[static_cast<size_t>(v)] = make_frame(geom, angles[v]);
+    Frame* dframes = ws<Frame>(c, S_FRAMES, frames.size() + 1);
+    if (n_views)
+      CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
+    const Geo g = make_geo(geom);
+    const RSet r = make_rs(rs);
+    const int chunk = views_per_chunk(n, n_views);
+    for (int v0 = 0; v0 < n_views && n > 0; v0 += chunk) {
+      const int cv = std::min(chunk, n_views - v0);
+      const float* gimg = grad_images + static_cast<int64_t>(v0) * npx;
+      if (grad_location == GSCT_HOST) {
+        float* dst = ws<float>(c, S_GRADIMG, static_cast<size_t>(npx) * cv);
+        CK(cudaMemcpyAsync(dst, gimg, static_cast<size_t>(npx) * cv * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        gimg = dst;
+      }
+      RasterRec* rec = ws<RasterRec>(c, S_REC, un * cv);
+      uint32_t* cnt = ws<uint32_t>(c, S_COUNT, un * cv);
+      launch_raster_preprocess(d, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
+      float* mom = ws<float>(c, S_MOMENTS, un * cv * 8);
+      launch_raster_bwd_pairs(rec, n, cv, geom->n_u, geom->n_v, gimg, mom, nullptr, c->stream);
+      launch_raster_tail(d, dframes + v0, cv, g, r, mom, v0 == 0, gp, gl, gq, gr, gn, gv, c->stream);
+      CK(cudaGetLastError());
+    }
+    if (out->location == GSCT_HOST && n > 0) {
+      CK(cudaMemcpyAsync(out->pos, gp, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(out->log_scale, gl, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(out->quat, gq, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(out->raw_density, gr, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(out->pos_grad_norm, gn, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(out->visible, gv, un, cudaMemcpyDeviceToHost, c->stream));
+    }
+    finish_sync(c, stats, false, stats ? &stats->backward_ms : nullptr);
+  });
+}
+
+// ---------------------------------------------------------------------------------------
+// Voxelizer
+// ---------------------------------------------------------------------------------------
+
+namespace {
+
+VoxGrid make_grid(const gsct_grid* g) {
+  contract(g != nullptr, "GridRegion: null grid");
+  contract(g->dims[0] >= 1 && g->dims[1] >= 1 && g->dims[2] >= 1, "GridRegion: dims must be at least 1");
+  contract(g->spacing > 0.0, "Volume: spacing must be positive");
+  VoxGrid v;
+  for (int k = 0; k < 3; ++k) {
+    v.dims[k] = g->dims[k];
+    v.origin[k] = g->origin[k];
+  }
+  v.spacing = g->spacing;
+  return v;
+}
+
+Window make_window(const gsct_grid* g, const gsct_window* w) {
+  Window win;
+  for (int k = 0; k < 3; ++k) {
+    win.lo[k] = w ? w->lo[k] : 0;
+    win.hi[k] = w ? w->hi[k] : g->dims[k];
+    contract(win.lo[k] >= 0 && win.lo[k] < win.hi[k] && win.hi[k] <= g->dims[k],
+             "GridRegion: region outside parent grid");
+  }
+  return win;
+}
+
+int64_t window_count(const Window& w) {
+  return static_cast<int64_t>(w.hi[0] - w.lo[0]) * (w.hi[1] - w.lo[1]) * (w.hi[2] - w.lo[2]);
+}
+
+// Backward pixel loop into moments[10][N] (zero-filled) for one window.
+void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window& win,
+                   const gsct_voxel_settings* vs, const float* grad, int grad_location, float* mom) {
+  const int64_t n = d.n;
+  const int64_t nvox = window_count(win);
+  if (grad_location == GSCT_HOST) {
+    float* dst = ws<float>(c, S_GRADVOL, static_cast<size_t>(nvox));
+    CK(cudaMemcpyAsync(dst, grad, static_cast<size_t>(nvox) * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    grad = dst;
+  }
+  CK(cudaMemsetAsync(mom, 0, static_cast<size_t>(n) * 10 * sizeof(float), c->stream));
+  if (n == 0) return;
+  VoxelRec* rec = ws<VoxelRec>(c, S_VREC, static_cast<size_t>(n));
+  launch_voxel_preprocess(d, grid, win, vs->tau_cut, vs->sigma_cap, rec, nullptr, nullptr, nullptr,
+                          nullptr, c->dstats, c->stream);
+  launch_voxel_bwd_pairs(rec, n, win, static_cast<float>(grid.spacing), grad, mom, nullptr, c->stream);
+  CK(cudaGetLastError());
+}
+
+struct GradPtrs {
+  double *gp, *gl, *gq, *gr, *gn;
+  uint8_t* gv;
+};
+
+GradPtrs grad_targets(gsct_ctx c, gsct_grads* out, size_t un) {
+  if (out->location == GSCT_HOST)
+    return GradPtrs{ws<double>(c, S_GPOS, 3 * un), ws<double>(c, S_GLS, 3 * un), ws<double>(c, S_GQ, 4 * un),
+                    ws<double>(c, S_GRAW, un),     ws<double>(c, S_GPGN, un),    ws<uint8_t>(c, S_GVIS, un)};
+  return GradPtrs{out->pos, out->log_scale, out->quat, out->raw_density, out->pos_grad_norm, out->visible};
+}
+
+void grads_to_host(gsct_ctx c, gsct_grads* out, const GradPtrs& p, size_t un) {
+  if (out->location != GSCT_HOST || un == 0) return;
+  CK(cudaMemcpyAsync(out->pos, p.gp, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(out->log_scale, p.gl, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(out->quat, p.gq, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(out->raw_density, p.gr, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(out->pos_grad_norm, p.gn, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(out->visible, p.gv, un, cudaMemcpyDeviceToHost, c->stream));
+}
+
+}  // namespace
+
+int gsct_voxelize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid,
+                      const gsct_window* window, const gsct_voxel_settings* vs, float* volume,
+                      int volume_location, gsct_stats* stats) {
+  return run(c, [&] {
+    const VoxGrid vg = make_grid(grid);
+    const Window win = make_window(grid, window);
+    contract(vs != nullptr, "VoxelSettings: null");
+    contract(volume != nullptr, "voxelize: null volume buffer");
+    if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    const int64_t n = d.n;
+    const int64_t nvox = window_count(win);
+    float* outv = volume;
+    if (volume_location == GSCT_HOST) outv = ws<float>(c, S_VOLUME, static_cast<size_t>(nvox));
+    const int nbx = (win.hi[0] - win.lo[0] + kBrick - 1) / kBrick;
+    const int nby = (win.hi[1] - win.lo[1] + kBrick - 1) / kBrick;
+    const int nbz = (win.hi[2] - win.lo[2] + kBrick - 1) / kBrick;
+    const uint64_t n_bricks = static_cast<uint64_t>(nbx) * nby * nbz;
+    contract(n_bricks < (uint64_t(1) << 31), "voxelize: grid too large");
+    if (n == 0) {
+      CK(cudaMemsetAsync(outv, 0, static_cast<size_t>(nvox) * sizeof(float), c->stream));
+    } else {
+      VoxelRec* rec = ws<VoxelRec>(c, S_VREC, static_cast<size_t>(n));
+      uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n));
+      launch_voxel_preprocess(d, vg, win, vs->tau_cut, vs->sigma_cap, rec, cnt, nullptr, nullptr, nullptr,
+                              c->dstats, c->stream);
+      uint32_t *keys, *vals, *start, *end;
+      bin_and_sort(
+          c, cnt, n, static_cast<uint32_t>(n_bricks),
+          [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
+            launch_emit_brick_pairs(rec, offsets, cnt, n, win, nbx, nby, k, v, c->stream);
+          },
+          &keys, &vals, &start, &end);
+      launch_voxel_fwd(rec, vals, start, end, win, nbx, nby, nbz, static_cast<float>(vg.spacing), outv, c->stream);
+      CK(cudaGetLastError());
+    }
+    if (volume_location == GSCT_HOST)
+      CK(cudaMemcpyAsync(volume, outv, static_cast<size_t>(nvox) * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
+  });
+}
+
+int gsct_voxelize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid,
+                      const gsct_window* window, const gsct_voxel_settings* vs,
+                      const float* grad_volume, int grad_location, gsct_grads* out,
+                      gsct_stats* stats) {
+  return run(c, [&] {
+    const VoxGrid vg = make_grid(grid);
+    const Window win = make_window(grid, window);
+    contract(vs != nullptr, "VoxelSettings: null");
+    contract(out != nullptr, "voxelize_backward: null gradient output");
+    contract(grad_volume != nullptr, "voxelize_backward: grad dims must match region");
+    if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    const size_t un = static_cast<size_t>(d.n);
+    float* mom = ws<float>(c, S_MOMENTS, un * 10 + 1);
+    voxel_moments(c, d, vg, win, vs, grad_volume, grad_location, mom);
+    const GradPtrs p = grad_targets(c, out, un);
+    launch_voxel_tail(d, vg, vs->tau_cut, vs->sigma_cap, mom, p.gp, p.gl, p.gq, p.gr, p.gn, p.gv, c->dstats,
+                      c->stream);
+    CK(cudaGetLastError());
+    grads_to_host(c, out, p, un);
+    finish_sync(c, stats, false, stats ? &stats->backward_ms : nullptr);
+  });
+}
+
+int gsct_voxelize_bwd_moments(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid,
+                              const gsct_window* window, const gsct_voxel_settings* vs,
+                              const float* grad_volume, int grad_location, float* moments_dev) {
+  return run(c, [&] {
+    const VoxGrid vg = make_grid(grid);
+    const Window win = make_window(grid, window);
+    contract(vs != nullptr && moments_dev != nullptr && grad_volume != nullptr, "voxelize_backward: null buffer");
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    voxel_moments(c, d, vg, win, vs, grad_volume, grad_location, moments_dev);
+    finish_sync(c, nullptr, false, nullptr);
+  });
+}
+
+int gsct_voxelize_bwd_finish(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid,
+                             const gsct_voxel_settings* vs, const float* moments_dev,
+                             gsct_grads* out) {
+  return run(c, [&] {
+    const VoxGrid vg = make_grid(grid);
+    contract(vs != nullptr && moments_dev != nullptr && out != nullptr, "voxelize_backward: null buffer");
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    const size_t un = static_cast<size_t>(d.n);
+    const GradPtrs p = grad_targets(c, out, un);
+    launch_voxel_tail(d, vg, vs->tau_cut, vs->sigma_cap, moments_dev, p.gp, p.gl, p.gq, p.gr, p.gn, p.gv,
+                      c->dstats, c->stream);
+    CK(cudaGetLastError());
+    grads_to_host(c, out, p, un);
+    finish_sync(c, nullptr, false, nullptr);
+  });
+}
+
+// ---------------------------------------------------------------------------------------
+// Parity hooks
+// ---------------------------------------------------------------------------------------
+
+int gsct_debug_project(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry* geom, double angle,
+                       const gsct_raster_settings* rs, int32_t* rect, uint8_t* flags, double* mean2d,
+                       double* conic, double* amplitude) {
+  return run(c, [&] {
+    validate_geometry(geom, &angle, 1);
+    contract(rs != nullptr, "RasterSettings: null");
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    const size_t un = static_cast<size_t>(d.n);
+    if (un == 0) return;
+    const Frame fr = make_frame(geom, angle);
+    Frame* df = ws<Frame>(c, S_FRAMES, 1);
+    CK(cudaMemcpyAsync(df, &fr, sizeof fr, cudaMemcpyHostToDevice, c->stream));
+    int32_t* drect = ws<int32_t>(c, S_DBG0, 4 * un);
+    uint8_t* dflags = ws<uint8_t>(c, S_DBG1, un);
+    double* dmean = ws<double>(c, S_DBG2, 2 * un);
+    double* dconic = ws<double>(c, S_DBG3, 4 * un);
+    double* damp = ws<double>(c, S_DBG4, un);
+    launch_debug_project(d, df, make_geo(geom), make_rs(rs), drect, dflags, dmean, dconic, damp, c->dstats,
+                         c->stream);
+    CK(cudaMemcpyAsync(rect, drect, 4 * un * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(flags, dflags, un, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(mean2d, dmean, 2 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(conic, dconic, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(amplitude, damp, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    finish_sync(c, nullptr, false, nullptr);
+  });
+}
+
+int gsct_debug_tile_pairs(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry* geom, const double* angles,
+                          int n_views, const gsct_raster_settings* rs, uint32_t* keys, uint32_t* values,
+                          int64_t capacity, int64_t* n_pairs) {
+  return run(c, [&] {
+    validate_geometry(geom, angles, n_views);
+    contract(rs != nullptr && rs->tile_size >= 1, "bin_tiles: tile size must be at least 1");
+    contract(n_pairs != nullptr, "debug_tile_pairs: null count");
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    const int64_t n = d.n;
+    *n_pairs = 0;
+    if (n == 0 || n_views == 0) {
+      finish_sync(c, nullptr, false, nullptr);
+      return;
+    }
+    const int ts = rs->tile_size;
+    const int tiles_u = (geom->n_u + ts - 1) / ts, tiles_v = (geom->n_v + ts - 1) / ts;
+    const int n_tiles = tiles_u * tiles_v;
+    std::vector<Frame> frames(static_cast<size_t>(n_views));
+    for (int v = 0; v < n_views; ++v) frames[static_cast<size_t>(v)] = make_frame(geom, angles[v]);
+    Frame* dframes = ws<Frame>(c, S_FRAMES, frames.size());
+    CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
+    RasterRec* rec = ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * n_views);
+    uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * n_views);
+    launch_raster_preprocess(d, dframes, n_views, make_geo(geom), make_rs(rs), ts, rec, cnt, c->dstats, c->stream);
+    uint32_t *dk, *dv, *start, *end;
+    const int64_t total = bin_and_sort(
+        c, cnt, n * n_views, static_cast<uint32_t>(n_views) * static_cast<uint32_t>(n_tiles),
+        [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
+          launch_emit_tile_pairs(rec, offsets, cnt, n, n_views, ts, tiles_u, n_tiles, k, v, c->stream);
+        },
+        &dk, &dv, &start, &end);
+    *n_pairs = total;
+    if (total > 0 && total <= capacity && keys && values) {
+      CK(cudaMemcpyAsync(keys, dk, static_cast<size_t>(total) * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(values, dv, static_cast<size_t>(total) * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    }
+    finish_sync(c, nullptr, false, nullptr);
+  });
+}
+
+int gsct_debug_voxel_boxes(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid, const gsct_window* window,
+                           const gsct_voxel_settings* vs, int32_t* lo, int32_t* hi, uint8_t* skip) {
+  return run(c, [&] {
+    const VoxGrid vg = make_grid(grid);
+    const Window win = make_window(grid, window);
+    contract(vs != nullptr, "VoxelSettings: null");
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    const size_t un = static_cast<size_t>(d.n);
+    if (un == 0) return;
+    int32_t* dlo = ws<int32_t>(c, S_DBG0, 3 * un);
+    int32_t* dhi = ws<int32_t>(c, S_DBG1, 3 * un);
+    uint8_t* dskip = ws<uint8_t>(c, S_DBG2, un);
+    launch_voxel_preprocess(d, vg, win, vs->tau_cut, vs->sigma_cap, nullptr, nullptr, dlo, dhi, dskip, c->dstats,
+                            c->stream);
+    CK(cudaMemcpyAsync(lo, dlo, 3 * un * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(hi, dhi, 3 * un * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(skip, dskip, un, cudaMemcpyDeviceToHost, c->stream));
+    finish_sync(c, nullptr, false, nullptr);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Internal types and kernel-launch wrappers shared by the CUDA translation units of
+// libgsct_b200.so. Nothing here crosses the C ABI (include/gsct_cuda.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "splat_fp64.cuh"
+
+namespace gsct_dev {
+
+constexpr int kTile = 16;       // reference default tile (projector.hpp:67); the raster
+                                // kernel is specialised for it, other sizes are rejected
+constexpr int kBrick = 8;       // voxel brick edge (8x8x8 voxels per CTA)
+constexpr float kLog2e = 1.4426950408889634f;
+
+// Device counters written by the set-up kernels (order-independent integer sums).
+struct DevStats {
+  unsigned long long culled, degenerate, tile_pairs, pixel_pairs;
+  unsigned long long error_key;  // min over (splat << 2 | code), ~0 if none
+};
+
+// Per (view, splat) raster record, fp32, 32 B. Coordinates are relative to the splat's
+// integer bbox corner (computed in fp64, then rounded) so fp32 per-pixel offsets are
+// exact-to-rounding at 2048^2 detectors. Exponent coefficients are pre-scaled by log2(e):
+//   exp(e) = exp2(A du^2 + B du dv + C dv^2), A=-a/2*log2e, B=-b*log2e, C=-c/2*log2e.
+struct __align__(16) RasterRec {
+  uint32_t urange;  // u_min | u_max << 16   (empty: u_min > u_max)
+  uint32_t vrange;  // v_min | v_max << 16
+  float mo_u, mo_v; // mean2d - (u_min, v_min)
+  float A, B, C, amp;
+};
+static_assert(sizeof(RasterRec) == 32, "RasterRec must be 32 B");
+
+// Per splat voxel record, fp32, 64 B. lo/hi: inclusive box in grid indices (already
+// clipped to the call's window), as exact floats. off = p - (origin + spacing*lo) (fp64,
+// rounded). q(d) coefficients pre-scaled by -0.5*log2e; cross terms carry the factor 2:
+//   exp(-q/2) = exp2(Q00 dx^2 + Q11 dy^2 + Q22 dz^2 + Q01 dx dy + Q02 dx dz + Q12 dy dz).
+struct __align__(16) VoxelRec {
+  float lox, loy, loz, rho;
+  float hix, hiy, hiz, Q00;
+  float offx, offy, offz, Q11;
+  float Q22, Q01, Q02, Q12;
+};
+static_assert(sizeof(VoxelRec) == 64, "VoxelRec must be 64 B");
+
+struct Cloud {
+  int64_t n;
+  const double* pos;
+  const double* ls;
+  const double* q;
+  const double* raw;
+};
+
+struct Window {
+  int lo[3], hi[3];  // [lo, hi)
+};
+
+// ---- launch wrappers (defined in preprocess.cu / raster.cu / voxel.cu) ----
+void launch_raster_preprocess(const Cloud& c, const Frame* frames_dev, int n_views,
+                              const Geo& g, const RSet& rs, int bin_ts, RasterRec* rec,
+                              uint32_t* tile_count, DevStats* stats, cudaStream_t st);
+void launch_raster_tail(const Cloud& c, const Frame* frames_dev, int n_views, const Geo& g,
+                        const RSet& rs, const float* moments, bool first_chunk, double* g_pos,
+                        double* g_ls, double* g_q, double* g_raw, double* g_pgn,
+                        uint8_t* visible, cudaStream_t st);
+void launch_debug_project(const Cloud& c, const Frame* frame_dev, const Geo& g, const RSet& rs,
+                          int32_t* rect, uint8_t* flags, double* mean2d, double* conic,
+                          double* amplitude, DevStats* stats, cudaStream_t st);
+void launch_voxel_preprocess(const Cloud& c, const VoxGrid& grid, const Window& win,
+                             double tau_cut, double sigma_cap, VoxelRec* rec,
+                             uint32_t* brick_count, int32_t* lo_out, int32_t* hi_out,
+                             uint8_t* skip_out, DevStats* stats, cudaStream_t st);
+void launch_voxel_tail(const Cloud& c, const VoxGrid& grid, double tau_cut, double sigma_cap,
+                       const float* moments, double* g_pos, double* g_ls, double* g_q,
+                       double* g_raw, double* g_pgn, uint8_t* visible, DevStats* stats,
+                       cudaStream_t st);
+
+void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets,
+                            const uint32_t* counts, int64_t n, int n_views, int ts, int tiles_u,
+                            int n_tiles, uint32_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t* start, uint32_t* end,
+                   cudaStream_t st);
+void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
+                       const uint32_t* end, int64_t n, int n_views, int n_u, int n_v,
+                       int tiles_u, int tiles_v, float* images, cudaStream_t st);
+void launch_raster_bwd_pairs(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v,
+                             const float* grad_images, float* moments, unsigned int* work_counter,
+                             cudaStream_t st);
+
+void launch_emit_brick_pairs(const VoxelRec* rec, const uint32_t* offsets,
+                             const uint32_t* counts, int64_t n, const Window& win, int nbx,
+                             int nby, uint32_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t* start,
+                      const uint32_t* end, const Window& win, int nbx, int nby, int nbz,
+                      float spacing, float* volume, cudaStream_t st);
+void launch_voxel_bwd_pairs(const VoxelRec* rec, int64_t n, const Window& win, float spacing,
+                            const float* grad_volume, float* moments, unsigned int* work_counter,
+                            cudaStream_t st);
+
+// Launch accounting (gsct_ctx_launch_count).
+extern thread_local int64_t* g_launch_counter;
+inline void count_launch(int k = 1) {
+  if (g_launch_counter) *g_launch_counter += k;
+}
+
+}  // namespace gsct_dev

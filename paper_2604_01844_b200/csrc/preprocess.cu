@@ -1,0 +1,388 @@
+// fp64 per-splat kernels: raster set-up (K1), raster chain-rule tail (K4b), voxel set-up
+// (K6), voxel chain-rule tail (K8b), and the projection parity hook.
+// Compiled with --fmad=false so the arithmetic is the reference's, operation by operation
+// (see splat_fp64.cuh): integer boxes and keys are bit-exact with the CPU oracle.
+#include <cuda_runtime.h>
+
+#include "gsct_internal.cuh"
+
+namespace gsct_dev {
+
+namespace {
+
+constexpr double kLog2eD = 1.4426950408889634074;
+
+__device__ __forceinline__ void flag_error(DevStats* st, int64_t i, int code) {
+  atomicMin(&st->error_key, (static_cast<unsigned long long>(i) << 2) | static_cast<unsigned>(code));
+}
+
+// Warp-aggregated add of small integer counters.
+__device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+__device__ __forceinline__ RasterRec empty_rec() {
+  RasterRec r;
+  r.urange = 0xFFFFu;  // u_min = 65535 > u_max = 0
+  r.vrange = 0xFFFFu;
+  r.mo_u = r.mo_v = r.A = r.B = r.C = r.amp = 0.f;
+  return r;
+}
+
+// K1: one thread per (splat, view): activate -> covariance -> project_full -> splat_bbox,
+// then the fp32 record, the binning tile count and the exact RenderStats counters.
+__global__ void __launch_bounds__(256) k_raster_preprocess(Cloud c, const Frame* __restrict__ frames,
+                                                           Geo g, RSet rs, int bin_ts,
+                                                           RasterRec* __restrict__ rec,
+                                                           uint32_t* __restrict__ tile_count,
+                                                           DevStats* __restrict__ st) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  unsigned long long n_culled = 0, n_degen = 0, n_tp = 0, n_pp = 0;
+  if (i < c.n) {
+    RasterRec r = empty_rec();
+    uint32_t cnt = 0;
+    Act a;
+    const int err = activate(c.pos, c.ls, c.q, c.raw, i, a);
+    if (err) {
+      if (v == 0) flag_error(st, i, err);
+    } else {
+      double sigma[9];
+      covariance(a.scales, a.uq, sigma);
+      Proj p;
+      project_full(frames[v], g, a.pos, sigma, a.density, rs, p);
+      if (p.degenerate) {
+        n_degen = 1;
+      } else if (p.culled) {
+        n_culled = 1;
+      } else {
+        const int u0 = p.rect[0], u1 = p.rect[1], v0 = p.rect[2], v1 = p.rect[3];
+        r.urange = static_cast<uint32_t>(u0) | (static_cast<uint32_t>(u1) << 16);
+        r.vrange = static_cast<uint32_t>(v0) | (static_cast<uint32_t>(v1) << 16);
+        r.mo_u = static_cast<float>(p.mean2d[0] - static_cast<double>(u0));
+        r.mo_v = static_cast<float>(p.mean2d[1] - static_cast<double>(v0));
+        r.A = static_cast<float>(-0.5 * kLog2eD * p.conic[0]);
+        r.B = static_cast<float>(-kLog2eD * p.conic[1]);
+        r.C = static_cast<float>(-0.5 * kLog2eD * p.conic[3]);
+        r.amp = static_cast<float>(p.amplitude);
+        // binning count at the kernel's tile size; stats at the requested tile size
+        cnt = static_cast<uint32_t>((u1 / bin_ts - u0 / bin_ts + 1) * (v1 / bin_ts - v0 / bin_ts + 1));
+        const int ts = rs.tile_size;
+        n_tp = static_cast<unsigned long long>((u1 / ts - u0 / ts + 1)) *
+               static_cast<unsigned long long>((v1 / ts - v0 / ts + 1));
+        n_pp = static_cast<unsigned long long>(u1 - u0 + 1) * static_cast<unsigned long long>(v1 - v0 + 1);
+      }
+    }
+    const int64_t item = static_cast<int64_t>(v) * c.n + i;
+    rec[item] = r;
+    tile_count[item] = cnt;
+  }
+  warp_add(&st->culled, n_culled);
+  warp_add(&st->degenerate, n_degen);
+  warp_add(&st->tile_pairs, n_tp);
+  warp_add(&st->pixel_pairs, n_pp);
+}
+
+// K4b: one thread per splat; for each view of the chunk (ascending) re-derive the fp64
+// projection, turn the fp32 pixel-loop moments into dL/d(amp, mean2d, conic) and run the
+// reference chain rule; per-view results are summed in view order (ParamGradients::add).
+__global__ void __launch_bounds__(128) k_raster_tail(Cloud c, const Frame* __restrict__ frames,
+                                                     int n_views, Geo g, RSet rs,
+                                                     const float4* __restrict__ moments,
+                                                     int first_chunk, double* __restrict__ g_pos,
+                                                     double* __restrict__ g_ls, double* __restrict__ g_q,
+                                                     double* __restrict__ g_raw,
+                                                     double* __restrict__ g_pgn,
+                                                     uint8_t* __restrict__ visible) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= c.n) return;
+  double tp[3] = {0, 0, 0}, tl[3] = {0, 0, 0}, tq[4] = {0, 0, 0, 0}, tr = 0.0, tn = 0.0;
+  uint8_t vis = 0;
+  if (!first_chunk) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      tp[k] = g_pos[3 * i + k];
+      tl[k] = g_ls[3 * i + k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tq[k] = g_q[4 * i + k];
+    tr = g_raw[i];
+    tn = g_pgn[i];
+    vis = visible[i];
+  }
+  Act a;
+  if (activate(c.pos, c.ls, c.q, c.raw, i, a) == 0) {
+    double sigma[9];
+    covariance(a.scales, a.uq, sigma);
+    for (int v = 0; v < n_views; ++v) {
+      Proj p;
+      project_full(frames[v], g, a.pos, sigma, a.density, rs, p);
+      if (p.degenerate || p.culled) continue;
+      vis = 1;
+      const int64_t item = static_cast<int64_t>(v) * c.n + i;
+      const float4 m0 = moments[2 * item];
+      const float4 m1 = moments[2 * item + 1];
+      // m0 = {sum t, sum t du, sum t dv, sum t du^2}, m1 = {sum t du dv, sum t dv^2, -, -}
+      const double amp = p.amplitude;
+      const double a_ = p.conic[0], b_ = p.conic[1], c_ = p.conic[3];
+      const double Mu = m0.y, Mv = m0.z;
+      double gm[2], gc[4];
+      gm[0] = amp * (a_ * Mu + b_ * Mv);
+      gm[1] = amp * (b_ * Mu + c_ * Mv);
+      gc[0] = -0.5 * amp * static_cast<double>(m0.w);
+      gc[1] = -0.5 * amp * static_cast<double>(m1.x);
+      gc[2] = gc[1];
+      gc[3] = -0.5 * amp * static_cast<double>(m1.y);
+      double vp[3], vl[3], vq[4], vr;
+      raster_chain_rule(frames[v], g, rs, a, sigma, p, static_cast<double>(m0.x), gm, gc, vp, vl,
+                        vq, vr);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        tp[k] += vp[k];
+        tl[k] += vl[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tq[k] += vq[k];
+      tr += vr;
+      tn += sqrt(gm[0] * gm[0] + gm[1] * gm[1]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g_pos[3 * i + k] = tp[k];
+    g_ls[3 * i + k] = tl[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) g_q[4 * i + k] = tq[k];
+  g_raw[i] = tr;
+  g_pgn[i] = tn;
+  visible[i] = vis;
+}
+
+__global__ void k_debug_project(Cloud c, const Frame* __restrict__ frame, Geo g, RSet rs,
+                                int32_t* rect, uint8_t* flags, double* mean2d, double* conic,
+                                double* amplitude, DevStats* st) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= c.n) return;
+  Act a;
+  const int err = activate(c.pos, c.ls, c.q, c.raw, i, a);
+  if (err) {
+    flag_error(st, i, err);
+    return;
+  }
+  double sigma[9];
+  covariance(a.scales, a.uq, sigma);
+  Proj p;
+  project_full(*frame, g, a.pos, sigma, a.density, rs, p);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    rect[4 * i + k] = p.rect[k];
+    conic[4 * i + k] = p.conic[k];
+  }
+  flags[i] = static_cast<uint8_t>((p.culled ? 1 : 0) | (p.degenerate ? 2 : 0));
+  mean2d[2 * i] = p.mean2d[0];
+  mean2d[2 * i + 1] = p.mean2d[1];
+  amplitude[i] = p.amplitude;
+}
+
+// K6: one thread per splat: prepare_voxel_splat in grid coordinates, clip to the window,
+// fp32 record relative to the clipped box corner, brick count, exact stats.
+__global__ void __launch_bounds__(256) k_voxel_preprocess(Cloud c, VoxGrid grid, Window win,
+                                                          double tau_cut, double sigma_cap,
+                                                          VoxelRec* __restrict__ rec,
+                                                          uint32_t* __restrict__ brick_count,
+                                                          int32_t* lo_out, int32_t* hi_out,
+                                                          uint8_t* skip_out, DevStats* st) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long n_culled = 0, n_pp = 0;
+  if (i < c.n) {
+    VoxelRec r;
+    r.lox = r.loy = r.loz = 1.f;
+    r.hix = r.hiy = r.hiz = 0.f;  // empty
+    r.rho = r.Q00 = r.offx = r.offy = r.offz = r.Q11 = r.Q22 = r.Q01 = r.Q02 = r.Q12 = 0.f;
+    uint32_t cnt = 0;
+    int lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+    bool vis = false;
+    Act a;
+    const int err = activate(c.pos, c.ls, c.q, c.raw, i, a);
+    if (err) {
+      flag_error(st, i, err);
+    } else {
+      double sigma[9], A[9];
+      covariance(a.scales, a.uq, sigma);
+      vis = prepare_voxel_splat(a, sigma, grid, tau_cut, sigma_cap, A, lo, hi);
+      // The record keeps the grid-clipped box (so per-voxel arithmetic does not depend on
+      // the window: z-slabs reproduce the full-grid volume bit for bit); the window clip
+      // only decides visibility, brick counts and stats.
+      int wlo[3], whi[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        wlo[k] = lo[k] > win.lo[k] ? lo[k] : win.lo[k];
+        whi[k] = hi[k] < win.hi[k] - 1 ? hi[k] : win.hi[k] - 1;
+        vis = vis && wlo[k] <= whi[k];
+      }
+      if (vis) {
+        r.lox = static_cast<float>(lo[0]);
+        r.loy = static_cast<float>(lo[1]);
+        r.loz = static_cast<float>(lo[2]);
+        r.hix = static_cast<float>(hi[0]);
+        r.hiy = static_cast<float>(hi[1]);
+        r.hiz = static_cast<float>(hi[2]);
+        r.rho = static_cast<float>(a.density);
+        r.offx = static_cast<float>(a.pos[0] - (grid.origin[0] + grid.spacing * lo[0]));
+        r.offy = static_cast<float>(a.pos[1] - (grid.origin[1] + grid.spacing * lo[1]));
+        r.offz = static_cast<float>(a.pos[2] - (grid.origin[2] + grid.spacing * lo[2]));
+        const double h = -0.5 * kLog2eD;
+        r.Q00 = static_cast<float>(h * GM3(A, 0, 0));
+        r.Q11 = static_cast<float>(h * GM3(A, 1, 1));
+        r.Q22 = static_cast<float>(h * GM3(A, 2, 2));
+        r.Q01 = static_cast<float>(2.0 * h * GM3(A, 0, 1));
+        r.Q02 = static_cast<float>(2.0 * h * GM3(A, 0, 2));
+        r.Q12 = static_cast<float>(2.0 * h * GM3(A, 1, 2));
+        cnt = 1;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          cnt *= static_cast<uint32_t>((whi[k] - win.lo[k]) / kBrick - (wlo[k] - win.lo[k]) / kBrick + 1);
+        n_pp = static_cast<unsigned long long>(whi[0] - wlo[0] + 1) *
+               static_cast<unsigned long long>(whi[1] - wlo[1] + 1) *
+               static_cast<unsigned long long>(whi[2] - wlo[2] + 1);
+      } else {
+        n_culled = 1;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = wlo[k];
+        hi[k] = whi[k];
+      }
+    }
+    if (rec) rec[i] = r;
+    if (brick_count) brick_count[i] = cnt;
+    if (lo_out) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        lo_out[3 * i + k] = vis ? lo[k] : 0;
+        hi_out[3 * i + k] = vis ? hi[k] : -1;
+      }
+      skip_out[i] = vis ? 0 : 1;
+    }
+  }
+  warp_add(&st->culled, n_culled);
+  warp_add(&st->pixel_pairs, n_pp);
+}
+
+// K8b: one thread per splat: from the fp32 voxel-loop moments (summed over all windows)
+// to dL/d(raw parameters) in fp64, voxelizer.hpp:250-255 + covariance_backward.
+__global__ void __launch_bounds__(128) k_voxel_tail(Cloud c, VoxGrid grid, double tau_cut,
+                                                    double sigma_cap, const float* __restrict__ m,
+                                                    double* __restrict__ g_pos,
+                                                    double* __restrict__ g_ls, double* __restrict__ g_q,
+                                                    double* __restrict__ g_raw,
+                                                    double* __restrict__ g_pgn,
+                                                    uint8_t* __restrict__ visible, DevStats* st) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= c.n) return;
+  const int64_t n = c.n;
+  double gp[3] = {0, 0, 0}, gl[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gr = 0.0, pgn = 0.0;
+  uint8_t vis = 0;
+  Act a;
+  const int err = activate(c.pos, c.ls, c.q, c.raw, i, a);
+  if (err) {
+    flag_error(st, i, err);
+  } else {
+    double sigma[9], A[9];
+    int lo[3], hi[3];
+    covariance(a.scales, a.uq, sigma);
+    if (prepare_voxel_splat(a, sigma, grid, tau_cut, sigma_cap, A, lo, hi)) {
+      vis = 1;
+      const double M0 = m[0 * n + i];
+      const double M1[3] = {m[1 * n + i], m[2 * n + i], m[3 * n + i]};
+      // second moments: xx, yy, zz, xy, xz, yz
+      const double sxx = m[4 * n + i], syy = m[5 * n + i], szz = m[6 * n + i];
+      const double sxy = m[7 * n + i], sxz = m[8 * n + i], syz = m[9 * n + i];
+      const double rho = a.density;
+      double am1[3];
+      mul3v(A, M1, am1);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) gp[k] = rho * am1[k];
+      const double hr = -0.5 * rho;
+      const double gA[9] = {hr * sxx, hr * sxy, hr * sxz, hr * sxy, hr * syy,
+                            hr * syz, hr * sxz, hr * syz, hr * szz};
+      double negA[9], t[9], gsig[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) negA[k] = -A[k];
+      mul33(negA, gA, t);
+      mul33(t, A, gsig);
+      gr = a.raw_density >= 0.0 ? M0 : 0.0;
+      pgn = sqrt(dot3(gp, gp));
+      covariance_backward(a.scales, a.uq, a.raw_q, gsig, gl, gq);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g_pos[3 * i + k] = gp[k];
+    g_ls[3 * i + k] = gl[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) g_q[4 * i + k] = gq[k];
+  g_raw[i] = gr;
+  g_pgn[i] = pgn;
+  visible[i] = vis;
+}
+
+inline unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
+
+}  // namespace
+
+void launch_raster_preprocess(const Cloud& c, const Frame* frames_dev, int n_views, const Geo& g,
+                              const RSet& rs, int bin_ts, RasterRec* rec, uint32_t* tile_count,
+                              DevStats* stats, cudaStream_t st) {
+  if (c.n == 0 || n_views == 0) return;
+  dim3 grid(blocks_for(c.n, 256), static_cast<unsigned>(n_views));
+  k_raster_preprocess<<<grid, 256, 0, st>>>(c, frames_dev, g, rs, bin_ts, rec, tile_count, stats);
+  count_launch();
+}
+
+void launch_raster_tail(const Cloud& c, const Frame* frames_dev, int n_views, const Geo& g,
+                        const RSet& rs, const float* moments, bool first_chunk, double* g_pos,
+                        double* g_ls, double* g_q, double* g_raw, double* g_pgn,
+                        uint8_t* visible, cudaStream_t st) {
+  if (c.n == 0) return;
+  k_raster_tail<<<blocks_for(c.n, 128), 128, 0, st>>>(
+      c, frames_dev, n_views, g, rs, reinterpret_cast<const float4*>(moments), first_chunk ? 1 : 0,
+      g_pos, g_ls, g_q, g_raw, g_pgn, visible);
+  count_launch();
+}
+
+void launch_debug_project(const Cloud& c, const Frame* frame_dev, const Geo& g, const RSet& rs,
+                          int32_t* rect, uint8_t* flags, double* mean2d, double* conic,
+                          double* amplitude, DevStats* stats, cudaStream_t st) {
+  if (c.n == 0) return;
+  k_debug_project<<<blocks_for(c.n, 128), 128, 0, st>>>(c, frame_dev, g, rs, rect, flags, mean2d,
+                                                        conic, amplitude, stats);
+  count_launch();
+}
+
+void launch_voxel_preprocess(const Cloud& c, const VoxGrid& grid, const Window& win,
+                             double tau_cut, double sigma_cap, VoxelRec* rec,
+                             uint32_t* brick_count, int32_t* lo_out, int32_t* hi_out,
+                             uint8_t* skip_out, DevStats* stats, cudaStream_t st) {
+  if (c.n == 0) return;
+  k_voxel_preprocess<<<blocks_for(c.n, 256), 256, 0, st>>>(c, grid, win, tau_cut, sigma_cap, rec,
+                                                           brick_count, lo_out, hi_out, skip_out,
+                                                           stats);
+  count_launch();
+}
+
+void launch_voxel_tail(const Cloud& c, const VoxGrid& grid, double tau_cut, double sigma_cap,
+                       const float* moments, double* g_pos, double* g_ls, double* g_q,
+                       double* g_raw, double* g_pgn, uint8_t* visible, DevStats* stats,
+                       cudaStream_t st) {
+  if (c.n == 0) return;
+  k_voxel_tail<<<blocks_for(c.n, 128), 128, 0, st>>>(c, grid, tau_cut, sigma_cap, moments, g_pos,
+                                                     g_ls, g_q, g_raw, g_pgn, visible, stats);
+  count_launch();
+}
+
+}  // namespace gsct_dev

@@ -1,0 +1,819 @@
+"""Python host mirror of the reference `gsct` operator API, over the C ABI of
+libgsct_b200.so (include/gsct_cuda.h) via ctypes.
+
+Names, argument meaning and error behaviour follow the reference C++ library
+(/root/reference/proj/include/gsct/): `rasterize_view` (projector.hpp:308),
+`rasterize_backward` (projector.hpp:371), `voxelize` (voxelizer.hpp:162),
+`voxelize_full` (voxelizer.hpp:203), `voxelize_backward` (voxelizer.hpp:214), plus the
+helpers `view_frame`, `project_cloud`, `bin_tiles`, `sample_subvolume`,
+`default_geometry` and the seeded `Rng`. Invalid input raises `ContractError`
+(gsct::contract_error). Batched forms (`rasterize_views`, `rasterize_backward_views`)
+process many views per call; gradients are summed over views in ascending order, exactly
+`ParamGradients::add` (core.hpp:152-162).
+
+Arrays may be numpy (host; copied in/out inside the call) or torch CUDA tensors
+(device-resident; used in place). There is no CPU fallback: without the CUDA library or
+a GPU every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Optional, Sequence
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "libgsct_b200.so"
+
+GSCT_OK, GSCT_ERR_CONTRACT, GSCT_ERR_CUDA, GSCT_ERR_OOM = 0, 1, 2, 3
+GSCT_HOST, GSCT_DEVICE = 0, 1
+
+
+class GsctError(RuntimeError):
+    """Base error (gsct::error)."""
+
+
+class ContractError(GsctError):
+    """Violated precondition (gsct::contract_error, common.hpp:15-17)."""
+
+
+class CudaError(GsctError):
+    pass
+
+
+class OutOfMemoryError(CudaError):
+    pass
+
+
+# ---------------------------------------------------------------------------------------
+# C structs (include/gsct_cuda.h)
+# ---------------------------------------------------------------------------------------
+class c_geometry(C.Structure):
+    _fields_ = [("cone", C.c_int), ("n_u", C.c_int), ("n_v", C.c_int), ("s_u", C.c_double),
+                ("s_v", C.c_double), ("source_to_origin", C.c_double), ("origin_to_detector", C.c_double)]
+
+
+class c_raster_settings(C.Structure):
+    _fields_ = [("tau_cut", C.c_double), ("sigma_cap", C.c_double), ("dilation_px2", C.c_double),
+                ("tile_size", C.c_int), ("dilate", C.c_int), ("bounding", C.c_int)]
+
+
+class c_voxel_settings(C.Structure):
+    _fields_ = [("tau_cut", C.c_double), ("sigma_cap", C.c_double)]
+
+
+class c_grid(C.Structure):
+    _fields_ = [("dims", C.c_int * 3), ("spacing", C.c_double), ("origin", C.c_double * 3)]
+
+
+class c_window(C.Structure):
+    _fields_ = [("lo", C.c_int * 3), ("hi", C.c_int * 3)]
+
+
+class c_stats(C.Structure):
+    _fields_ = [("culled", C.c_int64), ("degenerate", C.c_int64), ("tile_pairs", C.c_int64),
+                ("pixel_pairs", C.c_int64), ("forward_ms", C.c_double), ("backward_ms", C.c_double)]
+
+
+class c_cloud(C.Structure):
+    _fields_ = [("n", C.c_int64), ("pos", C.c_void_p), ("log_scale", C.c_void_p), ("quat", C.c_void_p),
+                ("raw_density", C.c_void_p), ("location", C.c_int)]
+
+
+class c_grads(C.Structure):
+    _fields_ = [("pos", C.c_void_p), ("log_scale", C.c_void_p), ("quat", C.c_void_p),
+                ("raw_density", C.c_void_p), ("pos_grad_norm", C.c_void_p), ("visible", C.c_void_p),
+                ("location", C.c_int)]
+
+
+_P = C.POINTER
+_SIGS = {
+    "gsct_abi_version": (C.c_int, []),
+    "gsct_ctx_create": (C.c_int, [C.c_int, _P(C.c_void_p)]),
+    "gsct_ctx_destroy": (None, [C.c_void_p]),
+    "gsct_ctx_last_error": (C.c_char_p, [C.c_void_p]),
+    "gsct_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gsct_ctx_stream": (C.c_void_p, [C.c_void_p]),
+    "gsct_ctx_set_async": (C.c_int, [C.c_void_p, C.c_int]),
+    "gsct_ctx_synchronize": (C.c_int, [C.c_void_p, _P(c_stats)]),
+    "gsct_ctx_workspace_bytes": (C.c_size_t, [C.c_void_p]),
+    "gsct_ctx_launch_count": (C.c_int64, [C.c_void_p]),
+    "gsct_rasterize_fwd": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), _P(C.c_double), C.c_int,
+                                     _P(c_raster_settings), C.c_void_p, C.c_int, _P(c_stats)]),
+    "gsct_rasterize_bwd": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), _P(C.c_double), C.c_int,
+                                     _P(c_raster_settings), C.c_void_p, C.c_int, _P(c_grads), _P(c_stats)]),
+    "gsct_voxelize_fwd": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_grid), _P(c_window), _P(c_voxel_settings),
+                                    C.c_void_p, C.c_int, _P(c_stats)]),
+    "gsct_voxelize_bwd": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_grid), _P(c_window), _P(c_voxel_settings),
+                                    C.c_void_p, C.c_int, _P(c_grads), _P(c_stats)]),
+    "gsct_voxelize_bwd_moments": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_grid), _P(c_window),
+                                            _P(c_voxel_settings), C.c_void_p, C.c_int, C.c_void_p]),
+    "gsct_voxelize_bwd_finish": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_grid), _P(c_voxel_settings),
+                                           C.c_void_p, _P(c_grads)]),
+    "gsct_debug_project": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), C.c_double, _P(c_raster_settings),
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gsct_debug_tile_pairs": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), _P(C.c_double), C.c_int,
+                                        _P(c_raster_settings), C.c_void_p, C.c_void_p, C.c_int64,
+                                        _P(C.c_int64)]),
+    "gsct_debug_voxel_boxes": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_grid), _P(c_window),
+                                         _P(c_voxel_settings), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gsct_host_view_frame": (None, [_P(c_geometry), C.c_double, _P(C.c_double)]),
+    "gsct_host_default_geometry": (None, [_P(C.c_int), C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          _P(c_geometry), _P(C.c_double)]),
+    "gsct_host_rng_create": (C.c_void_p, [C.c_uint64]),
+    "gsct_host_rng_destroy": (None, [C.c_void_p]),
+    "gsct_host_rng_uniform": (C.c_double, [C.c_void_p, C.c_double, C.c_double]),
+    "gsct_host_rng_normal": (C.c_double, [C.c_void_p]),
+    "gsct_host_rng_uniform_int": (C.c_int64, [C.c_void_p, C.c_int64]),
+    "gsct_host_sample_subvolume": (C.c_int, [_P(C.c_int), _P(C.c_int), C.c_void_p, _P(C.c_int), _P(C.c_int)]),
+    "gsct_host_make_cloud": (C.c_int, [C.c_int, C.c_int64, C.c_uint64, _P(C.c_double), C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p]),
+}
+
+_lib: Optional[C.CDLL] = None
+
+
+def lib() -> C.CDLL:
+    """Loads libgsct_b200.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise ImportError(f"{_LIB_PATH} is missing: run `python -m paper_2604_01844_b200.build_native` "
+                              "(there is no CPU fallback)")
+        l = C.CDLL(str(_LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(l, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGS)
+
+
+# ---------------------------------------------------------------------------------------
+# Reference-mirroring value types
+# ---------------------------------------------------------------------------------------
+@dataclass
+class ScanGeometry:
+    """gsct::ScanGeometry (core.hpp:203-222)."""
+    mode: str = "parallel"  # "parallel" | "cone"
+    n_u: int = 0
+    n_v: int = 0
+    s_u: float = 1.0
+    s_v: float = 1.0
+    angles: Sequence[float] = field(default_factory=list)
+    source_to_origin: float = 0.0
+    origin_to_detector: float = 0.0
+
+    def n_views(self) -> int:
+        return len(self.angles)
+
+    def c(self) -> c_geometry:
+        if self.mode not in ("parallel", "cone"):
+            raise ContractError(f"ScanGeometry: unknown mode {self.mode!r}")
+        return c_geometry(1 if self.mode == "cone" else 0, int(self.n_u), int(self.n_v), float(self.s_u),
+                          float(self.s_v), float(self.source_to_origin), float(self.origin_to_detector))
+
+
+@dataclass
+class RasterSettings:
+    """gsct::RasterSettings (projector.hpp:64-71)."""
+    tau_cut: float = 1e-4
+    sigma_cap: float = 3.0
+    tile_size: int = 16
+    dilate: bool = True
+    dilation_px2: float = 0.3
+    bounding: str = "rect_density_aware"  # | "square_circumscribed"
+
+    def c(self) -> c_raster_settings:
+        return c_raster_settings(float(self.tau_cut), float(self.sigma_cap), float(self.dilation_px2),
+                                 int(self.tile_size), 1 if self.dilate else 0,
+                                 1 if self.bounding == "square_circumscribed" else 0)
+
+
+@dataclass
+class VoxelSettings:
+    """gsct::VoxelSettings (voxelizer.hpp:99-102)."""
+    tau_cut: float = 1e-4
+    sigma_cap: float = 3.0
+
+    def c(self) -> c_voxel_settings:
+        return c_voxel_settings(float(self.tau_cut), float(self.sigma_cap))
+
+
+@dataclass
+class RenderStats:
+    """gsct::RenderStats (projector.hpp:73-80), accumulated with +=."""
+    culled: int = 0
+    degenerate: int = 0
+    tile_pairs: int = 0
+    pixel_pairs: int = 0
+    forward_ms: float = 0.0
+    backward_ms: float = 0.0
+
+    def _c(self) -> c_stats:
+        return c_stats(self.culled, self.degenerate, self.tile_pairs, self.pixel_pairs, self.forward_ms,
+                       self.backward_ms)
+
+    def _take(self, s: c_stats) -> None:
+        self.culled, self.degenerate = s.culled, s.degenerate
+        self.tile_pairs, self.pixel_pairs = s.tile_pairs, s.pixel_pairs
+        self.forward_ms, self.backward_ms = s.forward_ms, s.backward_ms
+
+
+@dataclass
+class GridSpec:
+    """gsct::GridSpec (voxelizer.hpp:22-41)."""
+    dims: tuple = (0, 0, 0)
+    spacing: float = 1.0
+    origin: tuple = (0.0, 0.0, 0.0)
+
+    @staticmethod
+    def centered(dims, spacing: float) -> "GridSpec":
+        return GridSpec(tuple(int(d) for d in dims), float(spacing),
+                        tuple(-0.5 * spacing * (d - 1) for d in dims))
+
+    def count(self) -> int:
+        return int(self.dims[0]) * int(self.dims[1]) * int(self.dims[2])
+
+
+@dataclass
+class GridRegion:
+    """gsct::GridRegion (voxelizer.hpp:43-71)."""
+    offset: tuple = (0, 0, 0)
+    dims: tuple = (0, 0, 0)
+    spacing: float = 1.0
+    origin: tuple = (0.0, 0.0, 0.0)
+
+    @staticmethod
+    def covering(parent: GridSpec) -> "GridRegion":
+        return GridRegion((0, 0, 0), tuple(parent.dims), parent.spacing, tuple(parent.origin))
+
+    @staticmethod
+    def of_parent(parent: GridSpec, offset, dims) -> "GridRegion":
+        for a in range(3):
+            if not dims[a] >= 1:
+                raise ContractError("GridRegion: dims must be at least 1")
+            if not (offset[a] >= 0 and offset[a] + dims[a] <= parent.dims[a]):
+                raise ContractError("GridRegion: region outside parent grid")
+        origin = tuple(parent.origin[a] + parent.spacing * float(offset[a]) for a in range(3))
+        return GridRegion(tuple(int(o) for o in offset), tuple(int(d) for d in dims), parent.spacing, origin)
+
+    def count(self) -> int:
+        return int(self.dims[0]) * int(self.dims[1]) * int(self.dims[2])
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+class GaussianCloud:
+    """gsct::GaussianCloud (core.hpp:30-59): raw parameters, AoS doubles.
+
+    Holds numpy float64 arrays (host) or torch float64 CUDA tensors (device-resident).
+    """
+
+    def __init__(self, positions, log_scales, rotations, raw_densities):
+        self.positions = positions
+        self.log_scales = log_scales
+        self.rotations = rotations
+        self.raw_densities = raw_densities
+        self.validate()
+
+    @staticmethod
+    def empty() -> "GaussianCloud":
+        return GaussianCloud(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0,)))
+
+    def size(self) -> int:
+        return int(self.positions.shape[0])
+
+    def __len__(self) -> int:
+        return self.size()
+
+    def validate(self) -> None:
+        n = self.positions.shape[0]
+        if not (self.log_scales.shape[0] == n and self.rotations.shape[0] == n and self.raw_densities.shape[0] == n):
+            raise ContractError("GaussianCloud: parameter arrays out of lockstep")
+
+    @property
+    def on_device(self) -> bool:
+        return _is_torch(self.positions) and self.positions.is_cuda
+
+    def to_device(self, device: int = 0) -> "GaussianCloud":
+        import torch
+        f = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(f"cuda:{device}")
+        return GaussianCloud(f(self.positions), f(self.log_scales), f(self.rotations), f(self.raw_densities))
+
+    def numpy(self) -> "GaussianCloud":
+        if not _is_torch(self.positions):
+            return self
+        f = lambda a: a.detach().cpu().numpy()
+        return GaussianCloud(f(self.positions), f(self.log_scales), f(self.rotations), f(self.raw_densities))
+
+    def _c(self, keep: list) -> c_cloud:
+        self.validate()
+        n = self.size()
+        if self.on_device:
+            arrs = [self.positions, self.log_scales, self.rotations, self.raw_densities]
+            for a in arrs:
+                if a.dtype != __import__("torch").float64 or not a.is_contiguous():
+                    raise ContractError("GaussianCloud: device arrays must be contiguous float64")
+            keep.extend(arrs)
+            return c_cloud(n, arrs[0].data_ptr(), arrs[1].data_ptr(), arrs[2].data_ptr(), arrs[3].data_ptr(),
+                           GSCT_DEVICE)
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (self.positions, self.log_scales, self.rotations, self.raw_densities)]
+        keep.extend(arrs)
+        ptr = lambda a: a.ctypes.data if a.size else None
+        return c_cloud(n, ptr(arrs[0]), ptr(arrs[1]), ptr(arrs[2]), ptr(arrs[3]), GSCT_HOST)
+
+
+@dataclass
+class ParamGradients:
+    """gsct::ParamGradients (core.hpp:135-163)."""
+    positions: object
+    log_scales: object
+    rotations: object
+    raw_densities: object
+    pos_grad_norm: object
+    visible: object
+
+    @staticmethod
+    def zeros(n: int, device: Optional[int] = None) -> "ParamGradients":
+        if device is None:
+            z = lambda *s: np.zeros(s, dtype=np.float64)
+            return ParamGradients(z(n, 3), z(n, 3), z(n, 4), z(n), z(n), np.zeros(n, dtype=np.uint8))
+        import torch
+        z = lambda *s: torch.zeros(s, dtype=torch.float64, device=f"cuda:{device}")
+        return ParamGradients(z(n, 3), z(n, 3), z(n, 4), z(n), z(n),
+                              torch.zeros(n, dtype=torch.uint8, device=f"cuda:{device}"))
+
+    def add(self, other: "ParamGradients") -> None:
+        """ParamGradients::add (core.hpp:152-162)."""
+        if other.positions.shape[0] != self.positions.shape[0]:
+            raise ContractError("ParamGradients::add: size mismatch")
+        self.positions = self.positions + other.positions
+        self.log_scales = self.log_scales + other.log_scales
+        self.rotations = self.rotations + other.rotations
+        self.raw_densities = self.raw_densities + other.raw_densities
+        self.pos_grad_norm = self.pos_grad_norm + other.pos_grad_norm
+        self.visible = self.visible | other.visible
+
+    def _c(self) -> c_grads:
+        arrs = [self.positions, self.log_scales, self.rotations, self.raw_densities, self.pos_grad_norm, self.visible]
+        if _is_torch(self.positions):
+            return c_grads(*[a.data_ptr() for a in arrs], GSCT_DEVICE)
+        return c_grads(*[a.ctypes.data if a.size else None for a in arrs], GSCT_HOST)
+
+
+# ---------------------------------------------------------------------------------------
+# Context (one per CUDA device)
+# ---------------------------------------------------------------------------------------
+class Context:
+    """Owns a gsct_ctx: stream, grow-only device workspace, last error."""
+
+    def __init__(self, device: int = 0):
+        self._lib = lib()
+        h = C.c_void_p()
+        st = self._lib.gsct_ctx_create(int(device), C.byref(h))
+        if st != GSCT_OK:
+            raise CudaError(f"gsct_ctx_create(device={device}) failed: no usable CUDA device "
+                            "(libgsct_b200 has no CPU fallback)")
+        self.handle = h
+        self.device = int(device)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.gsct_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, status: int) -> None:
+        if status == GSCT_OK:
+            return
+        msg = self._lib.gsct_ctx_last_error(self.handle).decode(errors="replace")
+        if status == GSCT_ERR_CONTRACT:
+            raise ContractError(msg)
+        if status == GSCT_ERR_OOM:
+            raise OutOfMemoryError(msg)
+        raise CudaError(msg)
+
+    def set_stream(self, stream_ptr: int) -> None:
+        self.check(self._lib.gsct_ctx_set_stream(self.handle, C.c_void_p(stream_ptr)))
+
+    def set_async(self, on: bool) -> None:
+        self.check(self._lib.gsct_ctx_set_async(self.handle, 1 if on else 0))
+
+    def synchronize(self, stats: Optional[RenderStats] = None) -> None:
+        s = stats._c() if stats is not None else c_stats()
+        self.check(self._lib.gsct_ctx_synchronize(self.handle, C.byref(s)))
+        if stats is not None:
+            stats._take(s)
+
+    def launch_count(self) -> int:
+        return int(self._lib.gsct_ctx_launch_count(self.handle))
+
+    def workspace_bytes(self) -> int:
+        return int(self._lib.gsct_ctx_workspace_bytes(self.handle))
+
+
+_contexts: dict[int, Context] = {}
+
+
+def context(device: int = 0) -> Context:
+    if device not in _contexts:
+        _contexts[device] = Context(device)
+    return _contexts[device]
+
+
+def _ptr(x, keep: list):
+    """(pointer, location) for a numpy array or torch CUDA tensor."""
+    if _is_torch(x):
+        if not x.is_cuda:
+            x = x.contiguous()
+            keep.append(x)
+            return x.data_ptr(), GSCT_HOST
+        if not x.is_contiguous():
+            raise ContractError("device buffers must be contiguous")
+        keep.append(x)
+        return x.data_ptr(), GSCT_DEVICE
+    keep.append(x)
+    return x.ctypes.data, GSCT_HOST
+
+
+def _ctx_for(cloud: GaussianCloud, ctx: Optional[Context]) -> Context:
+    if ctx is not None:
+        return ctx
+    dev = cloud.positions.device.index if cloud.on_device else 0
+    return context(dev or 0)
+
+
+def _angles(geometry: ScanGeometry, view_indices) -> np.ndarray:
+    angles = np.asarray(geometry.angles, dtype=np.float64)
+    if view_indices is None:
+        return np.ascontiguousarray(angles)
+    idx = np.asarray(view_indices, dtype=np.int64).reshape(-1)
+    if idx.size and (idx.min() < 0 or idx.max() >= angles.size):
+        raise ContractError("view_frame: angle index out of range")
+    return np.ascontiguousarray(angles[idx])
+
+
+# ---------------------------------------------------------------------------------------
+# Rasterizer (projector.hpp)
+# ---------------------------------------------------------------------------------------
+def rasterize_views(cloud: GaussianCloud, geometry: ScanGeometry, view_indices=None,
+                    settings: RasterSettings = RasterSettings(), stats: Optional[RenderStats] = None,
+                    out=None, ctx: Optional[Context] = None):
+    """Forward projection of several views: images [V, n_v, n_u] float32 (u fastest)."""
+    ctx = _ctx_for(cloud, ctx)
+    ang = _angles(geometry, view_indices)
+    keep: list = []
+    cc = cloud._c(keep)
+    if out is None:
+        if cloud.on_device:
+            import torch
+            out = torch.empty((ang.size, geometry.n_v, geometry.n_u), dtype=torch.float32,
+                              device=cloud.positions.device)
+        else:
+            out = np.empty((ang.size, geometry.n_v, geometry.n_u), dtype=np.float32)
+    optr, oloc = _ptr(out, keep)
+    s = stats._c() if stats is not None else c_stats()
+    g = geometry.c()
+    rs = settings.c()
+    ctx.check(ctx._lib.gsct_rasterize_fwd(ctx.handle, C.byref(cc), C.byref(g),
+                                          ang.ctypes.data_as(_P(C.c_double)), int(ang.size), C.byref(rs),
+                                          C.c_void_p(optr), oloc, C.byref(s) if stats is not None else None))
+    if stats is not None:
+        stats._take(s)
+    return out
+
+
+def rasterize_view(cloud: GaussianCloud, geometry: ScanGeometry, angle_index: int,
+                   settings: RasterSettings = RasterSettings(), stats: Optional[RenderStats] = None,
+                   ctx: Optional[Context] = None):
+    """gsct::rasterize_view: one view, image [n_v, n_u] float32."""
+    return rasterize_views(cloud, geometry, [angle_index], settings, stats, ctx=ctx)[0]
+
+
+def rasterize_backward_views(cloud: GaussianCloud, geometry: ScanGeometry, view_indices, grad_images,
+                             settings: RasterSettings = RasterSettings(), stats: Optional[RenderStats] = None,
+                             out: Optional[ParamGradients] = None, ctx: Optional[Context] = None) -> ParamGradients:
+    """Sum over views (ascending) of rasterize_backward; grad_images [V, n_v, n_u] float32."""
+    ctx = _ctx_for(cloud, ctx)
+    ang = _angles(geometry, view_indices)
+    shape = tuple(grad_images.shape)
+    if shape != (ang.size, geometry.n_v, geometry.n_u):
+        raise ContractError("rasterize_backward: grad image dims must match detector")
+    keep: list = []
+    cc = cloud._c(keep)
+    if _is_torch(grad_images):
+        import torch
+        if grad_images.dtype != torch.float32:
+            grad_images = grad_images.float()
+    else:
+        grad_images = np.ascontiguousarray(grad_images, dtype=np.float32)
+    gptr, gloc = _ptr(grad_images, keep)
+    if out is None:
+        out = ParamGradients.zeros(cloud.size(), cloud.positions.device.index if cloud.on_device else None)
+    cg = out._c()
+    s = stats._c() if stats is not None else c_stats()
+    g = geometry.c()
+    rs = settings.c()
+    ctx.check(ctx._lib.gsct_rasterize_bwd(ctx.handle, C.byref(cc), C.byref(g), ang.ctypes.data_as(_P(C.c_double)),
+                                          int(ang.size), C.byref(rs), C.c_void_p(gptr), gloc, C.byref(cg),
+                                          C.byref(s) if stats is not None else None))
+    if stats is not None:
+        stats._take(s)
+    return out
+
+
+def rasterize_backward(cloud: GaussianCloud, geometry: ScanGeometry, angle_index: int, grad_image,
+                       settings: RasterSettings = RasterSettings(), stats: Optional[RenderStats] = None,
+                       ctx: Optional[Context] = None) -> ParamGradients:
+    """gsct::rasterize_backward for one view."""
+    if tuple(grad_image.shape) != (geometry.n_v, geometry.n_u):
+        raise ContractError("rasterize_backward: grad image dims must match detector")
+    return rasterize_backward_views(cloud, geometry, [angle_index], grad_image[None], settings, stats, ctx=ctx)
+
+
+# ---------------------------------------------------------------------------------------
+# Voxelizer (voxelizer.hpp)
+# ---------------------------------------------------------------------------------------
+def _grid_c(region) -> c_grid:
+    return c_grid((C.c_int * 3)(*[int(d) for d in region.dims]), float(region.spacing),
+                  (C.c_double * 3)(*[float(o) for o in region.origin]))
+
+
+def _window_c(window) -> Optional[c_window]:
+    if window is None:
+        return None
+    lo, hi = window
+    return c_window((C.c_int * 3)(*[int(v) for v in lo]), (C.c_int * 3)(*[int(v) for v in hi]))
+
+
+def voxelize(cloud: GaussianCloud, region, settings: VoxelSettings = VoxelSettings(),
+             stats: Optional[RenderStats] = None, window=None, out=None, ctx: Optional[Context] = None):
+    """gsct::voxelize: volume [nz, ny, nx] float32 (x fastest). `window` = ((x0,y0,z0),(x1,y1,z1))
+    restricts the output to a sub-box of the region (z-slab sharding) without changing values."""
+    ctx = _ctx_for(cloud, ctx)
+    keep: list = []
+    cc = cloud._c(keep)
+    gr = _grid_c(region)
+    win = _window_c(window)
+    lo, hi = window if window is not None else ((0, 0, 0), tuple(region.dims))
+    shape = (hi[2] - lo[2], hi[1] - lo[1], hi[0] - lo[0])
+    if out is None:
+        if cloud.on_device:
+            import torch
+            out = torch.empty(shape, dtype=torch.float32, device=cloud.positions.device)
+        else:
+            out = np.empty(shape, dtype=np.float32)
+    optr, oloc = _ptr(out, keep)
+    s = stats._c() if stats is not None else c_stats()
+    vs = settings.c()
+    ctx.check(ctx._lib.gsct_voxelize_fwd(ctx.handle, C.byref(cc), C.byref(gr), C.byref(win) if win else None,
+                                         C.byref(vs), C.c_void_p(optr), oloc,
+                                         C.byref(s) if stats is not None else None))
+    if stats is not None:
+        stats._take(s)
+    return out
+
+
+def voxelize_full(cloud: GaussianCloud, grid: GridSpec, settings: VoxelSettings = VoxelSettings(),
+                  stats: Optional[RenderStats] = None, ctx: Optional[Context] = None):
+    """gsct::voxelize_full (voxelizer.hpp:203-206)."""
+    return voxelize(cloud, GridRegion.covering(grid), settings, stats, ctx=ctx)
+
+
+def voxelize_backward(cloud: GaussianCloud, region, grad_volume, settings: VoxelSettings = VoxelSettings(),
+                      stats: Optional[RenderStats] = None, out: Optional[ParamGradients] = None,
+                      ctx: Optional[Context] = None) -> ParamGradients:
+    """gsct::voxelize_backward; grad_volume [nz, ny, nx] float32."""
+    if tuple(grad_volume.shape) != (region.dims[2], region.dims[1], region.dims[0]):
+        raise ContractError("voxelize_backward: grad dims must match region")
+    ctx = _ctx_for(cloud, ctx)
+    keep: list = []
+    cc = cloud._c(keep)
+    if _is_torch(grad_volume):
+        grad_volume = grad_volume.float().contiguous()
+    else:
+        grad_volume = np.ascontiguousarray(grad_volume, dtype=np.float32)
+    gptr, gloc = _ptr(grad_volume, keep)
+    if out is None:
+        out = ParamGradients.zeros(cloud.size(), cloud.positions.device.index if cloud.on_device else None)
+    cg = out._c()
+    s = stats._c() if stats is not None else c_stats()
+    gr = _grid_c(region)
+    vs = settings.c()
+    ctx.check(ctx._lib.gsct_voxelize_bwd(ctx.handle, C.byref(cc), C.byref(gr), None, C.byref(vs), C.c_void_p(gptr),
+                                         gloc, C.byref(cg), C.byref(s) if stats is not None else None))
+    if stats is not None:
+        stats._take(s)
+    return out
+
+
+def voxelize_backward_moments(cloud: GaussianCloud, region, grad_window, window, moments,
+                              settings: VoxelSettings = VoxelSettings(), ctx: Optional[Context] = None):
+    """Per-splat partial sums over one window (z-slab) into device moments [10, N] float32."""
+    ctx = _ctx_for(cloud, ctx)
+    keep: list = []
+    cc = cloud._c(keep)
+    gptr, gloc = _ptr(grad_window, keep)
+    mptr, mloc = _ptr(moments, keep)
+    if mloc != GSCT_DEVICE:
+        raise ContractError("voxelize_backward_moments: moments must be a CUDA tensor")
+    gr = _grid_c(region)
+    win = _window_c(window)
+    vs = settings.c()
+    ctx.check(ctx._lib.gsct_voxelize_bwd_moments(ctx.handle, C.byref(cc), C.byref(gr), C.byref(win) if win else None,
+                                                 C.byref(vs), C.c_void_p(gptr), gloc, C.c_void_p(mptr)))
+    return moments
+
+
+def voxelize_backward_finish(cloud: GaussianCloud, region, moments, settings: VoxelSettings = VoxelSettings(),
+                             out: Optional[ParamGradients] = None, ctx: Optional[Context] = None) -> ParamGradients:
+    ctx = _ctx_for(cloud, ctx)
+    keep: list = []
+    cc = cloud._c(keep)
+    mptr, _ = _ptr(moments, keep)
+    if out is None:
+        out = ParamGradients.zeros(cloud.size(), cloud.positions.device.index if cloud.on_device else None)
+    cg = out._c()
+    gr = _grid_c(region)
+    vs = settings.c()
+    ctx.check(ctx._lib.gsct_voxelize_bwd_finish(ctx.handle, C.byref(cc), C.byref(gr), C.byref(vs), C.c_void_p(mptr),
+                                                C.byref(cg)))
+    return out
+
+
+# ---------------------------------------------------------------------------------------
+# Parity hooks and helpers
+# ---------------------------------------------------------------------------------------
+def project_cloud(cloud: GaussianCloud, geometry: ScanGeometry, angle_index: int,
+                  settings: RasterSettings = RasterSettings(), ctx: Optional[Context] = None) -> dict:
+    """gsct::project_cloud on the device: per-splat rect [N,4], culled, degenerate, mean2d, conic, amplitude."""
+    ctx = _ctx_for(cloud, ctx)
+    keep: list = []
+    cc = cloud._c(keep)
+    n = cloud.size()
+    rect = np.zeros((n, 4), dtype=np.int32)
+    flags = np.zeros(n, dtype=np.uint8)
+    mean2d = np.zeros((n, 2))
+    conic = np.zeros((n, 4))
+    amp = np.zeros(n)
+    theta = float(_angles(geometry, [angle_index])[0])
+    g = geometry.c()
+    rs = settings.c()
+    ctx.check(ctx._lib.gsct_debug_project(ctx.handle, C.byref(cc), C.byref(g), theta, C.byref(rs),
+                                          rect.ctypes.data, flags.ctypes.data, mean2d.ctypes.data,
+                                          conic.ctypes.data, amp.ctypes.data))
+    return dict(rect=rect, culled=(flags & 1).astype(bool), degenerate=(flags & 2).astype(bool), mean2d=mean2d,
+                conic=conic, amplitude=amp)
+
+
+def tile_pairs(cloud: GaussianCloud, geometry: ScanGeometry, view_indices=None,
+               settings: RasterSettings = RasterSettings(), ctx: Optional[Context] = None):
+    """Sorted (key, splat) pairs of the device binning (key = view*n_tiles + tile)."""
+    ctx = _ctx_for(cloud, ctx)
+    ang = _angles(geometry, view_indices)
+    keep: list = []
+    cc = cloud._c(keep)
+    g = geometry.c()
+    rs = settings.c()
+    n_pairs = C.c_int64(0)
+    ctx.check(ctx._lib.gsct_debug_tile_pairs(ctx.handle, C.byref(cc), C.byref(g), ang.ctypes.data_as(_P(C.c_double)),
+                                             int(ang.size), C.byref(rs), None, None, 0, C.byref(n_pairs)))
+    keys = np.zeros(max(n_pairs.value, 1), dtype=np.uint32)
+    vals = np.zeros(max(n_pairs.value, 1), dtype=np.uint32)
+    ctx.check(ctx._lib.gsct_debug_tile_pairs(ctx.handle, C.byref(cc), C.byref(g), ang.ctypes.data_as(_P(C.c_double)),
+                                             int(ang.size), C.byref(rs), keys.ctypes.data, vals.ctypes.data,
+                                             n_pairs.value, C.byref(n_pairs)))
+    return keys[: n_pairs.value], vals[: n_pairs.value]
+
+
+def bin_tiles(cloud: GaussianCloud, geometry: ScanGeometry, angle_index: int,
+              settings: RasterSettings = RasterSettings(), ctx: Optional[Context] = None) -> list:
+    """gsct::bin_tiles equivalent: per-tile ascending splat lists for one view."""
+    keys, vals = tile_pairs(cloud, geometry, [angle_index], settings, ctx)
+    ts = settings.tile_size
+    n_tiles = ((geometry.n_u + ts - 1) // ts) * ((geometry.n_v + ts - 1) // ts)
+    bins: list = [[] for _ in range(n_tiles)]
+    bounds = np.searchsorted(keys, np.arange(n_tiles + 1))
+    for t in range(n_tiles):
+        bins[t] = vals[bounds[t]:bounds[t + 1]].astype(np.int32).tolist()
+    return bins
+
+
+def voxel_boxes(cloud: GaussianCloud, region, settings: VoxelSettings = VoxelSettings(), window=None,
+                ctx: Optional[Context] = None):
+    """detail::prepare_voxel_splats boxes on the device: lo [N,3], hi [N,3], skip [N]."""
+    ctx = _ctx_for(cloud, ctx)
+    keep: list = []
+    cc = cloud._c(keep)
+    n = cloud.size()
+    lo = np.zeros((n, 3), dtype=np.int32)
+    hi = np.zeros((n, 3), dtype=np.int32)
+    skip = np.zeros(n, dtype=np.uint8)
+    gr = _grid_c(region)
+    win = _window_c(window)
+    vs = settings.c()
+    ctx.check(ctx._lib.gsct_debug_voxel_boxes(ctx.handle, C.byref(cc), C.byref(gr), C.byref(win) if win else None,
+                                              C.byref(vs), lo.ctypes.data, hi.ctypes.data, skip.ctypes.data))
+    return lo, hi, skip.astype(bool)
+
+
+# ---------------------------------------------------------------------------------------
+# Host-side harness (no GPU needed)
+# ---------------------------------------------------------------------------------------
+def view_frame(geometry: ScanGeometry, angle_index: int) -> dict:
+    """gsct::view_frame (projector.hpp:29-43)."""
+    theta = float(_angles(geometry, [angle_index])[0])
+    f = (C.c_double * 16)()
+    g = geometry.c()
+    lib().gsct_host_view_frame(C.byref(g), theta, f)
+    a = np.array(f[:])
+    return dict(u=a[0:3], v=a[3:6], d=a[6:9], detector_center=a[9:12], source=a[12:15], focal=a[15],
+                cone=geometry.mode == "cone")
+
+
+def default_geometry(dims, spacing: float, n_views: int, mode: str, n_u: int, n_v: int) -> ScanGeometry:
+    """gsct::default_geometry (synthetic.hpp:246-271) for a volume of `dims` at `spacing`."""
+    g = c_geometry()
+    angles = (C.c_double * max(n_views, 1))()
+    lib().gsct_host_default_geometry((C.c_int * 3)(*[int(d) for d in dims]), float(spacing), int(n_views),
+                                     1 if mode == "cone" else 0, int(n_u), int(n_v), C.byref(g), angles)
+    return ScanGeometry(mode, g.n_u, g.n_v, g.s_u, g.s_v, list(angles[:n_views]), g.source_to_origin,
+                        g.origin_to_detector)
+
+
+class Rng:
+    """gsct::Rng (rng.hpp:18-69): mt19937_64 with the reference's output mappings."""
+
+    def __init__(self, seed: int = 0):
+        self._lib = lib()
+        self._h = self._lib.gsct_host_rng_create(C.c_uint64(seed))
+
+    def __del__(self):
+        try:
+            self._lib.gsct_host_rng_destroy(self._h)
+        except Exception:
+            pass
+
+    def uniform(self, lo: float = 0.0, hi: float = 1.0) -> float:
+        return self._lib.gsct_host_rng_uniform(self._h, lo, hi)
+
+    def normal(self) -> float:
+        return self._lib.gsct_host_rng_normal(self._h)
+
+    def uniform_int(self, n: int) -> int:
+        if n <= 0:
+            raise ContractError("Rng::uniform_int: n must be positive")
+        return int(self._lib.gsct_host_rng_uniform_int(self._h, n))
+
+    def uniform_array(self, n: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+        return np.array([self.uniform(lo, hi) for _ in range(n)])
+
+
+def sample_subvolume(parent: GridSpec, sub_dims, rng: Rng) -> GridRegion:
+    """gsct::sample_subvolume (voxelizer.hpp:76-93)."""
+    off = (C.c_int * 3)()
+    dims = (C.c_int * 3)()
+    st = lib().gsct_host_sample_subvolume((C.c_int * 3)(*[int(d) for d in parent.dims]),
+                                          (C.c_int * 3)(*[int(d) for d in sub_dims]), rng._h, off, dims)
+    if st != 0:
+        raise ContractError("sample_subvolume: dims must be at least 1")
+    return GridRegion.of_parent(parent, tuple(off), tuple(dims))
+
+
+def make_cloud(kind: str, count: int, seed: int = 0, **kw) -> GaussianCloud:
+    """Seeded clouds: "synthetic" (bench.hpp:33-52), "random" (tests/oracles.hpp:168-184),
+    "shepp_logan" (SURVEY.md 8d benchmark phantom cloud)."""
+    if kind == "synthetic":
+        k, p = 0, [kw.get("half_extent", 0.8), kw.get("scale", 0.04), kw.get("anisotropy", 1.0),
+                   kw.get("density", 1.0)]
+    elif kind == "random":
+        k, p = 1, [kw.get("pos_range", 5.0), kw.get("scale_lo", 0.5), kw.get("scale_hi", 2.5)]
+    elif kind == "shepp_logan":
+        k, p = 2, [float(kw["side"]), float(kw.get("spacing", 1.0))]
+    else:
+        raise ContractError(f"make_cloud: unknown kind {kind!r}")
+    pos = np.zeros((count, 3))
+    ls = np.zeros((count, 3))
+    q = np.zeros((count, 4))
+    raw = np.zeros(count)
+    pa = (C.c_double * 4)(*(p + [0.0] * (4 - len(p))))
+    st = lib().gsct_host_make_cloud(k, int(count), C.c_uint64(seed), pa, pos.ctypes.data, ls.ctypes.data,
+                                    q.ctypes.data, raw.ctypes.data)
+    if st != 0:
+        raise ContractError("make_cloud failed")
+    return GaussianCloud(pos, ls, q, raw)
