@@ -132,6 +132,29 @@ size_t gsct_ctx_workspace_bytes(gsct_ctx ctx);
 int64_t gsct_ctx_launch_count(gsct_ctx ctx);
 int gsct_abi_version(void);
 
+/* Per-phase device timing (CUDA events on the context stream around each phase's
+ * launches; RenderStats-style tracing, projector.hpp:73-80). Off by default. */
+enum gsct_phase {
+  GSCT_PH_RASTER_SETUP = 0, /* K1: fp64 projection + bbox + record */
+  GSCT_PH_RASTER_BIN,       /* K2: scan + key emission + radix sort + tile ranges */
+  GSCT_PH_RASTER_FWD,       /* K3: per-tile forward accumulation */
+  GSCT_PH_RASTER_BWD,       /* K4a: per-splat backward pixel loop */
+  GSCT_PH_RASTER_TAIL,      /* K4b: fp64 chain rule + view sum */
+  GSCT_PH_VOXEL_SETUP,      /* K6 */
+  GSCT_PH_VOXEL_BIN,        /* brick scan + emission + sort + ranges */
+  GSCT_PH_VOXEL_FWD,        /* K7 */
+  GSCT_PH_VOXEL_BWD,        /* K8a */
+  GSCT_PH_VOXEL_TAIL,       /* K8b */
+  GSCT_NUM_PHASES
+};
+int gsct_ctx_set_profiling(gsct_ctx ctx, int on);
+/* Synchronizes, returns accumulated milliseconds and launch counts per phase, resets. */
+int gsct_ctx_phase_times(gsct_ctx ctx, double ms[GSCT_NUM_PHASES], int64_t counts[GSCT_NUM_PHASES]);
+
+/* On-box throughput microbenchmarks (roofline denominators): kind 0 = MUFU ex2.approx.f32
+ * per second, kind 1 = FP32 FFMA per second, over the whole device. */
+int gsct_microbench(gsct_ctx ctx, int kind, double* ops_per_second);
+
 /* ---- rasterizer ---------------------------------------------------------------- */
 /* Forward projection of n_views views (angles: host array, radians) into
  * images[n_views][n_v][n_u] (fp32). One call == n_views calls of rasterize_view. */

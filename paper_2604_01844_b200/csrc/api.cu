@@ -52,7 +52,21 @@ struct gsct_ctx_s {
   uint32_t* hscratch = nullptr; // pinned 2 x u32 for scan totals
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   gsct_stats pending{};          // async-mode stats accumulated at synchronize
+  // per-phase event timing (gsct_ctx_set_profiling)
+  bool profiling = false;
+  std::vector<cudaEvent_t> event_pool;
+  struct Mark {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<Mark> marks;
+  double phase_ms[GSCT_NUM_PHASES] = {};
+  int64_t phase_count[GSCT_NUM_PHASES] = {};
 };
+
+namespace gsct_dev {
+double run_microbench(int kind, cudaStream_t st);
+}
 
 namespace {
 
@@ -86,6 +100,51 @@ T* ws(gsct_ctx c, Slot s, size_t count) {
     b.cap = want;
   }
   return static_cast<T*>(b.p);
+}
+
+cudaEvent_t pooled_event(gsct_ctx c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+
+// Records CUDA events around one phase's launches when profiling is on.
+struct Phase {
+  gsct_ctx c;
+  int phase;
+  cudaEvent_t a = nullptr;
+  Phase(gsct_ctx ctx, int ph) : c(ctx), phase(ph) {
+    if (c->profiling) {
+      a = pooled_event(c);
+      CK(cudaEventRecord(a, c->stream));
+    }
+  }
+  ~Phase() {
+    if (!a) return;
+    cudaEvent_t b = pooled_event(c);
+    cudaEventRecord(b, c->stream);
+    c->marks.push_back({phase, a, b});
+  }
+};
+
+void resolve_marks(gsct_ctx c) {
+  if (c->marks.empty()) return;
+  CK(cudaStreamSynchronize(c->stream));
+  for (auto& m : c->marks) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, m.a, m.b) == cudaSuccess) {
+      c->phase_ms[m.phase] += ms;
+      c->phase_count[m.phase] += 1;
+    }
+    c->event_pool.push_back(m.a);
+    c->event_pool.push_back(m.b);
+  }
+  c->marks.clear();
 }
 
 struct Guard {  // sets the launch counter for the duration of an API call
@@ -308,6 +367,11 @@ void gsct_ctx_destroy(gsct_ctx c) {
   cudaFreeHost(c->hscratch);
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
+  for (auto& m : c->marks) {
+    cudaEventDestroy(m.a);
+    cudaEventDestroy(m.b);
+  }
+  for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -374,6 +438,34 @@ size_t gsct_ctx_workspace_bytes(gsct_ctx c) {
 
 int64_t gsct_ctx_launch_count(gsct_ctx c) { return c ? c->launches : 0; }
 
+int gsct_ctx_set_profiling(gsct_ctx c, int on) {
+  return run(c, [&] {
+    resolve_marks(c);
+    c->profiling = on != 0;
+  });
+}
+
+int gsct_ctx_phase_times(gsct_ctx c, double ms[GSCT_NUM_PHASES], int64_t counts[GSCT_NUM_PHASES]) {
+  return run(c, [&] {
+    resolve_marks(c);
+    for (int k = 0; k < GSCT_NUM_PHASES; ++k) {
+      if (ms) ms[k] = c->phase_ms[k];
+      if (counts) counts[k] = c->phase_count[k];
+      c->phase_ms[k] = 0.0;
+      c->phase_count[k] = 0;
+    }
+  });
+}
+
+int gsct_microbench(gsct_ctx c, int kind, double* ops_per_second) {
+  return run(c, [&] {
+    contract(ops_per_second != nullptr && (kind == 0 || kind == 1), "microbench: bad arguments");
+    CK(cudaStreamSynchronize(c->stream));
+    *ops_per_second = run_microbench(kind, c->stream);
+    CK(cudaGetLastError());
+  });
+}
+
 // ---------------------------------------------------------------------------------------
 // Rasterizer
 // ---------------------------------------------------------------------------------------
@@ -412,17 +504,26 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       RasterRec* rec = ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * cv);
       uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * cv);
-      launch_raster_preprocess(d, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
+      {
+        Phase ph(c, GSCT_PH_RASTER_SETUP);
+        launch_raster_preprocess(d, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
+      }
       CK(cudaGetLastError());
       uint32_t *keys, *vals, *start, *end;
       const uint32_t n_keys = static_cast<uint32_t>(cv) * static_cast<uint32_t>(n_tiles);
-      bin_and_sort(
-          c, cnt, n * cv, n_keys,
-          [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
-            launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kTile, tiles_u, n_tiles, k, v, c->stream);
-          },
-          &keys, &vals, &start, &end);
-      launch_raster_fwd(rec, vals, start, end, n, cv, geom->n_u, geom->n_v, tiles_u, tiles_v, img, c->stream);
+      {
+        Phase ph(c, GSCT_PH_RASTER_BIN);
+        bin_and_sort(
+            c, cnt, n * cv, n_keys,
+            [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
+              launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kTile, tiles_u, n_tiles, k, v, c->stream);
+            },
+            &keys, &vals, &start, &end);
+      }
+      {
+        Phase ph(c, GSCT_PH_RASTER_FWD);
+        launch_raster_fwd(rec, vals, start, end, n, cv, geom->n_u, geom->n_v, tiles_u, tiles_v, img, c->stream);
+      }
       CK(cudaGetLastError());
     }
     if (images_location == GSCT_HOST && n_views)
@@ -483,10 +584,19 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       RasterRec* rec = ws<RasterRec>(c, S_REC, un * cv);
       uint32_t* cnt = ws<uint32_t>(c, S_COUNT, un * cv);
-      launch_raster_preprocess(d, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
+      {
+        Phase ph(c, GSCT_PH_RASTER_SETUP);
+        launch_raster_preprocess(d, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
+      }
       float* mom = ws<float>(c, S_MOMENTS, un * cv * 8);
-      launch_raster_bwd_pairs(rec, n, cv, geom->n_u, geom->n_v, gimg, mom, nullptr, c->stream);
-      launch_raster_tail(d, dframes + v0, cv, g, r, mom, v0 == 0, gp, gl, gq, gr, gn, gv, c->stream);
+      {
+        Phase ph(c, GSCT_PH_RASTER_BWD);
+        launch_raster_bwd_pairs(rec, n, cv, geom->n_u, geom->n_v, gimg, mom, nullptr, c->stream);
+      }
+      {
+        Phase ph(c, GSCT_PH_RASTER_TAIL);
+        launch_raster_tail(d, dframes + v0, cv, g, r, mom, v0 == 0, gp, gl, gq, gr, gn, gv, c->stream);
+      }
       CK(cudaGetLastError());
     }
     if (out->location == GSCT_HOST && n > 0) {
@@ -548,9 +658,15 @@ void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window
   CK(cudaMemsetAsync(mom, 0, static_cast<size_t>(n) * 10 * sizeof(float), c->stream));
   if (n == 0) return;
   VoxelRec* rec = ws<VoxelRec>(c, S_VREC, static_cast<size_t>(n));
-  launch_voxel_preprocess(d, grid, win, vs->tau_cut, vs->sigma_cap, rec, nullptr, nullptr, nullptr,
-                          nullptr, c->dstats, c->stream);
-  launch_voxel_bwd_pairs(rec, n, win, static_cast<float>(grid.spacing), grad, mom, nullptr, c->stream);
+  {
+    Phase ph(c, GSCT_PH_VOXEL_SETUP);
+    launch_voxel_preprocess(d, grid, win, vs->tau_cut, vs->sigma_cap, rec, nullptr, nullptr, nullptr,
+                            nullptr, c->dstats, c->stream);
+  }
+  {
+    Phase ph(c, GSCT_PH_VOXEL_BWD);
+    launch_voxel_bwd_pairs(rec, n, win, static_cast<float>(grid.spacing), grad, mom, nullptr, c->stream);
+  }
   CK(cudaGetLastError());
 }
 
@@ -603,16 +719,26 @@ int gsct_voxelize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
     } else {
       VoxelRec* rec = ws<VoxelRec>(c, S_VREC, static_cast<size_t>(n));
       uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n));
-      launch_voxel_preprocess(d, vg, win, vs->tau_cut, vs->sigma_cap, rec, cnt, nullptr, nullptr, nullptr,
-                              c->dstats, c->stream);
+      {
+        Phase ph(c, GSCT_PH_VOXEL_SETUP);
+        launch_voxel_preprocess(d, vg, win, vs->tau_cut, vs->sigma_cap, rec, cnt, nullptr, nullptr, nullptr,
+                                c->dstats, c->stream);
+      }
       uint32_t *keys, *vals, *start, *end;
-      bin_and_sort(
-          c, cnt, n, static_cast<uint32_t>(n_bricks),
-          [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
-            launch_emit_brick_pairs(rec, offsets, cnt, n, win, nbx, nby, k, v, c->stream);
-          },
-          &keys, &vals, &start, &end);
-      launch_voxel_fwd(rec, vals, start, end, win, nbx, nby, nbz, static_cast<float>(vg.spacing), outv, c->stream);
+      {
+        Phase ph(c, GSCT_PH_VOXEL_BIN);
+        bin_and_sort(
+            c, cnt, n, static_cast<uint32_t>(n_bricks),
+            [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
+              launch_emit_brick_pairs(rec, offsets, cnt, n, win, nbx, nby, k, v, c->stream);
+            },
+            &keys, &vals, &start, &end);
+      }
+      {
+        Phase ph(c, GSCT_PH_VOXEL_FWD);
+        launch_voxel_fwd(rec, vals, start, end, win, nbx, nby, nbz, static_cast<float>(vg.spacing), outv,
+                         c->stream);
+      }
       CK(cudaGetLastError());
     }
     if (volume_location == GSCT_HOST)
@@ -638,8 +764,11 @@ int gsct_voxelize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
     float* mom = ws<float>(c, S_MOMENTS, un * 10 + 1);
     voxel_moments(c, d, vg, win, vs, grad_volume, grad_location, mom);
     const GradPtrs p = grad_targets(c, out, un);
-    launch_voxel_tail(d, vg, vs->tau_cut, vs->sigma_cap, mom, p.gp, p.gl, p.gq, p.gr, p.gn, p.gv, c->dstats,
-                      c->stream);
+    {
+      Phase ph(c, GSCT_PH_VOXEL_TAIL);
+      launch_voxel_tail(d, vg, vs->tau_cut, vs->sigma_cap, mom, p.gp, p.gl, p.gq, p.gr, p.gn, p.gv, c->dstats,
+                        c->stream);
+    }
     CK(cudaGetLastError());
     grads_to_host(c, out, p, un);
     finish_sync(c, stats, false, stats ? &stats->backward_ms : nullptr);
@@ -670,8 +799,11 @@ int gsct_voxelize_bwd_finish(gsct_ctx c, const gsct_cloud* cloud, const gsct_gri
     const Cloud d = upload_cloud(c, cloud);
     const size_t un = static_cast<size_t>(d.n);
     const GradPtrs p = grad_targets(c, out, un);
-    launch_voxel_tail(d, vg, vs->tau_cut, vs->sigma_cap, moments_dev, p.gp, p.gl, p.gq, p.gr, p.gn, p.gv,
-                      c->dstats, c->stream);
+    {
+      Phase ph(c, GSCT_PH_VOXEL_TAIL);
+      launch_voxel_tail(d, vg, vs->tau_cut, vs->sigma_cap, moments_dev, p.gp, p.gl, p.gq, p.gr, p.gn, p.gv,
+                        c->dstats, c->stream);
+    }
     CK(cudaGetLastError());
     grads_to_host(c, out, p, un);
     finish_sync(c, nullptr, false, nullptr);

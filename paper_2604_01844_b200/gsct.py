@@ -28,6 +28,9 @@ import numpy as np
 _LIB_PATH = Path(__file__).resolve().parent / "libgsct_b200.so"
 
 GSCT_OK, GSCT_ERR_CONTRACT, GSCT_ERR_CUDA, GSCT_ERR_OOM = 0, 1, 2, 3
+# enum gsct_phase (include/gsct_cuda.h)
+PHASES = ("raster_setup", "raster_bin", "raster_fwd", "raster_bwd", "raster_tail",
+          "voxel_setup", "voxel_bin", "voxel_fwd", "voxel_bwd", "voxel_tail")
 GSCT_HOST, GSCT_DEVICE = 0, 1
 
 
@@ -100,6 +103,9 @@ _SIGS = {
     "gsct_ctx_synchronize": (C.c_int, [C.c_void_p, _P(c_stats)]),
     "gsct_ctx_workspace_bytes": (C.c_size_t, [C.c_void_p]),
     "gsct_ctx_launch_count": (C.c_int64, [C.c_void_p]),
+    "gsct_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
+    "gsct_ctx_phase_times": (C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_int64)]),
+    "gsct_microbench": (C.c_int, [C.c_void_p, C.c_int, _P(C.c_double)]),
     "gsct_rasterize_fwd": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), _P(C.c_double), C.c_int,
                                      _P(c_raster_settings), C.c_void_p, C.c_int, _P(c_stats)]),
     "gsct_rasterize_bwd": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), _P(C.c_double), C.c_int,
@@ -425,6 +431,22 @@ class Context:
 
     def workspace_bytes(self) -> int:
         return int(self._lib.gsct_ctx_workspace_bytes(self.handle))
+
+    def set_profiling(self, on: bool) -> None:
+        self.check(self._lib.gsct_ctx_set_profiling(self.handle, 1 if on else 0))
+
+    def phase_times(self) -> dict:
+        """Accumulated device ms and launch counts per phase since the last call."""
+        ms = (C.c_double * len(PHASES))()
+        cnt = (C.c_int64 * len(PHASES))()
+        self.check(self._lib.gsct_ctx_phase_times(self.handle, ms, cnt))
+        return {name: (ms[i], cnt[i]) for i, name in enumerate(PHASES)}
+
+    def microbench(self, kind: str) -> float:
+        """Device-wide ops/s: "ex2" (MUFU ex2.approx.f32) or "ffma" (FP32 FFMA)."""
+        out = C.c_double(0.0)
+        self.check(self._lib.gsct_microbench(self.handle, {"ex2": 0, "ffma": 1}[kind], C.byref(out)))
+        return out.value
 
 
 _contexts: dict[int, Context] = {}
