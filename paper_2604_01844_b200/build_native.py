@@ -43,6 +43,29 @@ def _stale(out: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+def build_variant(tag: str, defines: list[str]) -> Path:
+    """Builds build/variants/libgsct_<tag>.so with extra -D flags (A/B experiments; the
+    product library is always the default build)."""
+    vdir = ROOT / "build" / "variants" / tag
+    vdir.mkdir(parents=True, exist_ok=True)
+    jobs, objs = [], []
+    for src in CU_SOURCES:
+        o = vdir / (src + ".o")
+        objs.append(o)
+        jobs.append(([NVCC] + NVFLAGS + PER_FILE.get(src, []) + [f"-D{d}" for d in defines] +
+                     ["-c", str(CSRC / src), "-o", str(o)], vdir / (src + ".log")))
+    for src in CXX_SOURCES:
+        o = vdir / (src + ".o")
+        objs.append(o)
+        jobs.append((["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-c", str(CSRC / src), "-o", str(o)],
+                     vdir / (src + ".log")))
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        list(ex.map(lambda j: _run(*j), jobs))
+    lib = ROOT / "build" / "variants" / f"libgsct_{tag}.so"
+    _run([NVCC] + ARCH + ["-shared", "-o", str(lib)] + [str(o) for o in objs], vdir / "link.log")
+    return lib
+
+
 def build(force: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
     headers = sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "gsct_cuda.h"]

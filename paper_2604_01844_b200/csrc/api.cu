@@ -24,7 +24,7 @@ namespace {
 enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
-  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_COUNT_SLOTS
+  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_ACC, S_COUNT_SLOTS
 };
 
 struct Buf {
@@ -292,9 +292,9 @@ int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32
   const uint32_t total = read_scan_total(c, offsets, counts, n_items);
   *start = ws<uint32_t>(c, S_START, n_keys);
   *end = ws<uint32_t>(c, S_END, n_keys);
-  CK(cudaMemsetAsync(*start, 0, n_keys * sizeof(uint32_t), c->stream));
-  CK(cudaMemsetAsync(*end, 0, n_keys * sizeof(uint32_t), c->stream));
   if (total == 0) {
+    CK(cudaMemsetAsync(*start, 0, n_keys * sizeof(uint32_t), c->stream));
+    CK(cudaMemsetAsync(*end, 0, n_keys * sizeof(uint32_t), c->stream));
     *keys_out = *vals_out = nullptr;
     return 0;
   }
@@ -311,15 +311,23 @@ int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32
   CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(total), 0, end_bit, c->stream));
   *keys_out = kb.Current();
   *vals_out = vb.Current();
-  launch_ranges(*keys_out, total, *start, *end, c->stream);
+  launch_ranges(*keys_out, total, n_keys, *start, *end, c->stream);
   return total;
 }
 
-int views_per_chunk(int64_t n, int n_views) {
+// Views per chunk: bounded (view, splat) items, and view*n_tiles + tile keys of at most
+// 16 bits so the stable radix sort needs two 8-bit passes.
+int views_per_chunk(int64_t n, int n_views, int64_t n_tiles) {
   const int64_t budget = int64_t(1) << 25;  // (view, splat) items per chunk
   int64_t v = n > 0 ? budget / n : n_views;
+  if (n_tiles > 0 && n_tiles <= 65536) v = std::min<int64_t>(v, 65536 / n_tiles);
   if (v < 1) v = 1;
   if (v > n_views) v = n_views;
+  // balance the chunks (e.g. 75 views -> 38 + 37, not 64 + 11) so no launch has a short tail
+  if (v > 0 && n_views > 0) {
+    const int64_t n_chunks = (n_views + v - 1) / v;
+    v = (n_views + n_chunks - 1) / n_chunks;
+  }
   return static_cast<int>(v);
 }
 
@@ -494,7 +502,12 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (images_location == GSCT_HOST && n_views) out = ws<float>(c, S_IMAGES, static_cast<size_t>(npx) * n_views);
     const Geo g = make_geo(geom);
     const RSet r = make_rs(rs);
-    int chunk = views_per_chunk(n, n_views);
+    PreSplat* pre = ws<PreSplat>(c, S_PRE, static_cast<size_t>(n) + 1);
+    if (n > 0) {
+      Phase ph(c, GSCT_PH_RASTER_SETUP);
+      launch_splat_prepare(d, pre, c->dstats, c->stream);
+    }
+    int chunk = views_per_chunk(n, n_views, n_tiles);
     for (int v0 = 0; v0 < n_views; v0 += chunk) {
       const int cv = std::min(chunk, n_views - v0);
       float* img = out + static_cast<int64_t>(v0) * npx;
@@ -506,7 +519,7 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * cv);
       {
         Phase ph(c, GSCT_PH_RASTER_SETUP);
-        launch_raster_preprocess(d, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
+        launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
       }
       CK(cudaGetLastError());
       uint32_t *keys, *vals, *start, *end;
@@ -573,7 +586,14 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
     const Geo g = make_geo(geom);
     const RSet r = make_rs(rs);
-    const int chunk = views_per_chunk(n, n_views);
+    PreSplat* pre = ws<PreSplat>(c, S_PRE, un + 1);
+    double* acc = ws<double>(c, S_ACC, 11 * un + 1);
+    if (n > 0) {
+      Phase ph(c, GSCT_PH_RASTER_SETUP);
+      launch_splat_prepare(d, pre, c->dstats, c->stream);
+    }
+    const int tiles_u = (geom->n_u + kTile - 1) / kTile, tiles_v = (geom->n_v + kTile - 1) / kTile;
+    const int chunk = views_per_chunk(n, n_views, static_cast<int64_t>(tiles_u) * tiles_v);
     for (int v0 = 0; v0 < n_views && n > 0; v0 += chunk) {
       const int cv = std::min(chunk, n_views - v0);
       const float* gimg = grad_images + static_cast<int64_t>(v0) * npx;
@@ -583,10 +603,9 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         gimg = dst;
       }
       RasterRec* rec = ws<RasterRec>(c, S_REC, un * cv);
-      uint32_t* cnt = ws<uint32_t>(c, S_COUNT, un * cv);
       {
         Phase ph(c, GSCT_PH_RASTER_SETUP);
-        launch_raster_preprocess(d, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
+        launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kTile, rec, nullptr, c->dstats, c->stream);
       }
       float* mom = ws<float>(c, S_MOMENTS, un * cv * 8);
       {
@@ -595,9 +614,13 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       {
         Phase ph(c, GSCT_PH_RASTER_TAIL);
-        launch_raster_tail(d, dframes + v0, cv, g, r, mom, v0 == 0, gp, gl, gq, gr, gn, gv, c->stream);
+        launch_raster_tail(pre, n, dframes + v0, cv, g, r, mom, v0 == 0, acc, gv, c->stream);
       }
       CK(cudaGetLastError());
+    }
+    if (n > 0 && n_views > 0) {
+      Phase ph(c, GSCT_PH_RASTER_TAIL);
+      launch_raster_finalize(d, acc, gp, gl, gq, gr, gn, c->stream);
     }
     if (out->location == GSCT_HOST && n > 0) {
       CK(cudaMemcpyAsync(out->pos, gp, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -832,7 +855,9 @@ int gsct_debug_project(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     double* dmean = ws<double>(c, S_DBG2, 2 * un);
     double* dconic = ws<double>(c, S_DBG3, 4 * un);
     double* damp = ws<double>(c, S_DBG4, un);
-    launch_debug_project(d, df, make_geo(geom), make_rs(rs), drect, dflags, dmean, dconic, damp, c->dstats,
+    PreSplat* pre = ws<PreSplat>(c, S_PRE, un);
+    launch_splat_prepare(d, pre, c->dstats, c->stream);
+    launch_debug_project(pre, d.n, df, make_geo(geom), make_rs(rs), drect, dflags, dmean, dconic, damp,
                          c->stream);
     CK(cudaMemcpyAsync(rect, drect, 4 * un * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(flags, dflags, un, cudaMemcpyDeviceToHost, c->stream));
@@ -867,7 +892,10 @@ int gsct_debug_tile_pairs(gsct_ctx c, const gsct_cloud* cloud, const gsct_geomet
     CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
     RasterRec* rec = ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * n_views);
     uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * n_views);
-    launch_raster_preprocess(d, dframes, n_views, make_geo(geom), make_rs(rs), ts, rec, cnt, c->dstats, c->stream);
+    PreSplat* pre = ws<PreSplat>(c, S_PRE, static_cast<size_t>(n));
+    launch_splat_prepare(d, pre, c->dstats, c->stream);
+    launch_raster_preprocess(pre, n, dframes, n_views, make_geo(geom), make_rs(rs), ts, rec, cnt, c->dstats,
+                             c->stream);
     uint32_t *dk, *dv, *start, *end;
     const int64_t total = bin_and_sort(
         c, cnt, n * n_views, static_cast<uint32_t>(n_views) * static_cast<uint32_t>(n_tiles),

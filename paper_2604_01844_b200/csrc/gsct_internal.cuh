@@ -57,16 +57,19 @@ struct Window {
 };
 
 // ---- launch wrappers (defined in preprocess.cu / raster.cu / voxel.cu) ----
-void launch_raster_preprocess(const Cloud& c, const Frame* frames_dev, int n_views,
+void launch_splat_prepare(const Cloud& c, PreSplat* pre, DevStats* stats, cudaStream_t st);
+void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
                               const Geo& g, const RSet& rs, int bin_ts, RasterRec* rec,
                               uint32_t* tile_count, DevStats* stats, cudaStream_t st);
-void launch_raster_tail(const Cloud& c, const Frame* frames_dev, int n_views, const Geo& g,
-                        const RSet& rs, const float* moments, bool first_chunk, double* g_pos,
-                        double* g_ls, double* g_q, double* g_raw, double* g_pgn,
-                        uint8_t* visible, cudaStream_t st);
-void launch_debug_project(const Cloud& c, const Frame* frame_dev, const Geo& g, const RSet& rs,
-                          int32_t* rect, uint8_t* flags, double* mean2d, double* conic,
-                          double* amplitude, DevStats* stats, cudaStream_t st);
+// acc: fp64 [11][N] running view-sum (g_pos 3, g_sigma 6, g_raw, sum |dL/dmean2d|)
+void launch_raster_tail(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
+                        const Geo& g, const RSet& rs, const float* moments, bool first_chunk,
+                        double* acc, uint8_t* visible, cudaStream_t st);
+void launch_raster_finalize(const Cloud& c, const double* acc, double* g_pos, double* g_ls,
+                            double* g_q, double* g_raw, double* g_pgn, cudaStream_t st);
+void launch_debug_project(const PreSplat* pre, int64_t n, const Frame* frame_dev, const Geo& g,
+                          const RSet& rs, int32_t* rect, uint8_t* flags, double* mean2d,
+                          double* conic, double* amplitude, cudaStream_t st);
 void launch_voxel_preprocess(const Cloud& c, const VoxGrid& grid, const Window& win,
                              double tau_cut, double sigma_cap, VoxelRec* rec,
                              uint32_t* brick_count, int32_t* lo_out, int32_t* hi_out,
@@ -79,8 +82,8 @@ void launch_voxel_tail(const Cloud& c, const VoxGrid& grid, double tau_cut, doub
 void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets,
                             const uint32_t* counts, int64_t n, int n_views, int ts, int tiles_u,
                             int n_tiles, uint32_t* keys, uint32_t* vals, cudaStream_t st);
-void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t* start, uint32_t* end,
-                   cudaStream_t st);
+void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start,
+                   uint32_t* end, cudaStream_t st);
 void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                        const uint32_t* end, int64_t n, int n_views, int n_u, int n_v,
                        int tiles_u, int tiles_v, float* images, cudaStream_t st);

@@ -1,5 +1,6 @@
-// fp64 per-splat kernels: raster set-up (K1), raster chain-rule tail (K4b), voxel set-up
-// (K6), voxel chain-rule tail (K8b), and the projection parity hook.
+// fp64 per-splat kernels: the view-independent splat pre-pass, raster set-up (K1), raster
+// chain-rule tail (K4b) + finalize, voxel set-up (K6), voxel chain-rule tail (K8b), and
+// the projection parity hook.
 // Compiled with --fmad=false so the arithmetic is the reference's, operation by operation
 // (see splat_fp64.cuh): integer boxes and keys are bit-exact with the CPU oracle.
 #include <cuda_runtime.h>
@@ -31,28 +32,44 @@ __device__ __forceinline__ RasterRec empty_rec() {
   return r;
 }
 
-// K1: one thread per (splat, view): activate -> covariance -> project_full -> splat_bbox,
-// then the fp32 record, the binning tile count and the exact RenderStats counters.
-__global__ void __launch_bounds__(256) k_raster_preprocess(Cloud c, const Frame* __restrict__ frames,
-                                                           Geo g, RSet rs, int bin_ts,
+// View-independent pre-pass, one thread per splat: activation, Sigma, det test, Sigma^-1
+// (computed once instead of once per view; identical values, so boxes stay bit-exact).
+__global__ void __launch_bounds__(128) k_splat_prepare(Cloud c, PreSplat* __restrict__ pre,
+                                                       DevStats* __restrict__ st) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= c.n) return;
+  PreSplat s;
+  prepare_splat(c.pos, c.ls, c.q, c.raw, i, s);
+  if (s.status) flag_error(st, i, s.status);
+  pre[i] = s;
+}
+
+// K1: one thread per (splat, view): project_full -> splat_bbox from the pre-pass, then the
+// fp32 record, the binning tile count and the exact RenderStats counters.
+// (launch bounds: 8 CTAs x 128 threads per SM -> <= 64 registers, 50% occupancy; the
+// kernel is fp64-latency bound, profiles/)
+#ifndef GSCT_PRE_MINB
+#define GSCT_PRE_MINB 8
+#endif
+#ifndef GSCT_TAIL_MINB
+#define GSCT_TAIL_MINB 4
+#endif
+__global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const PreSplat* __restrict__ pre, int64_t n,
+                                                           const Frame* __restrict__ frames, Geo g,
+                                                           RSet rs, int bin_ts,
                                                            RasterRec* __restrict__ rec,
                                                            uint32_t* __restrict__ tile_count,
                                                            DevStats* __restrict__ st) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int v = blockIdx.y;
   unsigned long long n_culled = 0, n_degen = 0, n_tp = 0, n_pp = 0;
-  if (i < c.n) {
+  if (i < n) {
     RasterRec r = empty_rec();
     uint32_t cnt = 0;
-    Act a;
-    const int err = activate(c.pos, c.ls, c.q, c.raw, i, a);
-    if (err) {
-      if (v == 0) flag_error(st, i, err);
-    } else {
-      double sigma[9];
-      covariance(a.scales, a.uq, sigma);
+    const PreSplat& s = pre[i];
+    if (s.status == 0) {
       Proj p;
-      project_full(frames[v], g, a.pos, sigma, a.density, rs, p);
+      project_full(frames[v], g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
       if (p.degenerate) {
         n_degen = 1;
       } else if (p.culled) {
@@ -75,9 +92,9 @@ __global__ void __launch_bounds__(256) k_raster_preprocess(Cloud c, const Frame*
         n_pp = static_cast<unsigned long long>(u1 - u0 + 1) * static_cast<unsigned long long>(v1 - v0 + 1);
       }
     }
-    const int64_t item = static_cast<int64_t>(v) * c.n + i;
+    const int64_t item = static_cast<int64_t>(v) * n + i;
     rec[item] = r;
-    tile_count[item] = cnt;
+    if (tile_count) tile_count[item] = cnt;
   }
   warp_add(&st->culled, n_culled);
   warp_add(&st->degenerate, n_degen);
@@ -85,43 +102,32 @@ __global__ void __launch_bounds__(256) k_raster_preprocess(Cloud c, const Frame*
   warp_add(&st->pixel_pairs, n_pp);
 }
 
-// K4b: one thread per splat; for each view of the chunk (ascending) re-derive the fp64
-// projection, turn the fp32 pixel-loop moments into dL/d(amp, mean2d, conic) and run the
-// reference chain rule; per-view results are summed in view order (ParamGradients::add).
-__global__ void __launch_bounds__(128) k_raster_tail(Cloud c, const Frame* __restrict__ frames,
-                                                     int n_views, Geo g, RSet rs,
-                                                     const float4* __restrict__ moments,
-                                                     int first_chunk, double* __restrict__ g_pos,
-                                                     double* __restrict__ g_ls, double* __restrict__ g_q,
-                                                     double* __restrict__ g_raw,
-                                                     double* __restrict__ g_pgn,
+// K4b: one warp per splat, lane l handles views l, l+32, ... of the chunk: re-derives the
+// fp64 projection, turns the fp32 pixel-loop moments into dL/d(amp, mean2d, conic) and runs
+// the reference chain rule up to dL/dSigma. Per-view results are summed over the chunk's
+// views with a fixed shuffle tree and added to the running fp64 accumulator (chunks in
+// ascending view order), i.e. ParamGradients::add up to fp64 reassociation.
+// acc layout [11][N]: g_pos(3), g_sigma(00,01,02,11,12,22), g_raw, sum |dL/dmean2d|.
+__global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSplat* __restrict__ pre, int64_t n,
+                                                     const Frame* __restrict__ frames, int n_views,
+                                                     Geo g, RSet rs, const float4* __restrict__ moments,
+                                                     int first_chunk, double* __restrict__ acc,
                                                      uint8_t* __restrict__ visible) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= c.n) return;
-  double tp[3] = {0, 0, 0}, tl[3] = {0, 0, 0}, tq[4] = {0, 0, 0, 0}, tr = 0.0, tn = 0.0;
-  uint8_t vis = 0;
-  if (!first_chunk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  double v[11];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      tp[k] = g_pos[3 * i + k];
-      tl[k] = g_ls[3 * i + k];
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) tq[k] = g_q[4 * i + k];
-    tr = g_raw[i];
-    tn = g_pgn[i];
-    vis = visible[i];
-  }
-  Act a;
-  if (activate(c.pos, c.ls, c.q, c.raw, i, a) == 0) {
-    double sigma[9];
-    covariance(a.scales, a.uq, sigma);
-    for (int v = 0; v < n_views; ++v) {
+  for (int k = 0; k < 11; ++k) v[k] = 0.0;
+  bool vis = false;
+  const PreSplat& s = pre[i];
+  if (s.status == 0) {
+    for (int vw = lane; vw < n_views; vw += 32) {
       Proj p;
-      project_full(frames[v], g, a.pos, sigma, a.density, rs, p);
+      project_full(frames[vw], g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
       if (p.degenerate || p.culled) continue;
-      vis = 1;
-      const int64_t item = static_cast<int64_t>(v) * c.n + i;
+      vis = true;
+      const int64_t item = static_cast<int64_t>(vw) * n + i;
       const float4 m0 = moments[2 * item];
       const float4 m1 = moments[2 * item + 1];
       // m0 = {sum t, sum t du, sum t dv, sum t du^2}, m1 = {sum t du dv, sum t dv^2, -, -}
@@ -135,47 +141,71 @@ __global__ void __launch_bounds__(128) k_raster_tail(Cloud c, const Frame* __res
       gc[1] = -0.5 * amp * static_cast<double>(m1.x);
       gc[2] = gc[1];
       gc[3] = -0.5 * amp * static_cast<double>(m1.y);
-      double vp[3], vl[3], vq[4], vr;
-      raster_chain_rule(frames[v], g, rs, a, sigma, p, static_cast<double>(m0.x), gm, gc, vp, vl,
-                        vq, vr);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        tp[k] += vp[k];
-        tl[k] += vl[k];
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) tq[k] += vq[k];
-      tr += vr;
-      tn += sqrt(gm[0] * gm[0] + gm[1] * gm[1]);
+      double gp[3], gs[9], gr;
+      raster_chain_rule(frames[vw], g, rs, s.density, s.raw_density, s.sigma, p, static_cast<double>(m0.x), gm,
+                        gc, gp, gs, gr);
+      v[0] += gp[0];
+      v[1] += gp[1];
+      v[2] += gp[2];
+      v[3] += gs[0];
+      v[4] += gs[1];
+      v[5] += gs[2];
+      v[6] += gs[4];
+      v[7] += gs[5];
+      v[8] += gs[8];
+      v[9] += gr;
+      v[10] += sqrt(gm[0] * gm[0] + gm[1] * gm[1]);
     }
   }
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    g_pos[3 * i + k] = tp[k];
-    g_ls[3 * i + k] = tl[k];
-  }
+  for (int k = 0; k < 11; ++k) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) g_q[4 * i + k] = tq[k];
-  g_raw[i] = tr;
-  g_pgn[i] = tn;
-  visible[i] = vis;
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  vis = __any_sync(0xffffffffu, vis);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 11; ++k) acc[k * n + i] = first_chunk ? v[k] : acc[k * n + i] + v[k];
+    visible[i] = first_chunk ? static_cast<uint8_t>(vis) : static_cast<uint8_t>(visible[i] | vis);
+  }
 }
 
-__global__ void k_debug_project(Cloud c, const Frame* __restrict__ frame, Geo g, RSet rs,
-                                int32_t* rect, uint8_t* flags, double* mean2d, double* conic,
-                                double* amplitude, DevStats* st) {
+// Per-splat finalize: covariance_backward (core.hpp:170-191) of the summed dL/dSigma.
+__global__ void __launch_bounds__(128) k_raster_finalize(Cloud c, const double* __restrict__ acc,
+                                                         double* __restrict__ g_pos, double* __restrict__ g_ls,
+                                                         double* __restrict__ g_q, double* __restrict__ g_raw,
+                                                         double* __restrict__ g_pgn) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= c.n) return;
+  const int64_t n = c.n;
+  double gl[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0};
   Act a;
-  const int err = activate(c.pos, c.ls, c.q, c.raw, i, a);
-  if (err) {
-    flag_error(st, i, err);
-    return;
+  if (activate(c.pos, c.ls, c.q, c.raw, i, a) == 0) {
+    const double s00 = acc[3 * n + i], s01 = acc[4 * n + i], s02 = acc[5 * n + i];
+    const double s11 = acc[6 * n + i], s12 = acc[7 * n + i], s22 = acc[8 * n + i];
+    const double gsig[9] = {s00, s01, s02, s01, s11, s12, s02, s12, s22};
+    covariance_backward(a.scales, a.uq, a.raw_q, gsig, gl, gq);
   }
-  double sigma[9];
-  covariance(a.scales, a.uq, sigma);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g_pos[3 * i + k] = acc[k * n + i];
+    g_ls[3 * i + k] = gl[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) g_q[4 * i + k] = gq[k];
+  g_raw[i] = acc[9 * n + i];
+  g_pgn[i] = acc[10 * n + i];
+}
+
+__global__ void k_debug_project(const PreSplat* __restrict__ pre, int64_t n, const Frame* __restrict__ frame,
+                                Geo g, RSet rs, int32_t* rect, uint8_t* flags, double* mean2d, double* conic,
+                                double* amplitude) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const PreSplat& s = pre[i];
+  if (s.status) return;
   Proj p;
-  project_full(*frame, g, a.pos, sigma, a.density, rs, p);
+  project_full(*frame, g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     rect[4 * i + k] = p.rect[k];
@@ -188,7 +218,7 @@ __global__ void k_debug_project(Cloud c, const Frame* __restrict__ frame, Geo g,
 }
 
 // K6: one thread per splat: prepare_voxel_splat in grid coordinates, clip to the window,
-// fp32 record relative to the clipped box corner, brick count, exact stats.
+// fp32 record relative to the grid-clipped box corner, brick count, exact stats.
 __global__ void __launch_bounds__(256) k_voxel_preprocess(Cloud c, VoxGrid grid, Window win,
                                                           double tau_cut, double sigma_cap,
                                                           VoxelRec* __restrict__ rec,
@@ -335,32 +365,44 @@ inline unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n +
 
 }  // namespace
 
-void launch_raster_preprocess(const Cloud& c, const Frame* frames_dev, int n_views, const Geo& g,
+void launch_splat_prepare(const Cloud& c, PreSplat* pre, DevStats* stats, cudaStream_t st) {
+  if (c.n == 0) return;
+  k_splat_prepare<<<blocks_for(c.n, 128), 128, 0, st>>>(c, pre, stats);
+  count_launch();
+}
+
+void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views, const Geo& g,
                               const RSet& rs, int bin_ts, RasterRec* rec, uint32_t* tile_count,
                               DevStats* stats, cudaStream_t st) {
-  if (c.n == 0 || n_views == 0) return;
-  dim3 grid(blocks_for(c.n, 256), static_cast<unsigned>(n_views));
-  k_raster_preprocess<<<grid, 256, 0, st>>>(c, frames_dev, g, rs, bin_ts, rec, tile_count, stats);
+  if (n == 0 || n_views == 0) return;
+  dim3 grid(blocks_for(n, 128), static_cast<unsigned>(n_views));
+  k_raster_preprocess<<<grid, 128, 0, st>>>(pre, n, frames_dev, g, rs, bin_ts, rec, tile_count, stats);
   count_launch();
 }
 
-void launch_raster_tail(const Cloud& c, const Frame* frames_dev, int n_views, const Geo& g,
-                        const RSet& rs, const float* moments, bool first_chunk, double* g_pos,
-                        double* g_ls, double* g_q, double* g_raw, double* g_pgn,
-                        uint8_t* visible, cudaStream_t st) {
-  if (c.n == 0) return;
-  k_raster_tail<<<blocks_for(c.n, 128), 128, 0, st>>>(
-      c, frames_dev, n_views, g, rs, reinterpret_cast<const float4*>(moments), first_chunk ? 1 : 0,
-      g_pos, g_ls, g_q, g_raw, g_pgn, visible);
+void launch_raster_tail(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views, const Geo& g,
+                        const RSet& rs, const float* moments, bool first_chunk, double* acc, uint8_t* visible,
+                        cudaStream_t st) {
+  if (n == 0) return;
+  k_raster_tail<<<blocks_for(n * 32, 128), 128, 0, st>>>(pre, n, frames_dev, n_views, g, rs,
+                                                         reinterpret_cast<const float4*>(moments),
+                                                         first_chunk ? 1 : 0, acc, visible);
   count_launch();
 }
 
-void launch_debug_project(const Cloud& c, const Frame* frame_dev, const Geo& g, const RSet& rs,
-                          int32_t* rect, uint8_t* flags, double* mean2d, double* conic,
-                          double* amplitude, DevStats* stats, cudaStream_t st) {
+void launch_raster_finalize(const Cloud& c, const double* acc, double* g_pos, double* g_ls, double* g_q,
+                            double* g_raw, double* g_pgn, cudaStream_t st) {
   if (c.n == 0) return;
-  k_debug_project<<<blocks_for(c.n, 128), 128, 0, st>>>(c, frame_dev, g, rs, rect, flags, mean2d,
-                                                        conic, amplitude, stats);
+  k_raster_finalize<<<blocks_for(c.n, 128), 128, 0, st>>>(c, acc, g_pos, g_ls, g_q, g_raw, g_pgn);
+  count_launch();
+}
+
+void launch_debug_project(const PreSplat* pre, int64_t n, const Frame* frame_dev, const Geo& g, const RSet& rs,
+                          int32_t* rect, uint8_t* flags, double* mean2d, double* conic, double* amplitude,
+                          cudaStream_t st) {
+  if (n == 0) return;
+  k_debug_project<<<blocks_for(n, 128), 128, 0, st>>>(pre, n, frame_dev, g, rs, rect, flags, mean2d, conic,
+                                                      amplitude);
   count_launch();
 }
 

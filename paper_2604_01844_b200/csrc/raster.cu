@@ -7,6 +7,13 @@
 // K4a follows rasterize_backward's pixel loop (projector.hpp:399-420): each splat is
 // owned by one warp that walks its own bbox; per-pixel terms are reduced with a fixed
 // xor-shuffle tree, so gradients are bit-stable without atomics.
+//
+// Both kernels are issue-bound rather than HBM-bound (profiles/), so the designs minimise
+// instructions per splat-pixel pair: the forward gives each lane an 8-pixel row segment and
+// advances the exponent along the row by second-order differences (2 FADD + 1 MUFU.EX2 +
+// 1 FFMA per pixel, per-splat set-up amortised over the 256 pixels of the tile); the
+// backward maps lanes to bbox columns x row groups so du is lane-constant and the six
+// moments need three per-lane accumulators.
 #include <cuda_runtime.h>
 
 #include "gsct_internal.cuh"
@@ -18,6 +25,12 @@ namespace {
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -45,112 +58,226 @@ __global__ void k_emit_tile_pairs(const RasterRec* __restrict__ rec,
     }
 }
 
-__global__ void k_ranges(const uint32_t* __restrict__ keys, int64_t n_pairs,
-                         uint32_t* __restrict__ start, uint32_t* __restrict__ end) {
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n_pairs) return;
-  const uint32_t key = keys[k];
-  if (k == 0 || keys[k - 1] != key) start[key] = static_cast<uint32_t>(k);
-  if (k == n_pairs - 1 || keys[k + 1] != key) end[key] = static_cast<uint32_t>(k + 1);
+// [start, end) of every key in the sorted key array: one thread per key, binary search
+// (n_keys * log2(pairs) reads instead of a pass over all pairs).
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__ a, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
 }
 
-// One CTA (256 threads) per 16x16 tile and view. Warp w owns an 8x4 pixel patch so that
-// splat rectangles that miss the patch are skipped warp-uniformly.
-__global__ void __launch_bounds__(256) k_raster_fwd(const RasterRec* __restrict__ rec,
-                                                    const uint32_t* __restrict__ vals,
-                                                    const uint32_t* __restrict__ start,
-                                                    const uint32_t* __restrict__ end, int64_t n,
-                                                    int n_u, int n_v, int tiles_u,
-                                                    float* __restrict__ images) {
-  __shared__ float4 s_rect[256];  // fu0, fu1, fv0, fv1
-  __shared__ float4 s_par[256];   // mo_u, mo_v, A, B
-  __shared__ float2 s_par2[256];  // C, amp
-  const int tile = blockIdx.x;
+__global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, uint32_t n_keys,
+                         uint32_t* __restrict__ start, uint32_t* __restrict__ end) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_keys) return;
+  start[k] = lower_bound_u32(keys, n_pairs, k);
+  end[k] = lower_bound_u32(keys, n_pairs, k + 1);
+}
+
+#ifndef GSCT_BWD_ASM
+#define GSCT_BWD_ASM 0
+#endif
+#ifndef GSCT_BWD_LOOP
+#define GSCT_BWD_LOOP 1  // 1: predicate-free 4-row main loop + remainder (A/B: 7.6 vs 8.3 ms)
+#endif
+
+constexpr int kFwdWarps = 4;  // tiles per CTA (one warp per 16x16 tile)
+constexpr int kPX = 8;        // pixels per lane (row segment)
+
+struct __align__(16) StagedRec {
+  int4 irect;  // u0, u1, v0, v1
+  float4 p;    // u0, v0 (exact floats), mo_u, mo_v
+  float4 q;    // A, B, C, amp
+};
+
+// One warp per 16x16 tile and view. Lane l owns the 8-pixel row segment at columns
+// 8*(l & 1) .. +7 of row (l >> 1). Per record a lane computes an 8-bit inside mask once
+// (R2P turns it into predicates) and walks its segment with second-order differences of
+// the exponent: MUFU.EX2 + 2 FADD + 1 predicated FFMA per pixel, which balances the issue
+// slots against the SFU rate (profiles/: both ~75-80% of peak).
+// Records of the tile list are staged 32 at a time in the warp's shared-memory slice
+// (one gather per lane, __syncwarp only; no block barriers), software-pipelined.
+__global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd(const RasterRec* __restrict__ rec,
+                                                               const uint32_t* __restrict__ vals,
+                                                               const uint32_t* __restrict__ start,
+                                                               const uint32_t* __restrict__ end, int64_t n,
+                                                               int n_u, int n_v, int tiles_u, int n_tiles,
+                                                               float* __restrict__ images) {
+  __shared__ StagedRec s_rec[kFwdWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kFwdWarps + warp;
+  if (tile >= n_tiles) return;  // whole warp exits together
   const int view = blockIdx.y;
-  const int n_tiles = gridDim.x;
   const int tu = tile % tiles_u, tv = tile / tiles_u;
-  const int t = threadIdx.x, w = t >> 5, l = t & 31;
-  const int pu0 = tu * kTile + (w & 1) * 8, pv0 = tv * kTile + (w >> 1) * 4;
-  const int px = pu0 + (l & 7), py = pv0 + (l >> 3);
-  const float fu = static_cast<float>(px), fv = static_cast<float>(py);
-  const float wu0 = static_cast<float>(pu0), wu1 = wu0 + 7.f;
-  const float wv0 = static_cast<float>(pv0), wv1 = wv0 + 3.f;
+  const int py = tv * kTile + (lane >> 1);
+  const int px0 = tu * kTile + (lane & 1) * kPX;
+  const float fr = static_cast<float>(py), fc0 = static_cast<float>(px0);
   const uint32_t key = static_cast<uint32_t>(view) * n_tiles + tile;
   const uint32_t b = start[key], e = end[key];
   const RasterRec* __restrict__ vrec = rec + static_cast<int64_t>(view) * n;
-  float acc = 0.f;
-  for (uint32_t base = b; base < e; base += 256) {
-    const int cnt = min(256u, e - base);
-    __syncthreads();
-    if (t < cnt) {
-      const RasterRec r = vrec[vals[base + t]];
-      s_rect[t] = make_float4(static_cast<float>(r.urange & 0xFFFF), static_cast<float>(r.urange >> 16),
-                              static_cast<float>(r.vrange & 0xFFFF), static_cast<float>(r.vrange >> 16));
-      s_par[t] = make_float4(r.mo_u, r.mo_v, r.A, r.B);
-      s_par2[t] = make_float2(r.C, r.amp);
+  StagedRec* sw = s_rec[warp];
+  float acc[kPX];
+#pragma unroll
+  for (int k = 0; k < kPX; ++k) acc[k] = 0.f;
+
+  // software pipeline: the record gather of batch i+1 and the index load of batch i+2 are
+  // in flight while batch i is processed
+  uint32_t idx_next = (b + 32 + lane < e) ? vals[b + 32 + lane] : 0u;
+  RasterRec r_cur;
+  if (b + lane < e) r_cur = vrec[vals[b + lane]];
+  for (uint32_t base = b; base < e; base += 32) {
+    const int cnt = min(32u, e - base);
+    const bool has_next = base + 32 + lane < e;
+    RasterRec r_next;
+    if (has_next) r_next = vrec[idx_next];
+    idx_next = (base + 64 + lane < e) ? vals[base + 64 + lane] : 0u;
+    if (lane < cnt) {
+      const RasterRec r = r_cur;
+      StagedRec s;
+      const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16, v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+      s.irect = make_int4(u0, u1, v0, v1);
+      s.p = make_float4(static_cast<float>(u0), static_cast<float>(v0), r.mo_u, r.mo_v);
+      s.q = make_float4(r.A, r.B, r.C, r.amp);
+      sw[lane] = s;
     }
-    __syncthreads();
+    __syncwarp();
     for (int j = 0; j < cnt; ++j) {
-      const float4 rc = s_rect[j];
-      if (rc.x > wu1 || rc.y < wu0 || rc.z > wv1 || rc.w < wv0) continue;  // warp-uniform
-      const float4 p = s_par[j];
-      const float2 p2 = s_par2[j];
-      const float du = (fu - rc.x) - p.x;
-      const float dv = (fv - rc.z) - p.y;
-      const float ex = ex2_approx(fmaf(fmaf(p.z, du, p.w * dv), du, p2.x * dv * dv));
-      if (fu >= rc.x && fu <= rc.y && fv >= rc.z && fv <= rc.w) acc = fmaf(p2.y, ex, acc);
+      const int4 ir = sw[j].irect;
+      const float4 p = sw[j].p;
+      const float4 q = sw[j].q;
+      // 8-bit mask of this lane's pixels inside the bbox (bits k with u0 <= px0+k <= u1)
+      const int lo = min(max(ir.x - px0, 0), kPX);
+      const int hi = min(max(ir.y - px0 + 1, 0), kPX);
+      unsigned mask = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+      if (py < ir.z || py > ir.w) mask = 0u;
+      const float du0 = (fc0 - p.x) - p.z;
+      const float dv = (fr - p.y) - p.w;
+      const float bdv = q.y * dv;
+      float ee = fmaf(fmaf(q.x, du0, bdv), du0, q.z * dv * dv);  // log2 of exp(e) at k = 0
+      float dd = fmaf(q.x, fmaf(2.f, du0, 1.f), bdv);            // first difference
+      const float a2 = 2.f * q.x;                                 // second difference
+#pragma unroll
+      for (int k = 0; k < kPX; ++k) {
+        const float ex = ex2_approx(ee);
+        if (mask & (1u << k)) acc[k] = fmaf(q.w, ex, acc[k]);
+        ee += dd;
+        dd += a2;
+      }
+    }
+    __syncwarp();
+    r_cur = r_next;
+  }
+  if (py < n_v) {
+    float* row = images + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(py) * n_u;
+    if (((n_u & 3) == 0) && px0 + kPX <= n_u) {
+      reinterpret_cast<float4*>(row + px0)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      reinterpret_cast<float4*>(row + px0)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kPX; ++k)
+        if (px0 + k < n_u) row[px0 + k] = acc[k];
     }
   }
-  if (px < n_u && py < n_v)
-    images[static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(py) * n_u + px] = acc;
 }
 
-// One warp per (view, splat) item, grid-stride. Lanes walk the bbox row-major in steps of
-// 32 pixels. Moments of t = exp(e) * w: {t, t du, t dv, t du^2, t du dv, t dv^2}.
+// One warp per (view, splat) item, grid-stride. Lanes = bbox columns (blocks of <= 32)
+// x row groups; each lane walks its column with stride G = 32 / cw rows. du is constant
+// per lane, so per pixel only {t, t dv, t dv^2} are accumulated and folded with du once.
+// Moments of t = exp(e) * w: {t, t du, t dv, t du^2, t du dv, t dv^2}.
 __global__ void __launch_bounds__(256) k_raster_bwd_pairs(const RasterRec* __restrict__ rec,
                                                           int64_t n_items, int64_t n, int n_u,
                                                           int n_v,
                                                           const float* __restrict__ grad,
-                                                          float4* __restrict__ moments) {
+                                                          float4* __restrict__ moments, double inv_n) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  RasterRec r_next;
+  if (warp < n_items) r_next = rec[warp];
   for (int64_t item = warp; item < n_items; item += n_warps) {
-    const RasterRec r = rec[item];
+    const RasterRec r = r_next;
+    if (item + n_warps < n_items) r_next = rec[item + n_warps];  // prefetch the next item
     const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
     const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
     const int W = u1 - u0 + 1, H = v1 - v0 + 1;
     if (W <= 0 || H <= 0) continue;
-    const int view = static_cast<int>(item / n);
-    const float* __restrict__ gi = grad + static_cast<int64_t>(view) * n_u * n_v;
-    const int npix = W * H;
-    int pu = lane % W, pv = lane / W;
-    const int su = 32 % W, sv = 32 / W;
-    float fpu = static_cast<float>(pu), fpv = static_cast<float>(pv);
-    const float fsu = static_cast<float>(su), fsv = static_cast<float>(sv), fW = static_cast<float>(W);
+    // view = item / n without a 64-bit integer division (exact: the quotient's fractional
+    // part is >= 0.5/n away from an integer, far above the fp64 rounding error)
+    const int view = static_cast<int>((static_cast<double>(item) + 0.5) * inv_n);
+    const float* __restrict__ gi = grad + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(v0) * n_u + u0;
+#if GSCT_BWD_ASM
+    // materialise the per-item base pointer so each load below is one IMAD.WIDE.U32 from a
+    // 32-bit offset instead of a 64-bit add + shift chain
+    asm volatile("mov.b64 %0, %0;" : "+l"(gi));
+#endif
     float m0 = 0.f, mu = 0.f, mv = 0.f, muu = 0.f, muv = 0.f, mvv = 0.f;
-    for (int p = lane; p < npix; p += 32) {
-      const float w = __ldg(gi + static_cast<int64_t>(v0 + pv) * n_u + (u0 + pu));
-      const float du = fpu - r.mo_u, dv = fpv - r.mo_v;
-      const float ex = ex2_approx(fmaf(fmaf(r.A, du, r.B * dv), du, r.C * dv * dv));
-      const float tt = ex * w;
-      m0 += tt;
-      const float tu_ = tt * du, tv_ = tt * dv;
-      mu += tu_;
-      mv += tv_;
-      muu = fmaf(tu_, du, muu);
-      muv = fmaf(tu_, dv, muv);
-      mvv = fmaf(tv_, dv, mvv);
-      pu += su;
-      pv += sv;
-      fpu += fsu;
-      fpv += fsv;
-      if (pu >= W) {
-        pu -= W;
-        pv += 1;
-        fpu -= fW;
-        fpv += 1.f;
+    for (int cb = 0; cb < W; cb += 32) {
+      const int cw = min(32, W - cb);
+      // lane -> (col, grp) and G = 32 / cw without integer division: floor((x + 0.5) / cw)
+      const float rc = rcp_approx(static_cast<float>(cw));
+      const int G = static_cast<int>(32.5f * rc);
+      const int grp = static_cast<int>((static_cast<float>(lane) + 0.5f) * rc);
+      const int col = lane - grp * cw;
+      if (grp >= G) continue;  // idle lanes (32 % cw)
+      const float du = static_cast<float>(cb + col) - r.mo_u;
+      const float a2 = r.A * du * du;
+      const float bdu = r.B * du;
+      float dv = static_cast<float>(grp) - r.mo_v;
+      const float fG = static_cast<float>(G);
+      float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+      // unsigned 32-bit element offsets from the bbox corner: one IMAD.WIDE.U32 per load
+      uint32_t off = static_cast<uint32_t>(grp * n_u + cb + col);
+      const uint32_t stride = static_cast<uint32_t>(G * n_u);
+      // rows of this lane: grp, grp + G, ... < H. Main loop: four rows per step, four grad
+      // loads in flight, no predicates; then at most three remainder rows.
+      int v = grp;
+#if GSCT_BWD_LOOP == 0
+      for (; v < H; v += 4 * G) {
+        float w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = (v + k * G < H) ? __ldg(gi + (off + k * stride)) : 0.f;
+#else
+      for (; v + 3 * G < H; v += 4 * G) {
+        const float w0 = __ldg(gi + off), w1 = __ldg(gi + (off + stride)), w2 = __ldg(gi + (off + 2 * stride)),
+                    w3 = __ldg(gi + (off + 3 * stride));
+        const float w[4] = {w0, w1, w2, w3};
+#endif
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float ex = ex2_approx(fmaf(dv, fmaf(r.C, dv, bdu), a2));
+          const float tt = ex * w[k];
+          t0 += tt;
+          const float tv = tt * dv;
+          t1 += tv;
+          t2 = fmaf(tv, dv, t2);
+          dv += fG;
+        }
+        off += 4 * stride;
       }
+      for (; v < H; v += G) {
+        const float w = __ldg(gi + off);
+        const float ex = ex2_approx(fmaf(dv, fmaf(r.C, dv, bdu), a2));
+        const float tt = ex * w;
+        t0 += tt;
+        const float tv = tt * dv;
+        t1 += tv;
+        t2 = fmaf(tv, dv, t2);
+        dv += fG;
+        off += stride;
+      }
+      m0 += t0;
+      mu = fmaf(t0, du, mu);
+      mv += t1;
+      const float t0du = t0 * du;
+      muu = fmaf(t0du, du, muu);
+      muv = fmaf(t1, du, muv);
+      mvv += t2;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -182,10 +309,10 @@ void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets, const
   count_launch();
 }
 
-void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t* start, uint32_t* end,
+void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start, uint32_t* end,
                    cudaStream_t st) {
-  if (n_pairs == 0) return;
-  k_ranges<<<blocks_for(n_pairs, 256), 256, 0, st>>>(keys, n_pairs, start, end);
+  if (n_keys == 0) return;
+  k_ranges<<<blocks_for(n_keys, 256), 256, 0, st>>>(keys, static_cast<uint32_t>(n_pairs), n_keys, start, end);
   count_launch();
 }
 
@@ -193,8 +320,9 @@ void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_
                        const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int tiles_u,
                        int tiles_v, float* images, cudaStream_t st) {
   if (n_views == 0) return;
-  dim3 grid(static_cast<unsigned>(tiles_u * tiles_v), static_cast<unsigned>(n_views));
-  k_raster_fwd<<<grid, 256, 0, st>>>(rec, vals, start, end, n, n_u, n_v, tiles_u, images);
+  const int n_tiles = tiles_u * tiles_v;
+  dim3 grid(static_cast<unsigned>((n_tiles + kFwdWarps - 1) / kFwdWarps), static_cast<unsigned>(n_views));
+  k_raster_fwd<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, tiles_u, n_tiles, images);
   count_launch();
 }
 
@@ -209,7 +337,7 @@ void launch_raster_bwd_pairs(const RasterRec* rec, int64_t n, int n_views, int n
   const int64_t want = (items + 7) / 8;  // 8 warps per block
   const unsigned blocks = static_cast<unsigned>(want < static_cast<int64_t>(sms) * 16 ? want : static_cast<int64_t>(sms) * 16);
   k_raster_bwd_pairs<<<blocks, 256, 0, st>>>(rec, items, n, n_u, n_v, grad_images,
-                                             reinterpret_cast<float4*>(moments));
+                                             reinterpret_cast<float4*>(moments), 1.0 / static_cast<double>(n));
   count_launch();
 }
 

@@ -288,14 +288,16 @@ struct Proj {
   double mean2d[2], cov2d[4], conic[4], amplitude;
   int rect[4];
   bool culled, degenerate;
-  double sigma_inv[9], ad[3], beta, mu, k, cov_px[4], d_ray[3];
+  double ad[3], beta, mu, k, cov_px[4], d_ray[3];
   double t_cam[3], jac[6], dist;
 };
 
 // detail::project_full (projector.hpp:143-236)
+// The view-independent part (det Sigma > 0 check and Sigma^-1, projector.hpp:151-156) is
+// hoisted into prepare_splat(); its results are passed in (sigma_inv, det_ok).
 __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, const double* position,
-                                             const double* cov3d, double density, const RSet& rs,
-                                             Proj& p) {
+                                             const double* cov3d, const double* sigma_inv, bool det_ok,
+                                             double density, const RSet& rs, Proj& p) {
   p.beta = 1.0;
   p.k = 1.0;
   p.mu = 0.0;
@@ -312,12 +314,10 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
   for (int k = 0; k < 6; ++k) p.jac[k] = 0.0;
   p.t_cam[0] = p.t_cam[1] = p.t_cam[2] = 0.0;
 
-  const double d3 = det3(cov3d);
-  if (!(d3 > 0.0) || !isfinite(d3)) {
+  if (!det_ok) {
     p.degenerate = true;
     return;
   }
-  inv3(cov3d, p.sigma_inv);
   const double cu = 0.5 * (g.n_u - 1);
   const double cv = 0.5 * (g.n_v - 1);
   if (!g.cone) {
@@ -392,7 +392,7 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
         p.cov_px[i * 2 + j] = acc;
       }
   }
-  mul3v(p.sigma_inv, p.d_ray, p.ad);
+  mul3v(sigma_inv, p.d_ray, p.ad);
   p.beta = dot3(p.d_ray, p.ad);
   if (!(p.beta > 0.0) || !isfinite(p.beta)) {
     p.degenerate = true;
@@ -431,16 +431,19 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
   }
 }
 
-// rasterize_backward chain rule (projector.hpp:422-474) from the pixel-loop sums.
-// gm: dL/dmean2d, gc: dL/dconic (row-major 2x2), g_amp: dL/damplitude.
+// rasterize_backward chain rule (projector.hpp:422-472) from the pixel-loop sums, up to
+// dL/dSigma: gm = dL/dmean2d, gc = dL/dconic (row-major 2x2), g_amp = dL/damplitude.
+// Outputs g_pos, g_sigma (row-major 3x3) and the gated density gradient; the map
+// dL/dSigma -> d(log_scale, raw quat) (covariance_backward, core.hpp:170-191) is linear in
+// dL/dSigma and applied once per splat to the view sum.
 __device__ __forceinline__ void raster_chain_rule(const Frame& fr, const Geo& g, const RSet& rs,
-                                                  const Act& act, const double* sigma,
-                                                  const Proj& p, double g_amp, const double* gm,
-                                                  const double* gc, double* g_pos, double* g_ls,
-                                                  double* g_q, double& g_raw) {
-  const double g_mu = act.density * p.k * g_amp;
+                                                  double density, double raw_density,
+                                                  const double* sigma, const Proj& p, double g_amp,
+                                                  const double* gm, const double* gc, double* g_pos,
+                                                  double* g_sigma, double& g_raw) {
+  const double g_mu = density * p.k * g_amp;
   const double g_rho = p.mu * p.k * g_amp;
-  const double g_k = p.mu * act.density * g_amp;
+  const double g_k = p.mu * density * g_amp;
 
   const double negc[4] = {-p.conic[0], -p.conic[1], -p.conic[2], -p.conic[3]};
   double tmp2[4], gcov[4];
@@ -575,8 +578,9 @@ __device__ __forceinline__ void raster_chain_rule(const Frame& fr, const Geo& g,
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k) g_pos[k] = gp[k];
-  g_raw = act.raw_density >= 0.0 ? g_rho : 0.0;
-  covariance_backward(act.scales, act.uq, act.raw_q, gsig, g_ls, g_q);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) g_sigma[k] = gsig[k];
+  g_raw = raw_density >= 0.0 ? g_rho : 0.0;
 }
 
 // Eigen direct_selfadjoint_eigenvalues<.,3> (SelfAdjointEigenSolver::computeDirect);
@@ -636,6 +640,36 @@ __device__ __forceinline__ double max_eig3(const double* mat) {
   if (e1 > mx) mx = e1;
   if (e2 > mx) mx = e2;
   return mx;
+}
+
+// View-independent per-splat set-up shared by every view of a call: activation
+// (core.hpp:80-97), Sigma (core.hpp:111-115) and the determinant test + Sigma^-1 of
+// project_full (projector.hpp:151-156). Symmetric matrices stored as full row-major 3x3.
+struct PreSplat {
+  double pos[3];
+  double sigma[9];
+  double sigma_inv[9];
+  double density;
+  double raw_density;
+  int det_ok;  // det Sigma > 0 and finite
+  int status;  // 0 ok, 1 non-finite parameter, 2 zero quaternion
+};
+
+__device__ __forceinline__ void prepare_splat(const double* __restrict__ pos, const double* __restrict__ ls,
+                                              const double* __restrict__ q, const double* __restrict__ raw,
+                                              int64_t i, PreSplat& s) {
+  Act a;
+  s.status = activate(pos, ls, q, raw, i, a);
+  s.det_ok = 0;
+  if (s.status) return;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) s.pos[k] = a.pos[k];
+  s.density = a.density;
+  s.raw_density = a.raw_density;
+  covariance(a.scales, a.uq, s.sigma);
+  const double d3 = det3(s.sigma);
+  s.det_ok = (d3 > 0.0) && isfinite(d3);
+  if (s.det_ok) inv3(s.sigma, s.sigma_inv);
 }
 
 struct VoxGrid {

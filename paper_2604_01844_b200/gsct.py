@@ -18,7 +18,7 @@ a GPU every compute call raises.
 from __future__ import annotations
 
 import ctypes as C
-import math
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Optional, Sequence
@@ -26,6 +26,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _LIB_PATH = Path(__file__).resolve().parent / "libgsct_b200.so"
+if os.environ.get("GSCT_LIB_PATH"):  # A/B experiments with alternative builds (tools/)
+    _LIB_PATH = Path(os.environ["GSCT_LIB_PATH"]).resolve()
 
 GSCT_OK, GSCT_ERR_CONTRACT, GSCT_ERR_CUDA, GSCT_ERR_OOM = 0, 1, 2, 3
 # enum gsct_phase (include/gsct_cuda.h)
