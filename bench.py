@@ -59,7 +59,9 @@ def make_workload(name: str, seed: int = 0):
 
 def shard_views(n_views: int, rank: int, world: int) -> list[int]:
     """View sharding: rank r owns views {v : v mod P == r}."""
-    return list(range(rank, n_views, world))
+    from paper_2604_01844_b200.sharding import shard_views as _sv
+
+    return _sv(n_views, rank, world)
 
 
 # ---------------------------------------------------------------------------------------
@@ -135,11 +137,9 @@ class DeviceStep:
         # dL/dimage: all-ones, as the reference sweep (bench.hpp:114-115)
         self.grad_images = torch.ones((nv, geom.n_v, geom.n_u), dtype=torch.float32, device=self.dev)
         # one flat fp64 buffer so a single all-reduce carries every gradient class
-        self.flat = torch.zeros(12 * n, dtype=torch.float64, device=self.dev)
-        f = self.flat
-        self.grads = gsct.ParamGradients(f[0:3 * n].view(n, 3), f[3 * n:6 * n].view(n, 3), f[6 * n:10 * n].view(n, 4),
-                                         f[10 * n:11 * n], f[11 * n:12 * n],
-                                         torch.zeros(n, dtype=torch.uint8, device=self.dev))
+        from paper_2604_01844_b200.sharding import pack_grads
+
+        self.flat, self.grads = pack_grads(n, like=self.images)
         self.stream = torch.cuda.ExternalStream(int(gsct.lib().gsct_ctx_stream(ctx.handle)), device=self.dev)
         self.rs = gsct.RasterSettings()
 
@@ -149,11 +149,10 @@ class DeviceStep:
         g.rasterize_backward_views(self.dcloud, self.geom, self.views, self.grad_images, self.rs, out=self.grads,
                                    ctx=self.ctx)
         if self.world > 1:
-            import torch.distributed as dist
+            from paper_2604_01844_b200.sharding import allreduce_grads
 
-            with self.torch.cuda.stream(self.stream):
-                dist.all_reduce(self.flat)
-                dist.all_reduce(self.grads.visible, op=dist.ReduceOp.MAX)
+            with self.torch.cuda.stream(self.stream):  # NCCL on the library's stream, no host sync
+                allreduce_grads(self.flat, self.grads.visible)
 
 
 def timed_steps(step, stream, k: int, flush) -> list[float]:

@@ -108,6 +108,15 @@ class Orc:
         if st != 0:
             raise OracleError(self.l.orc_last_error().decode())
 
+    def splat_bbox(self, g_peak, cov2d, mean2d, tau, n_u, n_v, sigma_cap=3.0, square=False):
+        """projector.hpp:101-117 -> (visible, [u_min, u_max, v_min, v_max])."""
+        cov = np.ascontiguousarray(cov2d, dtype=np.float64).reshape(4)
+        mean = np.ascontiguousarray(mean2d, dtype=np.float64)
+        rect = np.zeros(4, dtype=np.int32)
+        ok = self.l.orc_splat_bbox(C.c_double(g_peak), _p(cov), _p(mean), C.c_double(tau), int(n_u), int(n_v),
+                                   _p(rect), C.c_double(sigma_cap), 1 if square else 0)
+        return bool(ok), rect.tolist()
+
     def rasterize_view(self, cloud, geom, view: int, rs):
         p, l, q, r = _cloud_arrays(cloud)
         img = np.zeros((geom.n_v, geom.n_u))

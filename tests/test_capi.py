@@ -1,0 +1,137 @@
+"""CPU tests of the boundary and host-side logic (no compute calls without a GPU):
+libgsct_b200.so loads and exports every symbol include/gsct_cuda.h declares, the host
+harness reproduces the reference's RNG/geometry/region semantics, and the compute entry
+points fail loudly (no CPU fallback) when no device is present."""
+from __future__ import annotations
+
+import math
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, has_gpu, parallel_geometry
+from paper_2604_01844_b200 import gsct
+
+HEADER = ROOT / "include" / "gsct_cuda.h"
+
+
+def declared_functions() -> set[str]:
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(gsct_[a-z0-9_]+)\s*\(", text))
+
+
+def test_header_symbols_are_exported_and_bound():
+    names = declared_functions()
+    assert len(names) >= 30
+    lib = gsct.lib()
+    for name in sorted(names):
+        assert hasattr(lib, name), f"{name} declared in gsct_cuda.h but not exported"
+    assert names == set(gsct.exported_symbols()), names ^ set(gsct.exported_symbols())
+    assert lib.gsct_abi_version() == 1
+
+
+def test_library_is_sm100a_and_has_no_host_fallback():
+    import subprocess
+
+    so = ROOT / "paper_2604_01844_b200" / "libgsct_b200.so"
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(so)], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+    # no oracle / reference symbols in the product library
+    nm = subprocess.run(["nm", "-D", str(so)], capture_output=True, text=True).stdout
+    assert "orc_" not in nm and "ref_" not in nm
+
+
+@pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure mode")
+def test_compute_without_gpu_raises():
+    with pytest.raises(gsct.CudaError, match="no CPU fallback"):
+        gsct.Context(0)
+
+
+def test_view_frame_axis_cases():
+    """test_projector.cpp:51-67"""
+    geom = parallel_geometry(8, 1.0, [0.0, math.pi / 2])
+    f0 = gsct.view_frame(geom, 0)
+    assert np.allclose(f0["d"], [1, 0, 0]) and np.allclose(f0["u"], [0, 1, 0]) and np.allclose(f0["v"], [0, 0, 1])
+    f1 = gsct.view_frame(geom, 1)
+    assert np.allclose(f1["d"], [0, 1, 0], atol=1e-15)
+    cone = gsct.ScanGeometry("cone", 8, 8, 1.0, 1.0, [0.0], 2.0, 1.0)
+    fc = gsct.view_frame(cone, 0)
+    assert np.allclose(fc["source"], [-2, 0, 0]) and np.allclose(fc["detector_center"], [1, 0, 0])
+    assert fc["focal"] == pytest.approx(3.0)
+    with pytest.raises(gsct.ContractError, match="angle index out of range"):
+        gsct.view_frame(geom, 2)
+
+
+def test_sample_subvolume_semantics():
+    """test_voxelizer.cpp:131-180"""
+    rng = gsct.Rng(9)
+    parent = gsct.GridSpec.centered((32, 32, 32), 1.0)
+    for _ in range(5):
+        assert gsct.sample_subvolume(parent, (32, 32, 32), rng).offset == (0, 0, 0)
+    parent = gsct.GridSpec.centered((64, 64, 64), 1.0)
+    hist = np.zeros((3, 33))
+    draws = 10000
+    for _ in range(draws):
+        off = gsct.sample_subvolume(parent, (32, 32, 32), rng).offset
+        for a in range(3):
+            assert 0 <= off[a] <= 32
+            hist[a, off[a]] += 1
+    expected = draws / 33.0
+    for a in range(3):
+        assert np.sum((hist[a] - expected) ** 2 / expected) < 70.0
+    parent = gsct.GridSpec.centered((40, 40, 40), 1.0)
+    a, b = gsct.Rng(1234), gsct.Rng(1234)
+    for _ in range(10):
+        assert gsct.sample_subvolume(parent, (8, 8, 8), a).offset == gsct.sample_subvolume(parent, (8, 8, 8), b).offset
+    small = gsct.GridSpec.centered((16, 16, 16), 1.0)
+    assert gsct.sample_subvolume(small, (32, 32, 32), rng).dims == (16, 16, 16)
+
+
+def test_grid_region_contract():
+    grid = gsct.GridSpec.centered((24, 24, 24), 0.7)
+    r = gsct.GridRegion.of_parent(grid, (5, 8, 2), (10, 9, 14))
+    assert r.origin == tuple(grid.origin[a] + 0.7 * (5, 8, 2)[a] for a in range(3))
+    with pytest.raises(gsct.ContractError, match="outside parent"):
+        gsct.GridRegion.of_parent(grid, (20, 0, 0), (10, 1, 1))
+    with pytest.raises(gsct.ContractError, match="at least 1"):
+        gsct.GridRegion.of_parent(grid, (0, 0, 0), (0, 1, 1))
+
+
+def test_rng_mappings_match_reference_formulas():
+    """rng.hpp:25-54: uniform = (next >> 11) * 2^-53, Box-Muller normal, rejection uniform_int."""
+    r = gsct.Rng(0)
+    xs = np.array([r.uniform() for _ in range(20000)])
+    assert xs.min() >= 0.0 and xs.max() < 1.0 and abs(xs.mean() - 0.5) < 0.01
+    ns = np.array([r.normal() for _ in range(20000)])
+    assert abs(ns.mean()) < 0.03 and abs(ns.std() - 1.0) < 0.03
+    ks = np.array([r.uniform_int(7) for _ in range(7000)])
+    assert set(ks.tolist()) == set(range(7))
+    with pytest.raises(gsct.ContractError):
+        r.uniform_int(0)
+
+
+def test_shepp_logan_cloud():
+    c = gsct.make_cloud("shepp_logan", 5000, seed=0, side=128, spacing=1.0)
+    half = 64.0
+    p = c.positions / np.array([0.69 * half, 0.92 * half, 0.81 * half])
+    assert np.all(np.sum(p * p, axis=1) <= 1.0 + 1e-12)
+    assert np.allclose(np.linalg.norm(c.rotations, axis=1), 1.0)
+    assert c.raw_densities.min() >= 0.15 * 0.2 and c.raw_densities.max() <= 0.15
+    c2 = gsct.make_cloud("shepp_logan", 5000, seed=0, side=128, spacing=1.0)
+    assert np.array_equal(c.positions, c2.positions)
+
+
+def test_cloud_lockstep_and_param_gradients_add():
+    with pytest.raises(gsct.ContractError, match="lockstep"):
+        gsct.GaussianCloud(np.zeros((2, 3)), np.zeros((2, 3)), np.zeros((2, 4)), np.zeros(3))
+    a = gsct.ParamGradients.zeros(3)
+    b = gsct.ParamGradients.zeros(3)
+    b.positions[1] = [1, 2, 3]
+    b.visible[2] = 1
+    a.add(b)
+    assert np.array_equal(a.positions[1], [1, 2, 3]) and a.visible.tolist() == [0, 0, 1]
+    with pytest.raises(gsct.ContractError):
+        a.add(gsct.ParamGradients.zeros(4))
