@@ -1,0 +1,274 @@
+// gsct_b200.hpp — the reference's C++ operator API (namespace gsct) implemented on the
+// B200 C ABI (include/gsct_cuda.h, libgsct_b200.so).
+//
+// Include AFTER the reference's "gsct/projector.hpp" and "gsct/voxelizer.hpp" (this header
+// uses their types: GaussianCloud, ScanGeometry, Image, Volume, GridRegion, GridSpec,
+// RasterSettings, VoxelSettings, RenderStats, ParamGradients, contract_error). It defines,
+// in namespace gsct::b200, functions with exactly the reference signatures:
+//
+//   Image          rasterize_view    (cloud, geometry, angle_index, settings, stats)  projector.hpp:308-310
+//   ParamGradients rasterize_backward(cloud, geometry, angle_index, grad_image, ...) projector.hpp:371-375
+//   Volume         voxelize          (cloud, region, settings, stats)                 voxelizer.hpp:162-163
+//   Volume         voxelize_full     (cloud, grid, settings, stats)                   voxelizer.hpp:203-206
+//   ParamGradients voxelize_backward (cloud, region, grad_volume, settings, stats)    voxelizer.hpp:214-217
+//
+// plus batched forms (rasterize_views / rasterize_backward_views: many views per call,
+// gradients summed in view order as ParamGradients::add). Semantics: inputs are validated
+// like the reference (contract_error with the reference's messages), outputs are fresh
+// by-value containers, RenderStats accumulate with +=, calls are synchronous. Images and
+// volumes come back from fp32 device buffers widened to double; gradients are fp64.
+//
+// For a drop-in of the unchanged reference loops (optim.hpp, bench.hpp, CLI) include
+// gsct_b200_dropin.hpp first instead (it renames the CPU operators to *_cpu and exposes
+// these under the original names).
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gsct_cuda.h"
+
+namespace gsct {
+namespace b200 {
+
+// One context per thread and device (the C ABI context is single-threaded).
+class Device {
+ public:
+  static gsct_ctx ctx(int device = -1) {
+    thread_local Device d;
+    if (device >= 0 && device != d.device_) d.reset(device);
+    if (!d.ctx_) d.reset(d.device_ < 0 ? 0 : d.device_);
+    return d.ctx_;
+  }
+  ~Device() {
+    if (ctx_) gsct_ctx_destroy(ctx_);
+  }
+
+ private:
+  void reset(int device) {
+    if (ctx_) gsct_ctx_destroy(ctx_);
+    ctx_ = nullptr;
+    device_ = device;
+    if (gsct_ctx_create(device, &ctx_) != GSCT_OK)
+      throw error("gsct::b200: no usable CUDA device " + std::to_string(device) + " (no CPU fallback)");
+  }
+  gsct_ctx ctx_ = nullptr;
+  int device_ = -1;
+};
+
+namespace detail {
+
+inline void check_status(gsct_ctx c, int status) {
+  if (status == GSCT_OK) return;
+  const std::string msg = gsct_ctx_last_error(c);
+  if (status == GSCT_ERR_CONTRACT) throw contract_error(msg);
+  throw error("gsct::b200: " + msg);
+}
+
+// GaussianCloud stores std::vector<Vec3/Vec4>: fixed-size Eigen vectors are dense doubles
+// (24 / 32 bytes), so the vectors are used in place as AoS double arrays (no copy).
+inline gsct_cloud c_cloud(const GaussianCloud& cloud) {
+  cloud.validate();
+  static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be 3 dense doubles");
+  static_assert(sizeof(Vec4) == 4 * sizeof(double), "Vec4 must be 4 dense doubles");
+  gsct_cloud c;
+  c.n = static_cast<int64_t>(cloud.size());
+  c.pos = reinterpret_cast<const double*>(cloud.positions.data());
+  c.log_scale = reinterpret_cast<const double*>(cloud.log_scales.data());
+  c.quat = reinterpret_cast<const double*>(cloud.rotations.data());
+  c.raw_density = cloud.raw_densities.data();
+  c.location = GSCT_HOST;
+  return c;
+}
+
+inline gsct_geometry c_geometry(const ScanGeometry& g) {
+  gsct_geometry c;
+  c.cone = g.mode == BeamMode::cone ? 1 : 0;
+  c.n_u = g.n_u;
+  c.n_v = g.n_v;
+  c.s_u = g.s_u;
+  c.s_v = g.s_v;
+  c.source_to_origin = g.source_to_origin;
+  c.origin_to_detector = g.origin_to_detector;
+  return c;
+}
+
+inline gsct_raster_settings c_raster(const RasterSettings& s) {
+  gsct_raster_settings c;
+  c.tau_cut = s.tau_cut;
+  c.sigma_cap = s.sigma_cap;
+  c.dilation_px2 = s.dilation_px2;
+  c.tile_size = s.tile_size;
+  c.dilate = s.dilate ? 1 : 0;
+  c.bounding = s.bounding == BoundingMode::square_circumscribed ? 1 : 0;
+  return c;
+}
+
+inline gsct_voxel_settings c_voxel(const VoxelSettings& s) { return gsct_voxel_settings{s.tau_cut, s.sigma_cap}; }
+
+inline gsct_grid c_grid(const std::array<int, 3>& dims, double spacing, const Vec3& origin) {
+  gsct_grid g;
+  for (int a = 0; a < 3; ++a) {
+    g.dims[a] = dims[a];
+    g.origin[a] = origin[a];
+  }
+  g.spacing = spacing;
+  return g;
+}
+
+inline void take_stats(const gsct_stats& s, RenderStats* stats) {
+  if (!stats) return;
+  stats->culled = s.culled;
+  stats->degenerate = s.degenerate;
+  stats->tile_pairs = s.tile_pairs;
+  stats->pixel_pairs = s.pixel_pairs;
+  stats->forward_ms = s.forward_ms;
+  stats->backward_ms = s.backward_ms;
+}
+
+inline gsct_stats put_stats(const RenderStats* stats) {
+  gsct_stats s{};
+  if (stats) {
+    s.culled = stats->culled;
+    s.degenerate = stats->degenerate;
+    s.tile_pairs = stats->tile_pairs;
+    s.pixel_pairs = stats->pixel_pairs;
+    s.forward_ms = stats->forward_ms;
+    s.backward_ms = stats->backward_ms;
+  }
+  return s;
+}
+
+struct GradBuffers {
+  ParamGradients g;
+  gsct_grads c;
+  explicit GradBuffers(std::size_t n) {
+    g.resize(n);
+    c.pos = reinterpret_cast<double*>(g.positions.data());
+    c.log_scale = reinterpret_cast<double*>(g.log_scales.data());
+    c.quat = reinterpret_cast<double*>(g.rotations.data());
+    c.raw_density = g.raw_densities.data();
+    c.pos_grad_norm = g.pos_grad_norm.data();
+    c.visible = g.visible.data();
+    c.location = GSCT_HOST;
+  }
+};
+
+}  // namespace detail
+
+// Batched forward: images of angle_indices (all views when empty).
+inline std::vector<Image> rasterize_views(const GaussianCloud& cloud, const ScanGeometry& geometry,
+                                          const std::vector<std::size_t>& angle_indices,
+                                          const RasterSettings& settings = {}, RenderStats* stats = nullptr) {
+  geometry.validate();
+  std::vector<double> angles;
+  for (std::size_t v : angle_indices) {
+    check(v < geometry.angles.size(), "view_frame: angle index out of range");
+    angles.push_back(geometry.angles[v]);
+  }
+  gsct_ctx c = Device::ctx();
+  const gsct_cloud cc = detail::c_cloud(cloud);
+  const gsct_geometry cg = detail::c_geometry(geometry);
+  const gsct_raster_settings rs = detail::c_raster(settings);
+  const std::size_t npx = static_cast<std::size_t>(geometry.n_u) * geometry.n_v;
+  std::vector<float> buf(npx * angles.size());
+  gsct_stats st = detail::put_stats(stats);
+  detail::check_status(c, gsct_rasterize_fwd(c, &cc, &cg, angles.data(), static_cast<int>(angles.size()), &rs,
+                                              buf.data(), GSCT_HOST, stats ? &st : nullptr));
+  detail::take_stats(st, stats);
+  std::vector<Image> out(angles.size());
+  for (std::size_t v = 0; v < angles.size(); ++v) {
+    out[v] = Image::zeros(geometry.n_u, geometry.n_v);
+    for (std::size_t k = 0; k < npx; ++k) out[v].values[k] = buf[v * npx + k];
+  }
+  return out;
+}
+
+// gsct::rasterize_view (projector.hpp:308-360)
+inline Image rasterize_view(const GaussianCloud& cloud, const ScanGeometry& geometry, std::size_t angle_index,
+                            const RasterSettings& settings = {}, RenderStats* stats = nullptr) {
+  return rasterize_views(cloud, geometry, {angle_index}, settings, stats)[0];
+}
+
+// Batched backward: sum over the views (ascending) of rasterize_backward.
+inline ParamGradients rasterize_backward_views(const GaussianCloud& cloud, const ScanGeometry& geometry,
+                                               const std::vector<std::size_t>& angle_indices,
+                                               const std::vector<const Image*>& grad_images,
+                                               const RasterSettings& settings = {}, RenderStats* stats = nullptr) {
+  check(grad_images.size() == angle_indices.size(), "rasterize_backward: one grad image per view");
+  std::vector<double> angles;
+  const std::size_t npx = static_cast<std::size_t>(geometry.n_u) * geometry.n_v;
+  std::vector<float> gi(npx * angle_indices.size());
+  for (std::size_t k = 0; k < angle_indices.size(); ++k) {
+    check(grad_images[k]->n_u == geometry.n_u && grad_images[k]->n_v == geometry.n_v,
+          "rasterize_backward: grad image dims must match detector");
+    check(angle_indices[k] < geometry.angles.size(), "view_frame: angle index out of range");
+    angles.push_back(geometry.angles[angle_indices[k]]);
+    for (std::size_t p = 0; p < npx; ++p) gi[k * npx + p] = static_cast<float>(grad_images[k]->values[p]);
+  }
+  gsct_ctx c = Device::ctx();
+  const gsct_cloud cc = detail::c_cloud(cloud);
+  const gsct_geometry cg = detail::c_geometry(geometry);
+  const gsct_raster_settings rs = detail::c_raster(settings);
+  detail::GradBuffers gb(cloud.size());
+  gsct_stats st = detail::put_stats(stats);
+  detail::check_status(c, gsct_rasterize_bwd(c, &cc, &cg, angles.data(), static_cast<int>(angles.size()), &rs,
+                                              gi.data(), GSCT_HOST, &gb.c, stats ? &st : nullptr));
+  detail::take_stats(st, stats);
+  return gb.g;
+}
+
+// gsct::rasterize_backward (projector.hpp:371-482)
+inline ParamGradients rasterize_backward(const GaussianCloud& cloud, const ScanGeometry& geometry,
+                                         std::size_t angle_index, const Image& grad_image,
+                                         const RasterSettings& settings = {}, RenderStats* stats = nullptr) {
+  check(grad_image.n_u == geometry.n_u && grad_image.n_v == geometry.n_v,
+        "rasterize_backward: grad image dims must match detector");
+  return rasterize_backward_views(cloud, geometry, {angle_index}, {&grad_image}, settings, stats);
+}
+
+// gsct::voxelize (voxelizer.hpp:162-199)
+inline Volume voxelize(const GaussianCloud& cloud, const GridRegion& region, const VoxelSettings& settings = {},
+                       RenderStats* stats = nullptr) {
+  gsct_ctx c = Device::ctx();
+  const gsct_cloud cc = detail::c_cloud(cloud);
+  const gsct_grid g = detail::c_grid(region.dims, region.spacing, region.origin);
+  const gsct_voxel_settings vs = detail::c_voxel(settings);
+  Volume out = Volume::zeros(region.dims, region.spacing, region.origin);
+  std::vector<float> buf(out.values.size());
+  gsct_stats st = detail::put_stats(stats);
+  detail::check_status(c, gsct_voxelize_fwd(c, &cc, &g, nullptr, &vs, buf.data(), GSCT_HOST, stats ? &st : nullptr));
+  detail::take_stats(st, stats);
+  for (std::size_t k = 0; k < buf.size(); ++k) out.values[k] = buf[k];
+  return out;
+}
+
+// gsct::voxelize_full (voxelizer.hpp:203-206)
+inline Volume voxelize_full(const GaussianCloud& cloud, const GridSpec& grid, const VoxelSettings& settings = {},
+                            RenderStats* stats = nullptr) {
+  return voxelize(cloud, GridRegion::covering(grid), settings, stats);
+}
+
+// gsct::voxelize_backward (voxelizer.hpp:214-263)
+inline ParamGradients voxelize_backward(const GaussianCloud& cloud, const GridRegion& region,
+                                        const Volume& grad_volume, const VoxelSettings& settings = {},
+                                        RenderStats* stats = nullptr) {
+  check(grad_volume.dims == region.dims, "voxelize_backward: grad dims must match region");
+  gsct_ctx c = Device::ctx();
+  const gsct_cloud cc = detail::c_cloud(cloud);
+  const gsct_grid g = detail::c_grid(region.dims, region.spacing, region.origin);
+  const gsct_voxel_settings vs = detail::c_voxel(settings);
+  std::vector<float> gv(grad_volume.values.size());
+  for (std::size_t k = 0; k < gv.size(); ++k) gv[k] = static_cast<float>(grad_volume.values[k]);
+  detail::GradBuffers gb(cloud.size());
+  gsct_stats st = detail::put_stats(stats);
+  detail::check_status(c, gsct_voxelize_bwd(c, &cc, &g, nullptr, &vs, gv.data(), GSCT_HOST, &gb.c,
+                                             stats ? &st : nullptr));
+  detail::take_stats(st, stats);
+  return gb.g;
+}
+
+}  // namespace b200
+}  // namespace gsct
