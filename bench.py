@@ -142,6 +142,8 @@ class DeviceStep:
         self.flat, self.grads = pack_grads(n, like=self.images)
         self.stream = torch.cuda.ExternalStream(int(gsct.lib().gsct_ctx_stream(ctx.handle)), device=self.dev)
         self.rs = gsct.RasterSettings()
+        # training-loop usage: the backward reuses the forward's set-up (same cloud)
+        ctx.set_save_for_backward(True)
 
     def __call__(self):
         g = self.gsct

@@ -125,6 +125,12 @@ void* gsct_ctx_stream(gsct_ctx ctx);
 /* async != 0: calls only enqueue work (no host sync, no *_ms timing); device-side
  * stats/errors are collected by gsct_ctx_synchronize. Default: synchronous (reference). */
 int gsct_ctx_set_async(gsct_ctx ctx, int async);
+/* save != 0: gsct_rasterize_fwd keeps its per-(view, splat) set-up records and the next
+ * gsct_rasterize_bwd called with the same cloud pointers/size, geometry, angles and
+ * settings reuses them instead of recomputing (autograd-style saved state). The caller
+ * guarantees the cloud contents did not change in between. Default 0: every call
+ * recomputes, as the reference does (projector.hpp:393). */
+int gsct_ctx_set_save_for_backward(gsct_ctx ctx, int save);
 int gsct_ctx_synchronize(gsct_ctx ctx, gsct_stats* stats_accum);
 /* Bytes of device workspace currently held (grow-only arena). */
 size_t gsct_ctx_workspace_bytes(gsct_ctx ctx);

@@ -24,7 +24,8 @@ namespace {
 enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
-  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_ACC, S_COUNT_SLOTS
+  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_ACC, S_SAVED,
+  S_COUNT_SLOTS
 };
 
 struct Buf {
@@ -62,6 +63,10 @@ struct gsct_ctx_s {
   std::vector<Mark> marks;
   double phase_ms[GSCT_NUM_PHASES] = {};
   int64_t phase_count[GSCT_NUM_PHASES] = {};
+  // save-for-backward: forward set-up records kept for the matching backward call
+  bool save_fb = false;
+  bool saved_valid = false;
+  std::string saved_key;
 };
 
 namespace gsct_dev {
@@ -315,6 +320,36 @@ int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32
   return total;
 }
 
+// Identity of a rasterizer call for save-for-backward: cloud buffers and size, geometry,
+// angles and settings, field by field (no struct padding).
+std::string raster_call_key(const gsct_cloud* cl, const gsct_geometry* g, const double* angles, int n_views,
+                            const gsct_raster_settings* rs) {
+  std::string k;
+  auto put = [&k](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+  put(&cl->n, sizeof cl->n);
+  put(&cl->pos, sizeof cl->pos);
+  put(&cl->log_scale, sizeof cl->log_scale);
+  put(&cl->quat, sizeof cl->quat);
+  put(&cl->raw_density, sizeof cl->raw_density);
+  put(&cl->location, sizeof cl->location);
+  put(&g->cone, sizeof g->cone);
+  put(&g->n_u, sizeof g->n_u);
+  put(&g->n_v, sizeof g->n_v);
+  put(&g->s_u, sizeof g->s_u);
+  put(&g->s_v, sizeof g->s_v);
+  put(&g->source_to_origin, sizeof g->source_to_origin);
+  put(&g->origin_to_detector, sizeof g->origin_to_detector);
+  put(&n_views, sizeof n_views);
+  if (n_views > 0) put(angles, sizeof(double) * static_cast<size_t>(n_views));
+  put(&rs->tau_cut, sizeof rs->tau_cut);
+  put(&rs->sigma_cap, sizeof rs->sigma_cap);
+  put(&rs->dilation_px2, sizeof rs->dilation_px2);
+  put(&rs->tile_size, sizeof rs->tile_size);
+  put(&rs->dilate, sizeof rs->dilate);
+  put(&rs->bounding, sizeof rs->bounding);
+  return k;
+}
+
 // Views per chunk: bounded (view, splat) items, and view*n_tiles + tile keys of at most
 // 16 bits so the stable radix sort needs two 8-bit passes.
 int views_per_chunk(int64_t n, int n_views, int64_t n_tiles) {
@@ -446,6 +481,13 @@ size_t gsct_ctx_workspace_bytes(gsct_ctx c) {
 
 int64_t gsct_ctx_launch_count(gsct_ctx c) { return c ? c->launches : 0; }
 
+int gsct_ctx_set_save_for_backward(gsct_ctx c, int save) {
+  return run(c, [&] {
+    c->save_fb = save != 0;
+    c->saved_valid = false;
+  });
+}
+
 int gsct_ctx_set_profiling(gsct_ctx c, int on) {
   return run(c, [&] {
     resolve_marks(c);
@@ -502,11 +544,14 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (images_location == GSCT_HOST && n_views) out = ws<float>(c, S_IMAGES, static_cast<size_t>(npx) * n_views);
     const Geo g = make_geo(geom);
     const RSet r = make_rs(rs);
+    c->saved_valid = false;
     PreSplat* pre = ws<PreSplat>(c, S_PRE, static_cast<size_t>(n) + 1);
     if (n > 0) {
       Phase ph(c, GSCT_PH_RASTER_SETUP);
       launch_splat_prepare(d, pre, c->dstats, c->stream);
     }
+    // save-for-backward keeps every view's records in one buffer for the backward call
+    RasterRec* saved = c->save_fb && n > 0 ? ws<RasterRec>(c, S_SAVED, static_cast<size_t>(n) * n_views) : nullptr;
     int chunk = views_per_chunk(n, n_views, n_tiles);
     for (int v0 = 0; v0 < n_views; v0 += chunk) {
       const int cv = std::min(chunk, n_views - v0);
@@ -515,7 +560,7 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         CK(cudaMemsetAsync(img, 0, static_cast<size_t>(npx) * cv * sizeof(float), c->stream));
         continue;
       }
-      RasterRec* rec = ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * cv);
+      RasterRec* rec = saved ? saved + static_cast<int64_t>(v0) * n : ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * cv);
       uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * cv);
       {
         Phase ph(c, GSCT_PH_RASTER_SETUP);
@@ -542,6 +587,10 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (images_location == GSCT_HOST && n_views)
       CK(cudaMemcpyAsync(images, out, static_cast<size_t>(npx) * n_views * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
+    if (saved) {
+      c->saved_key = raster_call_key(cloud, geom, angles, n_views, rs);
+      c->saved_valid = true;
+    }
   });
 }
 
@@ -586,12 +635,16 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
     const Geo g = make_geo(geom);
     const RSet r = make_rs(rs);
+    // reuse the forward's set-up (PreSplat + records) when save-for-backward matched
+    const bool reuse = c->save_fb && c->saved_valid && n > 0 &&
+                       c->saved_key == raster_call_key(cloud, geom, angles, n_views, rs);
     PreSplat* pre = ws<PreSplat>(c, S_PRE, un + 1);
     double* acc = ws<double>(c, S_ACC, 11 * un + 1);
-    if (n > 0) {
+    if (n > 0 && !reuse) {
       Phase ph(c, GSCT_PH_RASTER_SETUP);
       launch_splat_prepare(d, pre, c->dstats, c->stream);
     }
+    RasterRec* saved = reuse ? ws<RasterRec>(c, S_SAVED, un * n_views) : nullptr;
     const int tiles_u = (geom->n_u + kTile - 1) / kTile, tiles_v = (geom->n_v + kTile - 1) / kTile;
     const int chunk = views_per_chunk(n, n_views, static_cast<int64_t>(tiles_u) * tiles_v);
     for (int v0 = 0; v0 < n_views && n > 0; v0 += chunk) {
@@ -602,8 +655,8 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         CK(cudaMemcpyAsync(dst, gimg, static_cast<size_t>(npx) * cv * sizeof(float), cudaMemcpyHostToDevice, c->stream));
         gimg = dst;
       }
-      RasterRec* rec = ws<RasterRec>(c, S_REC, un * cv);
-      {
+      RasterRec* rec = reuse ? saved + static_cast<int64_t>(v0) * n : ws<RasterRec>(c, S_REC, un * cv);
+      if (!reuse) {
         Phase ph(c, GSCT_PH_RASTER_SETUP);
         launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kTile, rec, nullptr, c->dstats, c->stream);
       }
@@ -686,9 +739,29 @@ void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window
     launch_voxel_preprocess(d, grid, win, vs->tau_cut, vs->sigma_cap, rec, nullptr, nullptr, nullptr,
                             nullptr, c->dstats, c->stream);
   }
+  // spatial walk order: sort splats by the 8^3 brick of their box corner
+  uint32_t* order = nullptr;
+  {
+    Phase ph(c, GSCT_PH_VOXEL_BIN);
+    const int nbx = (win.hi[0] - win.lo[0] + kBrick - 1) / kBrick;
+    const int nby = (win.hi[1] - win.lo[1] + kBrick - 1) / kBrick;
+    const int nbz = (win.hi[2] - win.lo[2] + kBrick - 1) / kBrick;
+    uint32_t* k1 = ws<uint32_t>(c, S_KEYS, static_cast<size_t>(n));
+    uint32_t* v1 = ws<uint32_t>(c, S_VALS, static_cast<size_t>(n));
+    uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, static_cast<size_t>(n));
+    uint32_t* v2 = ws<uint32_t>(c, S_VALS2, static_cast<size_t>(n));
+    launch_voxel_order_keys(rec, n, win, nbx, nby, k1, v1, c->stream);
+    cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
+    const int end_bit = bits_for(static_cast<uint64_t>(nbx) * nby * nbz + 1);
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(n), 0, end_bit, c->stream));
+    void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(n), 0, end_bit, c->stream));
+    order = vb.Current();
+  }
   {
     Phase ph(c, GSCT_PH_VOXEL_BWD);
-    launch_voxel_bwd_pairs(rec, n, win, static_cast<float>(grid.spacing), grad, mom, nullptr, c->stream);
+    launch_voxel_bwd_pairs(rec, order, n, win, static_cast<float>(grid.spacing), grad, mom, c->stream);
   }
   CK(cudaGetLastError());
 }
@@ -855,6 +928,7 @@ int gsct_debug_project(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     double* dmean = ws<double>(c, S_DBG2, 2 * un);
     double* dconic = ws<double>(c, S_DBG3, 4 * un);
     double* damp = ws<double>(c, S_DBG4, un);
+    c->saved_valid = false;  // S_PRE is reused below
     PreSplat* pre = ws<PreSplat>(c, S_PRE, un);
     launch_splat_prepare(d, pre, c->dstats, c->stream);
     launch_debug_project(pre, d.n, df, make_geo(geom), make_rs(rs), drect, dflags, dmean, dconic, damp,
@@ -892,6 +966,7 @@ int gsct_debug_tile_pairs(gsct_ctx c, const gsct_cloud* cloud, const gsct_geomet
     CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
     RasterRec* rec = ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * n_views);
     uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * n_views);
+    c->saved_valid = false;  // S_PRE / S_REC are reused below
     PreSplat* pre = ws<PreSplat>(c, S_PRE, static_cast<size_t>(n));
     launch_splat_prepare(d, pre, c->dstats, c->stream);
     launch_raster_preprocess(pre, n, dframes, n_views, make_geo(geom), make_rs(rs), ts, rec, cnt, c->dstats,

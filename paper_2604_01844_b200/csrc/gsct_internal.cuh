@@ -97,9 +97,11 @@ void launch_emit_brick_pairs(const VoxelRec* rec, const uint32_t* offsets,
 void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t* start,
                       const uint32_t* end, const Window& win, int nbx, int nby, int nbz,
                       float spacing, float* volume, cudaStream_t st);
-void launch_voxel_bwd_pairs(const VoxelRec* rec, int64_t n, const Window& win, float spacing,
-                            const float* grad_volume, float* moments, unsigned int* work_counter,
-                            cudaStream_t st);
+void launch_voxel_order_keys(const VoxelRec* rec, int64_t n, const Window& win, int nbx, int nby,
+                             uint32_t* keys, uint32_t* vals, cudaStream_t st);
+// order: splat walk order (a permutation of [0, n)) or nullptr for index order
+void launch_voxel_bwd_pairs(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
+                            float spacing, const float* grad_volume, float* moments, cudaStream_t st);
 
 // Launch accounting (gsct_ctx_launch_count).
 extern thread_local int64_t* g_launch_counter;

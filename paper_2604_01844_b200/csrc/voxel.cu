@@ -21,6 +21,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __global__ void k_emit_brick_pairs(const VoxelRec* __restrict__ rec,
                                    const uint32_t* __restrict__ offsets,
                                    const uint32_t* __restrict__ counts, int64_t n, Window win,
@@ -112,10 +118,27 @@ __global__ void __launch_bounds__(256) k_voxel_fwd(const VoxelRec* __restrict__ 
   }
 }
 
-// One warp per splat, grid-stride. Lanes walk the (window-clipped) box x-fastest in steps
-// of 32 voxels. Moments of t = exp(-q/2) * w with world-unit offsets d:
-// {t, t dx, t dy, t dz, t dx^2, t dy^2, t dz^2, t dx dy, t dx dz, t dy dz}.
+// Spatial walk order for the backward: key = 8^3 brick of the splat's (window-clipped) box
+// corner, value = splat; sorted, consecutive warps then own nearby splats, so the grad
+// volume is re-read from L2 instead of HBM (the walk order does not change any result:
+// every splat's sums are owned by one warp).
+__global__ void k_voxel_order_keys(const VoxelRec* __restrict__ rec, int64_t n, Window win, int nbx, int nby,
+                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const VoxelRec r = rec[i];
+  const int x = max(static_cast<int>(r.lox), win.lo[0]) - win.lo[0];
+  const int y = max(static_cast<int>(r.loy), win.lo[1]) - win.lo[1];
+  const int z = max(static_cast<int>(r.loz), win.lo[2]) - win.lo[2];
+  keys[i] = static_cast<uint32_t>(((z / kBrick) * nby + (y / kBrick)) * nbx + (x / kBrick));
+  vals[i] = static_cast<uint32_t>(i);
+}
+
+// One warp per splat, grid-stride over the spatial walk order. Lanes walk the
+// (window-clipped) box x-fastest in steps of 32 voxels. Moments of t = exp(-q/2) * w with
+// world-unit offsets d: {t, t dx, t dy, t dz, t dx^2, t dy^2, t dz^2, t dx dy, t dx dz, t dy dz}.
 __global__ void __launch_bounds__(256) k_voxel_bwd_pairs(const VoxelRec* __restrict__ rec,
+                                                         const uint32_t* __restrict__ order,
                                                          int64_t n, Window win, float sp,
                                                          const float* __restrict__ grad,
                                                          float* __restrict__ mom) {
@@ -123,7 +146,8 @@ __global__ void __launch_bounds__(256) k_voxel_bwd_pairs(const VoxelRec* __restr
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int wx = win.hi[0] - win.lo[0], wy = win.hi[1] - win.lo[1];
-  for (int64_t i = warp; i < n; i += n_warps) {
+  for (int64_t k = warp; k < n; k += n_warps) {
+    const int64_t i = order ? static_cast<int64_t>(order[k]) : k;
     const VoxelRec r = rec[i];
     // grid-clipped box of the record, clipped again to the window for iteration
     const int x0 = max(static_cast<int>(r.lox), win.lo[0]), y0 = max(static_cast<int>(r.loy), win.lo[1]),
@@ -135,46 +159,66 @@ __global__ void __launch_bounds__(256) k_voxel_bwd_pairs(const VoxelRec* __restr
     // offsets are relative to the record's (grid-clipped) corner
     const float bx = static_cast<float>(x0) - r.lox, by = static_cast<float>(y0) - r.loy,
                 bz = static_cast<float>(z0) - r.loz;
-    const int WH = W * H;
-    const int nvox = WH * D;
-    // lane start position and the per-step increment (32 voxels) in (x, y, z)
-    int px = lane % W, py = (lane / W) % H, pz = lane / WH;
-    const int sx = 32 % W, sy = (32 / W) % H, sz = 32 / WH;
+    // per-item base of the grad window at the box corner (32-bit offsets below)
+    const float* __restrict__ g0 =
+        grad + (static_cast<int64_t>(z0 - win.lo[2]) * wy + (y0 - win.lo[1])) * wx + (x0 - win.lo[0]);
+    const uint32_t zstride = static_cast<uint32_t>(wy * wx);
     float m[10];
 #pragma unroll
     for (int k = 0; k < 10; ++k) m[k] = 0.f;
-    for (int p = lane; p < nvox; p += 32) {
-      const int gx = x0 + px, gy = y0 + py, gz = z0 + pz;
-      const float w = __ldg(grad + (static_cast<int64_t>(gz - win.lo[2]) * wy + (gy - win.lo[1])) * wx +
-                            (gx - win.lo[0]));
-      const float dx = fmaf(bx + static_cast<float>(px), sp, -r.offx);
-      const float dy = fmaf(by + static_cast<float>(py), sp, -r.offy);
-      const float dz = fmaf(bz + static_cast<float>(pz), sp, -r.offz);
-      const float ex2 = fmaf(dx, fmaf(r.Q00, dx, fmaf(r.Q01, dy, r.Q02 * dz)),
-                             fmaf(dy, fmaf(r.Q11, dy, r.Q12 * dz), r.Q22 * dz * dz));
-      const float tt = ex2_approx(ex2) * w;
-      const float tx = tt * dx, ty = tt * dy, tz = tt * dz;
-      m[0] += tt;
-      m[1] += tx;
-      m[2] += ty;
-      m[3] += tz;
-      m[4] = fmaf(tx, dx, m[4]);
-      m[5] = fmaf(ty, dy, m[5]);
-      m[6] = fmaf(tz, dz, m[6]);
-      m[7] = fmaf(tx, dy, m[7]);
-      m[8] = fmaf(tx, dz, m[8]);
-      m[9] = fmaf(ty, dz, m[9]);
-      px += sx;
-      py += sy;
-      pz += sz;
-      if (px >= W) {
-        px -= W;
-        py += 1;
+    // Lanes = box columns (blocks of <= 32) x row groups over the H*D (y, z) rows: dx is
+    // lane-constant, so per voxel only {t, t dy, t dz, t dy^2, t dz^2, t dy dz} are
+    // accumulated and folded with dx once per column block.
+    for (int cb = 0; cb < W; cb += 32) {
+      const int cw = min(32, W - cb);
+      const float rc = rcp_approx(static_cast<float>(cw));
+      const int G = static_cast<int>(32.5f * rc);  // floor(32 / cw), exact
+      const int grp = static_cast<int>((static_cast<float>(lane) + 0.5f) * rc);
+      const int col = lane - grp * cw;
+      if (grp >= G) continue;
+      const float dx = fmaf(bx + static_cast<float>(cb + col), sp, -r.offx);
+      const float ax = r.Q00 * dx * dx, b1 = r.Q01 * dx, b2 = r.Q02 * dx;
+      const float fG = static_cast<float>(G);
+      const uint32_t ystride = static_cast<uint32_t>(G * wx);
+      float t0 = 0.f, ty_ = 0.f, tz_ = 0.f, tyy = 0.f, tzz = 0.f, tyz = 0.f;
+      for (int zz = 0; zz < D; ++zz) {
+        const float dz = fmaf(bz + static_cast<float>(zz), sp, -r.offz);
+        // per z-slice terms of the quadratic: e = dy (Q11 dy + Q12 dz + Q01 dx) + [dz (Q22 dz + Q02 dx) + Q00 dx^2]
+        const float cy = fmaf(r.Q12, dz, b1);
+        const float cz = fmaf(dz, fmaf(r.Q22, dz, b2), ax);
+        uint32_t off = static_cast<uint32_t>(zz) * zstride + static_cast<uint32_t>(grp * wx + cb + col);
+        float dy = fmaf(by + static_cast<float>(grp), sp, -r.offy);
+        const float ddy = fG * sp;
+        // rows grp, grp + G, ... < H of this slice; four grad loads in flight per step
+        for (int yy = grp; yy < H; yy += 4 * G) {
+          float w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) w[k] = (yy + k * G < H) ? __ldg(g0 + (off + k * ystride)) : 0.f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float tt = ex2_approx(fmaf(dy, fmaf(r.Q11, dy, cy), cz)) * w[k];  // w = 0 past the box
+            t0 += tt;
+            const float ty = tt * dy, tz = tt * dz;
+            ty_ += ty;
+            tz_ += tz;
+            tyy = fmaf(ty, dy, tyy);
+            tzz = fmaf(tz, dz, tzz);
+            tyz = fmaf(ty, dz, tyz);
+            dy += ddy;
+          }
+          off += 4 * ystride;
+        }
       }
-      if (py >= H) {
-        py -= H;
-        pz += 1;
-      }
+      m[0] += t0;
+      m[1] = fmaf(t0, dx, m[1]);
+      m[2] += ty_;
+      m[3] += tz_;
+      m[4] = fmaf(t0 * dx, dx, m[4]);
+      m[5] += tyy;
+      m[6] += tzz;
+      m[7] = fmaf(ty_, dx, m[7]);
+      m[8] = fmaf(tz_, dx, m[8]);
+      m[9] += tyz;
     }
 #pragma unroll
     for (int k = 0; k < 10; ++k) {
@@ -214,16 +258,22 @@ void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t*
   count_launch();
 }
 
-void launch_voxel_bwd_pairs(const VoxelRec* rec, int64_t n, const Window& win, float spacing,
-                            const float* grad_volume, float* moments, unsigned int* /*work*/,
-                            cudaStream_t st) {
+void launch_voxel_order_keys(const VoxelRec* rec, int64_t n, const Window& win, int nbx, int nby,
+                             uint32_t* keys, uint32_t* vals, cudaStream_t st) {
+  if (n == 0) return;
+  k_voxel_order_keys<<<blocks_for(n, 256), 256, 0, st>>>(rec, n, win, nbx, nby, keys, vals);
+  count_launch();
+}
+
+void launch_voxel_bwd_pairs(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
+                            float spacing, const float* grad_volume, float* moments, cudaStream_t st) {
   if (n == 0) return;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = (n + 7) / 8;
   const unsigned blocks = static_cast<unsigned>(want < static_cast<int64_t>(sms) * 16 ? want : static_cast<int64_t>(sms) * 16);
-  k_voxel_bwd_pairs<<<blocks, 256, 0, st>>>(rec, n, win, spacing, grad_volume, moments);
+  k_voxel_bwd_pairs<<<blocks, 256, 0, st>>>(rec, order, n, win, spacing, grad_volume, moments);
   count_launch();
 }
 

@@ -102,6 +102,7 @@ _SIGS = {
     "gsct_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gsct_ctx_stream": (C.c_void_p, [C.c_void_p]),
     "gsct_ctx_set_async": (C.c_int, [C.c_void_p, C.c_int]),
+    "gsct_ctx_set_save_for_backward": (C.c_int, [C.c_void_p, C.c_int]),
     "gsct_ctx_synchronize": (C.c_int, [C.c_void_p, _P(c_stats)]),
     "gsct_ctx_workspace_bytes": (C.c_size_t, [C.c_void_p]),
     "gsct_ctx_launch_count": (C.c_int64, [C.c_void_p]),
@@ -421,6 +422,10 @@ class Context:
 
     def set_async(self, on: bool) -> None:
         self.check(self._lib.gsct_ctx_set_async(self.handle, 1 if on else 0))
+
+    def set_save_for_backward(self, on: bool) -> None:
+        """Keep the forward's set-up for the matching backward (caller keeps the cloud fixed)."""
+        self.check(self._lib.gsct_ctx_set_save_for_backward(self.handle, 1 if on else 0))
 
     def synchronize(self, stats: Optional[RenderStats] = None) -> None:
         s = stats._c() if stats is not None else c_stats()

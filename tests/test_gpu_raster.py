@@ -256,6 +256,28 @@ def test_device_resident_matches_host(ctx):
         assert np.array_equal(getattr(gd, k).cpu().numpy(), getattr(gh, k)), k
 
 
+def test_save_for_backward_is_exact(ctx):
+    """Reusing the forward's set-up gives bit-identical gradients; a call that does not match
+    the saved forward (other views) recomputes."""
+    import torch
+
+    geom = cone_geometry(64, 0.5, np.linspace(0, 2 * np.pi, 9, endpoint=False))
+    cloud = gsct.make_cloud("random", 120, seed=9, pos_range=8.0).to_device(0)
+    gi = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, size=(9, 64, 64)).astype(np.float32)).cuda()
+    base = gsct.rasterize_backward_views(cloud, geom, None, gi, ctx=ctx)
+    try:
+        ctx.set_save_for_backward(True)
+        gsct.rasterize_views(cloud, geom, None, ctx=ctx)
+        reused = gsct.rasterize_backward_views(cloud, geom, None, gi, ctx=ctx)
+        other = gsct.rasterize_backward_views(cloud, geom, [0, 1, 2], gi[:3], ctx=ctx)  # no saved match
+    finally:
+        ctx.set_save_for_backward(False)
+    ref3 = gsct.rasterize_backward_views(cloud, geom, [0, 1, 2], gi[:3], ctx=ctx)
+    for k in ("positions", "log_scales", "rotations", "raw_densities", "pos_grad_norm", "visible"):
+        assert torch.equal(getattr(reused, k), getattr(base, k)), k
+        assert torch.equal(getattr(other, k), getattr(ref3, k)), k
+
+
 def test_view_chunking_invariance(ctx, orc):
     """Many views (chunked internally) give the same per-view images as single calls."""
     geom = cone_geometry(32, 0.9, np.linspace(0, 2 * np.pi, 23, endpoint=False))
