@@ -647,6 +647,8 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     RasterRec* saved = reuse ? ws<RasterRec>(c, S_SAVED, un * n_views) : nullptr;
     const int tiles_u = (geom->n_u + kTile - 1) / kTile, tiles_v = (geom->n_v + kTile - 1) / kTile;
     const int chunk = views_per_chunk(n, n_views, static_cast<int64_t>(tiles_u) * tiles_v);
+    // pixel-loop moments of every view, splat-major [N][n_views] x 8 fp32
+    float* mom = ws<float>(c, S_MOMENTS, un * static_cast<size_t>(n_views) * 8 + 1);
     for (int v0 = 0; v0 < n_views && n > 0; v0 += chunk) {
       const int cv = std::min(chunk, n_views - v0);
       const float* gimg = grad_images + static_cast<int64_t>(v0) * npx;
@@ -660,19 +662,15 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         Phase ph(c, GSCT_PH_RASTER_SETUP);
         launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kTile, rec, nullptr, c->dstats, c->stream);
       }
-      float* mom = ws<float>(c, S_MOMENTS, un * cv * 8);
       {
         Phase ph(c, GSCT_PH_RASTER_BWD);
-        launch_raster_bwd_pairs(rec, n, cv, geom->n_u, geom->n_v, gimg, mom, nullptr, c->stream);
-      }
-      {
-        Phase ph(c, GSCT_PH_RASTER_TAIL);
-        launch_raster_tail(pre, n, dframes + v0, cv, g, r, mom, v0 == 0, acc, gv, c->stream);
+        launch_raster_bwd_pairs(rec, n, cv, geom->n_u, geom->n_v, gimg, mom, v0, n_views, c->stream);
       }
       CK(cudaGetLastError());
     }
     if (n > 0 && n_views > 0) {
       Phase ph(c, GSCT_PH_RASTER_TAIL);
+      launch_raster_tail(pre, n, dframes, n_views, g, r, mom, acc, gv, c->stream);
       launch_raster_finalize(d, acc, gp, gl, gq, gr, gn, c->stream);
     }
     if (out->location == GSCT_HOST && n > 0) {

@@ -62,9 +62,10 @@ void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frame
                               const Geo& g, const RSet& rs, int bin_ts, RasterRec* rec,
                               uint32_t* tile_count, DevStats* stats, cudaStream_t st);
 // acc: fp64 [11][N] running view-sum (g_pos 3, g_sigma 6, g_raw, sum |dL/dmean2d|)
+// moments: splat-major [N][n_views] x 8 fp32 covering every view of the call
 void launch_raster_tail(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
-                        const Geo& g, const RSet& rs, const float* moments, bool first_chunk,
-                        double* acc, uint8_t* visible, cudaStream_t st);
+                        const Geo& g, const RSet& rs, const float* moments, double* acc,
+                        uint8_t* visible, cudaStream_t st);
 void launch_raster_finalize(const Cloud& c, const double* acc, double* g_pos, double* g_ls,
                             double* g_q, double* g_raw, double* g_pgn, cudaStream_t st);
 void launch_debug_project(const PreSplat* pre, int64_t n, const Frame* frame_dev, const Geo& g,
@@ -87,9 +88,10 @@ void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint3
 void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                        const uint32_t* end, int64_t n, int n_views, int n_u, int n_v,
                        int tiles_u, int tiles_v, float* images, cudaStream_t st);
+// moments written splat-major at [(i * total_views + view_offset + v) * 8]
 void launch_raster_bwd_pairs(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v,
-                             const float* grad_images, float* moments, unsigned int* work_counter,
-                             cudaStream_t st);
+                             const float* grad_images, float* moments, int view_offset,
+                             int total_views, cudaStream_t st);
 
 void launch_emit_brick_pairs(const VoxelRec* rec, const uint32_t* offsets,
                              const uint32_t* counts, int64_t n, const Window& win, int nbx,

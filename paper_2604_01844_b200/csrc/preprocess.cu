@@ -51,6 +51,9 @@ __global__ void __launch_bounds__(128) k_splat_prepare(Cloud c, PreSplat* __rest
 #ifndef GSCT_PRE_MINB
 #define GSCT_PRE_MINB 8
 #endif
+#ifndef GSCT_MOM_SPLAT_MAJOR
+#define GSCT_MOM_SPLAT_MAJOR 0  // must match raster.cu (moment slot layout)
+#endif
 #ifndef GSCT_TAIL_MINB
 #define GSCT_TAIL_MINB 4
 #endif
@@ -102,17 +105,25 @@ __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const 
   warp_add(&st->pixel_pairs, n_pp);
 }
 
-// K4b: one warp per splat, lane l handles views l, l+32, ... of the chunk: re-derives the
-// fp64 projection, turns the fp32 pixel-loop moments into dL/d(amp, mean2d, conic) and runs
-// the reference chain rule up to dL/dSigma. Per-view results are summed over the chunk's
-// views with a fixed shuffle tree and added to the running fp64 accumulator (chunks in
-// ascending view order), i.e. ParamGradients::add up to fp64 reassociation.
+// K4b: one warp per splat, lane l handles views l, l+32, ... of ALL views of the call:
+// re-derives the fp64 projection, turns the fp32 pixel-loop moments into
+// dL/d(amp, mean2d, conic) and runs the reference chain rule up to dL/dSigma. Per-view
+// results are summed with a fixed shuffle tree (ParamGradients::add up to fp64
+// reassociation). Moments are splat-major ([N][V] x 32 B) so a warp's loads are contiguous;
+// view frames are staged in shared memory when they fit.
 // acc layout [11][N]: g_pos(3), g_sigma(00,01,02,11,12,22), g_raw, sum |dL/dmean2d|.
 __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSplat* __restrict__ pre, int64_t n,
-                                                     const Frame* __restrict__ frames, int n_views,
+                                                     const Frame* __restrict__ frames_g, int n_views,
                                                      Geo g, RSet rs, const float4* __restrict__ moments,
-                                                     int first_chunk, double* __restrict__ acc,
+                                                     int frames_in_smem, double* __restrict__ acc,
                                                      uint8_t* __restrict__ visible) {
+  extern __shared__ Frame s_frames[];
+  const Frame* frames = frames_g;
+  if (frames_in_smem) {
+    for (int k = threadIdx.x; k < n_views; k += blockDim.x) s_frames[k] = frames_g[k];
+    __syncthreads();
+    frames = s_frames;
+  }
   const int lane = threadIdx.x & 31;
   const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
@@ -127,7 +138,11 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
       project_full(frames[vw], g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
       if (p.degenerate || p.culled) continue;
       vis = true;
+#if GSCT_MOM_SPLAT_MAJOR
+      const int64_t item = i * n_views + vw;
+#else
       const int64_t item = static_cast<int64_t>(vw) * n + i;
+#endif
       const float4 m0 = moments[2 * item];
       const float4 m1 = moments[2 * item + 1];
       // m0 = {sum t, sum t du, sum t dv, sum t du^2}, m1 = {sum t du dv, sum t dv^2, -, -}
@@ -165,8 +180,8 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
   vis = __any_sync(0xffffffffu, vis);
   if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < 11; ++k) acc[k * n + i] = first_chunk ? v[k] : acc[k * n + i] + v[k];
-    visible[i] = first_chunk ? static_cast<uint8_t>(vis) : static_cast<uint8_t>(visible[i] | vis);
+    for (int k = 0; k < 11; ++k) acc[k * n + i] = v[k];
+    visible[i] = static_cast<uint8_t>(vis);
   }
 }
 
@@ -381,12 +396,12 @@ void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frame
 }
 
 void launch_raster_tail(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views, const Geo& g,
-                        const RSet& rs, const float* moments, bool first_chunk, double* acc, uint8_t* visible,
-                        cudaStream_t st) {
+                        const RSet& rs, const float* moments, double* acc, uint8_t* visible, cudaStream_t st) {
   if (n == 0) return;
-  k_raster_tail<<<blocks_for(n * 32, 128), 128, 0, st>>>(pre, n, frames_dev, n_views, g, rs,
-                                                         reinterpret_cast<const float4*>(moments),
-                                                         first_chunk ? 1 : 0, acc, visible);
+  const size_t smem = static_cast<size_t>(n_views) * sizeof(Frame);
+  const bool in_smem = smem <= 24 * 1024;
+  k_raster_tail<<<blocks_for(n * 32, 128), 128, in_smem ? smem : 0, st>>>(
+      pre, n, frames_dev, n_views, g, rs, reinterpret_cast<const float4*>(moments), in_smem ? 1 : 0, acc, visible);
   count_launch();
 }
 

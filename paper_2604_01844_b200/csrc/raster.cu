@@ -83,6 +83,9 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, ui
 #ifndef GSCT_BWD_ASM
 #define GSCT_BWD_ASM 0
 #endif
+#ifndef GSCT_MOM_SPLAT_MAJOR
+#define GSCT_MOM_SPLAT_MAJOR 0  // must match preprocess.cu (moment slot layout)
+#endif
 #ifndef GSCT_BWD_LOOP
 #define GSCT_BWD_LOOP 1  // 1: predicate-free 4-row main loop + remainder (A/B: 7.6 vs 8.3 ms)
 #endif
@@ -194,7 +197,8 @@ __global__ void __launch_bounds__(256) k_raster_bwd_pairs(const RasterRec* __res
                                                           int64_t n_items, int64_t n, int n_u,
                                                           int n_v,
                                                           const float* __restrict__ grad,
-                                                          float4* __restrict__ moments, double inv_n) {
+                                                          float4* __restrict__ moments, double inv_n,
+                                                          int view_offset, int total_views) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -279,18 +283,41 @@ __global__ void __launch_bounds__(256) k_raster_bwd_pairs(const RasterRec* __res
       muv = fmaf(t1, du, muv);
       mvv += t2;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      m0 += __shfl_xor_sync(0xffffffffu, m0, o);
-      mu += __shfl_xor_sync(0xffffffffu, mu, o);
-      mv += __shfl_xor_sync(0xffffffffu, mv, o);
-      muu += __shfl_xor_sync(0xffffffffu, muu, o);
-      muv += __shfl_xor_sync(0xffffffffu, muv, o);
-      mvv += __shfl_xor_sync(0xffffffffu, mvv, o);
-    }
-    if (lane == 0) {
-      moments[2 * item] = make_float4(m0, mu, mv, muu);
-      moments[2 * item + 1] = make_float4(muv, mvv, 0.f, 0.f);
+    // Transposed butterfly: 6 moments (padded to 8) in 9 shuffles instead of 30. After the
+    // three halving exchanges lane l holds a partial of moment ((l>>4)&1)*4+((l>>3)&1)*2+
+    // ((l>>2)&1); two plain xor steps finish the sum inside each 4-lane group.
+    {
+      const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+      float w0, w1, w2, w3;
+      {
+        float s;
+        s = __shfl_xor_sync(0xffffffffu, b16 ? m0 : muv, 16);  w0 = (b16 ? muv : m0) + s;
+        s = __shfl_xor_sync(0xffffffffu, b16 ? mu : mvv, 16);  w1 = (b16 ? mvv : mu) + s;
+        s = __shfl_xor_sync(0xffffffffu, b16 ? mv : 0.f, 16);  w2 = (b16 ? 0.f : mv) + s;
+        s = __shfl_xor_sync(0xffffffffu, b16 ? muu : 0.f, 16); w3 = (b16 ? 0.f : muu) + s;
+      }
+      float x0, x1;
+      {
+        float s;
+        s = __shfl_xor_sync(0xffffffffu, b8 ? w0 : w2, 8); x0 = (b8 ? w2 : w0) + s;
+        s = __shfl_xor_sync(0xffffffffu, b8 ? w1 : w3, 8); x1 = (b8 ? w3 : w1) + s;
+      }
+      float y = (b4 ? x1 : x0) + __shfl_xor_sync(0xffffffffu, b4 ? x0 : x1, 4);
+      y += __shfl_xor_sync(0xffffffffu, y, 2);
+      y += __shfl_xor_sync(0xffffffffu, y, 1);
+#if GSCT_MOM_SPLAT_MAJOR
+      // splat-major slot (i, view_offset + view) so the tail's per-splat loads are contiguous
+      const int64_t i = item - static_cast<int64_t>(view) * n;
+      const int64_t slot = i * total_views + view_offset + view;
+#else
+      // view-major slot (view_offset + view, i): consecutive items write consecutive sectors
+      const int64_t slot = static_cast<int64_t>(view_offset) * n + item;
+#endif
+      // one full 32 B sector per item from 8 lanes (no partial-sector writes to DRAM)
+      if ((lane & 3) == 0) {
+        const int m = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
+        reinterpret_cast<float*>(moments)[slot * 8 + m] = y;
+      }
     }
   }
 }
@@ -327,7 +354,7 @@ void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_
 }
 
 void launch_raster_bwd_pairs(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v,
-                             const float* grad_images, float* moments, unsigned int* /*work*/,
+                             const float* grad_images, float* moments, int view_offset, int total_views,
                              cudaStream_t st) {
   const int64_t items = n * n_views;
   if (items == 0) return;
@@ -337,7 +364,8 @@ void launch_raster_bwd_pairs(const RasterRec* rec, int64_t n, int n_views, int n
   const int64_t want = (items + 7) / 8;  // 8 warps per block
   const unsigned blocks = static_cast<unsigned>(want < static_cast<int64_t>(sms) * 16 ? want : static_cast<int64_t>(sms) * 16);
   k_raster_bwd_pairs<<<blocks, 256, 0, st>>>(rec, items, n, n_u, n_v, grad_images,
-                                             reinterpret_cast<float4*>(moments), 1.0 / static_cast<double>(n));
+                                             reinterpret_cast<float4*>(moments), 1.0 / static_cast<double>(n),
+                                             view_offset, total_views);
   count_launch();
 }
 
