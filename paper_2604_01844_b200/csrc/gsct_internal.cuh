@@ -93,6 +93,15 @@ void launch_raster_bwd_pairs(const RasterRec* rec, int64_t n, int n_views, int n
                              const float* grad_images, float* moments, int view_offset,
                              int total_views, cudaStream_t st);
 
+// lane-per-item backward: shape sort keys, then the pixel walk in `order`
+int bwd_vec(int n_u, const float* grad_images);  // 8, 4 or 1 floats per row load
+// returns the number of key bits to sort on
+int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v, int vec,
+                          uint32_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_t n, int n_views, int n_u,
+                             int n_v, const float* grad_images, float* moments, int view_offset,
+                             cudaStream_t st);
+
 void launch_emit_brick_pairs(const VoxelRec* rec, const uint32_t* offsets,
                              const uint32_t* counts, int64_t n, const Window& win, int nbx,
                              int nby, uint32_t* keys, uint32_t* vals, cudaStream_t st);

@@ -322,6 +322,214 @@ __global__ void __launch_bounds__(256) k_raster_bwd_pairs(const RasterRec* __res
   }
 }
 
+typedef unsigned long long f2_t;  // two packed fp32 values (lo, hi)
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// Lane-per-item backward (K4a). The per-(view, splat) pixel loop is small (hundreds of
+// pixels), so warp-cooperative schemes spend more instructions on lane mapping and the
+// cross-lane moment reduction than on pixels. Here ONE LANE owns one item end to end: it
+// walks the bbox rows, each row as 16-byte aligned float4 chunks of the grad image (VEC=4;
+// the <= 3 columns left of u_min / right of u_max in the edge chunks are zeroed and add
+// exact zeros), and accumulates per row, in packed f32x2 arithmetic over column pairs,
+//   s0 = sum t, s1 = sum t k, s2 = sum t k^2,   t = exp2(A du^2 + B du dv + C dv^2) * w,
+// with k = column - round(mean) (du = k - delta, |delta| <= 1/2) and the exponent evaluated
+// directly as a quadratic in k (two packed FMAs per pixel pair, no error accumulation).
+// Rows fold into the six moments {t, t du, t dv, t du^2, t du dv, t dv^2}. No shuffles,
+// no shared memory; every item's result depends only on its own inputs (duplicated splats
+// get bit-identical moments). Items are processed in `order` (sorted by bbox shape, see
+// k_bwd_shape_keys) so the 32 lanes of a warp walk near-identical loop trip counts.
+__device__ __forceinline__ void ldg_v8(const float* p, float (&w)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(w[0]), "=f"(w[1]), "=f"(w[2]), "=f"(w[3]), "=f"(w[4]), "=f"(w[5]), "=f"(w[6]), "=f"(w[7])
+               : "l"(p));
+}
+
+#ifndef GSCT_LANES_MINB
+#define GSCT_LANES_MINB 4  // 64 registers: 32 resident warps per SM
+#endif
+template <int VEC>
+__global__ void __launch_bounds__(256, GSCT_LANES_MINB) k_raster_bwd_lanes(const RasterRec* __restrict__ rec,
+                                                          const uint32_t* __restrict__ order,
+                                                          int64_t n_items, int64_t n, int n_u, int n_v,
+                                                          const float* __restrict__ grad,
+                                                          float* __restrict__ moments, double inv_n,
+                                                          int view_offset) {
+  constexpr int CW = VEC == 8 ? 8 : 4;  // columns per chunk
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n_items) return;
+  const int64_t item = order ? static_cast<int64_t>(__ldg(order + t)) : t;
+  const RasterRec r = rec[item];
+  const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
+  const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+  const int W = u1 - u0 + 1, H = v1 - v0 + 1;
+  if (W <= 0 || H <= 0) return;
+  // view = item / n without a 64-bit integer division (exact: the quotient's fractional
+  // part is >= 0.5/n away from an integer, far above the fp64 rounding error)
+  const int view = static_cast<int>((static_cast<double>(item) + 0.5) * inv_n);
+  const int ua = VEC > 1 ? (u0 & ~(VEC - 1)) : u0;  // aligned first column
+  const int lead = u0 - ua;                         // extra columns left of the bbox
+  const int ncol = lead + W;                        // columns walked, relative to ua
+  const int nch = (ncol + CW - 1) / CW;             // chunks per row
+  const float rmu = rintf(r.mo_u);
+  const float delta = r.mo_u - rmu;
+  const float fcm = static_cast<float>(lead) + rmu;  // k = column - fcm
+  const f2_t A2 = f2_pack(r.A, r.A);
+  const f2_t TWO2 = f2_pack(2.f, 2.f);
+  const f2_t K0 = f2_pack(-fcm, 1.f - fcm);
+  const float m2a_d = -2.f * r.A * delta, mb_d = -r.B * delta, a_dd = r.A * delta * delta;
+  const float* __restrict__ prow = grad + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(v0) * n_u + ua;
+  float m0 = 0.f, mu = 0.f, mv = 0.f, muu = 0.f, muv = 0.f, mvv = 0.f;
+  float dv = -r.mo_v;
+  // one flat loop over (row, chunk) so the load of the next chunk (possibly the next
+  // row's first) is in flight while the current chunk is computed
+  auto load = [&](const float* q, float (&w)[CW], int c) {
+    if constexpr (VEC == 8) {
+      ldg_v8(q, w);
+    } else if constexpr (VEC == 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(q));
+      w[0] = x.x, w[1] = x.y, w[2] = x.z, w[3] = x.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < CW; ++k) w[k] = (k == 0 || c + k < ncol) ? __ldg(q + k) : 0.f;
+    }
+  };
+  float wn[CW];
+  load(prow, wn, 0);
+  f2_t BP2, CP2;
+  auto row_coeffs = [&]() {
+    // E(k) = A k^2 + B' k + C'  (du = k - delta)
+    const float bp = fmaf(r.B, dv, m2a_d);
+    const float cp = fmaf(dv, fmaf(r.C, dv, mb_d), a_dd);
+    BP2 = f2_pack(bp, bp);
+    CP2 = f2_pack(cp, cp);
+  };
+  row_coeffs();
+  f2_t s0 = f2_pack(0.f, 0.f), s1 = s0, s2 = s0;
+  f2_t kA = K0;
+  const int total = H * nch;
+  int j = 0;
+  for (int it = 0; it < total; ++it) {
+    float w[CW];
+#pragma unroll
+    for (int k = 0; k < CW; ++k) w[k] = wn[k];
+    const int c = CW * j;
+    if (it + 1 < total) {
+      if (j + 1 < nch)
+        load(prow + c + CW, wn, c + CW);
+      else
+        load(prow + n_u, wn, 0);
+    }
+    if (VEC > 1) {
+      if (j == 0) {  // columns left of u_min
+#pragma unroll
+        for (int q = 0; q < CW - 1; ++q)
+          if (q < lead) w[q] = 0.f;
+      }
+      if (j == nch - 1) {  // columns right of u_max
+#pragma unroll
+        for (int q = 1; q < CW; ++q)
+          if (c + q >= ncol) w[q] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < CW / 2; ++h) {
+      const f2_t e = f2_fma(f2_fma(A2, kA, BP2), kA, CP2);
+      float e0, e1;
+      f2_unpack(e, e0, e1);
+      const f2_t tt = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), f2_pack(w[2 * h], w[2 * h + 1]));
+      s0 = f2_add(s0, tt);
+      const f2_t tk = f2_mul(tt, kA);
+      s1 = f2_add(s1, tk);
+      s2 = f2_fma(tk, kA, s2);
+      kA = f2_add(kA, TWO2);
+    }
+    if (++j == nch) {  // row done: fold into the moments
+      float t0, t1, t2;
+      {
+        float a, b;
+        f2_unpack(s0, a, b);
+        t0 = a + b;
+        f2_unpack(s1, a, b);
+        t1 = a + b;
+        f2_unpack(s2, a, b);
+        t2 = a + b;
+      }
+      // sum t du = t1 - delta t0;  sum t du^2 = t2 - 2 delta t1 + delta^2 t0
+      const float su = fmaf(-delta, t0, t1);
+      const float suu = fmaf(delta, fmaf(delta, t0, -2.f * t1), t2);
+      m0 += t0;
+      mu += su;
+      mv = fmaf(dv, t0, mv);
+      muu += suu;
+      muv = fmaf(dv, su, muv);
+      mvv = fmaf(dv * dv, t0, mvv);
+      j = 0;
+      prow += n_u;
+      dv += 1.f;
+      row_coeffs();
+      s0 = f2_pack(0.f, 0.f), s1 = s0, s2 = s0;
+      kA = K0;
+    }
+  }
+  // view-major slot (view_offset + view, i) = view_offset * n + item; [m0 mu mv muu muv mvv 0 0]
+  float4* dst = reinterpret_cast<float4*>(moments + (static_cast<int64_t>(view_offset) * n + item) * 8);
+  dst[0] = make_float4(m0, mu, mv, muu);
+  dst[1] = make_float4(muv, mvv, 0.f, 0.f);
+}
+
+// Bbox-shape sort keys for the lane-per-item backward: (chunks per row, rows), each clamped
+// to 6 bits, so a warp's 32 items have near-identical loop trip counts. Empty items sort
+// last. Values = item index (the stable sort keeps index order inside a shape class).
+#ifndef GSCT_KEY_MODE
+#define GSCT_KEY_MODE 1  // 0: shape; 1: shape | view | detector region (L1 locality inside a warp)
+#endif
+__global__ void k_bwd_shape_keys(const RasterRec* __restrict__ rec, int64_t n_items, int64_t n, int vec,
+                                 int region_shift, int region_bits, int view_bits,
+                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  const RasterRec r = rec[i];
+  const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
+  const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+  const int W = u1 - u0 + 1, H = v1 - v0 + 1;
+  const int low_bits = region_bits + view_bits;
+  uint32_t key = (1u << (11 + low_bits)) - 1u;  // empty items sort last
+  if (W > 0 && H > 0) {
+    const int cw = vec == 8 ? 8 : 4;
+    const int lead = vec > 1 ? (u0 & (vec - 1)) : 0;
+    const int nch = (lead + W + cw - 1) / cw;
+    const uint32_t shape = (static_cast<uint32_t>(min(nch, 31)) << 6) | static_cast<uint32_t>(min(H, 63));
+    const int half = region_bits / 2;
+    const uint32_t ru = min(u0 >> region_shift, (1 << half) - 1), rv = min(v0 >> region_shift, (1 << half) - 1);
+    const uint32_t view = static_cast<uint32_t>(i / n);
+    key = (shape << low_bits) | (view << region_bits) | (rv << half) | ru;
+  }
+  keys[i] = key;
+  vals[i] = static_cast<uint32_t>(i);
+}
+
 inline unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
 
 }  // namespace
@@ -340,6 +548,51 @@ void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint3
                    cudaStream_t st) {
   if (n_keys == 0) return;
   k_ranges<<<blocks_for(n_keys, 256), 256, 0, st>>>(keys, static_cast<uint32_t>(n_pairs), n_keys, start, end);
+  count_launch();
+}
+
+#ifndef GSCT_BWD_VEC
+#define GSCT_BWD_VEC 8  // widest grad-image row load of the lane-per-item backward (8: 32 B)
+#endif
+int bwd_vec(int n_u, const float* grad_images) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(grad_images);
+  if (GSCT_BWD_VEC >= 8 && n_u % 8 == 0 && a % 32 == 0) return 8;
+  if (n_u % 4 == 0 && a % 16 == 0) return 4;
+  return 1;
+}
+
+int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v, int vec,
+                          uint32_t* keys, uint32_t* vals, cudaStream_t st) {
+  const int64_t n_items = n * n_views;
+  if (n_items == 0) return 11;
+  int view_bits = 0, region_bits = 0, region_shift = 0;
+#if GSCT_KEY_MODE == 1
+  while ((1 << view_bits) < n_views) ++view_bits;
+  region_bits = 6;  // 8 x 8 detector regions
+  const int side = n_u > n_v ? n_u : n_v;
+  while ((side >> region_shift) > 8) ++region_shift;
+#endif
+  k_bwd_shape_keys<<<blocks_for(n_items, 256), 256, 0, st>>>(rec, n_items, n, vec, region_shift, region_bits,
+                                                             view_bits, keys, vals);
+  count_launch();
+  return 11 + view_bits + region_bits;  // key bits
+}
+
+void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_t n, int n_views, int n_u,
+                             int n_v, const float* grad_images, float* moments, int view_offset,
+                             cudaStream_t st) {
+  const int64_t items = n * n_views;
+  if (items == 0) return;
+  const int vec = bwd_vec(n_u, grad_images);
+  if (vec == 8)
+    k_raster_bwd_lanes<8><<<blocks_for(items, 256), 256, 0, st>>>(rec, order, items, n, n_u, n_v, grad_images,
+                                                                  moments, 1.0 / static_cast<double>(n), view_offset);
+  else if (vec == 4)
+    k_raster_bwd_lanes<4><<<blocks_for(items, 256), 256, 0, st>>>(rec, order, items, n, n_u, n_v, grad_images,
+                                                                  moments, 1.0 / static_cast<double>(n), view_offset);
+  else
+    k_raster_bwd_lanes<1><<<blocks_for(items, 256), 256, 0, st>>>(rec, order, items, n, n_u, n_v, grad_images,
+                                                                  moments, 1.0 / static_cast<double>(n), view_offset);
   count_launch();
 }
 

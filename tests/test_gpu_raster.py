@@ -285,3 +285,24 @@ def test_view_chunking_invariance(ctx, orc):
     imgs = gsct.rasterize_views(cloud, geom, None, ctx=ctx)
     for v in (0, 7, 22):
         assert np.array_equal(imgs[v], gsct.rasterize_view(cloud, geom, v, ctx=ctx))
+
+
+@pytest.mark.parametrize("spacing", [0.35, 0.12, 0.045])
+def test_backward_bbox_size_sweep(ctx, orc, spacing):
+    """Backward column-block plan across bbox regimes: W, H from a few pixels to > 128
+    (the plan table's clamp / fallback paths), anisotropic splats (W != H)."""
+    geom = parallel_geometry(300, spacing, [0.4, 1.9])
+    rs = gsct.RasterSettings()
+    cloud = gsct.make_cloud("random", 24, seed=123, pos_range=3.0, scale_lo=0.05, scale_hi=1.6)
+    rng = np.random.default_rng(5)
+    gi = rng.uniform(-1, 1, size=(len(geom.angles), geom.n_v, geom.n_u)).astype(np.float32)
+    grads = gsct.rasterize_backward_views(cloud, geom, None, gi, rs, ctx=ctx)
+    acc = None
+    for view in range(len(geom.angles)):
+        g = orc.rasterize_backward(cloud, geom, view, gi[view].astype(np.float64), rs)
+        acc = g if acc is None else {k: (acc[k] | g[k]) if k == "visible" else acc[k] + g[k] for k in g}
+    errs = grad_class_errors(grads, acc)
+    assert all(e <= GRAD_TOL for e in errs.values()), errs
+    pc = orc.project_cloud(cloud, geom, 0, rs)
+    w = pc["rect"][:, 1] - pc["rect"][:, 0] + 1
+    assert w.max() > 8  # the sweep really covers multi-block boxes
