@@ -34,6 +34,44 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
+typedef unsigned long long f2_t;  // two packed fp32 values (lo, hi)
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// Lane-per-item backward (K4a). The per-(view, splat) pixel loop is small (hundreds of
+// pixels), so warp-cooperative schemes spend more instructions on lane mapping and the
+// cross-lane moment reduction than on pixels. Here ONE LANE owns one item end to end: it
+// walks the bbox rows, each row as 16-byte aligned float4 chunks of the grad image (VEC=4;
+// the <= 3 columns left of u_min / right of u_max in the edge chunks are zeroed and add
+// exact zeros), and accumulates per row, in packed f32x2 arithmetic over column pairs,
+//   s0 = sum t, s1 = sum t k, s2 = sum t k^2,   t = exp2(A du^2 + B du dv + C dv^2) * w,
+// with k = column - round(mean) (du = k - delta, |delta| <= 1/2) and the exponent evaluated
+// directly as a quadratic in k (two packed FMAs per pixel pair, no error accumulation).
+// Rows fold into the six moments {t, t du, t dv, t du^2, t du dv, t dv^2}. No shuffles,
+// no shared memory; every item's result depends only on its own inputs (duplicated splats
+// get bit-identical moments). Items are processed in `order` (sorted by bbox shape, see
+// k_bwd_shape_keys) so the 32 lanes of a warp walk near-identical loop trip counts.
 __global__ void k_emit_tile_pairs(const RasterRec* __restrict__ rec,
                                   const uint32_t* __restrict__ offsets,
                                   const uint32_t* __restrict__ counts, int64_t n, int n_views,
@@ -189,6 +227,186 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd(const RasterRec* 
   }
 }
 
+// Forward v2 (K3): one warp per 16x16 tile and view; lane l owns the 2 x 4 pixel block at
+// rows 2(l>>2) .. +1, columns 4(l&3) .. +3, the two rows held in the halves of packed f32x2
+// registers. Records of the tile list (ascending splat index = the reference's per-pixel
+// accumulation order) are staged 32 at a time in the warp's shared-memory slice; the
+// staging lane also derives the per-splat ratio c = exp2(2A) and a "chain-safe" flag.
+// Along a row the Gaussian is evaluated multiplicatively: with e(k) = E0 + k D + k(k-1) A,
+//   g(k+1) = g(k) r(k),  r(k+1) = r(k) c,   g(0) = amp 2^E0,  r(0) = 2^D,
+// i.e. 2 packed FMULs per pixel pair instead of one MUFU.EX2 per pixel; the column mask
+// predicates the accumulation, row validity is folded into g(0). The chain is used when no
+// value in the tile's (4-column aligned) bbox window under/overflows fp32 (the flag);
+// otherwise the splat takes the direct MUFU path. Both give amp * exp(e) to a few ulps.
+struct __align__(16) StagedRec2 {
+  float4 p;  // du_t = (tx0 - u0) - mo_u, dv_t = (ty0 - v0) - mo_v (tile-origin offsets), A, B
+  float4 q;  // C, amp, c = exp2(2A), chain-safe flag (1/0)
+  uint4 m;   // column mask (bit c: tile column c in the bbox) | row mask << 16, lane mask, -, -
+};
+
+__device__ __forceinline__ float quad_e(float A, float B, float C, float du, float dv) {
+  return fmaf(fmaf(A, du, B * dv), du, C * dv * dv);
+}
+
+// 32 x 32 bit-matrix transpose across a warp: on entry lane j holds row j (bit l = lane l
+// is relevant to record j); on exit lane l holds column l (bit j = record j is relevant to
+// lane l). Five xor-shuffle stages.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  const uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const int s = 16 >> t;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~M[t]) | ((y >> s) & M[t])) : ((x & M[t]) | ((y << s) & ~M[t]));
+  }
+  return x;
+}
+
+#ifndef GSCT_FWD_FILTER
+#define GSCT_FWD_FILTER 1  // 1: each lane walks only the records touching its 2x4 block
+#endif
+
+__global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd2(const RasterRec* __restrict__ rec,
+                                                                const uint32_t* __restrict__ vals,
+                                                                const uint32_t* __restrict__ start,
+                                                                const uint32_t* __restrict__ end, int64_t n,
+                                                                int n_u, int n_v, int tiles_u, int n_tiles,
+                                                                float* __restrict__ images) {
+  __shared__ StagedRec2 s_rec[kFwdWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kFwdWarps + warp;
+  if (tile >= n_tiles) return;  // whole warp exits together
+  const int view = blockIdx.y;
+  const int tu = tile % tiles_u, tv = tile / tiles_u;
+  const int tx0 = tu * kTile, ty0 = tv * kTile;
+  const int lr = 2 * (lane >> 2), lc = 4 * (lane & 3);  // lane block offset inside the tile
+  const float flr = static_cast<float>(lr), flc = static_cast<float>(lc);
+  const uint32_t key = static_cast<uint32_t>(view) * n_tiles + tile;
+  const uint32_t b = start[key], e = end[key];
+  const RasterRec* __restrict__ vrec = rec + static_cast<int64_t>(view) * n;
+  StagedRec2* sw = s_rec[warp];
+  float acc0[4], acc1[4];  // rows lr, lr + 1
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc0[k] = acc1[k] = 0.f;
+
+  uint32_t idx_next = (b + 32 + lane < e) ? vals[b + 32 + lane] : 0u;
+  RasterRec r_cur;
+  if (b + lane < e) r_cur = vrec[vals[b + lane]];
+  for (uint32_t base = b; base < e; base += 32) {
+    const int cnt = min(32u, e - base);
+    const bool has_next = base + 32 + lane < e;
+    RasterRec r_next;
+    if (has_next) r_next = vrec[idx_next];
+    idx_next = (base + 64 + lane < e) ? vals[base + 64 + lane] : 0u;
+    uint32_t lanes_rel = 0u;  // lanes whose 2x4 block meets this record's bbox
+    if (lane < cnt) {
+      const RasterRec r = r_cur;
+      StagedRec2 s;
+      const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16, v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+      const float du_t = (static_cast<float>(tx0) - static_cast<float>(u0)) - r.mo_u;
+      const float dv_t = (static_cast<float>(ty0) - static_cast<float>(v0)) - r.mo_v;
+      // bbox n tile in tile coordinates (non-empty: the splat is on this tile's list)
+      const int c0 = max(u0 - tx0, 0), c1 = min(u1 - tx0, kTile - 1);
+      const int r0 = max(v0 - ty0, 0), r1 = min(v1 - ty0, kTile - 1);
+      const uint32_t cm = ((2u << c1) - 1u) & ~((1u << c0) - 1u);
+      const uint32_t rm = ((2u << r1) - 1u) & ~((1u << r0) - 1u);
+      // lane mask: column quads c0/4..c1/4 x row pairs r0/2..r1/2 (lane = 4 * pair + quad)
+      const uint32_t quads = ((2u << (c1 >> 2)) - 1u) & ~((1u << (c0 >> 2)) - 1u);
+      const uint32_t pairs = (0x11111111u >> (4 * (7 - (r1 >> 1)))) & (0x11111111u << (4 * (r0 >> 1)));
+      lanes_rel = pairs * quads;
+      // chain-safety window: rows r0..r1 x 4-aligned columns; the exponent is concave (min at
+      // a corner), the ratio exponent D = A (2 du + 1) + B dv is linear (extremes at corners)
+      const float dua = du_t + static_cast<float>(c0 & ~3), dub = du_t + static_cast<float>(c1 | 3);
+      const float dva = dv_t + static_cast<float>(r0), dvb = dv_t + static_cast<float>(r1);
+      const float emin = fminf(fminf(quad_e(r.A, r.B, r.C, dua, dva), quad_e(r.A, r.B, r.C, dua, dvb)),
+                               fminf(quad_e(r.A, r.B, r.C, dub, dva), quad_e(r.A, r.B, r.C, dub, dvb)));
+      const float da = r.A * fmaf(2.f, dua, 1.f), db = r.A * fmaf(2.f, dub, 1.f);
+      const float dmax = fmaxf(fmaxf(fabsf(fmaf(r.B, dva, da)), fabsf(fmaf(r.B, dvb, da))),
+                               fmaxf(fabsf(fmaf(r.B, dva, db)), fabsf(fmaf(r.B, dvb, db))));
+      const bool safe = emin > -100.f && dmax < 100.f && r.A > -50.f;
+      s.p = make_float4(du_t, dv_t, r.A, r.B);
+      s.q = make_float4(r.C, r.amp, ex2_approx(2.f * r.A), safe ? 1.f : 0.f);
+      s.m = make_uint4(cm | (rm << 16), lanes_rel, 0u, 0u);
+      sw[lane] = s;
+    }
+    __syncwarp();
+#if GSCT_FWD_FILTER
+    uint32_t todo = warp_transpose32(lanes_rel, lane);  // records touching this lane's block
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1u;
+#else
+    for (int j = 0; j < cnt; ++j) {
+#endif
+      const float4 p = sw[j].p;
+      const float4 q = sw[j].q;
+      const uint32_t mm = sw[j].m.x;
+      const uint32_t mask = (mm >> lc) & 15u;        // this lane's 4 columns
+      const uint32_t rows = (mm >> (16 + lr)) & 3u;  // this lane's 2 rows
+      const f2_t AMP = f2_pack((rows & 1u) ? q.y : 0.f, (rows & 2u) ? q.y : 0.f);
+      const float du0 = p.x + flc;
+      const float dv0 = p.y + flr;
+      const f2_t DV = f2_pack(dv0, dv0 + 1.f);
+      const float bdu = p.w * du0, au2 = p.z * du0 * du0;
+      const f2_t CC = f2_pack(q.x, q.x);
+      f2_t g[4];
+      if (q.w != 0.f) {
+        // E0 = A du0^2 + B du0 dv + C dv^2;  D = A (2 du0 + 1) + B dv
+        const f2_t E0 = f2_fma(DV, f2_fma(CC, DV, f2_pack(bdu, bdu)), f2_pack(au2, au2));
+        const float a1 = p.z * fmaf(2.f, du0, 1.f);
+        const f2_t D = f2_fma(f2_pack(p.w, p.w), DV, f2_pack(a1, a1));
+        float e0, e1, d0, d1;
+        f2_unpack(E0, e0, e1);
+        f2_unpack(D, d0, d1);
+        g[0] = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), AMP);
+        f2_t rr = f2_pack(ex2_approx(d0), ex2_approx(d1));
+        const f2_t c2 = f2_pack(q.z, q.z);
+        g[1] = f2_mul(g[0], rr);
+        rr = f2_mul(rr, c2);
+        g[2] = f2_mul(g[1], rr);
+        rr = f2_mul(rr, c2);
+        g[3] = f2_mul(g[2], rr);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float duk = du0 + static_cast<float>(k);
+          const f2_t ek = f2_fma(DV, f2_fma(CC, DV, f2_pack(p.w * duk, p.w * duk)),
+                                 f2_pack(p.z * duk * duk, p.z * duk * duk));
+          float e0, e1;
+          f2_unpack(ek, e0, e1);
+          g[k] = f2_mul(AMP, f2_pack(ex2_approx(e0), ex2_approx(e1)));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float glo, ghi;
+        f2_unpack(g[k], glo, ghi);
+        if (mask & (1u << k)) {
+          acc0[k] += glo;
+          acc1[k] += ghi;
+        }
+      }
+    }
+    __syncwarp();
+    r_cur = r_next;
+  }
+  const int px0 = tx0 + lc;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int py = ty0 + lr + h;
+    if (py >= n_v) continue;
+    const float* v = h ? acc1 : acc0;
+    float* row = images + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(py) * n_u;
+    if (((n_u & 3) == 0) && px0 + 4 <= n_u) {
+      reinterpret_cast<float4*>(row + px0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (px0 + k < n_u) row[px0 + k] = v[k];
+    }
+  }
+}
+
 // One warp per (view, splat) item, grid-stride. Lanes = bbox columns (blocks of <= 32)
 // x row groups; each lane walks its column with stride G = 32 / cw rows. du is constant
 // per lane, so per pixel only {t, t dv, t dv^2} are accumulated and folded with du once.
@@ -322,44 +540,6 @@ __global__ void __launch_bounds__(256) k_raster_bwd_pairs(const RasterRec* __res
   }
 }
 
-typedef unsigned long long f2_t;  // two packed fp32 values (lo, hi)
-__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
-  f2_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void f2_unpack(f2_t v, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
-  f2_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
-  f2_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
-  f2_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-
-// Lane-per-item backward (K4a). The per-(view, splat) pixel loop is small (hundreds of
-// pixels), so warp-cooperative schemes spend more instructions on lane mapping and the
-// cross-lane moment reduction than on pixels. Here ONE LANE owns one item end to end: it
-// walks the bbox rows, each row as 16-byte aligned float4 chunks of the grad image (VEC=4;
-// the <= 3 columns left of u_min / right of u_max in the edge chunks are zeroed and add
-// exact zeros), and accumulates per row, in packed f32x2 arithmetic over column pairs,
-//   s0 = sum t, s1 = sum t k, s2 = sum t k^2,   t = exp2(A du^2 + B du dv + C dv^2) * w,
-// with k = column - round(mean) (du = k - delta, |delta| <= 1/2) and the exponent evaluated
-// directly as a quadratic in k (two packed FMAs per pixel pair, no error accumulation).
-// Rows fold into the six moments {t, t du, t dv, t du^2, t du dv, t dv^2}. No shuffles,
-// no shared memory; every item's result depends only on its own inputs (duplicated splats
-// get bit-identical moments). Items are processed in `order` (sorted by bbox shape, see
-// k_bwd_shape_keys) so the 32 lanes of a warp walk near-identical loop trip counts.
 __device__ __forceinline__ void ldg_v8(const float* p, float (&w)[8]) {
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(w[0]), "=f"(w[1]), "=f"(w[2]), "=f"(w[3]), "=f"(w[4]), "=f"(w[5]), "=f"(w[6]), "=f"(w[7])
@@ -602,7 +782,14 @@ void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_
   if (n_views == 0) return;
   const int n_tiles = tiles_u * tiles_v;
   dim3 grid(static_cast<unsigned>((n_tiles + kFwdWarps - 1) / kFwdWarps), static_cast<unsigned>(n_views));
+#ifndef GSCT_FWD_KERNEL
+#define GSCT_FWD_KERNEL 2  // 2: 2x4 pixel blocks, multiplicative row chain; 1: 8-pixel rows, MUFU per pixel
+#endif
+#if GSCT_FWD_KERNEL == 2
+  k_raster_fwd2<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, tiles_u, n_tiles, images);
+#else
   k_raster_fwd<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, tiles_u, n_tiles, images);
+#endif
   count_launch();
 }
 
