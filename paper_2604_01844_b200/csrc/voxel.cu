@@ -118,6 +118,215 @@ __global__ void __launch_bounds__(256) k_voxel_fwd(const VoxelRec* __restrict__ 
   }
 }
 
+typedef unsigned long long f2_t;  // two packed fp32 values (lo, hi)
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_bc(float x) { return f2_pack(x, x); }
+
+// 32 x 32 bit-matrix transpose across a warp (see raster.cu): lane j's row -> lane l's column.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  const uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const int s = 16 >> t;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~M[t]) | ((y >> s) & M[t])) : ((x & M[t]) | ((y << s) & ~M[t]));
+  }
+  return x;
+}
+
+__device__ __forceinline__ float vox_e(const VoxelRec& r, float dx, float dy, float dz) {
+  // Q00 dx^2 + Q11 dy^2 + Q22 dz^2 + Q01 dx dy + Q02 dx dz + Q12 dy dz
+  return fmaf(dx, fmaf(r.Q00, dx, fmaf(r.Q01, dy, r.Q02 * dz)), fmaf(dy, fmaf(r.Q11, dy, r.Q12 * dz), r.Q22 * dz * dz));
+}
+
+struct __align__(16) StagedVox {
+  float4 p;  // dx_b, dy_b (offsets of the brick origin voxel), z0 - lo_z (exact), rho
+  float4 q;  // Q00, Q11, Q22, Q01
+  float4 r;  // Q02, Q12, c = exp2(2 Q00 sp^2), chain-safe flag
+  uint4 m;   // x mask | y mask << 8, lane mask, lane of the exact-peak row (or ~0), bits of off_z
+};
+
+// Forward v2 (K7): one WARP per 8^3 brick (4 bricks per CTA); lane l owns the two x-rows
+// (y = 2(l & 3), +1; z = l >> 2) of 8 voxels, the rows in the halves of packed f32x2
+// registers. The brick's splat list (ascending index = the reference's per-voxel order) is
+// staged 32 records at a time in warp-private shared memory; each lane walks only the
+// records whose box meets its rows (32x32 warp bit transpose of the staged lane masks).
+// Along x the Gaussian is a 1-D quadratic in the exponent, evaluated multiplicatively
+// (g <- g r, r <- r c: 2 packed FMULs per voxel pair, one MUFU pair per row pair to start),
+// with a per-record safety flag (no fp32 under/overflow anywhere in the brick window)
+// falling back to direct exp2; the row holding an exactly-on-lattice centre also uses the
+// direct path so the peak voxel is rho * exp2(0) = rho exactly (test_voxelizer.cpp:16-22).
+__global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__ rec,
+                                                   const uint32_t* __restrict__ vals,
+                                                   const uint32_t* __restrict__ start,
+                                                   const uint32_t* __restrict__ end, Window win,
+                                                   int nbx, int nby, int n_bricks, float sp,
+                                                   float* __restrict__ volume) {
+  __shared__ StagedVox s_rec[4][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int brick = blockIdx.x * 4 + warp;
+  if (brick >= n_bricks) return;
+  const int bx = brick % nbx, by = (brick / nbx) % nby, bz = brick / (nbx * nby);
+  const int gx0 = win.lo[0] + bx * kBrick, gy0 = win.lo[1] + by * kBrick, gz0 = win.lo[2] + bz * kBrick;
+  const int yp = lane & 3, zl = lane >> 2;
+  const float fy = static_cast<float>(2 * yp) * sp, fzl = static_cast<float>(zl);
+  const uint32_t b = start[brick], e = end[brick];
+  StagedVox* sw = s_rec[warp];
+  float acc0[8], acc1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.f;
+  for (uint32_t base = b; base < e; base += 32) {
+    const int cnt = min(32u, e - base);
+    uint32_t lanes_rel = 0u;
+    if (lane < cnt) {
+      const VoxelRec r = rec[vals[base + lane]];
+      StagedVox s;
+      const int ilx = static_cast<int>(r.lox), ily = static_cast<int>(r.loy), ilz = static_cast<int>(r.loz);
+      const int x_lo = max(ilx - gx0, 0), x_hi = min(static_cast<int>(r.hix) - gx0, kBrick - 1);
+      const int y_lo = max(ily - gy0, 0), y_hi = min(static_cast<int>(r.hiy) - gy0, kBrick - 1);
+      const int z_lo = max(ilz - gz0, 0), z_hi = min(static_cast<int>(r.hiz) - gz0, kBrick - 1);
+      const uint32_t xm = ((2u << x_hi) - 1u) & ~((1u << x_lo) - 1u);
+      const uint32_t ym = ((2u << y_hi) - 1u) & ~((1u << y_lo) - 1u);
+      const uint32_t pairs = ((2u << (y_hi >> 1)) - 1u) & ~((1u << (y_lo >> 1)) - 1u);
+      const uint32_t zs = (0x11111111u >> (4 * (7 - z_hi))) & (0x11111111u << (4 * z_lo));
+      lanes_rel = zs * pairs;
+      const float dxb = fmaf(static_cast<float>(gx0 - ilx), sp, -r.offx);
+      const float dyb = fmaf(static_cast<float>(gy0 - ily), sp, -r.offy);
+      // z offsets are formed per lane from the absolute slice index (fmaf(z - lo, sp, -off)),
+      // and the safety window spans the whole box in z, so z-slab windows reproduce the
+      // full-grid volume bit for bit
+      const float fgz = static_cast<float>(gz0 - ilz);
+      // chain-safety window: x 0..7, rows (y_lo & ~1) .. (y_hi | 1), z_lo .. z_hi
+      const float xa = dxb, xb = dxb + 7.f * sp, xc = dxb + 6.f * sp;
+      const float ya = dyb + static_cast<float>(y_lo & ~1) * sp, yb = dyb + static_cast<float>(y_hi | 1) * sp;
+      const float za = -r.offz, zb = fmaf(static_cast<float>(static_cast<int>(r.hiz) - ilz), sp, -r.offz);
+      float emin = fminf(fminf(fminf(vox_e(r, xa, ya, za), vox_e(r, xa, ya, zb)), fminf(vox_e(r, xa, yb, za), vox_e(r, xa, yb, zb))),
+                         fminf(fminf(vox_e(r, xb, ya, za), vox_e(r, xb, ya, zb)), fminf(vox_e(r, xb, yb, za), vox_e(r, xb, yb, zb))));
+      // D(x) = e(x + sp) - e(x) = Q00 (2 x sp + sp^2) + (Q01 y + Q02 z) sp: linear, extremes at corners
+      float dmax = 0.f;
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx)
+#pragma unroll
+        for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+          for (int cz = 0; cz < 2; ++cz) {
+            const float x = cx ? xc : xa, y = cy ? yb : ya, z = cz ? zb : za;
+            dmax = fmaxf(dmax, fabsf(fmaf(r.Q00, fmaf(2.f * x, sp, sp * sp), fmaf(r.Q01, y, r.Q02 * z) * sp)));
+          }
+      const float c2e = 2.f * r.Q00 * sp * sp;
+      const bool safe = emin > -100.f && dmax < 100.f && c2e > -60.f;
+      // exactly-on-lattice centre inside this brick -> that row takes the direct path
+      uint32_t peak = 0xFFFFFFFFu;
+      const float cxf = r.offx / sp, cyf = r.offy / sp, czf = r.offz / sp;
+      if (cxf == rintf(cxf) && cyf == rintf(cyf) && czf == rintf(czf)) {
+        const int px = ilx + static_cast<int>(cxf) - gx0, py = ily + static_cast<int>(cyf) - gy0,
+                  pz = ilz + static_cast<int>(czf) - gz0;
+        if (px >= 0 && px < kBrick && py >= 0 && py < kBrick && pz >= 0 && pz < kBrick)
+          peak = static_cast<uint32_t>(pz * 4 + (py >> 1));  // the lane owning that row
+      }
+      s.p = make_float4(dxb, dyb, fgz, r.rho);
+      s.q = make_float4(r.Q00, r.Q11, r.Q22, r.Q01);
+      s.r = make_float4(r.Q02, r.Q12, ex2_approx(c2e), safe ? 1.f : 0.f);
+      s.m = make_uint4(xm | (ym << 8), lanes_rel, peak, __float_as_uint(r.offz));
+      sw[lane] = s;
+    }
+    __syncwarp();
+    uint32_t todo = warp_transpose32(lanes_rel, lane);
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1u;
+      const float4 p = sw[j].p;
+      const float4 q = sw[j].q;
+      const float4 rr4 = sw[j].r;
+      const uint4 m = sw[j].m;
+      const uint32_t xm = m.x & 0xFFu;
+      const uint32_t rows = (m.x >> (8 + 2 * yp)) & 3u;
+      const f2_t RHO = f2_pack((rows & 1u) ? p.w : 0.f, (rows & 2u) ? p.w : 0.f);
+      const float dy0 = p.y + fy, dz = fmaf(p.z + fzl, sp, -__uint_as_float(m.w)), dx0 = p.x;
+      const f2_t DY = f2_pack(dy0, dy0 + sp);
+      // e(dx) = Q00 dx^2 + L dx + K,  L = Q01 dy + Q02 dz,  K = Q11 dy^2 + Q12 dy dz + Q22 dz^2
+      const f2_t L = f2_fma(f2_bc(q.w), DY, f2_bc(rr4.x * dz));
+      const f2_t K = f2_fma(DY, f2_fma(f2_bc(q.y), DY, f2_bc(rr4.y * dz)), f2_bc(q.z * dz * dz));
+      f2_t g[8];
+      if (rr4.w != 0.f && m.z != static_cast<uint32_t>(lane)) {
+        const f2_t E0 = f2_fma(L, f2_bc(dx0), f2_add(K, f2_bc(q.x * dx0 * dx0)));
+        const f2_t D0 = f2_fma(L, f2_bc(sp), f2_bc(q.x * fmaf(2.f * dx0, sp, sp * sp)));
+        float e0, e1, d0, d1;
+        f2_unpack(E0, e0, e1);
+        f2_unpack(D0, d0, d1);
+        g[0] = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
+        f2_t ratio = f2_pack(ex2_approx(d0), ex2_approx(d1));
+        const f2_t C2 = f2_bc(rr4.z);
+#pragma unroll
+        for (int k = 1; k < 8; ++k) {
+          g[k] = f2_mul(g[k - 1], ratio);
+          if (k < 7) ratio = f2_mul(ratio, C2);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float dx = fmaf(static_cast<float>(k), sp, dx0);
+          const f2_t ek = f2_fma(f2_add(f2_bc(q.x * dx), L), f2_bc(dx), K);
+          float e0, e1;
+          f2_unpack(ek, e0, e1);
+          g[k] = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float glo, ghi;
+        f2_unpack(g[k], glo, ghi);
+        if (xm & (1u << k)) {
+          acc0[k] += glo;
+          acc1[k] += ghi;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  const int wx = win.hi[0] - win.lo[0], wy = win.hi[1] - win.lo[1];
+  const int z = gz0 + zl;
+  if (z >= win.hi[2]) return;
+  const int x0 = gx0 - win.lo[0];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int y = gy0 + 2 * yp + h;
+    if (y >= win.hi[1]) continue;
+    const float* v = h ? acc1 : acc0;
+    float* row = volume + (static_cast<int64_t>(z - win.lo[2]) * wy + (y - win.lo[1])) * wx;
+    if ((wx & 3) == 0 && x0 + 8 <= wx) {
+      reinterpret_cast<float4*>(row + x0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(row + x0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (x0 + k < wx) row[x0 + k] = v[k];
+    }
+  }
+}
+
 // Spatial walk order for the backward: key = 8^3 brick of the splat's (window-clipped) box
 // corner, value = splat; sorted, consecutive warps then own nearby splats, so the grad
 // volume is re-read from L2 instead of HBM (the walk order does not change any result:
@@ -253,8 +462,16 @@ void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t*
                       float spacing, float* volume, cudaStream_t st) {
   const int64_t bricks = static_cast<int64_t>(nbx) * nby * nbz;
   if (bricks == 0) return;
+#ifndef GSCT_VFWD_KERNEL
+#define GSCT_VFWD_KERNEL 2  // 2: warp per brick, x-row chains, per-lane filtering; 1: CTA per brick
+#endif
+#if GSCT_VFWD_KERNEL == 2
+  k_voxel_fwd2<<<static_cast<unsigned>((bricks + 3) / 4), 128, 0, st>>>(rec, vals, start, end, win, nbx, nby,
+                                                                        static_cast<int>(bricks), spacing, volume);
+#else
   k_voxel_fwd<<<static_cast<unsigned>(bricks), 256, 0, st>>>(rec, vals, start, end, win, nbx, nby,
                                                              spacing, volume);
+#endif
   count_launch();
 }
 

@@ -145,3 +145,34 @@ def test_voxel_contract_errors(ctx):
         gsct.voxelize_backward(gsct.make_cloud("random", 5, seed=2),
                                gsct.GridRegion.covering(gsct.GridSpec.centered((8, 8, 8), 1.0)),
                                np.zeros((8, 8, 7), np.float32), ctx=ctx)
+
+
+@pytest.mark.parametrize("spacing", [0.25, 0.5, 2.0])
+def test_peak_is_density_binary_spacings(ctx, spacing):
+    """Exactly-on-lattice centres at power-of-two spacings, off-centre in the brick (the
+    multiplicative x-chain must not be used for the peak row)."""
+    grid = gsct.GridSpec.centered((21, 19, 23), spacing)
+    origin = -0.5 * spacing * (np.array(grid.dims) - 1)
+    idx = np.array([[3, 5, 7], [13, 9, 15], [18, 2, 20]])
+    pos = origin + spacing * idx
+    cloud = gsct.GaussianCloud(pos, np.full((3, 3), np.log(1.3 * spacing)), np.tile([1.0, 0, 0, 0], (3, 1)),
+                               np.array([0.8, 1.7, 0.35]))
+    vol = gsct.voxelize_full(cloud, grid, ctx=ctx)
+    for (x, y, z), rho in zip(idx, (0.8, 1.7, 0.35)):
+        assert vol[z, y, x] >= np.float32(rho)  # peak term exact; neighbours add >= 0
+
+
+def test_forward_extreme_shapes(ctx, orc):
+    """Needle splats (box corners underflow fp32 exp: the chain-safety fallback) and
+    sub-voxel splats next to ordinary ones."""
+    grid = gsct.GridSpec.centered((30, 28, 26), 0.5)
+    base = gsct.make_cloud("random", 36, seed=61, pos_range=5.0)
+    rng = np.random.default_rng(4)
+    ls = base.log_scales.copy()
+    ls[:12] = np.stack([np.full(12, -3.5), np.full(12, 0.9), np.full(12, -3.0)], axis=1)
+    ls[12:24] = rng.uniform(-4.0, -2.5, size=(12, 3))
+    cloud = gsct.GaussianCloud(base.positions, ls, base.rotations, base.raw_densities)
+    region = gsct.GridRegion.covering(grid)
+    vol = gsct.voxelize(cloud, region, gsct.VoxelSettings(), ctx=ctx)
+    ref, _ = orc.voxelize(cloud, region, gsct.VoxelSettings())
+    assert max_err_rel_peak(vol, ref) <= VOL_TOL
