@@ -664,10 +664,6 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       {
         Phase ph(c, GSCT_PH_RASTER_BWD);
-#ifndef GSCT_BWD_KERNEL
-#define GSCT_BWD_KERNEL 5  // 5: lane per item in bbox-shape order; 2: warp per item (column lanes)
-#endif
-#if GSCT_BWD_KERNEL == 5
         const int64_t items = n * cv;
         uint32_t* k1 = ws<uint32_t>(c, S_KEYS, static_cast<size_t>(items));
         uint32_t* v1 = ws<uint32_t>(c, S_VALS, static_cast<size_t>(items));
@@ -680,9 +676,6 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
         CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
         launch_raster_bwd_lanes(rec, vb.Current(), n, cv, geom->n_u, geom->n_v, gimg, mom, v0, c->stream);
-#else
-        launch_raster_bwd_pairs(rec, n, cv, geom->n_u, geom->n_v, gimg, mom, v0, n_views, c->stream);
-#endif
       }
       CK(cudaGetLastError());
     }

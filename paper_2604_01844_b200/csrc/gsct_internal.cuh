@@ -61,8 +61,9 @@ void launch_splat_prepare(const Cloud& c, PreSplat* pre, DevStats* stats, cudaSt
 void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
                               const Geo& g, const RSet& rs, int bin_ts, RasterRec* rec,
                               uint32_t* tile_count, DevStats* stats, cudaStream_t st);
-// acc: fp64 [11][N] running view-sum (g_pos 3, g_sigma 6, g_raw, sum |dL/dmean2d|)
-// moments: splat-major [N][n_views] x 8 fp32 covering every view of the call
+// (tail.cu) acc: fp64 [11][N] view sum (g_pos 3, g_sigma 6, g_raw, sum |dL/dmean2d|);
+// moments: view-major [n_views][N] x 8 fp32 {t, t du, t dv, t du^2, t du dv, t dv^2,
+// visible, 0} covering every view of the call
 void launch_raster_tail(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
                         const Geo& g, const RSet& rs, const float* moments, double* acc,
                         uint8_t* visible, cudaStream_t st);
@@ -88,11 +89,6 @@ void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint3
 void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                        const uint32_t* end, int64_t n, int n_views, int n_u, int n_v,
                        int tiles_u, int tiles_v, float* images, cudaStream_t st);
-// moments written splat-major at [(i * total_views + view_offset + v) * 8]
-void launch_raster_bwd_pairs(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v,
-                             const float* grad_images, float* moments, int view_offset,
-                             int total_views, cudaStream_t st);
-
 // lane-per-item backward: shape sort keys, then the pixel walk in `order`
 int bwd_vec(int n_u, const float* grad_images);  // 8, 4 or 1 floats per row load
 // returns the number of key bits to sort on

@@ -51,12 +51,6 @@ __global__ void __launch_bounds__(128) k_splat_prepare(Cloud c, PreSplat* __rest
 #ifndef GSCT_PRE_MINB
 #define GSCT_PRE_MINB 8
 #endif
-#ifndef GSCT_MOM_SPLAT_MAJOR
-#define GSCT_MOM_SPLAT_MAJOR 0  // must match raster.cu (moment slot layout)
-#endif
-#ifndef GSCT_TAIL_MINB
-#define GSCT_TAIL_MINB 4
-#endif
 __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const PreSplat* __restrict__ pre, int64_t n,
                                                            const Frame* __restrict__ frames, Geo g,
                                                            RSet rs, int bin_ts,
@@ -103,113 +97,6 @@ __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const 
   warp_add(&st->degenerate, n_degen);
   warp_add(&st->tile_pairs, n_tp);
   warp_add(&st->pixel_pairs, n_pp);
-}
-
-// K4b: one warp per splat, lane l handles views l, l+32, ... of ALL views of the call:
-// re-derives the fp64 projection, turns the fp32 pixel-loop moments into
-// dL/d(amp, mean2d, conic) and runs the reference chain rule up to dL/dSigma. Per-view
-// results are summed with a fixed shuffle tree (ParamGradients::add up to fp64
-// reassociation). Moments are splat-major ([N][V] x 32 B) so a warp's loads are contiguous;
-// view frames are staged in shared memory when they fit.
-// acc layout [11][N]: g_pos(3), g_sigma(00,01,02,11,12,22), g_raw, sum |dL/dmean2d|.
-__global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSplat* __restrict__ pre, int64_t n,
-                                                     const Frame* __restrict__ frames_g, int n_views,
-                                                     Geo g, RSet rs, const float4* __restrict__ moments,
-                                                     int frames_in_smem, double* __restrict__ acc,
-                                                     uint8_t* __restrict__ visible) {
-  extern __shared__ Frame s_frames[];
-  const Frame* frames = frames_g;
-  if (frames_in_smem) {
-    for (int k = threadIdx.x; k < n_views; k += blockDim.x) s_frames[k] = frames_g[k];
-    __syncthreads();
-    frames = s_frames;
-  }
-  const int lane = threadIdx.x & 31;
-  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (i >= n) return;
-  double v[11];
-#pragma unroll
-  for (int k = 0; k < 11; ++k) v[k] = 0.0;
-  bool vis = false;
-  const PreSplat& s = pre[i];
-  if (s.status == 0) {
-    for (int vw = lane; vw < n_views; vw += 32) {
-      Proj p;
-      project_full(frames[vw], g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
-      if (p.degenerate || p.culled) continue;
-      vis = true;
-#if GSCT_MOM_SPLAT_MAJOR
-      const int64_t item = i * n_views + vw;
-#else
-      const int64_t item = static_cast<int64_t>(vw) * n + i;
-#endif
-      const float4 m0 = moments[2 * item];
-      const float4 m1 = moments[2 * item + 1];
-      // m0 = {sum t, sum t du, sum t dv, sum t du^2}, m1 = {sum t du dv, sum t dv^2, -, -}
-      const double amp = p.amplitude;
-      const double a_ = p.conic[0], b_ = p.conic[1], c_ = p.conic[3];
-      const double Mu = m0.y, Mv = m0.z;
-      double gm[2], gc[4];
-      gm[0] = amp * (a_ * Mu + b_ * Mv);
-      gm[1] = amp * (b_ * Mu + c_ * Mv);
-      gc[0] = -0.5 * amp * static_cast<double>(m0.w);
-      gc[1] = -0.5 * amp * static_cast<double>(m1.x);
-      gc[2] = gc[1];
-      gc[3] = -0.5 * amp * static_cast<double>(m1.y);
-      double gp[3], gs[9], gr;
-      raster_chain_rule(frames[vw], g, rs, s.density, s.raw_density, s.sigma, p, static_cast<double>(m0.x), gm,
-                        gc, gp, gs, gr);
-      v[0] += gp[0];
-      v[1] += gp[1];
-      v[2] += gp[2];
-      v[3] += gs[0];
-      v[4] += gs[1];
-      v[5] += gs[2];
-      v[6] += gs[4];
-      v[7] += gs[5];
-      v[8] += gs[8];
-      v[9] += gr;
-      v[10] += sqrt(gm[0] * gm[0] + gm[1] * gm[1]);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 11; ++k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-  }
-  vis = __any_sync(0xffffffffu, vis);
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < 11; ++k) acc[k * n + i] = v[k];
-    visible[i] = static_cast<uint8_t>(vis);
-  }
-}
-
-// Per-splat finalize: covariance_backward (core.hpp:170-191) of the summed dL/dSigma.
-__global__ void __launch_bounds__(128) k_raster_finalize(Cloud c, const double* __restrict__ acc,
-                                                         double* __restrict__ g_pos, double* __restrict__ g_ls,
-                                                         double* __restrict__ g_q, double* __restrict__ g_raw,
-                                                         double* __restrict__ g_pgn) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= c.n) return;
-  const int64_t n = c.n;
-  double gl[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0};
-  Act a;
-  if (activate(c.pos, c.ls, c.q, c.raw, i, a) == 0) {
-    const double s00 = acc[3 * n + i], s01 = acc[4 * n + i], s02 = acc[5 * n + i];
-    const double s11 = acc[6 * n + i], s12 = acc[7 * n + i], s22 = acc[8 * n + i];
-    const double gsig[9] = {s00, s01, s02, s01, s11, s12, s02, s12, s22};
-    covariance_backward(a.scales, a.uq, a.raw_q, gsig, gl, gq);
-  }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    g_pos[3 * i + k] = acc[k * n + i];
-    g_ls[3 * i + k] = gl[k];
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) g_q[4 * i + k] = gq[k];
-  g_raw[i] = acc[9 * n + i];
-  g_pgn[i] = acc[10 * n + i];
 }
 
 __global__ void k_debug_project(const PreSplat* __restrict__ pre, int64_t n, const Frame* __restrict__ frame,
@@ -395,22 +282,6 @@ void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frame
   count_launch();
 }
 
-void launch_raster_tail(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views, const Geo& g,
-                        const RSet& rs, const float* moments, double* acc, uint8_t* visible, cudaStream_t st) {
-  if (n == 0) return;
-  const size_t smem = static_cast<size_t>(n_views) * sizeof(Frame);
-  const bool in_smem = smem <= 24 * 1024;
-  k_raster_tail<<<blocks_for(n * 32, 128), 128, in_smem ? smem : 0, st>>>(
-      pre, n, frames_dev, n_views, g, rs, reinterpret_cast<const float4*>(moments), in_smem ? 1 : 0, acc, visible);
-  count_launch();
-}
-
-void launch_raster_finalize(const Cloud& c, const double* acc, double* g_pos, double* g_ls, double* g_q,
-                            double* g_raw, double* g_pgn, cudaStream_t st) {
-  if (c.n == 0) return;
-  k_raster_finalize<<<blocks_for(c.n, 128), 128, 0, st>>>(c, acc, g_pos, g_ls, g_q, g_raw, g_pgn);
-  count_launch();
-}
 
 void launch_debug_project(const PreSplat* pre, int64_t n, const Frame* frame_dev, const Geo& g, const RSet& rs,
                           int32_t* rect, uint8_t* flags, double* mean2d, double* conic, double* amplitude,

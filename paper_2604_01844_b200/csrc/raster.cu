@@ -59,19 +59,6 @@ __device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
   return d;
 }
 
-// Lane-per-item backward (K4a). The per-(view, splat) pixel loop is small (hundreds of
-// pixels), so warp-cooperative schemes spend more instructions on lane mapping and the
-// cross-lane moment reduction than on pixels. Here ONE LANE owns one item end to end: it
-// walks the bbox rows, each row as 16-byte aligned float4 chunks of the grad image (VEC=4;
-// the <= 3 columns left of u_min / right of u_max in the edge chunks are zeroed and add
-// exact zeros), and accumulates per row, in packed f32x2 arithmetic over column pairs,
-//   s0 = sum t, s1 = sum t k, s2 = sum t k^2,   t = exp2(A du^2 + B du dv + C dv^2) * w,
-// with k = column - round(mean) (du = k - delta, |delta| <= 1/2) and the exponent evaluated
-// directly as a quadratic in k (two packed FMAs per pixel pair, no error accumulation).
-// Rows fold into the six moments {t, t du, t dv, t du^2, t du dv, t dv^2}. No shuffles,
-// no shared memory; every item's result depends only on its own inputs (duplicated splats
-// get bit-identical moments). Items are processed in `order` (sorted by bbox shape, see
-// k_bwd_shape_keys) so the 32 lanes of a warp walk near-identical loop trip counts.
 __global__ void k_emit_tile_pairs(const RasterRec* __restrict__ rec,
                                   const uint32_t* __restrict__ offsets,
                                   const uint32_t* __restrict__ counts, int64_t n, int n_views,
@@ -120,9 +107,6 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, ui
 
 #ifndef GSCT_BWD_ASM
 #define GSCT_BWD_ASM 0
-#endif
-#ifndef GSCT_MOM_SPLAT_MAJOR
-#define GSCT_MOM_SPLAT_MAJOR 0  // must match preprocess.cu (moment slot layout)
 #endif
 #ifndef GSCT_BWD_LOOP
 #define GSCT_BWD_LOOP 1  // 1: predicate-free 4-row main loop + remainder (A/B: 7.6 vs 8.3 ms)
@@ -407,139 +391,19 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd2(const RasterRec*
   }
 }
 
-// One warp per (view, splat) item, grid-stride. Lanes = bbox columns (blocks of <= 32)
-// x row groups; each lane walks its column with stride G = 32 / cw rows. du is constant
-// per lane, so per pixel only {t, t dv, t dv^2} are accumulated and folded with du once.
-// Moments of t = exp(e) * w: {t, t du, t dv, t du^2, t du dv, t dv^2}.
-__global__ void __launch_bounds__(256) k_raster_bwd_pairs(const RasterRec* __restrict__ rec,
-                                                          int64_t n_items, int64_t n, int n_u,
-                                                          int n_v,
-                                                          const float* __restrict__ grad,
-                                                          float4* __restrict__ moments, double inv_n,
-                                                          int view_offset, int total_views) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  RasterRec r_next;
-  if (warp < n_items) r_next = rec[warp];
-  for (int64_t item = warp; item < n_items; item += n_warps) {
-    const RasterRec r = r_next;
-    if (item + n_warps < n_items) r_next = rec[item + n_warps];  // prefetch the next item
-    const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
-    const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
-    const int W = u1 - u0 + 1, H = v1 - v0 + 1;
-    if (W <= 0 || H <= 0) continue;
-    // view = item / n without a 64-bit integer division (exact: the quotient's fractional
-    // part is >= 0.5/n away from an integer, far above the fp64 rounding error)
-    const int view = static_cast<int>((static_cast<double>(item) + 0.5) * inv_n);
-    const float* __restrict__ gi = grad + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(v0) * n_u + u0;
-#if GSCT_BWD_ASM
-    // materialise the per-item base pointer so each load below is one IMAD.WIDE.U32 from a
-    // 32-bit offset instead of a 64-bit add + shift chain
-    asm volatile("mov.b64 %0, %0;" : "+l"(gi));
-#endif
-    float m0 = 0.f, mu = 0.f, mv = 0.f, muu = 0.f, muv = 0.f, mvv = 0.f;
-    for (int cb = 0; cb < W; cb += 32) {
-      const int cw = min(32, W - cb);
-      // lane -> (col, grp) and G = 32 / cw without integer division: floor((x + 0.5) / cw)
-      const float rc = rcp_approx(static_cast<float>(cw));
-      const int G = static_cast<int>(32.5f * rc);
-      const int grp = static_cast<int>((static_cast<float>(lane) + 0.5f) * rc);
-      const int col = lane - grp * cw;
-      if (grp >= G) continue;  // idle lanes (32 % cw)
-      const float du = static_cast<float>(cb + col) - r.mo_u;
-      const float a2 = r.A * du * du;
-      const float bdu = r.B * du;
-      float dv = static_cast<float>(grp) - r.mo_v;
-      const float fG = static_cast<float>(G);
-      float t0 = 0.f, t1 = 0.f, t2 = 0.f;
-      // unsigned 32-bit element offsets from the bbox corner: one IMAD.WIDE.U32 per load
-      uint32_t off = static_cast<uint32_t>(grp * n_u + cb + col);
-      const uint32_t stride = static_cast<uint32_t>(G * n_u);
-      // rows of this lane: grp, grp + G, ... < H. Main loop: four rows per step, four grad
-      // loads in flight, no predicates; then at most three remainder rows.
-      int v = grp;
-#if GSCT_BWD_LOOP == 0
-      for (; v < H; v += 4 * G) {
-        float w[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) w[k] = (v + k * G < H) ? __ldg(gi + (off + k * stride)) : 0.f;
-#else
-      for (; v + 3 * G < H; v += 4 * G) {
-        const float w0 = __ldg(gi + off), w1 = __ldg(gi + (off + stride)), w2 = __ldg(gi + (off + 2 * stride)),
-                    w3 = __ldg(gi + (off + 3 * stride));
-        const float w[4] = {w0, w1, w2, w3};
-#endif
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float ex = ex2_approx(fmaf(dv, fmaf(r.C, dv, bdu), a2));
-          const float tt = ex * w[k];
-          t0 += tt;
-          const float tv = tt * dv;
-          t1 += tv;
-          t2 = fmaf(tv, dv, t2);
-          dv += fG;
-        }
-        off += 4 * stride;
-      }
-      for (; v < H; v += G) {
-        const float w = __ldg(gi + off);
-        const float ex = ex2_approx(fmaf(dv, fmaf(r.C, dv, bdu), a2));
-        const float tt = ex * w;
-        t0 += tt;
-        const float tv = tt * dv;
-        t1 += tv;
-        t2 = fmaf(tv, dv, t2);
-        dv += fG;
-        off += stride;
-      }
-      m0 += t0;
-      mu = fmaf(t0, du, mu);
-      mv += t1;
-      const float t0du = t0 * du;
-      muu = fmaf(t0du, du, muu);
-      muv = fmaf(t1, du, muv);
-      mvv += t2;
-    }
-    // Transposed butterfly: 6 moments (padded to 8) in 9 shuffles instead of 30. After the
-    // three halving exchanges lane l holds a partial of moment ((l>>4)&1)*4+((l>>3)&1)*2+
-    // ((l>>2)&1); two plain xor steps finish the sum inside each 4-lane group.
-    {
-      const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
-      float w0, w1, w2, w3;
-      {
-        float s;
-        s = __shfl_xor_sync(0xffffffffu, b16 ? m0 : muv, 16);  w0 = (b16 ? muv : m0) + s;
-        s = __shfl_xor_sync(0xffffffffu, b16 ? mu : mvv, 16);  w1 = (b16 ? mvv : mu) + s;
-        s = __shfl_xor_sync(0xffffffffu, b16 ? mv : 0.f, 16);  w2 = (b16 ? 0.f : mv) + s;
-        s = __shfl_xor_sync(0xffffffffu, b16 ? muu : 0.f, 16); w3 = (b16 ? 0.f : muu) + s;
-      }
-      float x0, x1;
-      {
-        float s;
-        s = __shfl_xor_sync(0xffffffffu, b8 ? w0 : w2, 8); x0 = (b8 ? w2 : w0) + s;
-        s = __shfl_xor_sync(0xffffffffu, b8 ? w1 : w3, 8); x1 = (b8 ? w3 : w1) + s;
-      }
-      float y = (b4 ? x1 : x0) + __shfl_xor_sync(0xffffffffu, b4 ? x0 : x1, 4);
-      y += __shfl_xor_sync(0xffffffffu, y, 2);
-      y += __shfl_xor_sync(0xffffffffu, y, 1);
-#if GSCT_MOM_SPLAT_MAJOR
-      // splat-major slot (i, view_offset + view) so the tail's per-splat loads are contiguous
-      const int64_t i = item - static_cast<int64_t>(view) * n;
-      const int64_t slot = i * total_views + view_offset + view;
-#else
-      // view-major slot (view_offset + view, i): consecutive items write consecutive sectors
-      const int64_t slot = static_cast<int64_t>(view_offset) * n + item;
-#endif
-      // one full 32 B sector per item from 8 lanes (no partial-sector writes to DRAM)
-      if ((lane & 3) == 0) {
-        const int m = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
-        reinterpret_cast<float*>(moments)[slot * 8 + m] = y;
-      }
-    }
-  }
-}
-
+// Lane-per-item backward (K4a). The per-(view, splat) pixel loop is small (hundreds of
+// pixels), so warp-cooperative schemes spend more instructions on lane mapping and the
+// cross-lane moment reduction than on pixels. Here ONE LANE owns one item end to end: it
+// walks the bbox rows, each row as 16-byte aligned float4 chunks of the grad image (VEC=4;
+// the <= 3 columns left of u_min / right of u_max in the edge chunks are zeroed and add
+// exact zeros), and accumulates per row, in packed f32x2 arithmetic over column pairs,
+//   s0 = sum t, s1 = sum t k, s2 = sum t k^2,   t = exp2(A du^2 + B du dv + C dv^2) * w,
+// with k = column - round(mean) (du = k - delta, |delta| <= 1/2) and the exponent evaluated
+// directly as a quadratic in k (two packed FMAs per pixel pair, no error accumulation).
+// Rows fold into the six moments {t, t du, t dv, t du^2, t du dv, t dv^2}. No shuffles,
+// no shared memory; every item's result depends only on its own inputs (duplicated splats
+// get bit-identical moments). Items are processed in `order` (sorted by bbox shape, see
+// k_bwd_shape_keys) so the 32 lanes of a warp walk near-identical loop trip counts.
 __device__ __forceinline__ void ldg_v8(const float* p, float (&w)[8]) {
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(w[0]), "=f"(w[1]), "=f"(w[2]), "=f"(w[3]), "=f"(w[4]), "=f"(w[5]), "=f"(w[6]), "=f"(w[7])
@@ -564,7 +428,12 @@ __global__ void __launch_bounds__(256, GSCT_LANES_MINB) k_raster_bwd_lanes(const
   const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
   const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
   const int W = u1 - u0 + 1, H = v1 - v0 + 1;
-  if (W <= 0 || H <= 0) return;
+  float4* dst = reinterpret_cast<float4*>(moments + (static_cast<int64_t>(view_offset) * n + item) * 8);
+  if (W <= 0 || H <= 0) {  // culled or degenerate in this view: visibility flag 0 for the tail
+    dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   // view = item / n without a 64-bit integer division (exact: the quotient's fractional
   // part is >= 0.5/n away from an integer, far above the fp64 rounding error)
   const int view = static_cast<int>((static_cast<double>(item) + 0.5) * inv_n);
@@ -673,10 +542,10 @@ __global__ void __launch_bounds__(256, GSCT_LANES_MINB) k_raster_bwd_lanes(const
       kA = K0;
     }
   }
-  // view-major slot (view_offset + view, i) = view_offset * n + item; [m0 mu mv muu muv mvv 0 0]
-  float4* dst = reinterpret_cast<float4*>(moments + (static_cast<int64_t>(view_offset) * n + item) * 8);
+  // view-major slot (view_offset + view, i) = view_offset * n + item;
+  // [m0 mu mv muu muv mvv visible=1 0]
   dst[0] = make_float4(m0, mu, mv, muu);
-  dst[1] = make_float4(muv, mvv, 0.f, 0.f);
+  dst[1] = make_float4(muv, mvv, 1.f, 0.f);
 }
 
 // Bbox-shape sort keys for the lane-per-item backward: (chunks per row, rows), each clamped
@@ -793,20 +662,5 @@ void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_
   count_launch();
 }
 
-void launch_raster_bwd_pairs(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v,
-                             const float* grad_images, float* moments, int view_offset, int total_views,
-                             cudaStream_t st) {
-  const int64_t items = n * n_views;
-  if (items == 0) return;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (items + 7) / 8;  // 8 warps per block
-  const unsigned blocks = static_cast<unsigned>(want < static_cast<int64_t>(sms) * 16 ? want : static_cast<int64_t>(sms) * 16);
-  k_raster_bwd_pairs<<<blocks, 256, 0, st>>>(rec, items, n, n_u, n_v, grad_images,
-                                             reinterpret_cast<float4*>(moments), 1.0 / static_cast<double>(n),
-                                             view_offset, total_views);
-  count_launch();
-}
 
 }  // namespace gsct_dev

@@ -295,6 +295,9 @@ struct Proj {
 // detail::project_full (projector.hpp:143-236)
 // The view-independent part (det Sigma > 0 check and Sigma^-1, projector.hpp:151-156) is
 // hoisted into prepare_splat(); its results are passed in (sigma_inv, det_ok).
+// kBox = false (backward tail): the bounding box, the eigenvalue-ratio test and the cull
+// are skipped -- the caller already knows the splat is visible in this view.
+template <bool kBox = true>
 __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, const double* position,
                                              const double* cov3d, const double* sigma_inv, bool det_ok,
                                              double density, const RSet& rs, Proj& p) {
@@ -408,11 +411,13 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
     p.k = sqrt(det_raw / det2(cr));
   }
   const double dt2 = det2(cr);
-  const double lam_max = max_eig2(cr);
-  const double lam_min = dt2 / dmax_(lam_max, DBL_MIN);
-  if (!(dt2 > 0.0) || !(lam_max / lam_min < 1e12) || !isfinite(dt2)) {
-    p.degenerate = true;
-    return;
+  if (kBox) {
+    const double lam_max = max_eig2(cr);
+    const double lam_min = dt2 / dmax_(lam_max, DBL_MIN);
+    if (!(dt2 > 0.0) || !(lam_max / lam_min < 1e12) || !isfinite(dt2)) {
+      p.degenerate = true;
+      return;
+    }
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) p.cov2d[k] = cr[k];
@@ -421,6 +426,10 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
   p.conic[2] = -cr[2] / dt2;
   p.conic[3] = cr[0] / dt2;
   p.amplitude = p.mu * density * p.k;
+  if (!kBox) {
+    p.culled = false;
+    return;
+  }
   p.culled = !splat_bbox(p.amplitude, p.cov2d, p.mean2d, rs.tau_cut, g.n_u, g.n_v, p.rect,
                          rs.sigma_cap, rs.bounding);
   if (p.culled) {
