@@ -351,15 +351,16 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     pairs_per_launch = stats.pixel_pairs / launches_per_step
     achieved_gbs = algo_bytes / (avg_ms / 1e3) / 1e9
     pair_rate = pairs_per_launch / (avg_ms / 1e3)
+    kernel = "k_raster_fwd2" if dom == "raster_fwd" else "k_raster_bwd_lanes"
     traffic = None  # dram read+write bytes per launch from the committed ncu --set full capture
     try:
         prof = json.loads((ROOT / "profiles" / "r1" / "summary.json").read_text())
-        hit = [d for d in prof if d["kernel"] == ("k_raster_fwd" if dom == "raster_fwd" else "k_raster_bwd_pairs")]
+        hit = [d for d in prof if d["kernel"] == kernel and "dram_bytes" in d]
         if hit and args.config == "c2":
-            traffic = int(hit[0]["dram_bytes"])
+            traffic = int(np.mean([d["dram_bytes"] for d in hit]))
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": "k_raster_fwd" if dom == "raster_fwd" else "k_raster_bwd_pairs",
+    roofline = {"bound": "hbm", "kernel": kernel,
                 "achieved": round(achieved_gbs, 2), "peak": hbm_peak,
                 "unit": "GB/s", "frac": round(achieved_gbs / hbm_peak, 4), "traffic": traffic,
                 "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(algo_bytes),

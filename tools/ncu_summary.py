@@ -38,15 +38,21 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12
               "s": 1e3, "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}
 
 
-def raw(rep: str) -> tuple[list[str], list[str], list[str]]:
+def raw(rep: str) -> tuple[list[str], list[str], list[list[str]]]:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    return rows[0], rows[1], rows[2]
+    return rows[0], rows[1], rows[2:]
 
 
-def summarise(rep: str) -> dict:
-    h, units, v = raw(rep)
-    d = {"kernel": v[h.index("Kernel Name")].split("(")[0].split("::")[-1] if "Kernel Name" in h else Path(rep).stem}
+def kname(full: str) -> str:
+    """Bare kernel name: text before the first template/argument list, last scope."""
+    full = full.replace("<unnamed>", "anon").replace("(anonymous namespace)", "anon")
+    cut = min([i for i in (full.find("<"), full.find("(")) if i >= 0] or [len(full)])
+    return full[:cut].replace("void ", "").split("::")[-1].strip()
+
+
+def summarise_row(h: list[str], units: list[str], v: list[str], stem: str) -> dict:
+    d = {"kernel": kname(v[h.index("Kernel Name")]) if "Kernel Name" in h else stem}
     for key, (metric, _) in METRICS.items():
         if metric in h:
             i = h.index(metric)
@@ -68,12 +74,34 @@ def summarise(rep: str) -> dict:
     return d
 
 
+def summarise(rep: str) -> list[dict]:
+    """One entry per captured launch of the report."""
+    h, units, vals = raw(rep)
+    return [summarise_row(h, units, v, Path(rep).stem) for v in vals if len(v) == len(h)]
+
+
+def launch_shares(path: str) -> list[tuple[str, int, float]]:
+    """(kernel, launches, total ms) from a --metrics gpu__time_duration.sum launch list."""
+    agg: dict[str, list] = {}
+    with open(path) as f:
+        lines = [ln for ln in f if ln.startswith('"')]
+    for r in csv.DictReader(io.StringIO("".join(lines))):
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = kname(r["Kernel Name"])
+        ms = float(r["Metric Value"].replace(",", "")) * UNIT_SCALE.get(r["Metric Unit"], 1e-6)
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += ms
+    return sorted(((k, v[0], v[1]) for k, v in agg.items()), key=lambda t: -t[2])
+
+
 def main() -> None:
     tag = sys.argv[1]
     reps = sorted(glob.glob(sys.argv[2]))
     out = ROOT / "profiles" / tag
     out.mkdir(parents=True, exist_ok=True)
-    rows = [summarise(r) for r in reps]
+    rows = [d for r in reps for d in summarise(r)]
     (out / "summary.json").write_text(json.dumps(rows, indent=1))
     lines = ["| kernel | ms (ncu) | DRAM MB | issue % | XU % | FMA % | ALU % | FP64 % | warps % | regs | top stall |",
              "|---|---|---|---|---|---|---|---|---|---|---|"]
@@ -83,9 +111,14 @@ def main() -> None:
                      f"{d.get('issue_active_pct', 0):.1f} | {d.get('xu_pipe_pct', 0):.1f} | {d.get('fma_pipe_pct', 0):.1f} | "
                      f"{d.get('alu_pipe_pct', 0):.1f} | {d.get('fp64_pipe_pct', 0):.1f} | {d.get('warps_active_pct', 0):.1f} | "
                      f"{int(d.get('registers', 0))} | {top[0]} {top[1]:.2f} |")
-    (out / "summary.md").write_text("\n".join(lines) + "\n")
     if len(sys.argv) > 3:
         shutil.copy(sys.argv[3], out / "launches.csv")
+        sh = launch_shares(sys.argv[3])
+        tot = sum(t[2] for t in sh) or 1.0
+        lines += ["", "Launch list (`--metrics gpu__time_duration.sum --clock-control none`, cold-cache, serialised):", "",
+                  "| kernel | launches | total ms | share |", "|---|---|---|---|"]
+        lines += [f"| {k} | {c} | {ms:.3f} | {100 * ms / tot:.1f}% |" for k, c, ms in sh]
+    (out / "summary.md").write_text("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 
