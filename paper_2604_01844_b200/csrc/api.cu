@@ -24,7 +24,7 @@ namespace {
 enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
-  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_ACC, S_SAVED,
+  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED,
   S_COUNT_SLOTS
 };
 
@@ -546,9 +546,10 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     const RSet r = make_rs(rs);
     c->saved_valid = false;
     PreSplat* pre = ws<PreSplat>(c, S_PRE, static_cast<size_t>(n) + 1);
+    PreSplat* pre_aos = ws<PreSplat>(c, S_PRE_AOS, static_cast<size_t>(n) + 1);
     if (n > 0) {
       Phase ph(c, GSCT_PH_RASTER_SETUP);
-      launch_splat_prepare(d, pre, c->dstats, c->stream);
+      launch_splat_prepare(d, pre, pre_aos, c->dstats, c->stream);
     }
     // save-for-backward keeps every view's records in one buffer for the backward call
     RasterRec* saved = c->save_fb && n > 0 ? ws<RasterRec>(c, S_SAVED, static_cast<size_t>(n) * n_views) : nullptr;
@@ -639,10 +640,11 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     const bool reuse = c->save_fb && c->saved_valid && n > 0 &&
                        c->saved_key == raster_call_key(cloud, geom, angles, n_views, rs);
     PreSplat* pre = ws<PreSplat>(c, S_PRE, un + 1);
+    PreSplat* pre_aos = ws<PreSplat>(c, S_PRE_AOS, un + 1);
     double* acc = ws<double>(c, S_ACC, 11 * un + 1);
     if (n > 0 && !reuse) {
       Phase ph(c, GSCT_PH_RASTER_SETUP);
-      launch_splat_prepare(d, pre, c->dstats, c->stream);
+      launch_splat_prepare(d, pre, pre_aos, c->dstats, c->stream);
     }
     RasterRec* saved = reuse ? ws<RasterRec>(c, S_SAVED, un * n_views) : nullptr;
     const int tiles_u = (geom->n_u + kTile - 1) / kTile, tiles_v = (geom->n_v + kTile - 1) / kTile;
@@ -681,7 +683,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     }
     if (n > 0 && n_views > 0) {
       Phase ph(c, GSCT_PH_RASTER_TAIL);
-      launch_raster_tail(pre, n, dframes, n_views, g, r, mom, acc, gv, c->stream);
+      launch_raster_tail(pre_aos, n, dframes, n_views, g, r, mom, acc, gv, c->stream);
       launch_raster_finalize(d, acc, gp, gl, gq, gr, gn, c->stream);
     }
     if (out->location == GSCT_HOST && n > 0) {
@@ -939,7 +941,7 @@ int gsct_debug_project(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     double* damp = ws<double>(c, S_DBG4, un);
     c->saved_valid = false;  // S_PRE is reused below
     PreSplat* pre = ws<PreSplat>(c, S_PRE, un);
-    launch_splat_prepare(d, pre, c->dstats, c->stream);
+    launch_splat_prepare(d, pre, ws<PreSplat>(c, S_PRE_AOS, un), c->dstats, c->stream);
     launch_debug_project(pre, d.n, df, make_geo(geom), make_rs(rs), drect, dflags, dmean, dconic, damp,
                          c->stream);
     CK(cudaMemcpyAsync(rect, drect, 4 * un * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
@@ -977,7 +979,7 @@ int gsct_debug_tile_pairs(gsct_ctx c, const gsct_cloud* cloud, const gsct_geomet
     uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * n_views);
     c->saved_valid = false;  // S_PRE / S_REC are reused below
     PreSplat* pre = ws<PreSplat>(c, S_PRE, static_cast<size_t>(n));
-    launch_splat_prepare(d, pre, c->dstats, c->stream);
+    launch_splat_prepare(d, pre, ws<PreSplat>(c, S_PRE_AOS, static_cast<size_t>(n)), c->dstats, c->stream);
     launch_raster_preprocess(pre, n, dframes, n_views, make_geo(geom), make_rs(rs), ts, rec, cnt, c->dstats,
                              c->stream);
     uint32_t *dk, *dv, *start, *end;

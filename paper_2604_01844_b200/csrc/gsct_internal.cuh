@@ -57,14 +57,15 @@ struct Window {
 };
 
 // ---- launch wrappers (defined in preprocess.cu / raster.cu / voxel.cu) ----
-void launch_splat_prepare(const Cloud& c, PreSplat* pre, DevStats* stats, cudaStream_t st);
+// pre: structure-of-arrays set-up (pre_store/pre_load); pre_aos: the same, array-of-structs
+void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevStats* stats, cudaStream_t st);
 void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
                               const Geo& g, const RSet& rs, int bin_ts, RasterRec* rec,
                               uint32_t* tile_count, DevStats* stats, cudaStream_t st);
 // (tail.cu) acc: fp64 [11][N] view sum (g_pos 3, g_sigma 6, g_raw, sum |dL/dmean2d|);
 // moments: view-major [n_views][N] x 8 fp32 {t, t du, t dv, t du^2, t du dv, t dv^2,
 // visible, 0} covering every view of the call
-void launch_raster_tail(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
+void launch_raster_tail(const PreSplat* pre_aos, int64_t n, const Frame* frames_dev, int n_views,
                         const Geo& g, const RSet& rs, const float* moments, double* acc,
                         uint8_t* visible, cudaStream_t st);
 void launch_raster_finalize(const Cloud& c, const double* acc, double* g_pos, double* g_ls,

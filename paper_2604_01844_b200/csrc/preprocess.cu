@@ -34,14 +34,19 @@ __device__ __forceinline__ RasterRec empty_rec() {
 
 // View-independent pre-pass, one thread per splat: activation, Sigma, det test, Sigma^-1
 // (computed once instead of once per view; identical values, so boxes stay bit-exact).
+// Writes the set-up twice: structure-of-arrays for the per-(view, splat) set-up kernel
+// (coalesced field loads) and array-of-structs for the backward tail (lazy L1 re-reads
+// keep its register pressure down).
 __global__ void __launch_bounds__(128) k_splat_prepare(Cloud c, PreSplat* __restrict__ pre,
+                                                       PreSplat* __restrict__ pre_aos,
                                                        DevStats* __restrict__ st) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= c.n) return;
   PreSplat s;
   prepare_splat(c.pos, c.ls, c.q, c.raw, i, s);
   if (s.status) flag_error(st, i, s.status);
-  pre[i] = s;
+  pre_store(pre, c.n, i, s);
+  pre_aos[i] = s;
 }
 
 // K1: one thread per (splat, view): project_full -> splat_bbox from the pre-pass, then the
@@ -63,7 +68,8 @@ __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const 
   if (i < n) {
     RasterRec r = empty_rec();
     uint32_t cnt = 0;
-    const PreSplat& s = pre[i];
+    PreSplat s;
+    pre_load(pre, n, i, s);
     if (s.status == 0) {
       Proj p;
       project_full(frames[v], g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
@@ -104,7 +110,8 @@ __global__ void k_debug_project(const PreSplat* __restrict__ pre, int64_t n, con
                                 double* amplitude) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const PreSplat& s = pre[i];
+  PreSplat s;
+    pre_load(pre, n, i, s);
   if (s.status) return;
   Proj p;
   project_full(*frame, g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
@@ -267,9 +274,9 @@ inline unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n +
 
 }  // namespace
 
-void launch_splat_prepare(const Cloud& c, PreSplat* pre, DevStats* stats, cudaStream_t st) {
+void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevStats* stats, cudaStream_t st) {
   if (c.n == 0) return;
-  k_splat_prepare<<<blocks_for(c.n, 128), 128, 0, st>>>(c, pre, stats);
+  k_splat_prepare<<<blocks_for(c.n, 128), 128, 0, st>>>(c, pre, pre_aos, stats);
   count_launch();
 }
 

@@ -664,6 +664,31 @@ struct PreSplat {
   int status;  // 0 ok, 1 non-finite parameter, 2 zero quaternion
 };
 
+// PreSplat buffers are stored structure-of-arrays (same total size as n PreSplat structs):
+// double field f of splat i at d[f * n + i] (23 doubles: pos, sigma, sigma_inv, density,
+// raw_density), then det_ok and status as int arrays. A warp's loads of one field are one
+// coalesced 256 B request instead of 32 strided 184 B structs.
+constexpr int kPreDoubles = 23;
+static_assert(sizeof(PreSplat) == kPreDoubles * 8 + 8, "PreSplat layout");
+__device__ __forceinline__ void pre_store(PreSplat* buf, int64_t n, int64_t i, const PreSplat& s) {
+  double* d = reinterpret_cast<double*>(buf);
+  const double* src = reinterpret_cast<const double*>(&s);
+#pragma unroll
+  for (int f = 0; f < kPreDoubles; ++f) d[f * n + i] = src[f];
+  int* ip = reinterpret_cast<int*>(d + kPreDoubles * n);
+  ip[i] = s.det_ok;
+  ip[n + i] = s.status;
+}
+__device__ __forceinline__ void pre_load(const PreSplat* buf, int64_t n, int64_t i, PreSplat& s) {
+  const double* d = reinterpret_cast<const double*>(buf);
+  double* dst = reinterpret_cast<double*>(&s);
+#pragma unroll
+  for (int f = 0; f < kPreDoubles; ++f) dst[f] = __ldg(d + f * n + i);
+  const int* ip = reinterpret_cast<const int*>(d + kPreDoubles * n);
+  s.det_ok = __ldg(ip + i);
+  s.status = __ldg(ip + n + i);
+}
+
 __device__ __forceinline__ void prepare_splat(const double* __restrict__ pos, const double* __restrict__ ls,
                                               const double* __restrict__ q, const double* __restrict__ raw,
                                               int64_t i, PreSplat& s) {

@@ -21,7 +21,7 @@ namespace {
 #ifndef GSCT_TAIL_MINB
 #define GSCT_TAIL_MINB 4  // 128 registers
 #endif
-__global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSplat* __restrict__ pre, int64_t n,
+__global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSplat* __restrict__ pre /* AoS */, int64_t n,
                                                      const Frame* __restrict__ frames_g, int n_views,
                                                      Geo g, RSet rs, const float4* __restrict__ moments,
                                                      int frames_in_smem, double* __restrict__ acc,
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
   for (int k = 0; k < 11; ++k) v[k] = 0.0;
   bool vis = false;
   if (live) {
-    const PreSplat& s = pre[i];
+    const PreSplat& s = pre[i];  // array-of-structs copy (fields re-read from L1 as needed)
     if (s.status == 0) {
       for (int vw = q; vw < n_views; vw += 4) {
         const int64_t item = static_cast<int64_t>(vw) * n + i;
