@@ -750,7 +750,9 @@ void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window
     launch_voxel_preprocess(d, grid, win, vs->tau_cut, vs->sigma_cap, rec, nullptr, nullptr, nullptr,
                             nullptr, c->dstats, c->stream);
   }
-  // spatial walk order: sort splats by the 8^3 brick of their box corner
+#ifndef GSCT_VBWD_LANES
+#define GSCT_VBWD_LANES 1  // 1: lane per splat (region/shape order); 0: warp per splat (brick order)
+#endif
   uint32_t* order = nullptr;
   {
     Phase ph(c, GSCT_PH_VOXEL_BIN);
@@ -761,9 +763,16 @@ void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window
     uint32_t* v1 = ws<uint32_t>(c, S_VALS, static_cast<size_t>(n));
     uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, static_cast<size_t>(n));
     uint32_t* v2 = ws<uint32_t>(c, S_VALS2, static_cast<size_t>(n));
-    launch_voxel_order_keys(rec, n, win, nbx, nby, k1, v1, c->stream);
+    int end_bit;
+    if (GSCT_VBWD_LANES) {
+      end_bit = launch_voxel_lane_keys(rec, n, win, voxel_bwd_vec(win, grad), k1, v1, c->stream);
+      if (end_bit > 32) end_bit = 32;
+    } else {
+      // spatial walk order: sort splats by the 8^3 brick of their box corner
+      launch_voxel_order_keys(rec, n, win, nbx, nby, k1, v1, c->stream);
+      end_bit = bits_for(static_cast<uint64_t>(nbx) * nby * nbz + 1);
+    }
     cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
-    const int end_bit = bits_for(static_cast<uint64_t>(nbx) * nby * nbz + 1);
     size_t tmp_bytes = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(n), 0, end_bit, c->stream));
     void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
@@ -772,7 +781,10 @@ void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window
   }
   {
     Phase ph(c, GSCT_PH_VOXEL_BWD);
-    launch_voxel_bwd_pairs(rec, order, n, win, static_cast<float>(grid.spacing), grad, mom, c->stream);
+    if (GSCT_VBWD_LANES)
+      launch_voxel_bwd_lanes(rec, order, n, win, static_cast<float>(grid.spacing), grad, mom, c->stream);
+    else
+      launch_voxel_bwd_pairs(rec, order, n, win, static_cast<float>(grid.spacing), grad, mom, c->stream);
   }
   CK(cudaGetLastError());
 }

@@ -107,6 +107,13 @@ void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t*
                       float spacing, float* volume, cudaStream_t st);
 void launch_voxel_order_keys(const VoxelRec* rec, int64_t n, const Window& win, int nbx, int nby,
                              uint32_t* keys, uint32_t* vals, cudaStream_t st);
+// lane-per-splat voxel backward: row-load width (8 or 1), walk-order keys (returns key
+// bits), the pixel walk
+int voxel_bwd_vec(const Window& win, const float* grad_volume);
+int launch_voxel_lane_keys(const VoxelRec* rec, int64_t n, const Window& win, int vec, uint32_t* keys,
+                           uint32_t* vals, cudaStream_t st);
+void launch_voxel_bwd_lanes(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
+                            float spacing, const float* grad_volume, float* moments, cudaStream_t st);
 // order: splat walk order (a permutation of [0, n)) or nullptr for index order
 void launch_voxel_bwd_pairs(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
                             float spacing, const float* grad_volume, float* moments, cudaStream_t st);

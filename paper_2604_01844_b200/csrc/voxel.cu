@@ -444,6 +444,158 @@ __global__ void __launch_bounds__(256) k_voxel_bwd_pairs(const VoxelRec* __restr
   }
 }
 
+__device__ __forceinline__ void ldg_v8(const float* p, float (&w)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(w[0]), "=f"(w[1]), "=f"(w[2]), "=f"(w[3]), "=f"(w[4]), "=f"(w[5]), "=f"(w[6]), "=f"(w[7])
+               : "l"(p));
+}
+
+// Voxel backward v2 (K8a): ONE LANE per splat (the raster backward's lane-per-item scheme).
+// The lane walks the (window-clipped) box as x-rows of 32-byte aligned 8-voxel chunks of
+// the grad volume (VEC = 8; VEC = 1 scalar fallback for unaligned windows; voxels outside
+// the box in the edge chunks are zeroed), accumulating per row, in packed f32x2 over voxel
+// pairs, s0 = sum t, s1 = sum t k, s2 = sum t k^2 with t = exp2(e) * w and
+// dx = sp k - delta (k = x - round(centre), |delta| <= sp/2). The exponent along the row is a
+// quadratic in k evaluated directly. Rows fold into the ten moments
+// {t, t dx, t dy, t dz, t dx^2, t dy^2, t dz^2, t dx dy, t dx dz, t dy dz}. No shuffles; each
+// splat's sums depend only on its own inputs. Splats run in `order` (detector-region major,
+// then box shape) so warps see uniform trip counts and the grad volume stays L2-resident.
+template <int VEC>
+__global__ void __launch_bounds__(256, 4) k_voxel_bwd_lanes(const VoxelRec* __restrict__ rec,
+                                                            const uint32_t* __restrict__ order, int64_t n,
+                                                            Window win, float sp, const float* __restrict__ grad,
+                                                            float* __restrict__ mom) {
+  constexpr int CW = VEC == 8 ? 8 : 4;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t i = order ? static_cast<int64_t>(__ldg(order + t)) : t;
+  const VoxelRec r = rec[i];
+  const int x0 = max(static_cast<int>(r.lox), win.lo[0]), y0 = max(static_cast<int>(r.loy), win.lo[1]),
+            z0 = max(static_cast<int>(r.loz), win.lo[2]);
+  const int W = min(static_cast<int>(r.hix), win.hi[0] - 1) - x0 + 1,
+            H = min(static_cast<int>(r.hiy), win.hi[1] - 1) - y0 + 1,
+            D = min(static_cast<int>(r.hiz), win.hi[2] - 1) - z0 + 1;
+  if (W <= 0 || H <= 0 || D <= 0) return;  // moments were zero-filled
+  const int wx = win.hi[0] - win.lo[0], wy = win.hi[1] - win.lo[1];
+  const int xa = VEC > 1 ? x0 - ((x0 - win.lo[0]) & (VEC - 1)) : x0;  // aligned first column
+  const int lead = x0 - xa, ncol = lead + W, nch = (ncol + CW - 1) / CW;
+  // k = x - xc (xc = round of the centre's x index); dx = (x - lo) sp - off = sp k - delta
+  const float cxf = r.lox + r.offx / sp;
+  const float xc = rintf(cxf);
+  const float delta = fmaf(r.lox - xc, sp, r.offx);  // off - (xc - lo) sp
+  const float fk0 = static_cast<float>(xa) - xc;      // k of the first walked column
+  const float sp2 = sp * sp;
+  const f2_t A2 = f2_bc(r.Q00 * sp2);
+  const f2_t TWO2 = f2_bc(2.f);
+  const f2_t K0 = f2_pack(fk0, fk0 + 1.f);
+  const float* __restrict__ gz = grad + (static_cast<int64_t>(z0 - win.lo[2]) * wy + (y0 - win.lo[1])) * wx +
+                                 (xa - win.lo[0]);
+  float m[10];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) m[k] = 0.f;
+  for (int zz = 0; zz < D; ++zz) {
+    const float dz = fmaf(static_cast<float>(z0 + zz) - r.loz, sp, -r.offz);
+    const float* __restrict__ prow = gz + static_cast<int64_t>(zz) * wy * wx;
+    for (int yy = 0; yy < H; ++yy, prow += wx) {
+      const float dy = fmaf(static_cast<float>(y0 + yy) - r.loy, sp, -r.offy);
+      // e(dx) = Q00 dx^2 + L dx + K;  in k: A' k^2 + B' k + C'
+      const float L = fmaf(r.Q01, dy, r.Q02 * dz);
+      const float K = fmaf(dy, fmaf(r.Q11, dy, r.Q12 * dz), r.Q22 * dz * dz);
+      const float bp = sp * fmaf(-2.f * r.Q00, delta, L);
+      const float cp = fmaf(delta, fmaf(r.Q00, delta, -L), K);
+      const f2_t BP2 = f2_bc(bp), CP2 = f2_bc(cp);
+      f2_t s0 = f2_bc(0.f), s1 = s0, s2 = s0;
+      f2_t kA = K0;
+      for (int j = 0; j < nch; ++j) {
+        float w[CW];
+        const int c = CW * j;
+        if constexpr (VEC == 8) {
+          ldg_v8(prow + c, w);
+        } else {
+#pragma unroll
+          for (int q = 0; q < CW; ++q) w[q] = (c + q < ncol) ? __ldg(prow + c + q) : 0.f;
+        }
+        if (VEC > 1) {
+          if (j == 0) {  // columns left of the box
+#pragma unroll
+            for (int q = 0; q < CW - 1; ++q)
+              if (q < lead) w[q] = 0.f;
+          }
+          if (j == nch - 1) {  // columns right of the box
+#pragma unroll
+            for (int q = 1; q < CW; ++q)
+              if (c + q >= ncol) w[q] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < CW / 2; ++h) {
+          const f2_t e = f2_fma(f2_fma(A2, kA, BP2), kA, CP2);
+          float e0, e1;
+          f2_unpack(e, e0, e1);
+          const f2_t tt = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), f2_pack(w[2 * h], w[2 * h + 1]));
+          s0 = f2_add(s0, tt);
+          const f2_t tk = f2_mul(tt, kA);
+          s1 = f2_add(s1, tk);
+          s2 = f2_fma(tk, kA, s2);
+          kA = f2_add(kA, TWO2);
+        }
+      }
+      float t0, t1, t2;
+      {
+        float a, b;
+        f2_unpack(s0, a, b);
+        t0 = a + b;
+        f2_unpack(s1, a, b);
+        t1 = a + b;
+        f2_unpack(s2, a, b);
+        t2 = a + b;
+      }
+      // sum t dx = sp t1 - delta t0;  sum t dx^2 = sp^2 t2 - 2 sp delta t1 + delta^2 t0
+      const float sx = fmaf(sp, t1, -delta * t0);
+      const float sxx = fmaf(sp2, t2, delta * fmaf(delta, t0, -2.f * sp * t1));
+      m[0] += t0;
+      m[1] += sx;
+      m[2] = fmaf(dy, t0, m[2]);
+      m[3] = fmaf(dz, t0, m[3]);
+      m[4] += sxx;
+      m[5] = fmaf(dy * dy, t0, m[5]);
+      m[6] = fmaf(dz * dz, t0, m[6]);
+      m[7] = fmaf(dy, sx, m[7]);
+      m[8] = fmaf(dz, sx, m[8]);
+      m[9] = fmaf(dy * dz, t0, m[9]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 10; ++k) mom[static_cast<int64_t>(k) * n + i] = m[k];
+}
+
+// Walk order for the lane-per-splat backward: 64^3 region of the box corner (L2 locality of
+// the grad volume), then box shape (chunks per row, y-z rows / 16) for uniform warp trip
+// counts. Returns the key bits through *bits.
+__global__ void k_voxel_lane_keys(const VoxelRec* __restrict__ rec, int64_t n, Window win, int nrx, int nry,
+                                  int vec, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const VoxelRec r = rec[i];
+  const int x0 = max(static_cast<int>(r.lox), win.lo[0]), y0 = max(static_cast<int>(r.loy), win.lo[1]),
+            z0 = max(static_cast<int>(r.loz), win.lo[2]);
+  const int W = min(static_cast<int>(r.hix), win.hi[0] - 1) - x0 + 1,
+            H = min(static_cast<int>(r.hiy), win.hi[1] - 1) - y0 + 1,
+            D = min(static_cast<int>(r.hiz), win.hi[2] - 1) - z0 + 1;
+  uint32_t key = 0xFFFFFFFFu;  // empty boxes last
+  if (W > 0 && H > 0 && D > 0) {
+    const int cw = vec == 8 ? 8 : 4;
+    const int lead = vec > 1 ? ((x0 - win.lo[0]) & (vec - 1)) : 0;
+    const uint32_t nch = min((lead + W + cw - 1) / cw, 7);
+    const uint32_t rows = min((H * D) >> 4, 63);
+    const uint32_t region = static_cast<uint32_t>((((z0 - win.lo[2]) >> 6) * nry + ((y0 - win.lo[1]) >> 6)) * nrx +
+                                                  ((x0 - win.lo[0]) >> 6));
+    key = (region << 9) | (nch << 6) | rows;
+  }
+  keys[i] = key;
+  vals[i] = static_cast<uint32_t>(i);
+}
+
 inline unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
 
 }  // namespace
@@ -479,6 +631,34 @@ void launch_voxel_order_keys(const VoxelRec* rec, int64_t n, const Window& win, 
                              uint32_t* keys, uint32_t* vals, cudaStream_t st) {
   if (n == 0) return;
   k_voxel_order_keys<<<blocks_for(n, 256), 256, 0, st>>>(rec, n, win, nbx, nby, keys, vals);
+  count_launch();
+}
+
+int voxel_bwd_vec(const Window& win, const float* grad_volume) {
+  const int wx = win.hi[0] - win.lo[0];
+  return (wx % 8 == 0 && reinterpret_cast<uintptr_t>(grad_volume) % 32 == 0) ? 8 : 1;
+}
+
+int launch_voxel_lane_keys(const VoxelRec* rec, int64_t n, const Window& win, int vec, uint32_t* keys,
+                           uint32_t* vals, cudaStream_t st) {
+  const int nrx = (win.hi[0] - win.lo[0] + 63) >> 6, nry = (win.hi[1] - win.lo[1] + 63) >> 6,
+            nrz = (win.hi[2] - win.lo[2] + 63) >> 6;
+  int rb = 0;
+  while ((int64_t(1) << rb) < int64_t(nrx) * nry * nrz) ++rb;
+  if (n > 0) {
+    k_voxel_lane_keys<<<blocks_for(n, 256), 256, 0, st>>>(rec, n, win, nrx, nry, vec, keys, vals);
+    count_launch();
+  }
+  return 9 + rb + 1;  // + 1: the all-ones key of empty boxes sorts after every region
+}
+
+void launch_voxel_bwd_lanes(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
+                            float spacing, const float* grad_volume, float* moments, cudaStream_t st) {
+  if (n == 0) return;
+  if (voxel_bwd_vec(win, grad_volume) == 8)
+    k_voxel_bwd_lanes<8><<<blocks_for(n, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume, moments);
+  else
+    k_voxel_bwd_lanes<1><<<blocks_for(n, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume, moments);
   count_launch();
 }
 
