@@ -354,7 +354,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     kernel = "k_raster_fwd2" if dom == "raster_fwd" else "k_raster_bwd_lanes"
     traffic = None  # dram read+write bytes per launch from the committed ncu --set full capture
     try:
-        prof = json.loads((ROOT / "profiles" / "r1" / "summary.json").read_text())
+        prof = json.loads((ROOT / "profiles" / "r1" / "raster" / "summary.json").read_text())
         hit = [d for d in prof if d["kernel"] == kernel and "dram_bytes" in d]
         if hit and args.config == "c2":
             traffic = int(np.mean([d["dram_bytes"] for d in hit]))
