@@ -43,6 +43,9 @@ struct CallError {
 struct gsct_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // host<->device image traffic of the C-ABI host-buffer path runs here, chunk by chunk,
+  // overlapped with the compute stream (event-ordered both ways)
+  cudaStream_t copy_stream = nullptr;
   bool own_stream = false;
   bool async = false;
   std::string err;
@@ -116,6 +119,15 @@ cudaEvent_t pooled_event(gsct_ctx c) {
   cudaEvent_t e;
   CK(cudaEventCreate(&e));
   return e;
+}
+
+// `waiter` waits for the work enqueued so far on `signaller` (pooled event, recycled once
+// the wait is enqueued: re-recording a pooled event later does not affect that wait).
+void stream_after(gsct_ctx c, cudaStream_t waiter, cudaStream_t signaller) {
+  cudaEvent_t e = pooled_event(c);
+  CK(cudaEventRecord(e, signaller));
+  CK(cudaStreamWaitEvent(waiter, e, 0));
+  c->event_pool.push_back(e);
 }
 
 // Records CUDA events around one phase's launches when profiling is on.
@@ -210,7 +222,21 @@ RSet make_rs(const gsct_raster_settings* r) {
   return RSet{r->tau_cut, r->sigma_cap, r->dilation_px2, r->tile_size, r->dilate, r->bounding};
 }
 
-Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl) {
+// Device view of a cloud; host arrays get device copies (allocated here; the copy is
+// enqueued on `st` unless `copy` is false -- then copy_cloud() does it later).
+Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl, cudaStream_t st = nullptr, bool copy = true);
+
+void copy_cloud(gsct_ctx c, const gsct_cloud* cl, const Cloud& d, cudaStream_t st) {
+  const size_t n = static_cast<size_t>(cl->n);
+  if (st != c->stream) stream_after(c, st, c->stream);  // after the (re)allocation and prior readers
+  CK(cudaMemcpyAsync(const_cast<double*>(d.pos), cl->pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(const_cast<double*>(d.ls), cl->log_scale, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(const_cast<double*>(d.q), cl->quat, 4 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(const_cast<double*>(d.raw), cl->raw_density, n * sizeof(double), cudaMemcpyHostToDevice, st));
+}
+
+Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl, cudaStream_t st, bool copy) {
+  if (!st) st = c->stream;
   contract(cl != nullptr && cl->n >= 0, "GaussianCloud: invalid cloud");
   contract(cl->n < (int64_t(1) << 31), "GaussianCloud: more than 2^31 splats unsupported");
   Cloud d{cl->n, cl->pos, cl->log_scale, cl->quat, cl->raw_density};
@@ -219,18 +245,11 @@ Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl) {
            "GaussianCloud: parameter arrays out of lockstep");
   if (cl->location == GSCT_HOST) {
     const size_t n = static_cast<size_t>(cl->n);
-    double* p = ws<double>(c, S_POS, 3 * n);
-    double* l = ws<double>(c, S_LS, 3 * n);
-    double* q = ws<double>(c, S_Q, 4 * n);
-    double* r = ws<double>(c, S_RAW, n);
-    CK(cudaMemcpyAsync(p, cl->pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(l, cl->log_scale, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(q, cl->quat, 4 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(r, cl->raw_density, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    d.pos = p;
-    d.ls = l;
-    d.q = q;
-    d.raw = r;
+    d.pos = ws<double>(c, S_POS, 3 * n);
+    d.ls = ws<double>(c, S_LS, 3 * n);
+    d.q = ws<double>(c, S_Q, 4 * n);
+    d.raw = ws<double>(c, S_RAW, n);
+    if (copy) copy_cloud(c, cl, d, st);
   }
   return d;
 }
@@ -386,7 +405,8 @@ int gsct_ctx_create(int device, gsct_ctx* out) {
       cudaMalloc(&c->dstats, sizeof(DevStats)) != cudaSuccess ||
       cudaMallocHost(&c->hstats, sizeof(DevStats)) != cudaSuccess ||
       cudaMallocHost(&c->hscratch, 4 * sizeof(uint32_t)) != cudaSuccess ||
-      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();
     delete c;
     return GSCT_ERR_CUDA;
@@ -415,6 +435,10 @@ void gsct_ctx_destroy(gsct_ctx c) {
     cudaEventDestroy(m.b);
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -559,6 +583,11 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       float* img = out + static_cast<int64_t>(v0) * npx;
       if (n == 0) {
         CK(cudaMemsetAsync(img, 0, static_cast<size_t>(npx) * cv * sizeof(float), c->stream));
+        if (images_location == GSCT_HOST) {
+          stream_after(c, c->copy_stream, c->stream);
+          CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0) * npx, img, static_cast<size_t>(npx) * cv * sizeof(float),
+                             cudaMemcpyDeviceToHost, c->copy_stream));
+        }
         continue;
       }
       RasterRec* rec = saved ? saved + static_cast<int64_t>(v0) * n : ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * cv);
@@ -584,9 +613,13 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         launch_raster_fwd(rec, vals, start, end, n, cv, geom->n_u, geom->n_v, tiles_u, tiles_v, img, c->stream);
       }
       CK(cudaGetLastError());
+      if (images_location == GSCT_HOST) {  // this chunk's images go down while the next computes
+        stream_after(c, c->copy_stream, c->stream);
+        CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0) * npx, img, static_cast<size_t>(npx) * cv * sizeof(float),
+                           cudaMemcpyDeviceToHost, c->copy_stream));
+      }
     }
-    if (images_location == GSCT_HOST && n_views)
-      CK(cudaMemcpyAsync(images, out, static_cast<size_t>(npx) * n_views * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    if (images_location == GSCT_HOST && n_views) stream_after(c, c->stream, c->copy_stream);
     finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
     if (saved) {
       c->saved_key = raster_call_key(cloud, geom, angles, n_views, rs);
@@ -607,7 +640,14 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     contract(grad_images != nullptr || n_views == 0, "rasterize_backward: grad image dims must match detector");
     if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
     reset_stats(c);
-    const Cloud d = upload_cloud(c, cloud);
+    // reuse the forward's set-up (PreSplat + records) when save-for-backward matched; then
+    // the cloud itself is only needed by the final covariance_backward, so a host cloud
+    // goes up on the copy stream, overlapped with the pixel walk
+    const bool reuse = c->save_fb && c->saved_valid && cloud != nullptr && cloud->n > 0 &&
+                       c->saved_key == raster_call_key(cloud, geom, angles, n_views, rs);
+    const bool late_cloud = reuse && cloud->location == GSCT_HOST;
+    const Cloud d = upload_cloud(c, cloud, c->stream, !late_cloud);
+    cudaEvent_t cloud_up = nullptr;
     const int64_t n = d.n;
     const size_t un = static_cast<size_t>(n);
     const int64_t npx = static_cast<int64_t>(geom->n_u) * geom->n_v;
@@ -636,9 +676,6 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
     const Geo g = make_geo(geom);
     const RSet r = make_rs(rs);
-    // reuse the forward's set-up (PreSplat + records) when save-for-backward matched
-    const bool reuse = c->save_fb && c->saved_valid && n > 0 &&
-                       c->saved_key == raster_call_key(cloud, geom, angles, n_views, rs);
     PreSplat* pre = ws<PreSplat>(c, S_PRE, un + 1);
     PreSplat* pre_aos = ws<PreSplat>(c, S_PRE_AOS, un + 1);
     double* acc = ws<double>(c, S_ACC, 11 * un + 1);
@@ -649,16 +686,32 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     RasterRec* saved = reuse ? ws<RasterRec>(c, S_SAVED, un * n_views) : nullptr;
     const int tiles_u = (geom->n_u + kTile - 1) / kTile, tiles_v = (geom->n_v + kTile - 1) / kTile;
     const int chunk = views_per_chunk(n, n_views, static_cast<int64_t>(tiles_u) * tiles_v);
-    // pixel-loop moments of every view, splat-major [N][n_views] x 8 fp32
+    // pixel-loop moments of every view, view-major [n_views][N] x 8 fp32
     float* mom = ws<float>(c, S_MOMENTS, un * static_cast<size_t>(n_views) * 8 + 1);
-    for (int v0 = 0; v0 < n_views && n > 0; v0 += chunk) {
-      const int cv = std::min(chunk, n_views - v0);
-      const float* gimg = grad_images + static_cast<int64_t>(v0) * npx;
-      if (grad_location == GSCT_HOST) {
-        float* dst = ws<float>(c, S_GRADIMG, static_cast<size_t>(npx) * cv);
-        CK(cudaMemcpyAsync(dst, gimg, static_cast<size_t>(npx) * cv * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-        gimg = dst;
+    // host grad images: every chunk is queued up front on the copy stream (after the work
+    // already on the compute stream, which may still read the buffer), one event per chunk;
+    // chunk k's pixel walk waits only for its own upload
+    float* gdev = nullptr;
+    std::vector<cudaEvent_t> up_done;
+    if (grad_location == GSCT_HOST && n > 0 && n_views > 0) {
+      gdev = ws<float>(c, S_GRADIMG, static_cast<size_t>(npx) * n_views);
+      stream_after(c, c->copy_stream, c->stream);
+      for (int v0 = 0; v0 < n_views; v0 += chunk) {
+        const int cv = std::min(chunk, n_views - v0);
+        CK(cudaMemcpyAsync(gdev + static_cast<int64_t>(v0) * npx, grad_images + static_cast<int64_t>(v0) * npx,
+                           static_cast<size_t>(npx) * cv * sizeof(float), cudaMemcpyHostToDevice, c->copy_stream));
+        up_done.push_back(pooled_event(c));
+        CK(cudaEventRecord(up_done.back(), c->copy_stream));
       }
+    }
+    if (late_cloud) {  // queued behind the grad images: needed only by the finalize
+      copy_cloud(c, cloud, d, c->copy_stream);
+      cloud_up = pooled_event(c);
+      CK(cudaEventRecord(cloud_up, c->copy_stream));
+    }
+    for (int v0 = 0, ci = 0; v0 < n_views && n > 0; v0 += chunk, ++ci) {
+      const int cv = std::min(chunk, n_views - v0);
+      const float* gimg = gdev ? gdev + static_cast<int64_t>(v0) * npx : grad_images + static_cast<int64_t>(v0) * npx;
       RasterRec* rec = reuse ? saved + static_cast<int64_t>(v0) * n : ws<RasterRec>(c, S_REC, un * cv);
       if (!reuse) {
         Phase ph(c, GSCT_PH_RASTER_SETUP);
@@ -677,6 +730,10 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
         void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
         CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
+        if (gdev) {
+          CK(cudaStreamWaitEvent(c->stream, up_done[static_cast<size_t>(ci)], 0));
+          c->event_pool.push_back(up_done[static_cast<size_t>(ci)]);
+        }
         launch_raster_bwd_lanes(rec, vb.Current(), n, cv, geom->n_u, geom->n_v, gimg, mom, v0, c->stream);
       }
       CK(cudaGetLastError());
@@ -684,7 +741,12 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (n > 0 && n_views > 0) {
       Phase ph(c, GSCT_PH_RASTER_TAIL);
       launch_raster_tail(pre_aos, n, dframes, n_views, g, r, mom, acc, gv, c->stream);
+      if (cloud_up) CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));
       launch_raster_finalize(d, acc, gp, gl, gq, gr, gn, c->stream);
+    }
+    if (cloud_up) {
+      CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));  // also when n_views == 0
+      c->event_pool.push_back(cloud_up);
     }
     if (out->location == GSCT_HOST && n > 0) {
       CK(cudaMemcpyAsync(out->pos, gp, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
