@@ -557,7 +557,8 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     const Cloud d = upload_cloud(c, cloud);
     const int64_t n = d.n;
     const int64_t npx = static_cast<int64_t>(geom->n_u) * geom->n_v;
-    const int tiles_u = (geom->n_u + kTile - 1) / kTile, tiles_v = (geom->n_v + kTile - 1) / kTile;
+    // binned at 32x32 super-tiles (kBinTile); RenderStats::tile_pairs stays at rs->tile_size
+    const int tiles_u = (geom->n_u + kBinTile - 1) / kBinTile, tiles_v = (geom->n_v + kBinTile - 1) / kBinTile;
     const int n_tiles = tiles_u * tiles_v;
     std::vector<Frame> frames(static_cast<size_t>(n_views));
     for (int v = 0; v < n_views; ++v) frames[static_cast<size_t>(v)] = make_frame(geom, angles[v]);
@@ -594,7 +595,7 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * cv);
       {
         Phase ph(c, GSCT_PH_RASTER_SETUP);
-        launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kTile, rec, cnt, c->dstats, c->stream);
+        launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream);
       }
       CK(cudaGetLastError());
       uint32_t *keys, *vals, *start, *end;
@@ -604,19 +605,27 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         bin_and_sort(
             c, cnt, n * cv, n_keys,
             [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
-              launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kTile, tiles_u, n_tiles, k, v, c->stream);
+              launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kBinTile, tiles_u, n_tiles, k, v, c->stream);
             },
             &keys, &vals, &start, &end);
       }
-      {
-        Phase ph(c, GSCT_PH_RASTER_FWD);
-        launch_raster_fwd(rec, vals, start, end, n, cv, geom->n_u, geom->n_v, tiles_u, tiles_v, img, c->stream);
-      }
-      CK(cudaGetLastError());
-      if (images_location == GSCT_HOST) {  // this chunk's images go down while the next computes
-        stream_after(c, c->copy_stream, c->stream);
-        CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0) * npx, img, static_cast<size_t>(npx) * cv * sizeof(float),
-                           cudaMemcpyDeviceToHost, c->copy_stream));
+      // host output: launch in view sub-ranges so each one's images go down while the next
+      // computes (the kernel indexes keys/records/images by its own view range)
+      const int sub = images_location == GSCT_HOST ? std::max(1, (cv + 3) / 4) : cv;
+      for (int vs = 0; vs < cv; vs += sub) {
+        const int nvs = std::min(sub, cv - vs);
+        {
+          Phase ph(c, GSCT_PH_RASTER_FWD);
+          launch_raster_fwd_super(rec + static_cast<int64_t>(vs) * n, vals, start + static_cast<int64_t>(vs) * n_tiles,
+                                  end + static_cast<int64_t>(vs) * n_tiles, n, nvs, geom->n_u, geom->n_v, tiles_u,
+                                  tiles_v, img + static_cast<int64_t>(vs) * npx, c->stream);
+        }
+        CK(cudaGetLastError());
+        if (images_location == GSCT_HOST) {
+          stream_after(c, c->copy_stream, c->stream);
+          CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0 + vs) * npx, img + static_cast<int64_t>(vs) * npx,
+                             static_cast<size_t>(npx) * nvs * sizeof(float), cudaMemcpyDeviceToHost, c->copy_stream));
+        }
       }
     }
     if (images_location == GSCT_HOST && n_views) stream_after(c, c->stream, c->copy_stream);

@@ -11,6 +11,7 @@ namespace gsct_dev {
 
 constexpr int kTile = 16;       // reference default tile (projector.hpp:67); the raster
                                 // kernel is specialised for it, other sizes are rejected
+constexpr int kBinTile = 32;   // forward binning granularity (32x32 super-tiles of 4 tiles)
 constexpr int kBrick = 8;       // voxel brick edge (8x8x8 voxels per CTA)
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -87,6 +88,10 @@ void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets,
                             int n_tiles, uint32_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start,
                    uint32_t* end, cudaStream_t st);
+// forward over 32x32 super-tile lists (keys = view * n_stiles + super-tile)
+void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
+                             const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
+                             int stiles_v, float* images, cudaStream_t st);
 void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                        const uint32_t* end, int64_t n, int n_views, int n_u, int n_v,
                        int tiles_u, int tiles_v, float* images, cudaStream_t st);

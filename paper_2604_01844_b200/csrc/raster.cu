@@ -263,18 +263,20 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd2(const RasterRec*
                                                                 const uint32_t* __restrict__ vals,
                                                                 const uint32_t* __restrict__ start,
                                                                 const uint32_t* __restrict__ end, int64_t n,
-                                                                int n_u, int n_v, int tiles_u, int n_tiles,
+                                                                int n_u, int n_v, int stiles_u, int n_stiles,
                                                                 float* __restrict__ images) {
+  // one CTA per 32x32 super-tile list and view; warp w owns the 16x16 tile (w & 1, w >> 1)
+  // and walks the super-tile list independently (warp-private staging, no block barriers);
+  // records that miss its tile get an all-zero lane mask and cost one staging lane
   __shared__ StagedRec2 s_rec[kFwdWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kFwdWarps + warp;
-  if (tile >= n_tiles) return;  // whole warp exits together
-  const int view = blockIdx.y;
-  const int tu = tile % tiles_u, tv = tile / tiles_u;
-  const int tx0 = tu * kTile, ty0 = tv * kTile;
+  const int st = blockIdx.x, view = blockIdx.y;
+  const int tx0 = (st % stiles_u) * kBinTile + (warp & 1) * kTile;
+  const int ty0 = (st / stiles_u) * kBinTile + (warp >> 1) * kTile;
+  if (tx0 >= n_u || ty0 >= n_v) return;  // whole warp exits together
   const int lr = 2 * (lane >> 2), lc = 4 * (lane & 3);  // lane block offset inside the tile
   const float flr = static_cast<float>(lr), flc = static_cast<float>(lc);
-  const uint32_t key = static_cast<uint32_t>(view) * n_tiles + tile;
+  const uint32_t key = static_cast<uint32_t>(view) * n_stiles + st;
   const uint32_t b = start[key], e = end[key];
   const RasterRec* __restrict__ vrec = rec + static_cast<int64_t>(view) * n;
   StagedRec2* sw = s_rec[warp];
@@ -298,9 +300,10 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd2(const RasterRec*
       const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16, v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
       const float du_t = (static_cast<float>(tx0) - static_cast<float>(u0)) - r.mo_u;
       const float dv_t = (static_cast<float>(ty0) - static_cast<float>(v0)) - r.mo_v;
-      // bbox n tile in tile coordinates (non-empty: the splat is on this tile's list)
+      // bbox n tile in tile coordinates (may be empty: the list is the super-tile's)
       const int c0 = max(u0 - tx0, 0), c1 = min(u1 - tx0, kTile - 1);
       const int r0 = max(v0 - ty0, 0), r1 = min(v1 - ty0, kTile - 1);
+      if (c0 <= c1 && r0 <= r1) {
       const uint32_t cm = ((2u << c1) - 1u) & ~((1u << c0) - 1u);
       const uint32_t rm = ((2u << r1) - 1u) & ~((1u << r0) - 1u);
       // lane mask: column quads c0/4..c1/4 x row pairs r0/2..r1/2 (lane = 4 * pair + quad)
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd2(const RasterRec*
       s.q = make_float4(r.C, r.amp, ex2_approx(2.f * r.A), safe ? 1.f : 0.f);
       s.m = make_uint4(cm | (rm << 16), lanes_rel, 0u, 0u);
       sw[lane] = s;
+      }
     }
     __syncwarp();
 #if GSCT_FWD_FILTER
@@ -639,15 +643,23 @@ void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_
   count_launch();
 }
 
+void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
+                             const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
+                             int stiles_v, float* images, cudaStream_t st) {
+  if (n_views == 0) return;
+  const int n_stiles = stiles_u * stiles_v;
+  dim3 grid(static_cast<unsigned>(n_stiles), static_cast<unsigned>(n_views));
+  k_raster_fwd2<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, images);
+  count_launch();
+}
+
 void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                        const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int tiles_u,
                        int tiles_v, float* images, cudaStream_t st) {
   if (n_views == 0) return;
   const int n_tiles = tiles_u * tiles_v;
   dim3 grid(static_cast<unsigned>((n_tiles + kFwdWarps - 1) / kFwdWarps), static_cast<unsigned>(n_views));
-#ifndef GSCT_FWD_KERNEL
-#define GSCT_FWD_KERNEL 2  // 2: 2x4 pixel blocks, multiplicative row chain; 1: 8-pixel rows, MUFU per pixel
-#endif
+  k_raster_fwd<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, tiles_u, n_tiles, images);
 #if GSCT_FWD_KERNEL == 2
   k_raster_fwd2<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, tiles_u, n_tiles, images);
 #else
