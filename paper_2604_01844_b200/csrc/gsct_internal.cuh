@@ -92,9 +92,6 @@ void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint3
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
                              int stiles_v, float* images, cudaStream_t st);
-void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
-                       const uint32_t* end, int64_t n, int n_views, int n_u, int n_v,
-                       int tiles_u, int tiles_v, float* images, cudaStream_t st);
 // lane-per-item backward: shape sort keys, then the pixel walk in `order`
 int bwd_vec(int n_u, const float* grad_images);  // 8, 4 or 1 floats per row load
 // returns the number of key bits to sort on

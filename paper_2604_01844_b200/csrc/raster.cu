@@ -1,19 +1,17 @@
-// Rasterizer pair kernels (fp32): tile-pair emission (K2), tile ranges, the per-tile
-// forward accumulation (K3) and the per-splat backward pixel loop (K4a).
+// Rasterizer pair kernels (fp32): tile-pair emission (K2), key ranges, the per-tile
+// forward accumulation (K3), the backward walk-order keys and the per-item backward pixel
+// walk (K4a).
 //
-// K3 follows rasterize_view (projector.hpp:321-347): every pixel sums the splats of its
-// tile list in ascending splat index (the list order produced by the stable sort), only
-// over pixels inside each splat's bbox, value amp * exp(-0.5 (a du^2 + c dv^2) - b du dv).
-// K4a follows rasterize_backward's pixel loop (projector.hpp:399-420): each splat is
-// owned by one warp that walks its own bbox; per-pixel terms are reduced with a fixed
-// xor-shuffle tree, so gradients are bit-stable without atomics.
+// K3 follows rasterize_view (projector.hpp:321-347): every pixel sums the splats whose
+// bbox covers it in ascending splat index (the list order produced by the stable sort),
+// value amp * exp(-0.5 (a du^2 + c dv^2) - b du dv). K4a follows rasterize_backward's pixel
+// loop (projector.hpp:399-420): each (view, splat) item is owned by ONE lane that walks its
+// own bbox sequentially, so gradients are bit-stable without atomics or cross-lane trees.
 //
-// Both kernels are issue-bound rather than HBM-bound (profiles/), so the designs minimise
-// instructions per splat-pixel pair: the forward gives each lane an 8-pixel row segment and
-// advances the exponent along the row by second-order differences (2 FADD + 1 MUFU.EX2 +
-// 1 FFMA per pixel, per-splat set-up amortised over the 256 pixels of the tile); the
-// backward maps lanes to bbox columns x row groups so du is lane-constant and the six
-// moments need three per-lane accumulators.
+// Both are issue-bound rather than HBM-bound (profiles/r1/raster): the designs minimise
+// issue slots per splat-pixel pair (packed f32x2 arithmetic, multiplicative exp chains in
+// the forward) and wasted lanes (per-lane record filtering in the forward, lane-per-item
+// with shape-sorted work in the backward). See DESIGN.md section 4.
 #include <cuda_runtime.h>
 
 #include "gsct_internal.cuh"
@@ -109,116 +107,13 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, ui
   end[k] = lower_bound_u32(keys, n_pairs, k + 1);
 }
 
-#ifndef GSCT_BWD_ASM
-#define GSCT_BWD_ASM 0
-#endif
-#ifndef GSCT_BWD_LOOP
-#define GSCT_BWD_LOOP 1  // 1: predicate-free 4-row main loop + remainder (A/B: 7.6 vs 8.3 ms)
-#endif
+constexpr int kFwdWarps = 4;  // tiles per CTA (one warp per 16x16 tile of a 32x32 super-tile)
 
-constexpr int kFwdWarps = 4;  // tiles per CTA (one warp per 16x16 tile)
-constexpr int kPX = 8;        // pixels per lane (row segment)
-
-struct __align__(16) StagedRec {
-  int4 irect;  // u0, u1, v0, v1
-  float4 p;    // u0, v0 (exact floats), mo_u, mo_v
-  float4 q;    // A, B, C, amp
-};
-
-// One warp per 16x16 tile and view. Lane l owns the 8-pixel row segment at columns
-// 8*(l & 1) .. +7 of row (l >> 1). Per record a lane computes an 8-bit inside mask once
-// (R2P turns it into predicates) and walks its segment with second-order differences of
-// the exponent: MUFU.EX2 + 2 FADD + 1 predicated FFMA per pixel, which balances the issue
-// slots against the SFU rate (profiles/: both ~75-80% of peak).
-// Records of the tile list are staged 32 at a time in the warp's shared-memory slice
-// (one gather per lane, __syncwarp only; no block barriers), software-pipelined.
-__global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd(const RasterRec* __restrict__ rec,
-                                                               const uint32_t* __restrict__ vals,
-                                                               const uint32_t* __restrict__ start,
-                                                               const uint32_t* __restrict__ end, int64_t n,
-                                                               int n_u, int n_v, int tiles_u, int n_tiles,
-                                                               float* __restrict__ images) {
-  __shared__ StagedRec s_rec[kFwdWarps][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kFwdWarps + warp;
-  if (tile >= n_tiles) return;  // whole warp exits together
-  const int view = blockIdx.y;
-  const int tu = tile % tiles_u, tv = tile / tiles_u;
-  const int py = tv * kTile + (lane >> 1);
-  const int px0 = tu * kTile + (lane & 1) * kPX;
-  const float fr = static_cast<float>(py), fc0 = static_cast<float>(px0);
-  const uint32_t key = static_cast<uint32_t>(view) * n_tiles + tile;
-  const uint32_t b = start[key], e = end[key];
-  const RasterRec* __restrict__ vrec = rec + static_cast<int64_t>(view) * n;
-  StagedRec* sw = s_rec[warp];
-  float acc[kPX];
-#pragma unroll
-  for (int k = 0; k < kPX; ++k) acc[k] = 0.f;
-
-  // software pipeline: the record gather of batch i+1 and the index load of batch i+2 are
-  // in flight while batch i is processed
-  uint32_t idx_next = (b + 32 + lane < e) ? vals[b + 32 + lane] : 0u;
-  RasterRec r_cur;
-  if (b + lane < e) r_cur = vrec[vals[b + lane]];
-  for (uint32_t base = b; base < e; base += 32) {
-    const int cnt = min(32u, e - base);
-    const bool has_next = base + 32 + lane < e;
-    RasterRec r_next;
-    if (has_next) r_next = vrec[idx_next];
-    idx_next = (base + 64 + lane < e) ? vals[base + 64 + lane] : 0u;
-    if (lane < cnt) {
-      const RasterRec r = r_cur;
-      StagedRec s;
-      const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16, v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
-      s.irect = make_int4(u0, u1, v0, v1);
-      s.p = make_float4(static_cast<float>(u0), static_cast<float>(v0), r.mo_u, r.mo_v);
-      s.q = make_float4(r.A, r.B, r.C, r.amp);
-      sw[lane] = s;
-    }
-    __syncwarp();
-    for (int j = 0; j < cnt; ++j) {
-      const int4 ir = sw[j].irect;
-      const float4 p = sw[j].p;
-      const float4 q = sw[j].q;
-      // 8-bit mask of this lane's pixels inside the bbox (bits k with u0 <= px0+k <= u1)
-      const int lo = min(max(ir.x - px0, 0), kPX);
-      const int hi = min(max(ir.y - px0 + 1, 0), kPX);
-      unsigned mask = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
-      if (py < ir.z || py > ir.w) mask = 0u;
-      const float du0 = (fc0 - p.x) - p.z;
-      const float dv = (fr - p.y) - p.w;
-      const float bdv = q.y * dv;
-      float ee = fmaf(fmaf(q.x, du0, bdv), du0, q.z * dv * dv);  // log2 of exp(e) at k = 0
-      float dd = fmaf(q.x, fmaf(2.f, du0, 1.f), bdv);            // first difference
-      const float a2 = 2.f * q.x;                                 // second difference
-#pragma unroll
-      for (int k = 0; k < kPX; ++k) {
-        const float ex = ex2_approx(ee);
-        if (mask & (1u << k)) acc[k] = fmaf(q.w, ex, acc[k]);
-        ee += dd;
-        dd += a2;
-      }
-    }
-    __syncwarp();
-    r_cur = r_next;
-  }
-  if (py < n_v) {
-    float* row = images + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(py) * n_u;
-    if (((n_u & 3) == 0) && px0 + kPX <= n_u) {
-      reinterpret_cast<float4*>(row + px0)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      reinterpret_cast<float4*>(row + px0)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < kPX; ++k)
-        if (px0 + k < n_u) row[px0 + k] = acc[k];
-    }
-  }
-}
-
-// Forward v2 (K3): one warp per 16x16 tile and view; lane l owns the 2 x 4 pixel block at
+// Forward (K3): one warp per 16x16 tile and view; lane l owns the 2 x 4 pixel block at
 // rows 2(l>>2) .. +1, columns 4(l&3) .. +3, the two rows held in the halves of packed f32x2
-// registers. Records of the tile list (ascending splat index = the reference's per-pixel
-// accumulation order) are staged 32 at a time in the warp's shared-memory slice; the
+// registers. Records of the 32x32 super-tile list containing the tile (ascending splat
+// index = the reference's per-pixel accumulation order) are staged 32 at a time in the
+// warp's shared-memory slice; the
 // staging lane also derives the per-splat ratio c = exp2(2A) and a "chain-safe" flag.
 // Along a row the Gaussian is evaluated multiplicatively: with e(k) = E0 + k D + k(k-1) A,
 //   g(k+1) = g(k) r(k),  r(k+1) = r(k) c,   g(0) = amp 2^E0,  r(0) = 2^D,
@@ -649,24 +544,11 @@ void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const u
   if (n_views == 0) return;
   const int n_stiles = stiles_u * stiles_v;
   dim3 grid(static_cast<unsigned>(n_stiles), static_cast<unsigned>(n_views));
+  // (A/B: CTA-shared 128-record staging with block barriers was slower, 3.88 vs 3.63 ms)
   k_raster_fwd2<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, images);
   count_launch();
 }
 
-void launch_raster_fwd(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
-                       const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int tiles_u,
-                       int tiles_v, float* images, cudaStream_t st) {
-  if (n_views == 0) return;
-  const int n_tiles = tiles_u * tiles_v;
-  dim3 grid(static_cast<unsigned>((n_tiles + kFwdWarps - 1) / kFwdWarps), static_cast<unsigned>(n_views));
-  k_raster_fwd<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, tiles_u, n_tiles, images);
-#if GSCT_FWD_KERNEL == 2
-  k_raster_fwd2<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, tiles_u, n_tiles, images);
-#else
-  k_raster_fwd<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, tiles_u, n_tiles, images);
-#endif
-  count_launch();
-}
 
 
 }  // namespace gsct_dev
