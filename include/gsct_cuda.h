@@ -198,6 +198,33 @@ int gsct_voxelize_bwd_finish(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_g
                              const gsct_voxel_settings* vs, const float* moments_dev,
                              gsct_grads* out);
 
+/* ---- next-row operators ----------------------------------------------- */
+/* Image loss of the reconstruction loop: total_loss_recon (losses.hpp:613-637) with
+ * alpha_tv = 0, i.e. L1 (losses.hpp:28-45) + alpha_ssim * SSIM2D (losses.hpp:214-272) per
+ * view. losses[3 * n_views] (host): {l1, ssim loss (1 - mean SSIM), total} per view;
+ * grad_images = d total / d rendered (fp32, same [n_views][n_v][n_u] layout as the images,
+ * ready for gsct_rasterize_bwd). location applies to rendered, measured and grad_images. */
+int gsct_image_loss(gsct_ctx ctx, const float* rendered, const float* measured, int n_views, int n_u,
+                    int n_v, double alpha_ssim, float* grad_images, int location, double* losses);
+
+/* Adam (optim.hpp:133-182): beta1 0.9, beta2 0.999, eps 1e-15; splats with a non-finite
+ * gradient are skipped and counted; raw densities re-projected to >= 0. Parameters (the
+ * cloud arrays, updated in place), moments and gradients are device arrays (fp64). The
+ * update is bit-identical to the reference's adam_step. */
+typedef struct {
+  double position, log_scale, rotation, density;
+} gsct_learning_rates;
+typedef struct {
+  double *m_pos, *v_pos;  /* 3N each */
+  double *m_ls, *v_ls;    /* 3N */
+  double *m_rot, *v_rot;  /* 4N */
+  double *m_dens, *v_dens;/* N */
+  int64_t step;           /* incremented by the call (OptimState::step) */
+  int64_t skipped_updates;/* accumulated (OptimState::skipped_updates) */
+} gsct_adam_state;
+int gsct_adam_step(gsct_ctx ctx, gsct_cloud* params, gsct_adam_state* state, const gsct_grads* grads,
+                   const gsct_learning_rates* lrs);
+
 /* ---- parity hooks (bit-exactness checks against the CPU oracle) ------------------ */
 /* Per splat for one view: rect[4N] (u_min,u_max,v_min,v_max), flags[N] (bit0 culled,
  * bit1 degenerate), mean2d[2N], conic[4N] (row-major), amplitude[N]; host outputs. */

@@ -307,6 +307,33 @@ class Ref:
                                     int(cone), int(n_u), int(n_v), C.byref(g), _p(ang))
         return g, ang
 
+    # -- next-row operators (unchanged reference losses.hpp / optim.hpp) --------------
+    def total_loss_recon(self, rendered: np.ndarray, measured: np.ndarray, alpha_ssim: float):
+        """(l1, ssim, total), grad for one image (losses.hpp:613-637, alpha_tv = 0)."""
+        r = np.ascontiguousarray(rendered, dtype=np.float64)
+        m = np.ascontiguousarray(measured, dtype=np.float64)
+        g = np.zeros_like(r)
+        out = np.zeros(3)
+        f = self.l.ref_total_loss_recon
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_void_p]
+        self._chk(f(_p(r), _p(m), r.shape[1], r.shape[0], float(alpha_ssim), _p(g), _p(out)))
+        return out, g
+
+    def adam_step(self, params: dict, moments: dict, grads: dict, lrs, step: int, skipped: int):
+        """adam_step (optim.hpp:158-182) on flat fp64 arrays, updated in place; returns
+        (step, skipped)."""
+        f = self.l.ref_adam_step
+        f.argtypes = [C.c_int64] + [C.c_void_p] * 4 + [C.c_void_p] + [C.c_void_p] * 4 + [C.c_void_p] * 3
+        keys = ("m_pos", "v_pos", "m_ls", "v_ls", "m_rot", "v_rot", "m_dens", "v_dens")
+        mv = (C.c_void_p * 8)(*[moments[k].ctypes.data for k in keys])
+        lr = np.array([lrs.position, lrs.log_scale, lrs.rotation, lrs.density], dtype=np.float64)
+        st = C.c_int64(step)
+        sk = C.c_int64(skipped)
+        n = len(params["raw"])
+        self._chk(f(n, _p(params["pos"]), _p(params["ls"]), _p(params["q"]), _p(params["raw"]), mv, _p(grads["pos"]),
+                    _p(grads["ls"]), _p(grads["q"]), _p(grads["raw"]), _p(lr), C.byref(st), C.byref(sk)))
+        return int(st.value), int(sk.value)
+
 
 def _ref_random_cloud(self, seed, count, pos_range=5.0, scale_lo=0.5, scale_hi=2.5):
     pos = np.zeros((count, 3))

@@ -10,6 +10,8 @@
 
 #include "gsct/bench.hpp"
 #include "gsct/core.hpp"
+#include "gsct/losses.hpp"
+#include "gsct/optim.hpp"
 #include "gsct/parallel.hpp"
 #include "gsct/projector.hpp"
 #include "gsct/synthetic.hpp"
@@ -292,4 +294,92 @@ void ref_default_geometry(int nx, int ny, int nz, double spacing, int n_views, i
   for (int i = 0; i < n_views; ++i) angles[i] = g.angles[static_cast<std::size_t>(i)];
 }
 
+
+constexpr std::array<int, 3> kOneVox{{1, 1, 1}};
+
+// total_loss_recon (losses.hpp:613-637) with alpha_tv = 0 on one image: out3 = {l1, ssim,
+// total}, grad[n_v * n_u] = d total / d rendered.
+int ref_total_loss_recon(const double* rendered, const double* measured, int n_u, int n_v, double alpha_ssim,
+                         double* grad, double* out3) {
+  GUARD({
+    Image r;
+    Image m;
+    r.n_u = m.n_u = n_u;
+    r.n_v = m.n_v = n_v;
+    r.values.assign(rendered, rendered + static_cast<std::size_t>(n_u) * n_v);
+    m.values.assign(measured, measured + static_cast<std::size_t>(n_u) * n_v);
+    LossWeights wts;
+    wts.alpha_ssim = alpha_ssim;
+    wts.alpha_tv = 0.0;
+    const Volume sub = Volume::zeros(kOneVox, 1.0, Vec3::Zero());
+    const ReconLoss L = total_loss_recon(r, m, sub, wts);
+    out3[0] = L.l1;
+    out3[1] = L.ssim;
+    out3[2] = L.total;
+    std::memcpy(grad, L.grad_image.values.data(), L.grad_image.values.size() * sizeof(double));
+  });
+}
+
+// adam_step (optim.hpp:158-182) on a cloud (arrays updated in place) with moments in the
+// same flat layouts; step / skipped in-out.
+int ref_adam_step(int64_t n, double* pos, double* ls, double* q, double* raw, double* const* mv,
+                  const double* gpos, const double* gls, const double* gq, const double* graw, const double* lrs,
+                  int64_t* step, int64_t* skipped) {
+  GUARD({
+    GaussianCloud c;
+    for (int64_t i = 0; i < n; ++i)
+      c.push_back(Vec3(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]), Vec3(ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]),
+                  Vec4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]), raw[i]);
+    OptimState st;
+    st.init(static_cast<std::size_t>(n), 0);
+    ParamGradients g;
+    g.resize(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      for (int a = 0; a < 3; ++a) {
+        st.m_pos[i][a] = mv[0][3 * i + a];
+        st.v_pos[i][a] = mv[1][3 * i + a];
+        st.m_ls[i][a] = mv[2][3 * i + a];
+        st.v_ls[i][a] = mv[3][3 * i + a];
+        g.positions[i][a] = gpos[3 * i + a];
+        g.log_scales[i][a] = gls[3 * i + a];
+      }
+      for (int a = 0; a < 4; ++a) {
+        st.m_rot[i][a] = mv[4][4 * i + a];
+        st.v_rot[i][a] = mv[5][4 * i + a];
+        g.rotations[i][a] = gq[4 * i + a];
+      }
+      st.m_dens[i] = mv[6][i];
+      st.v_dens[i] = mv[7][i];
+      g.raw_densities[i] = graw[i];
+    }
+    st.step = *step;
+    st.skipped_updates = *skipped;
+    LearningRates lr;
+    lr.position = lrs[0];
+    lr.log_scale = lrs[1];
+    lr.rotation = lrs[2];
+    lr.density = lrs[3];
+    adam_step(c, st, g, lr);
+    for (int64_t i = 0; i < n; ++i) {
+      for (int a = 0; a < 3; ++a) {
+        pos[3 * i + a] = c.positions[i][a];
+        ls[3 * i + a] = c.log_scales[i][a];
+        mv[0][3 * i + a] = st.m_pos[i][a];
+        mv[1][3 * i + a] = st.v_pos[i][a];
+        mv[2][3 * i + a] = st.m_ls[i][a];
+        mv[3][3 * i + a] = st.v_ls[i][a];
+      }
+      for (int a = 0; a < 4; ++a) {
+        q[4 * i + a] = c.rotations[i][a];
+        mv[4][4 * i + a] = st.m_rot[i][a];
+        mv[5][4 * i + a] = st.v_rot[i][a];
+      }
+      raw[i] = c.raw_densities[i];
+      mv[6][i] = st.m_dens[i];
+      mv[7][i] = st.v_dens[i];
+    }
+    *step = st.step;
+    *skipped = st.skipped_updates;
+  });
+}
 }  // extern "C"

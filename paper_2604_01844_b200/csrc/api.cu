@@ -24,7 +24,7 @@ namespace {
 enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
-  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED,
+  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP,
   S_COUNT_SLOTS
 };
 
@@ -1078,6 +1078,84 @@ int gsct_debug_tile_pairs(gsct_ctx c, const gsct_cloud* cloud, const gsct_geomet
       CK(cudaMemcpyAsync(values, dv, static_cast<size_t>(total) * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     }
     finish_sync(c, nullptr, false, nullptr);
+  });
+}
+
+// ---------------------------------------------------------------------------------------
+// Next-row operators: image loss, Adam
+// ---------------------------------------------------------------------------------------
+
+int gsct_image_loss(gsct_ctx c, const float* rendered, const float* measured, int n_views, int n_u, int n_v,
+                    double alpha_ssim, float* grad_images, int location, double* losses) {
+  return run(c, [&] {
+    contract(n_views >= 0, "image_loss: n_views must be >= 0");
+    contract(n_u >= 11 && n_v >= 11, "ssim2d: image smaller than the 11x11 window");
+    contract(std::isfinite(alpha_ssim) && alpha_ssim >= 0.0, "LossWeights: alpha_ssim invalid");
+    contract(n_views == 0 || (rendered && measured && grad_images && losses), "image_loss: null buffer");
+    if (n_views == 0) return;
+    // the reference's normalised sigma-1.5 window (losses.hpp:85-98), host libm
+    double w[11], sum = 0.0;
+    for (int i = 0; i < 11; ++i) {
+      const double d = i - 5;
+      w[i] = std::exp(-0.5 * d * d / (1.5 * 1.5));
+      sum += w[i];
+    }
+    for (double& x : w) x /= sum;
+    const size_t npx = static_cast<size_t>(n_u) * n_v * n_views;
+    const float* p = rendered;
+    const float* t = measured;
+    float* g = grad_images;
+    if (location == GSCT_HOST) {
+      float* dp = ws<float>(c, S_LOSS_IN, npx);
+      float* dt = ws<float>(c, S_LOSS_TGT, npx);
+      CK(cudaMemcpyAsync(dp, rendered, npx * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(dt, measured, npx * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+      p = dp, t = dt;
+      g = ws<float>(c, S_LOSS_GRAD, npx);
+    }
+    const size_t nout = static_cast<size_t>(n_u - 10) * (n_v - 10) * n_views;
+    float* coef = ws<float>(c, S_LOSS_COEF, 3 * nout);
+    const int64_t nparts = image_loss_partials(n_views, n_u, n_v);
+    double* parts = ws<double>(c, S_LOSS_PART, static_cast<size_t>(nparts) + 3 * static_cast<size_t>(n_views));
+    const int64_t n_s = nparts - static_cast<int64_t>(n_views) * ((n_u + 31) / 32) * ((n_v + 15) / 16);
+    double* out3 = parts + nparts;
+    launch_image_loss(p, t, n_views, n_u, n_v, w, alpha_ssim, coef, parts, parts + n_s, g, out3, c->stream);
+    CK(cudaGetLastError());
+    if (location == GSCT_HOST)
+      CK(cudaMemcpyAsync(grad_images, g, npx * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(losses, out3, 3 * static_cast<size_t>(n_views) * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int gsct_adam_step(gsct_ctx c, gsct_cloud* params, gsct_adam_state* state, const gsct_grads* grads,
+                   const gsct_learning_rates* lrs) {
+  return run(c, [&] {
+    contract(params && state && grads && lrs, "adam_step: null argument");
+    contract(params->location == GSCT_DEVICE && grads->location == GSCT_DEVICE,
+             "adam_step: parameters and gradients must be device-resident");
+    contract(lrs->position > 0.0 && lrs->log_scale > 0.0 && lrs->rotation > 0.0 && lrs->density > 0.0,
+             "lr_schedule: rates must be positive");
+    state->step += 1;
+    const double bias1 = 1.0 - std::pow(0.9, static_cast<double>(state->step));
+    const double bias2 = 1.0 - std::pow(0.999, static_cast<double>(state->step));
+    const int64_t n = params->n;
+    if (n == 0) return;
+    double* const mv[8] = {state->m_pos, state->v_pos, state->m_ls, state->v_ls,
+                           state->m_rot, state->v_rot, state->m_dens, state->v_dens};
+    const double lr[4] = {lrs->position, lrs->log_scale, lrs->rotation, lrs->density};
+    unsigned long long* skipped = ws<unsigned long long>(c, S_ADAM_SKIP, 1);
+    CK(cudaMemsetAsync(skipped, 0, sizeof(unsigned long long), c->stream));
+    launch_adam_step(n, const_cast<double*>(params->pos), const_cast<double*>(params->log_scale),
+                     const_cast<double*>(params->quat), const_cast<double*>(params->raw_density), mv, grads->pos,
+                     grads->log_scale, grads->quat, grads->raw_density, lr, bias1, bias2, skipped, c->stream);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(c->hscratch, skipped, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(&h, c->hscratch, sizeof h);
+    state->skipped_updates += static_cast<int64_t>(h);
   });
 }
 

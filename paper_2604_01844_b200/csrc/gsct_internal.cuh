@@ -120,6 +120,19 @@ void launch_voxel_bwd_lanes(const VoxelRec* rec, const uint32_t* order, int64_t 
 void launch_voxel_bwd_pairs(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
                             float spacing, const float* grad_volume, float* moments, cudaStream_t st);
 
+// (loss.cu) fused L1 + SSIM2D image loss: coef = 3 * n_views * n_out fp32 scratch,
+// part_s / part_l1 = per-tile partials (image_loss_partials total), out3[3 * n_views] =
+// {l1, ssim loss, total} per view (device), grad = d total / d pred (fp32, device)
+void launch_image_loss(const float* pred, const float* targ, int n_views, int nu, int nv, const double* window,
+                       double alpha, float* coef, double* part_s, double* part_l1, float* grad, double* out3,
+                       cudaStream_t st);
+int64_t image_loss_partials(int n_views, int nu, int nv);
+// (preprocess.cu) adam_step; mv = {m_pos, v_pos, m_ls, v_ls, m_rot, v_rot, m_dens, v_dens},
+// lrs = {position, log_scale, rotation, density}
+void launch_adam_step(int64_t n, double* pos, double* ls, double* q, double* raw, double* const* mv,
+                      const double* g_pos, const double* g_ls, const double* g_q, const double* g_raw,
+                      const double* lrs, double bias1, double bias2, unsigned long long* skipped, cudaStream_t st);
+
 // Launch accounting (gsct_ctx_launch_count).
 extern thread_local int64_t* g_launch_counter;
 inline void count_launch(int k = 1) {

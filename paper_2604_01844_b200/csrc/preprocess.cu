@@ -321,3 +321,67 @@ void launch_voxel_tail(const Cloud& c, const VoxGrid& grid, double tau_cut, doub
 }
 
 }  // namespace gsct_dev
+
+namespace gsct_dev {
+namespace {
+
+// adam_update (optim.hpp:149-156), operation for operation: this TU is compiled without
+// FMA contraction and double sqrt / division are IEEE-rounded, so with the host-side
+// bias terms (std::pow) the update is bit-identical to the reference's.
+__device__ __forceinline__ void adam_update(double& param, double& m, double& v, double grad, double lr,
+                                            double bias1, double bias2) {
+  constexpr double b1 = 0.9, b2 = 0.999, eps = 1e-15;
+  m = b1 * m + (1.0 - b1) * grad;
+  v = b2 * v + (1.0 - b2) * grad * grad;
+  param -= lr * (m / bias1) / (sqrt(v / bias2) + eps);
+}
+
+// adam_step (optim.hpp:158-182): one thread per splat; splats with any non-finite
+// gradient are skipped and counted; raw densities are re-projected to >= 0.
+__global__ void k_adam_step(int64_t n, double* __restrict__ pos, double* __restrict__ ls, double* __restrict__ q,
+                            double* __restrict__ raw, double* __restrict__ m_pos, double* __restrict__ v_pos,
+                            double* __restrict__ m_ls, double* __restrict__ v_ls, double* __restrict__ m_rot,
+                            double* __restrict__ v_rot, double* __restrict__ m_dens, double* __restrict__ v_dens,
+                            const double* __restrict__ g_pos, const double* __restrict__ g_ls,
+                            const double* __restrict__ g_q, const double* __restrict__ g_raw, double lr_pos,
+                            double lr_ls, double lr_rot, double lr_dens, double bias1, double bias2,
+                            unsigned long long* __restrict__ skipped) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool skip = false;
+  if (i < n) {
+    bool ok = isfinite(g_raw[i]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ok = ok && isfinite(g_pos[3 * i + a]) && isfinite(g_ls[3 * i + a]);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) ok = ok && isfinite(g_q[4 * i + a]);
+    skip = !ok;
+    if (ok) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        adam_update(pos[3 * i + a], m_pos[3 * i + a], v_pos[3 * i + a], g_pos[3 * i + a], lr_pos, bias1, bias2);
+        adam_update(ls[3 * i + a], m_ls[3 * i + a], v_ls[3 * i + a], g_ls[3 * i + a], lr_ls, bias1, bias2);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        adam_update(q[4 * i + a], m_rot[4 * i + a], v_rot[4 * i + a], g_q[4 * i + a], lr_rot, bias1, bias2);
+      adam_update(raw[i], m_dens[i], v_dens[i], g_raw[i], lr_dens, bias1, bias2);
+      if (raw[i] < 0.0) raw[i] = 0.0;
+    }
+  }
+  const unsigned ball = __ballot_sync(0xffffffffu, skip);
+  if ((threadIdx.x & 31) == 0 && ball) atomicAdd(skipped, static_cast<unsigned long long>(__popc(ball)));
+}
+
+}  // namespace
+
+void launch_adam_step(int64_t n, double* pos, double* ls, double* q, double* raw, double* const* mv,
+                      const double* g_pos, const double* g_ls, const double* g_q, const double* g_raw,
+                      const double* lrs, double bias1, double bias2, unsigned long long* skipped, cudaStream_t st) {
+  if (n == 0) return;
+  k_adam_step<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+      n, pos, ls, q, raw, mv[0], mv[1], mv[2], mv[3], mv[4], mv[5], mv[6], mv[7], g_pos, g_ls, g_q, g_raw, lrs[0],
+      lrs[1], lrs[2], lrs[3], bias1, bias2, skipped);
+  count_launch();
+}
+
+}  // namespace gsct_dev

@@ -87,6 +87,16 @@ class c_cloud(C.Structure):
                 ("raw_density", C.c_void_p), ("location", C.c_int)]
 
 
+class c_learning_rates(C.Structure):
+    _fields_ = [("position", C.c_double), ("log_scale", C.c_double), ("rotation", C.c_double),
+                ("density", C.c_double)]
+
+
+class c_adam_state(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("m_pos", "v_pos", "m_ls", "v_ls", "m_rot", "v_rot", "m_dens", "v_dens")] + \
+               [("step", C.c_int64), ("skipped_updates", C.c_int64)]
+
+
 class c_grads(C.Structure):
     _fields_ = [("pos", C.c_void_p), ("log_scale", C.c_void_p), ("quat", C.c_void_p),
                 ("raw_density", C.c_void_p), ("pos_grad_norm", C.c_void_p), ("visible", C.c_void_p),
@@ -128,6 +138,9 @@ _SIGS = {
                                         _P(C.c_int64)]),
     "gsct_debug_voxel_boxes": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_grid), _P(c_window),
                                          _P(c_voxel_settings), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gsct_image_loss": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double,
+                                  C.c_void_p, C.c_int, _P(C.c_double)]),
+    "gsct_adam_step": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_adam_state), _P(c_grads), _P(c_learning_rates)]),
     "gsct_host_view_frame": (None, [_P(c_geometry), C.c_double, _P(C.c_double)]),
     "gsct_host_default_geometry": (None, [_P(C.c_int), C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                           _P(c_geometry), _P(C.c_double)]),
@@ -846,3 +859,76 @@ def make_cloud(kind: str, count: int, seed: int = 0, **kw) -> GaussianCloud:
     if st != 0:
         raise ContractError("make_cloud failed")
     return GaussianCloud(pos, ls, q, raw)
+
+
+# ---------------------------------------------------------------------------------------
+# Next-row operators: image loss, Adam
+# ---------------------------------------------------------------------------------------
+def image_loss(rendered, measured, alpha_ssim: float = 0.25, grad_out=None, ctx: Optional[Context] = None):
+    """total_loss_recon (losses.hpp:613-637) with alpha_tv = 0, per view, on [V, n_v, n_u]
+    float32 images (numpy or CUDA tensors). Returns (losses [V, 3] = {l1, ssim, total},
+    grad [V, n_v, n_u] float32 = d total / d rendered, same kind as the inputs)."""
+    if tuple(rendered.shape) != tuple(measured.shape) or len(rendered.shape) not in (2, 3):
+        raise ContractError("l1: image shape mismatch")
+    shape = tuple(rendered.shape)
+    nv_, nv, nu = (1,) + shape if len(shape) == 2 else shape
+    keep: list = []
+    dev = _is_torch(rendered) and rendered.is_cuda
+    if ctx is None:
+        ctx = context(rendered.device.index or 0) if dev else context(0)
+    if grad_out is None:
+        if dev:
+            import torch
+            grad_out = torch.empty(shape, dtype=torch.float32, device=rendered.device)
+        else:
+            grad_out = np.empty(shape, dtype=np.float32)
+    rp, rl = _ptr(rendered if dev else np.ascontiguousarray(rendered, dtype=np.float32), keep)
+    mp, ml = _ptr(measured if dev else np.ascontiguousarray(measured, dtype=np.float32), keep)
+    gp, gl = _ptr(grad_out, keep)
+    if not (rl == ml == gl):
+        raise ContractError("image_loss: rendered, measured and grad must share one location")
+    losses = np.zeros((nv_, 3), dtype=np.float64)
+    ctx.check(ctx._lib.gsct_image_loss(ctx.handle, C.c_void_p(rp), C.c_void_p(mp), nv_, nu, nv, float(alpha_ssim),
+                                       C.c_void_p(gp), rl, losses.ctypes.data_as(C.POINTER(C.c_double))))
+    return losses, grad_out
+
+
+@dataclass
+class LearningRates:
+    """optim.hpp:63-68"""
+    position: float = 1e-4
+    log_scale: float = 5e-3
+    rotation: float = 1e-3
+    density: float = 1e-2
+
+
+class AdamState:
+    """OptimState's Adam moments (optim.hpp:84-114) as device fp64 tensors."""
+
+    def __init__(self, n: int, device: int = 0):
+        import torch
+        z = lambda *s: torch.zeros(s, dtype=torch.float64, device=f"cuda:{device}")
+        self.m_pos, self.v_pos, self.m_ls, self.v_ls = z(n, 3), z(n, 3), z(n, 3), z(n, 3)
+        self.m_rot, self.v_rot, self.m_dens, self.v_dens = z(n, 4), z(n, 4), z(n), z(n)
+        self.step = 0
+        self.skipped_updates = 0
+
+    def _c(self) -> c_adam_state:
+        arrs = (self.m_pos, self.v_pos, self.m_ls, self.v_ls, self.m_rot, self.v_rot, self.m_dens, self.v_dens)
+        return c_adam_state(*[a.data_ptr() for a in arrs], self.step, self.skipped_updates)
+
+
+def adam_step(cloud: GaussianCloud, state: AdamState, grads: ParamGradients, lrs: LearningRates = LearningRates(),
+              ctx: Optional[Context] = None) -> None:
+    """adam_step (optim.hpp:158-182) on a device-resident cloud (updated in place)."""
+    if not cloud.on_device or not _is_torch(grads.positions):
+        raise ContractError("adam_step: parameters and gradients must be device-resident")
+    ctx = _ctx_for(cloud, ctx)
+    keep: list = []
+    cc = cloud._c(keep)
+    st = state._c()
+    gg = grads._c()
+    lr = c_learning_rates(lrs.position, lrs.log_scale, lrs.rotation, lrs.density)
+    ctx.check(ctx._lib.gsct_adam_step(ctx.handle, C.byref(cc), C.byref(st), C.byref(gg), C.byref(lr)))
+    state.step = int(st.step)
+    state.skipped_updates = int(st.skipped_updates)

@@ -1,0 +1,119 @@
+"""Next-row operators: the fused L1 + SSIM2D image loss and device Adam.
+
+CPU part (not gpu): the oracle for both is the UNCHANGED reference compiled here
+(oracle/_ref: losses.hpp total_loss_recon, optim.hpp adam_step; its own test_losses passes,
+test_reference_suite.py). Here the reference loss is further pinned against an independent
+brute-force numpy SSIM (every 11x11 window summed directly) and central differences.
+GPU part: the CUDA operators through the C ABI against that reference:
+  * image loss: per-view l1 / ssim / total within 1e-6 relative, gradient max|d| <= 1e-5 of
+    the max |g_ref| (fp32 images and gradient, fp64 moments);
+  * Adam: bit-identical parameters and moments after several steps (incl. a non-finite
+    gradient that must be skipped and a density clamped at 0)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+from paper_2604_01844_b200 import gsct
+
+
+def _brute_ssim_loss(p: np.ndarray, t: np.ndarray) -> float:
+    d = np.arange(11) - 5.0
+    w1 = np.exp(-0.5 * d * d / 2.25)
+    w1 /= w1.sum()
+    w = np.outer(w1, w1)
+    nv, nu = p.shape
+    vals = []
+    for y in range(nv - 10):
+        for x in range(nu - 10):
+            a, b = p[y:y + 11, x:x + 11], t[y:y + 11, x:x + 11]
+            mx, my = (w * a).sum(), (w * b).sum()
+            sx = (w * a * a).sum() - mx * mx
+            sy = (w * b * b).sum() - my * my
+            sxy = (w * a * b).sum() - mx * my
+            vals.append((2 * mx * my + 1e-4) * (2 * sxy + 9e-4) / ((mx * mx + my * my + 1e-4) * (sx + sy + 9e-4)))
+    return 1.0 - float(np.mean(vals))
+
+
+def test_reference_loss_pinned_by_brute_force_and_fd(ref):
+    rng = np.random.default_rng(0)
+    p = rng.uniform(0, 1, size=(17, 19))
+    t = np.clip(p + rng.normal(0, 0.1, size=p.shape), 0, 1)
+    (l1, ssim, total), g = ref.total_loss_recon(p, t, 0.25)
+    assert abs(l1 - np.mean(np.abs(p - t))) < 1e-14
+    assert abs(ssim - _brute_ssim_loss(p, t)) < 1e-12
+    assert abs(total - (l1 + 0.25 * ssim)) < 1e-14
+    # central differences of the total at a few pixels away from |p - t| kinks
+    for (y, x) in [(3, 4), (8, 9), (16, 18), (0, 0)]:
+        if abs(p[y, x] - t[y, x]) < 1e-3:
+            continue
+        h = 1e-6
+        pp, pm = p.copy(), p.copy()
+        pp[y, x] += h
+        pm[y, x] -= h
+        fd = (ref.total_loss_recon(pp, t, 0.25)[0][2] - ref.total_loss_recon(pm, t, 0.25)[0][2]) / (2 * h)
+        assert abs(fd - g[y, x]) <= 1e-6 * max(1.0, abs(g[y, x])) + 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(3, 48, 64), (2, 11, 11), (1, 70, 45)])
+def test_image_loss_matches_reference(ref, ctx, shape):
+    import torch
+    rng = np.random.default_rng(sum(shape))
+    p = rng.uniform(0, 1, size=shape).astype(np.float32)
+    t = np.clip(p + rng.normal(0, 0.15, size=shape), 0, 1).astype(np.float32)
+    t[0, :3, :3] = p[0, :3, :3]  # exact ties: sign(0) = 0
+    for dev in (False, True):
+        pi = torch.from_numpy(p).cuda() if dev else p
+        ti = torch.from_numpy(t).cuda() if dev else t
+        losses, grad = gsct.image_loss(pi, ti, 0.25, ctx=ctx)
+        grad = grad.cpu().numpy() if dev else grad
+        for v in range(shape[0]):
+            want, gref = ref.total_loss_recon(p[v].astype(np.float64), t[v].astype(np.float64), 0.25)
+            np.testing.assert_allclose(losses[v], want, rtol=1e-6, atol=1e-9)
+            assert np.max(np.abs(grad[v] - gref)) <= 1e-5 * np.max(np.abs(gref))
+
+
+@pytest.mark.gpu
+def test_image_loss_contract(ctx):
+    a = np.zeros((1, 10, 40), dtype=np.float32)
+    with pytest.raises(gsct.ContractError, match="11x11"):
+        gsct.image_loss(a, a, 0.25, ctx=ctx)
+
+
+@pytest.mark.gpu
+def test_adam_step_bit_identical(ref, ctx):
+    import torch
+    n = 257
+    cloud = gsct.make_cloud("random", n, seed=5)
+    cloud.raw_densities[:5] = 1e-7  # pushed below 0 by the update -> clamped
+    rng = np.random.default_rng(1)
+    host = {"pos": cloud.positions.copy(), "ls": cloud.log_scales.copy(), "q": cloud.rotations.copy(),
+            "raw": cloud.raw_densities.copy()}
+    keys = ("m_pos", "v_pos", "m_ls", "v_ls", "m_rot", "v_rot", "m_dens", "v_dens")
+    shapes = {"m_pos": (n, 3), "v_pos": (n, 3), "m_ls": (n, 3), "v_ls": (n, 3), "m_rot": (n, 4), "v_rot": (n, 4),
+              "m_dens": (n,), "v_dens": (n,)}
+    hm = {k: np.zeros(shapes[k]) for k in keys}
+    dcloud = cloud.to_device(0)
+    st = gsct.AdamState(n, 0)
+    lrs = gsct.LearningRates()
+    step = skipped = 0
+    for it in range(4):
+        g = {"pos": rng.normal(size=(n, 3)), "ls": rng.normal(size=(n, 3)), "q": rng.normal(size=(n, 4)),
+             "raw": np.abs(rng.normal(size=n)) * 1e3}
+        if it == 2:
+            g["q"][7, 1] = np.nan
+            g["pos"][9, 0] = np.inf
+        dg = gsct.ParamGradients(*[torch.from_numpy(np.ascontiguousarray(g[k])).cuda() for k in ("pos", "ls", "q", "raw")],
+                                 torch.zeros(n, dtype=torch.float64, device="cuda"),
+                                 torch.zeros(n, dtype=torch.uint8, device="cuda"))
+        gsct.adam_step(dcloud, st, dg, lrs, ctx=ctx)
+        step, skipped = ref.adam_step(host, hm, g, lrs, step, skipped)
+    assert st.step == step == 4 and st.skipped_updates == skipped == 2
+    got = dcloud.numpy()
+    for a, k in ((got.positions, "pos"), (got.log_scales, "ls"), (got.rotations, "q"), (got.raw_densities, "raw")):
+        assert np.array_equal(a, host[k]), k
+    assert np.all(got.raw_densities >= 0.0) and np.any(got.raw_densities[:5] == 0.0)
+    for k in keys:
+        assert np.array_equal(getattr(st, k).cpu().numpy(), hm[k]), k

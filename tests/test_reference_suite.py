@@ -1,6 +1,7 @@
 """The reference's OWN hot-path test executables (test_core, test_projector,
-test_voxelizer, test_bench from /root/reference/proj/tests), compiled unchanged with the
-test-only Eigen/Catch2 shims into oracle/_ref/. All 43 test cases must pass: this pins the
+test_voxelizer, test_bench, and test_losses for the next-row image loss, from
+/root/reference/proj/tests), compiled unchanged with the test-only Eigen/Catch2 shims into
+oracle/_ref/. All 50 test cases must pass: this pins the
 shims (and therefore the restatement oracle, which equals the reference bit for bit, see
 test_oracle_vs_ref.py) against the reference's known answers and fixtures."""
 from __future__ import annotations
@@ -15,7 +16,7 @@ REF = ROOT / "oracle" / "_ref"
 
 
 @pytest.mark.parametrize("name,cases", [("test_core", 10), ("test_projector", 17), ("test_voxelizer", 11),
-                                        ("test_bench", 5)])
+                                        ("test_bench", 5), ("test_losses", 7)])
 def test_reference_suite_passes(name, cases):
     exe = REF / name
     if not exe.exists():
