@@ -207,6 +207,16 @@ int gsct_voxelize_bwd_finish(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_g
 int gsct_image_loss(gsct_ctx ctx, const float* rendered, const float* measured, int n_views, int n_u,
                     int n_v, double alpha_ssim, float* grad_images, int location, double* losses);
 
+/* Volume-fit loss total_loss_fit (losses.hpp:648-664): L1 + alpha_ssim * SSIM3D (11^3
+ * Gaussian window, losses.hpp:275-516) on a volume of dims {nx, ny, nz} (x fastest);
+ * out3 (host) = {l1, ssim loss, total}; grad = d total / d rendered (fp32). */
+int gsct_volume_loss(gsct_ctx ctx, const float* rendered, const float* target, const int dims[3],
+                     double alpha_ssim, float* grad, int location, double* out3);
+/* TV3D (losses.hpp:530-595): isotropic forward-difference TV, mean over interior voxels;
+ * *value (host) and grad (fp32, same layout). */
+int gsct_tv3d(gsct_ctx ctx, const float* volume, const int dims[3], float* grad, int location,
+              double* value);
+
 /* Adam (optim.hpp:133-182): beta1 0.9, beta2 0.999, eps 1e-15; splats with a non-finite
  * gradient are skipped and counted; raw densities re-projected to >= 0. Parameters (the
  * cloud arrays, updated in place), moments and gradients are device arrays (fp64). The

@@ -335,6 +335,29 @@ class Ref:
         return int(st.value), int(sk.value)
 
 
+    def total_loss_fit(self, rendered: np.ndarray, target: np.ndarray, alpha_ssim: float, streaming: bool = True):
+        """(l1, ssim, total), grad for a [nz, ny, nx] volume (losses.hpp:648-664)."""
+        r = np.ascontiguousarray(rendered, dtype=np.float64)
+        t = np.ascontiguousarray(target, dtype=np.float64)
+        dims = np.array([r.shape[2], r.shape[1], r.shape[0]], dtype=np.int32)
+        g = np.zeros_like(r)
+        out = np.zeros(3)
+        f = self.l.ref_total_loss_fit
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.c_void_p]
+        self._chk(f(_p(r), _p(t), dims.ctypes.data, float(alpha_ssim), 1 if streaming else 0, _p(g), _p(out)))
+        return out, g
+
+    def tv3d(self, volume: np.ndarray):
+        """value, grad (losses.hpp:530-595) for a [nz, ny, nx] volume."""
+        v = np.ascontiguousarray(volume, dtype=np.float64)
+        dims = np.array([v.shape[2], v.shape[1], v.shape[0]], dtype=np.int32)
+        g = np.zeros_like(v)
+        val = C.c_double(0)
+        f = self.l.ref_tv3d
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        self._chk(f(_p(v), dims.ctypes.data, _p(g), C.byref(val)))
+        return float(val.value), g
+
 def _ref_random_cloud(self, seed, count, pos_range=5.0, scale_lo=0.5, scale_hi=2.5):
     pos = np.zeros((count, 3))
     ls = np.zeros((count, 3))

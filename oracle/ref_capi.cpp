@@ -106,9 +106,9 @@ void put_grads(const ParamGradients& g, double* gp, double* gl, double* gq, doub
 }
 }  // namespace
 
-#define GUARD(body)                      \
+#define GUARD(...)                       \
   try {                                  \
-    body;                                \
+    __VA_ARGS__;                         \
     return 0;                            \
   } catch (const contract_error& e) {    \
     g_err = e.what();                    \
@@ -380,6 +380,35 @@ int ref_adam_step(int64_t n, double* pos, double* ls, double* q, double* raw, do
     }
     *step = st.step;
     *skipped = st.skipped_updates;
+  });
+}
+
+// total_loss_fit (losses.hpp:648-664) on a volume (x fastest): out3 = {l1, ssim, total}
+int ref_total_loss_fit(const double* rendered, const double* target, const int* dims, double alpha_ssim,
+                       int streaming, double* grad, double* out3) {
+  GUARD({
+    const std::array<int, 3> d{{dims[0], dims[1], dims[2]}};
+    Volume r = Volume::zeros(d, 1.0, Vec3::Zero());
+    Volume t = Volume::zeros(d, 1.0, Vec3::Zero());
+    std::memcpy(r.values.data(), rendered, r.values.size() * sizeof(double));
+    std::memcpy(t.values.data(), target, t.values.size() * sizeof(double));
+    const FitLoss L = total_loss_fit(r, t, alpha_ssim, streaming ? SsimPath::streaming : SsimPath::materialized);
+    out3[0] = L.l1;
+    out3[1] = L.ssim;
+    out3[2] = L.total;
+    std::memcpy(grad, L.grad.values.data(), L.grad.values.size() * sizeof(double));
+  });
+}
+
+// tv3d (losses.hpp:530-595)
+int ref_tv3d(const double* volume, const int* dims, double* grad, double* value) {
+  GUARD({
+    const std::array<int, 3> d{{dims[0], dims[1], dims[2]}};
+    Volume v = Volume::zeros(d, 1.0, Vec3::Zero());
+    std::memcpy(v.values.data(), volume, v.values.size() * sizeof(double));
+    const Tv3dResult R = tv3d(v);
+    *value = R.value;
+    std::memcpy(grad, R.grad.values.data(), R.grad.values.size() * sizeof(double));
   });
 }
 }  // extern "C"

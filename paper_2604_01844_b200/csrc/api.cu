@@ -24,7 +24,7 @@ namespace {
 enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
-  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP,
+  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR,
   S_COUNT_SLOTS
 };
 
@@ -1085,6 +1085,18 @@ int gsct_debug_tile_pairs(gsct_ctx c, const gsct_cloud* cloud, const gsct_geomet
 // Next-row operators: image loss, Adam
 // ---------------------------------------------------------------------------------------
 
+namespace {
+void ssim_window(double w[11]) {  // losses.hpp:85-98 on the host libm
+  double sum = 0.0;
+  for (int i = 0; i < 11; ++i) {
+    const double d = i - 5;
+    w[i] = std::exp(-0.5 * d * d / (1.5 * 1.5));
+    sum += w[i];
+  }
+  for (int i = 0; i < 11; ++i) w[i] /= sum;
+}
+}  // namespace
+
 int gsct_image_loss(gsct_ctx c, const float* rendered, const float* measured, int n_views, int n_u, int n_v,
                     double alpha_ssim, float* grad_images, int location, double* losses) {
   return run(c, [&] {
@@ -1093,14 +1105,8 @@ int gsct_image_loss(gsct_ctx c, const float* rendered, const float* measured, in
     contract(std::isfinite(alpha_ssim) && alpha_ssim >= 0.0, "LossWeights: alpha_ssim invalid");
     contract(n_views == 0 || (rendered && measured && grad_images && losses), "image_loss: null buffer");
     if (n_views == 0) return;
-    // the reference's normalised sigma-1.5 window (losses.hpp:85-98), host libm
-    double w[11], sum = 0.0;
-    for (int i = 0; i < 11; ++i) {
-      const double d = i - 5;
-      w[i] = std::exp(-0.5 * d * d / (1.5 * 1.5));
-      sum += w[i];
-    }
-    for (double& x : w) x /= sum;
+    double w[11];  // the reference's normalised sigma-1.5 window (losses.hpp:85-98), host libm
+    ssim_window(w);
     const size_t npx = static_cast<size_t>(n_u) * n_v * n_views;
     const float* p = rendered;
     const float* t = measured;
@@ -1126,6 +1132,73 @@ int gsct_image_loss(gsct_ctx c, const float* rendered, const float* measured, in
     CK(cudaMemcpyAsync(losses, out3, 3 * static_cast<size_t>(n_views) * sizeof(double), cudaMemcpyDeviceToHost,
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+
+int gsct_volume_loss(gsct_ctx c, const float* rendered, const float* target, const int dims[3], double alpha_ssim,
+                     float* grad, int location, double* out3) {
+  return run(c, [&] {
+    contract(dims != nullptr && rendered && target && grad && out3, "volume_loss: null argument");
+    contract(dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1, "l1: empty input");
+    contract(std::isfinite(alpha_ssim) && alpha_ssim >= 0.0, "total_loss_fit: alpha_ssim invalid");
+    if (alpha_ssim > 0.0)
+      contract(dims[0] >= 11 && dims[1] >= 11 && dims[2] >= 11, "ssim3d: volume smaller than the 11^3 window");
+    const size_t nvox = static_cast<size_t>(dims[0]) * dims[1] * dims[2];
+    const float* p = rendered;
+    const float* t = target;
+    float* g = grad;
+    if (location == GSCT_HOST) {
+      float* dp = ws<float>(c, S_LOSS_IN, nvox);
+      float* dt = ws<float>(c, S_LOSS_TGT, nvox);
+      CK(cudaMemcpyAsync(dp, rendered, nvox * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(dt, target, nvox * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+      p = dp, t = dt;
+      g = ws<float>(c, S_LOSS_GRAD, nvox);
+    }
+    double w[11];
+    ssim_window(w);
+    const int64_t ns = volume_loss_scratch_doubles(dims);
+    double* scr = ws<double>(c, S_VLOSS_SCR, static_cast<size_t>(ns));
+    launch_volume_loss(p, t, dims, w, alpha_ssim, scr, g, out3, c->stream);
+    CK(cudaGetLastError());
+    if (location == GSCT_HOST) CK(cudaMemcpyAsync(grad, g, nvox * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    double sums[2] = {0, 0};
+    // {sum s, sum |d|} sit after the two 5-channel buffers and the two partial arrays
+    const int64_t nb = (static_cast<int64_t>(nvox) + 255) / 256;
+    CK(cudaMemcpyAsync(sums, scr + 10 * static_cast<int64_t>(nvox) + 2 * nb, sizeof sums, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const double nout = static_cast<double>(dims[0] - 10) * (dims[1] - 10) * (dims[2] - 10);
+    out3[0] = sums[1] / static_cast<double>(nvox);
+    out3[1] = alpha_ssim > 0.0 ? 1.0 - sums[0] / nout : 0.0;
+    out3[2] = out3[0] + alpha_ssim * out3[1];
+  });
+}
+
+int gsct_tv3d(gsct_ctx c, const float* volume, const int dims[3], float* grad, int location, double* value) {
+  return run(c, [&] {
+    contract(dims != nullptr && volume && grad && value, "tv3d: null argument");
+    contract(dims[0] >= 2 && dims[1] >= 2 && dims[2] >= 2, "tv3d: dims must be at least 2 in every axis");
+    const size_t nvox = static_cast<size_t>(dims[0]) * dims[1] * dims[2];
+    const float* v = volume;
+    float* g = grad;
+    if (location == GSCT_HOST) {
+      float* dv = ws<float>(c, S_LOSS_IN, nvox);
+      CK(cudaMemcpyAsync(dv, volume, nvox * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+      v = dv;
+      g = ws<float>(c, S_LOSS_GRAD, nvox);
+    }
+    const int64_t ns = tv3d_scratch_doubles(dims);
+    double* scr = ws<double>(c, S_VLOSS_SCR, static_cast<size_t>(ns));
+    launch_tv3d(v, dims, scr, g, c->stream);
+    CK(cudaGetLastError());
+    if (location == GSCT_HOST) CK(cudaMemcpyAsync(grad, g, nvox * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    const int64_t nint = static_cast<int64_t>(dims[0] - 1) * (dims[1] - 1) * (dims[2] - 1);
+    double sum = 0.0;
+    CK(cudaMemcpyAsync(&sum, scr + nint + (nint + 255) / 256, sizeof sum, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *value = sum / static_cast<double>(nint);
   });
 }
 

@@ -127,6 +127,13 @@ void launch_image_loss(const float* pred, const float* targ, int n_views, int nu
                        double alpha, float* coef, double* part_s, double* part_l1, float* grad, double* out3,
                        cudaStream_t st);
 int64_t image_loss_partials(int n_views, int nu, int nv);
+// (loss.cu) volume-fit loss L1 + alpha * SSIM3D and TV3D; the scalar sums land at the end of
+// the scratch ({sum s, sum |d|} / {sum g}), the caller forms the means
+int64_t volume_loss_scratch_doubles(const int dims[3]);
+void launch_volume_loss(const float* pred, const float* targ, const int dims[3], const double* window, double alpha,
+                        double* scratch, float* grad, double* out3, cudaStream_t st);
+int64_t tv3d_scratch_doubles(const int dims[3]);
+void launch_tv3d(const float* vol, const int dims[3], double* scratch, float* grad, cudaStream_t st);
 // (preprocess.cu) adam_step; mv = {m_pos, v_pos, m_ls, v_ls, m_rot, v_rot, m_dens, v_dens},
 // lrs = {position, log_scale, rotation, density}
 void launch_adam_step(int64_t n, double* pos, double* ls, double* q, double* raw, double* const* mv,

@@ -140,6 +140,9 @@ _SIGS = {
                                          _P(c_voxel_settings), C.c_void_p, C.c_void_p, C.c_void_p]),
     "gsct_image_loss": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double,
                                   C.c_void_p, C.c_int, _P(C.c_double)]),
+    "gsct_volume_loss": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, _P(C.c_int), C.c_double, C.c_void_p,
+                                   C.c_int, _P(C.c_double)]),
+    "gsct_tv3d": (C.c_int, [C.c_void_p, C.c_void_p, _P(C.c_int), C.c_void_p, C.c_int, _P(C.c_double)]),
     "gsct_adam_step": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_adam_state), _P(c_grads), _P(c_learning_rates)]),
     "gsct_host_view_frame": (None, [_P(c_geometry), C.c_double, _P(C.c_double)]),
     "gsct_host_default_geometry": (None, [_P(C.c_int), C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -891,6 +894,59 @@ def image_loss(rendered, measured, alpha_ssim: float = 0.25, grad_out=None, ctx:
     ctx.check(ctx._lib.gsct_image_loss(ctx.handle, C.c_void_p(rp), C.c_void_p(mp), nv_, nu, nv, float(alpha_ssim),
                                        C.c_void_p(gp), rl, losses.ctypes.data_as(C.POINTER(C.c_double))))
     return losses, grad_out
+
+
+def _vol_args(volume, ctx):
+    if len(volume.shape) != 3:
+        raise ContractError("volume: expected a [nz, ny, nx] array")
+    dev = _is_torch(volume) and volume.is_cuda
+    if ctx is None:
+        ctx = context(volume.device.index or 0) if dev else context(0)
+    nz, ny, nx = (int(d) for d in volume.shape)
+    return dev, ctx, (C.c_int * 3)(nx, ny, nz)
+
+
+def volume_loss(rendered, target, alpha_ssim: float = 0.2, grad_out=None, ctx: Optional[Context] = None):
+    """total_loss_fit (losses.hpp:648-664): L1 + alpha * SSIM3D on [nz, ny, nx] float32
+    volumes. Returns ((l1, ssim, total), grad float32)."""
+    if tuple(rendered.shape) != tuple(target.shape):
+        raise ContractError("l1: volume shape mismatch")
+    dev, ctx, dims = _vol_args(rendered, ctx)
+    keep: list = []
+    if grad_out is None:
+        if dev:
+            import torch
+            grad_out = torch.empty(tuple(rendered.shape), dtype=torch.float32, device=rendered.device)
+        else:
+            grad_out = np.empty(tuple(rendered.shape), dtype=np.float32)
+    rp, rl = _ptr(rendered if dev else np.ascontiguousarray(rendered, dtype=np.float32), keep)
+    tp, tl = _ptr(target if dev else np.ascontiguousarray(target, dtype=np.float32), keep)
+    gp, gl = _ptr(grad_out, keep)
+    if not (rl == tl == gl):
+        raise ContractError("volume_loss: rendered, target and grad must share one location")
+    out = (C.c_double * 3)()
+    ctx.check(ctx._lib.gsct_volume_loss(ctx.handle, C.c_void_p(rp), C.c_void_p(tp), dims, float(alpha_ssim),
+                                        C.c_void_p(gp), rl, out))
+    return (out[0], out[1], out[2]), grad_out
+
+
+def tv3d(volume, grad_out=None, ctx: Optional[Context] = None):
+    """tv3d (losses.hpp:530-595) on a [nz, ny, nx] float32 volume: (value, grad)."""
+    dev, ctx, dims = _vol_args(volume, ctx)
+    keep: list = []
+    if grad_out is None:
+        if dev:
+            import torch
+            grad_out = torch.empty(tuple(volume.shape), dtype=torch.float32, device=volume.device)
+        else:
+            grad_out = np.empty(tuple(volume.shape), dtype=np.float32)
+    vp, vl = _ptr(volume if dev else np.ascontiguousarray(volume, dtype=np.float32), keep)
+    gp, gl = _ptr(grad_out, keep)
+    if vl != gl:
+        raise ContractError("tv3d: volume and grad must share one location")
+    val = C.c_double(0.0)
+    ctx.check(ctx._lib.gsct_tv3d(ctx.handle, C.c_void_p(vp), dims, C.c_void_p(gp), vl, C.byref(val)))
+    return float(val.value), grad_out
 
 
 @dataclass

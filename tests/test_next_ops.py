@@ -117,3 +117,50 @@ def test_adam_step_bit_identical(ref, ctx):
     assert np.all(got.raw_densities >= 0.0) and np.any(got.raw_densities[:5] == 0.0)
     for k in keys:
         assert np.array_equal(getattr(st, k).cpu().numpy(), hm[k]), k
+
+
+def test_reference_ssim3d_paths_and_tv_fd(ref):
+    """The reference's streaming and materialised SSIM3D agree bit for bit
+    (test_losses.cpp:140-149); TV3D gradient vs central differences."""
+    rng = np.random.default_rng(2)
+    v = rng.uniform(0, 1, size=(12, 13, 14))
+    t = np.clip(v + rng.normal(0, 0.1, size=v.shape), 0, 1)
+    a, ga = ref.total_loss_fit(v, t, 0.2, streaming=True)
+    b, gb = ref.total_loss_fit(v, t, 0.2, streaming=False)
+    assert np.array_equal(a, b) and np.array_equal(ga, gb)
+    val, g = ref.tv3d(v)
+    for idx in [(3, 4, 5), (0, 0, 0), (11, 12, 13)]:
+        h = 1e-6
+        vp, vm = v.copy(), v.copy()
+        vp[idx] += h
+        vm[idx] -= h
+        fd = (ref.tv3d(vp)[0] - ref.tv3d(vm)[0]) / (2 * h)
+        assert abs(fd - g[idx]) <= 1e-6 * max(1.0, abs(g[idx]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,alpha", [((12, 13, 14), 0.2), ((20, 11, 16), 0.5), ((5, 6, 7), 0.0)])
+def test_volume_loss_matches_reference(ref, ctx, shape, alpha):
+    import torch
+    rng = np.random.default_rng(sum(shape))
+    v = rng.uniform(0, 1, size=shape).astype(np.float32)
+    t = np.clip(v + rng.normal(0, 0.1, size=shape), 0, 1).astype(np.float32)
+    want, gref = ref.total_loss_fit(v.astype(np.float64), t.astype(np.float64), alpha)
+    for dev in (False, True):
+        vi = torch.from_numpy(v).cuda() if dev else v
+        ti = torch.from_numpy(t).cuda() if dev else t
+        got, g = gsct.volume_loss(vi, ti, alpha, ctx=ctx)
+        g = g.cpu().numpy() if dev else g
+        np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-9)
+        assert np.max(np.abs(g - gref)) <= 1e-5 * np.max(np.abs(gref))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(32, 32, 32), (2, 3, 4), (9, 17, 5)])
+def test_tv3d_matches_reference(ref, ctx, shape):
+    rng = np.random.default_rng(len(shape) + shape[0])
+    v = rng.uniform(0, 1, size=shape).astype(np.float32)
+    val, g = gsct.tv3d(v, ctx=ctx)
+    rv, rg = ref.tv3d(v.astype(np.float64))
+    assert abs(val - rv) <= 1e-9 * max(1.0, abs(rv))
+    assert np.max(np.abs(g - rg)) <= 1e-6 * np.max(np.abs(rg))
