@@ -311,8 +311,15 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd2(const RasterRec*
 // no shared memory; every item's result depends only on its own inputs (duplicated splats
 // get bit-identical moments). Items are processed in `order` (sorted by bbox shape, see
 // k_bwd_shape_keys) so the 32 lanes of a warp walk near-identical loop trip counts.
+#ifndef GSCT_LD_NA
+#define GSCT_LD_NA 0  // 1: grad-image row loads bypass L1 allocation (A/B: 3.77 vs 3.59 ms, off)
+#endif
 __device__ __forceinline__ void ldg_v8(const float* p, float (&w)[8]) {
+#if GSCT_LD_NA
+  asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#else
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#endif
                : "=f"(w[0]), "=f"(w[1]), "=f"(w[2]), "=f"(w[3]), "=f"(w[4]), "=f"(w[5]), "=f"(w[6]), "=f"(w[7])
                : "l"(p));
 }
