@@ -824,28 +824,16 @@ void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window
     launch_voxel_preprocess(d, grid, win, vs->tau_cut, vs->sigma_cap, rec, nullptr, nullptr, nullptr,
                             nullptr, c->dstats, c->stream);
   }
-#ifndef GSCT_VBWD_LANES
-#define GSCT_VBWD_LANES 1  // 1: lane per splat (region/shape order); 0: warp per splat (brick order)
-#endif
   uint32_t* order = nullptr;
   {
+    // walk order: 64^3 region of the box corner, then box shape (k_voxel_lane_keys)
     Phase ph(c, GSCT_PH_VOXEL_BIN);
-    const int nbx = (win.hi[0] - win.lo[0] + kBrick - 1) / kBrick;
-    const int nby = (win.hi[1] - win.lo[1] + kBrick - 1) / kBrick;
-    const int nbz = (win.hi[2] - win.lo[2] + kBrick - 1) / kBrick;
     uint32_t* k1 = ws<uint32_t>(c, S_KEYS, static_cast<size_t>(n));
     uint32_t* v1 = ws<uint32_t>(c, S_VALS, static_cast<size_t>(n));
     uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, static_cast<size_t>(n));
     uint32_t* v2 = ws<uint32_t>(c, S_VALS2, static_cast<size_t>(n));
-    int end_bit;
-    if (GSCT_VBWD_LANES) {
-      end_bit = launch_voxel_lane_keys(rec, n, win, voxel_bwd_vec(win, grad), k1, v1, c->stream);
-      if (end_bit > 32) end_bit = 32;
-    } else {
-      // spatial walk order: sort splats by the 8^3 brick of their box corner
-      launch_voxel_order_keys(rec, n, win, nbx, nby, k1, v1, c->stream);
-      end_bit = bits_for(static_cast<uint64_t>(nbx) * nby * nbz + 1);
-    }
+    int end_bit = launch_voxel_lane_keys(rec, n, win, voxel_bwd_vec(win, grad), k1, v1, c->stream);
+    if (end_bit > 32) end_bit = 32;
     cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
     size_t tmp_bytes = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(n), 0, end_bit, c->stream));
@@ -855,10 +843,7 @@ void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window
   }
   {
     Phase ph(c, GSCT_PH_VOXEL_BWD);
-    if (GSCT_VBWD_LANES)
-      launch_voxel_bwd_lanes(rec, order, n, win, static_cast<float>(grid.spacing), grad, mom, c->stream);
-    else
-      launch_voxel_bwd_pairs(rec, order, n, win, static_cast<float>(grid.spacing), grad, mom, c->stream);
+    launch_voxel_bwd_lanes(rec, order, n, win, static_cast<float>(grid.spacing), grad, mom, c->stream);
   }
   CK(cudaGetLastError());
 }

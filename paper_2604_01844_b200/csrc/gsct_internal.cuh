@@ -107,8 +107,6 @@ void launch_emit_brick_pairs(const VoxelRec* rec, const uint32_t* offsets,
 void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t* start,
                       const uint32_t* end, const Window& win, int nbx, int nby, int nbz,
                       float spacing, float* volume, cudaStream_t st);
-void launch_voxel_order_keys(const VoxelRec* rec, int64_t n, const Window& win, int nbx, int nby,
-                             uint32_t* keys, uint32_t* vals, cudaStream_t st);
 // lane-per-splat voxel backward: row-load width (8 or 1), walk-order keys (returns key
 // bits), the pixel walk
 int voxel_bwd_vec(const Window& win, const float* grad_volume);
@@ -116,10 +114,6 @@ int launch_voxel_lane_keys(const VoxelRec* rec, int64_t n, const Window& win, in
                            uint32_t* vals, cudaStream_t st);
 void launch_voxel_bwd_lanes(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
                             float spacing, const float* grad_volume, float* moments, cudaStream_t st);
-// order: splat walk order (a permutation of [0, n)) or nullptr for index order
-void launch_voxel_bwd_pairs(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
-                            float spacing, const float* grad_volume, float* moments, cudaStream_t st);
-
 // (loss.cu) fused L1 + SSIM2D image loss: coef = 3 * n_views * n_out fp32 scratch,
 // part_s / part_l1 = per-tile partials (image_loss_partials total), out3[3 * n_views] =
 // {l1, ssim loss, total} per view (device), grad = d total / d pred (fp32, device)
