@@ -390,11 +390,17 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     pair_rate = pairs_per_launch / (avg_ms / 1e3)
     kernel = "k_raster_fwd2" if dom == "raster_fwd" else "k_raster_bwd_lanes"
     traffic = None  # dram read+write bytes per launch from the committed ncu --set full capture
+    measured = None  # the pipes that do bind (same capture): issue slots, L1/L2 throughput
     try:
         prof = json.loads((ROOT / "profiles" / "r1" / "raster" / "summary.json").read_text())
         hit = [d for d in prof if d["kernel"] == kernel and "dram_bytes" in d]
         if hit and args.config == "c2":
             traffic = int(np.mean([d["dram_bytes"] for d in hit]))
+            measured = {"kernel": kernel, "source": "profiles/r1/raster/summary.json (ncu --set full, C2)"}
+            for key in ("issue_active_pct", "l1tex_throughput_pct", "l2_throughput_pct", "xu_pipe_pct",
+                        "fma_pipe_pct", "warps_active_pct"):
+                if key in hit[0]:
+                    measured[key] = round(float(np.mean([d[key] for d in hit])), 1)
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": kernel,
@@ -422,7 +428,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                    "settings": "reference defaults: tau 1e-4, sigma_cap 3, 16x16 tiles, 0.3 px^2 dilation"},
         "work": {"tile_pairs_per_step": stats.tile_pairs, "pixel_pairs_per_pass": stats.pixel_pairs,
                  "culled": stats.culled, "degenerate": stats.degenerate},
-        "roofline": roofline, "roofline_sfu": roofline_sfu,
+        "roofline": roofline, "roofline_sfu": roofline_sfu, "roofline_measured": measured,
         "phase_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }

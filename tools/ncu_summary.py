@@ -33,6 +33,8 @@ METRICS = {
     "l2_hit_pct": ("lts__t_sector_hit_rate.pct", 1.0),
     "sm_clock_hz": ("sm__cycles_elapsed.avg.per_second", None),
     "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
+    "l1tex_throughput_pct": ("l1tex__throughput.avg.pct_of_peak_sustained_active", 1.0),
+    "l2_throughput_pct": ("lts__throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ms": 1.0, "us": 1e-3, "ns": 1e-6,
               "s": 1e3, "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}
@@ -103,12 +105,13 @@ def main() -> None:
     out.mkdir(parents=True, exist_ok=True)
     rows = [d for r in reps for d in summarise(r)]
     (out / "summary.json").write_text(json.dumps(rows, indent=1))
-    lines = ["| kernel | ms (ncu) | DRAM MB | issue % | XU % | FMA % | ALU % | FP64 % | warps % | regs | top stall |",
-             "|---|---|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| kernel | ms (ncu) | DRAM MB | issue % | L1 % | L2 % | XU % | FMA % | ALU % | FP64 % | warps % | regs | top stall |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for d in rows:
         top = next(iter(d["top_stalls"].items()), ("-", 0))
         lines.append(f"| {d['kernel']} | {d.get('duration_ms', 0):.3f} | {d.get('dram_bytes', 0) / 1e6:.1f} | "
-                     f"{d.get('issue_active_pct', 0):.1f} | {d.get('xu_pipe_pct', 0):.1f} | {d.get('fma_pipe_pct', 0):.1f} | "
+                     f"{d.get('issue_active_pct', 0):.1f} | {d.get('l1tex_throughput_pct', 0):.1f} | "
+                     f"{d.get('l2_throughput_pct', 0):.1f} | {d.get('xu_pipe_pct', 0):.1f} | {d.get('fma_pipe_pct', 0):.1f} | "
                      f"{d.get('alu_pipe_pct', 0):.1f} | {d.get('fp64_pipe_pct', 0):.1f} | {d.get('warps_active_pct', 0):.1f} | "
                      f"{int(d.get('registers', 0))} | {top[0]} {top[1]:.2f} |")
     if len(sys.argv) > 3:
