@@ -512,12 +512,19 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # plumbing check only: gloo lets several ranks share one GPU (NCCL refuses duplicate
+    # devices); the real multi-GPU run uses the default nccl
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: the timing rules require >= 3 warm-up steps")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world > 1 and args.dist_backend == "gloo":
+        import torch
+
+        local_rank %= max(torch.cuda.device_count(), 1)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -526,7 +533,10 @@ def main() -> None:
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        else:
+            dist.init_process_group("gloo")
     try:
         run_ours(args, rank, world, local_rank)
     finally:
