@@ -217,6 +217,14 @@ int gsct_volume_loss(gsct_ctx ctx, const float* rendered, const float* target, c
 int gsct_tv3d(gsct_ctx ctx, const float* volume, const int dims[3], float* grad, int location,
               double* value);
 
+/* Ray-marched line integrals of a voxel volume (raymarch_project, synthetic.hpp:171-232):
+ * the synthetic ground-truth generator, trilinear samples at spacing/2 along every pixel ray.
+ * volume: fp32, grid dims (x fastest), grid->origin = centre of voxel (0,0,0);
+ * images[n_views][n_v][n_u] fp32. */
+int gsct_raymarch_project(gsct_ctx ctx, const float* volume, const gsct_grid* grid, int volume_location,
+                          const gsct_geometry* geom, const double* angles, int n_views, float* images,
+                          int images_location);
+
 /* Adam (optim.hpp:133-182): beta1 0.9, beta2 0.999, eps 1e-15; splats with a non-finite
  * gradient are skipped and counted; raw densities re-projected to >= 0. Parameters (the
  * cloud arrays, updated in place), moments and gradients are device arrays (fp64). The

@@ -358,6 +358,18 @@ class Ref:
         self._chk(f(_p(v), dims.ctypes.data, _p(g), C.byref(val)))
         return float(val.value), g
 
+    def raymarch_project(self, volume: np.ndarray, spacing: float, origin, geom):
+        """raymarch_project (synthetic.hpp:171-232): images [n_angles, n_v, n_u]."""
+        v = np.ascontiguousarray(volume, dtype=np.float64)
+        dims = np.array([v.shape[2], v.shape[1], v.shape[0]], dtype=np.int32)
+        org = np.ascontiguousarray(origin, dtype=np.float64)
+        ang = self._angles(geom)
+        out = np.zeros((len(ang), geom.n_v, geom.n_u))
+        f = self.l.ref_raymarch_project
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+        self._chk(f(_p(v), dims.ctypes.data, float(spacing), _p(org), C.byref(_geo(geom)), _p(ang), len(ang), _p(out)))
+        return out
+
 def _ref_random_cloud(self, seed, count, pos_range=5.0, scale_lo=0.5, scale_hi=2.5):
     pos = np.zeros((count, 3))
     ls = np.zeros((count, 3))

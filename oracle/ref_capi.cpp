@@ -411,4 +411,18 @@ int ref_tv3d(const double* volume, const int* dims, double* grad, double* value)
     std::memcpy(grad, R.grad.values.data(), R.grad.values.size() * sizeof(double));
   });
 }
+
+// raymarch_project (synthetic.hpp:171-232): images[n_angles][n_v][n_u]
+int ref_raymarch_project(const double* volume, const int* dims, double spacing, const double* origin, const Geo* g,
+                         const double* angles, int n_angles, double* images) {
+  GUARD({
+    const std::array<int, 3> d{{dims[0], dims[1], dims[2]}};
+    Volume v = Volume::zeros(d, spacing, Vec3(origin[0], origin[1], origin[2]));
+    std::memcpy(v.values.data(), volume, v.values.size() * sizeof(double));
+    const ProjectionSet P = raymarch_project(v, to_geom(g, angles, n_angles));
+    const std::size_t npx = static_cast<std::size_t>(g->n_u) * g->n_v;
+    for (int k = 0; k < n_angles; ++k)
+      std::memcpy(images + k * npx, P.images[static_cast<std::size_t>(k)].values.data(), npx * sizeof(double));
+  });
+}
 }  // extern "C"

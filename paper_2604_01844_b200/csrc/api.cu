@@ -1190,6 +1190,37 @@ int gsct_tv3d(gsct_ctx c, const float* volume, const int dims[3], float* grad, i
   });
 }
 
+int gsct_raymarch_project(gsct_ctx c, const float* volume, const gsct_grid* grid, int volume_location,
+                          const gsct_geometry* geom, const double* angles, int n_views, float* images,
+                          int images_location) {
+  return run(c, [&] {
+    validate_geometry(geom, angles, n_views);
+    contract(grid != nullptr && volume != nullptr, "raymarch_project: null volume");
+    contract(grid->dims[0] >= 1 && grid->dims[1] >= 1 && grid->dims[2] >= 1, "Volume: dims must be at least 1");
+    contract(grid->spacing > 0.0, "Volume: spacing must be positive");
+    contract(images != nullptr || n_views == 0, "raymarch_project: null image buffer");
+    if (n_views == 0) return;
+    const size_t nvox = static_cast<size_t>(grid->dims[0]) * grid->dims[1] * grid->dims[2];
+    const float* v = volume;
+    if (volume_location == GSCT_HOST) {
+      float* dv = ws<float>(c, S_LOSS_IN, nvox);
+      CK(cudaMemcpyAsync(dv, volume, nvox * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+      v = dv;
+    }
+    std::vector<Frame> frames(static_cast<size_t>(n_views));
+    for (int k = 0; k < n_views; ++k) frames[static_cast<size_t>(k)] = make_frame(geom, angles[k]);
+    Frame* df = ws<Frame>(c, S_FRAMES, frames.size());
+    CK(cudaMemcpyAsync(df, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
+    const size_t npx = static_cast<size_t>(geom->n_u) * geom->n_v * n_views;
+    float* out = images_location == GSCT_HOST ? ws<float>(c, S_LOSS_GRAD, npx) : images;
+    launch_raymarch(v, grid->dims, grid->spacing, grid->origin, df, make_geo(geom), n_views, out, c->stream);
+    CK(cudaGetLastError());
+    if (images_location == GSCT_HOST)
+      CK(cudaMemcpyAsync(images, out, npx * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int gsct_adam_step(gsct_ctx c, gsct_cloud* params, gsct_adam_state* state, const gsct_grads* grads,
                    const gsct_learning_rates* lrs) {
   return run(c, [&] {

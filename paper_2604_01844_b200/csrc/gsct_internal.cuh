@@ -127,6 +127,9 @@ int64_t volume_loss_scratch_doubles(const int dims[3]);
 void launch_volume_loss(const float* pred, const float* targ, const int dims[3], const double* window, double alpha,
                         double* scratch, float* grad, double* out3, cudaStream_t st);
 int64_t tv3d_scratch_doubles(const int dims[3]);
+// (loss.cu) raymarch_project: images[n_views][n_v][n_u] (fp32) of an fp32 volume
+void launch_raymarch(const float* vol, const int dims[3], double spacing, const double origin[3], const Frame* frames,
+                     const Geo& g, int n_views, float* images, cudaStream_t st);
 void launch_tv3d(const float* vol, const int dims[3], double* scratch, float* grad, cudaStream_t st);
 // (preprocess.cu) adam_step; mv = {m_pos, v_pos, m_ls, v_ls, m_rot, v_rot, m_dens, v_dens},
 // lrs = {position, log_scale, rotation, density}

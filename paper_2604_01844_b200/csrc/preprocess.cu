@@ -385,3 +385,117 @@ void launch_adam_step(int64_t n, double* pos, double* ls, double* q, double* raw
 }
 
 }  // namespace gsct_dev
+
+// ---------------------------------------------------------------------------------------
+// Ray-marched volume projector: raymarch_project (synthetic.hpp:
+// 171-232), the synthetic ground-truth generator -- trilinear samples at spacing/2 steps along
+// every pixel's ray, independent of the splat rasterizer. One thread per (view, pixel); ray
+// set-up, positions and the sum in fp64 (the reference's arithmetic), trilinear weights and
+// voxel values in fp32 (the volume is fp32 on the device). Lives in this --fmad=false TU
+// and divides where the reference divides, so ray entry/exit and the step count
+// ceil((t1 - t0) / step) are the reference's exactly (a knife edge for axis-aligned rays).
+// ---------------------------------------------------------------------------------------
+namespace gsct_dev {
+namespace {
+
+struct VolDesc {
+  int nx, ny, nz;
+  double spacing, ox, oy, oz;
+};
+
+__global__ void __launch_bounds__(256) k_raymarch(const float* __restrict__ vol, VolDesc vd,
+                                                  const Frame* __restrict__ frames, Geo g, int n_views,
+                                                  float* __restrict__ images) {
+  const int64_t npx = static_cast<int64_t>(g.n_u) * g.n_v;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= npx * n_views) return;
+  const int view = static_cast<int>(gid / npx);
+  const int64_t px = gid - view * npx;
+  const int u = static_cast<int>(px % g.n_u), v = static_cast<int>(px / g.n_u);
+  const Frame fr = frames[view];
+  const double cu = 0.5 * (g.n_u - 1), cv = 0.5 * (g.n_v - 1);
+  double pix[3], org[3], dir[3];
+  for (int k = 0; k < 3; ++k)  // pixel_center_world (projector.hpp:47-53)
+    pix[k] = fr.dc[k] + (u - cu) * g.s_u * fr.u[k] + (v - cv) * g.s_v * fr.v[k];
+  if (g.cone) {
+    double n2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      org[k] = fr.src[k];
+      dir[k] = pix[k] - fr.src[k];
+      n2 += dir[k] * dir[k];
+    }
+    const double nrm = sqrt(n2);  // Eigen normalized(): v / v.norm()
+    for (int k = 0; k < 3; ++k) dir[k] /= nrm;
+  } else {
+    for (int k = 0; k < 3; ++k) {
+      org[k] = pix[k];
+      dir[k] = fr.d[k];
+    }
+  }
+  const double o3[3] = {vd.ox, vd.oy, vd.oz};
+  const int n3[3] = {vd.nx, vd.ny, vd.nz};
+  double t0 = -INFINITY, t1 = INFINITY;
+  for (int a = 0; a < 3; ++a) {
+    const double lo = o3[a] - 0.5 * vd.spacing, hi = o3[a] + vd.spacing * (n3[a] - 1) + 0.5 * vd.spacing;
+    if (fabs(dir[a]) < 1e-300) {
+      if (org[a] < lo || org[a] > hi) {
+        t0 = 1.0;
+        t1 = 0.0;
+        break;
+      }
+      continue;
+    }
+    double ta = (lo - org[a]) / dir[a], tb = (hi - org[a]) / dir[a];
+    if (ta > tb) {
+      const double s = ta;
+      ta = tb;
+      tb = s;
+    }
+    t0 = fmax(t0, ta);
+    t1 = fmin(t1, tb);
+  }
+  double value = 0.0;
+  if (t1 > t0) {
+    const double step = 0.5 * vd.spacing;
+    const int64_t n_steps = max(static_cast<int64_t>(1), static_cast<int64_t>(ceil((t1 - t0) / step)));
+    const double dt = (t1 - t0) / static_cast<double>(n_steps);
+    for (int64_t i = 0; i < n_steps; ++i) {
+      const double t = t0 + (static_cast<double>(i) + 0.5) * dt;
+      double gc[3];
+      for (int a = 0; a < 3; ++a) {  // sample_trilinear (core.hpp:320-339)
+        const double w = org[a] + t * dir[a];
+        gc[a] = fmin(fmax((w - o3[a]) / vd.spacing, 0.0), static_cast<double>(n3[a] - 1));
+      }
+      const int x0 = min(static_cast<int>(gc[0]), vd.nx - 2 >= 0 ? vd.nx - 2 : 0);
+      const int y0 = min(static_cast<int>(gc[1]), vd.ny - 2 >= 0 ? vd.ny - 2 : 0);
+      const int z0 = min(static_cast<int>(gc[2]), vd.nz - 2 >= 0 ? vd.nz - 2 : 0);
+      const int x1 = min(x0 + 1, vd.nx - 1), y1 = min(y0 + 1, vd.ny - 1), z1 = min(z0 + 1, vd.nz - 1);
+      const float tx = static_cast<float>(gc[0] - x0), ty = static_cast<float>(gc[1] - y0),
+                  tz = static_cast<float>(gc[2] - z0);
+      auto at = [&](int x, int y, int z) {
+        return __ldg(vol + (static_cast<int64_t>(z) * vd.ny + y) * vd.nx + x);
+      };
+      const float c00 = fmaf(at(x1, y0, z0) - at(x0, y0, z0), tx, at(x0, y0, z0));
+      const float c10 = fmaf(at(x1, y1, z0) - at(x0, y1, z0), tx, at(x0, y1, z0));
+      const float c01 = fmaf(at(x1, y0, z1) - at(x0, y0, z1), tx, at(x0, y0, z1));
+      const float c11 = fmaf(at(x1, y1, z1) - at(x0, y1, z1), tx, at(x0, y1, z1));
+      const float c0 = fmaf(c10 - c00, ty, c00), c1 = fmaf(c11 - c01, ty, c01);
+      value += static_cast<double>(fmaf(c1 - c0, tz, c0));
+    }
+    value *= dt;
+  }
+  images[gid] = static_cast<float>(value);
+}
+
+}  // namespace
+
+void launch_raymarch(const float* vol, const int dims[3], double spacing, const double origin[3], const Frame* frames,
+                     const Geo& g, int n_views, float* images, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(g.n_u) * g.n_v * n_views;
+  if (total == 0) return;
+  VolDesc vd{dims[0], dims[1], dims[2], spacing, origin[0], origin[1], origin[2]};
+  k_raymarch<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(vol, vd, frames, g, n_views, images);
+  count_launch();
+}
+
+}  // namespace gsct_dev

@@ -143,6 +143,8 @@ _SIGS = {
     "gsct_volume_loss": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, _P(C.c_int), C.c_double, C.c_void_p,
                                    C.c_int, _P(C.c_double)]),
     "gsct_tv3d": (C.c_int, [C.c_void_p, C.c_void_p, _P(C.c_int), C.c_void_p, C.c_int, _P(C.c_double)]),
+    "gsct_raymarch_project": (C.c_int, [C.c_void_p, C.c_void_p, _P(c_grid), C.c_int, _P(c_geometry), _P(C.c_double),
+                                        C.c_int, C.c_void_p, C.c_int]),
     "gsct_adam_step": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_adam_state), _P(c_grads), _P(c_learning_rates)]),
     "gsct_host_view_frame": (None, [_P(c_geometry), C.c_double, _P(C.c_double)]),
     "gsct_host_default_geometry": (None, [_P(C.c_int), C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -947,6 +949,31 @@ def tv3d(volume, grad_out=None, ctx: Optional[Context] = None):
     val = C.c_double(0.0)
     ctx.check(ctx._lib.gsct_tv3d(ctx.handle, C.c_void_p(vp), dims, C.c_void_p(gp), vl, C.byref(val)))
     return float(val.value), grad_out
+
+
+def raymarch_project(volume, grid: GridSpec, geometry: ScanGeometry, view_indices=None, out=None,
+                     ctx: Optional[Context] = None):
+    """raymarch_project (synthetic.hpp:171-232) of a [nz, ny, nx] float32 volume laid out on
+    `grid` (origin = centre of voxel 0): images [V, n_v, n_u] float32, same kind as `volume`."""
+    dev, ctx, _ = _vol_args(volume, ctx)
+    if tuple(volume.shape) != (grid.dims[2], grid.dims[1], grid.dims[0]):
+        raise ContractError("raymarch_project: volume shape does not match the grid")
+    ang = _angles(geometry, view_indices)
+    keep: list = []
+    if out is None:
+        if dev:
+            import torch
+            out = torch.empty((ang.size, geometry.n_v, geometry.n_u), dtype=torch.float32, device=volume.device)
+        else:
+            out = np.empty((ang.size, geometry.n_v, geometry.n_u), dtype=np.float32)
+    vp, vl = _ptr(volume if dev else np.ascontiguousarray(volume, dtype=np.float32), keep)
+    op, ol = _ptr(out, keep)
+    gr = _grid_c(GridRegion.covering(grid))
+    g = geometry.c()
+    ctx.check(ctx._lib.gsct_raymarch_project(ctx.handle, C.c_void_p(vp), C.byref(gr), vl, C.byref(g),
+                                             ang.ctypes.data_as(C.POINTER(C.c_double)), int(ang.size),
+                                             C.c_void_p(op), ol))
+    return out
 
 
 @dataclass
