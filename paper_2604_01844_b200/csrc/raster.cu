@@ -298,6 +298,153 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd2(const RasterRec*
   }
 }
 
+// Forward v4 (K3): one warp per 32x16 half of a 32x32 super-tile; lane l owns a 2 x 8 pixel
+// block (rows 2(l>>2), +1; columns 8(l&3) .. +7), rows packed in f32x2 halves. Same
+// super-tile list walk, per-lane filtering and multiplicative row chains as k_raster_fwd2,
+// but twice the pixels per (lane, record): the per-record set-up (mask decode, exponent
+// origin, four MUFU) is amortised over 16 pixels instead of 8, and each super-tile list is
+// staged by 2 warps instead of 4.
+__global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict__ rec,
+                                                     const uint32_t* __restrict__ vals,
+                                                     const uint32_t* __restrict__ start,
+                                                     const uint32_t* __restrict__ end, int64_t n, int n_u,
+                                                     int n_v, int stiles_u, int n_stiles,
+                                                     float* __restrict__ images) {
+  constexpr int kHW = 2 * kTile, kHH = kTile;  // half-tile: 32 wide, 16 tall
+  __shared__ StagedRec2 s_rec[4][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = blockIdx.x * 4 + warp;  // 2 halves per super-tile
+  if (half >= 2 * n_stiles) return;
+  const int st = half >> 1, view = blockIdx.y;
+  const int tx0 = (st % stiles_u) * kBinTile;
+  const int ty0 = (st / stiles_u) * kBinTile + (half & 1) * kHH;
+  if (ty0 >= n_v) return;
+  const int lr = 2 * (lane >> 2), lc = 8 * (lane & 3);
+  const float flr = static_cast<float>(lr), flc = static_cast<float>(lc);
+  const uint32_t key = static_cast<uint32_t>(view) * n_stiles + st;
+  const uint32_t b = start[key], e = end[key];
+  const RasterRec* __restrict__ vrec = rec + static_cast<int64_t>(view) * n;
+  StagedRec2* sw = s_rec[warp];
+  float acc0[8], acc1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.f;
+
+  uint32_t idx_next = (b + 32 + lane < e) ? vals[b + 32 + lane] : 0u;
+  RasterRec r_cur;
+  if (b + lane < e) r_cur = vrec[vals[b + lane]];
+  for (uint32_t base = b; base < e; base += 32) {
+    const int cnt = min(32u, e - base);
+    const bool has_next = base + 32 + lane < e;
+    RasterRec r_next;
+    if (has_next) r_next = vrec[idx_next];
+    idx_next = (base + 64 + lane < e) ? vals[base + 64 + lane] : 0u;
+    uint32_t lanes_rel = 0u;
+    if (lane < cnt) {
+      const RasterRec r = r_cur;
+      const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16, v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+      const int c0 = max(u0 - tx0, 0), c1 = min(u1 - tx0, kHW - 1);
+      const int r0 = max(v0 - ty0, 0), r1 = min(v1 - ty0, kHH - 1);
+      if (c0 <= c1 && r0 <= r1) {
+        StagedRec2 s;
+        const float du_t = (static_cast<float>(tx0) - static_cast<float>(u0)) - r.mo_u;
+        const float dv_t = (static_cast<float>(ty0) - static_cast<float>(v0)) - r.mo_v;
+        const uint32_t cm = (c1 == 31 ? 0xFFFFFFFFu : ((2u << c1) - 1u)) & ~((1u << c0) - 1u);
+        const uint32_t rm = ((2u << r1) - 1u) & ~((1u << r0) - 1u);
+        // lane mask: column octets c0/8..c1/8 x row pairs r0/2..r1/2 (lane = 4 * pair + octet)
+        const uint32_t octs = ((2u << (c1 >> 3)) - 1u) & ~((1u << (c0 >> 3)) - 1u);
+        const uint32_t pairs = (0x11111111u >> (4 * (7 - (r1 >> 1)))) & (0x11111111u << (4 * (r0 >> 1)));
+        lanes_rel = pairs * octs;
+        // chain-safety window: rows r0..r1 x 8-aligned columns
+        const float dua = du_t + static_cast<float>(c0 & ~7), dub = du_t + static_cast<float>(c1 | 7);
+        const float dva = dv_t + static_cast<float>(r0 & ~1), dvb = dv_t + static_cast<float>(r1 | 1);
+        const float emin = fminf(fminf(quad_e(r.A, r.B, r.C, dua, dva), quad_e(r.A, r.B, r.C, dua, dvb)),
+                                 fminf(quad_e(r.A, r.B, r.C, dub, dva), quad_e(r.A, r.B, r.C, dub, dvb)));
+        const float da = r.A * fmaf(2.f, dua, 1.f), db = r.A * fmaf(2.f, dub, 1.f);
+        const float dmax = fmaxf(fmaxf(fabsf(fmaf(r.B, dva, da)), fabsf(fmaf(r.B, dvb, da))),
+                                 fmaxf(fabsf(fmaf(r.B, dva, db)), fabsf(fmaf(r.B, dvb, db))));
+        const bool safe = emin > -100.f && dmax < 100.f && r.A > -25.f;
+        s.p = make_float4(du_t, dv_t, r.A, r.B);
+        s.q = make_float4(r.C, r.amp, ex2_approx(2.f * r.A), safe ? 1.f : 0.f);
+        s.m = make_uint4(cm, rm, lanes_rel, 0u);
+        sw[lane] = s;
+      }
+    }
+    __syncwarp();
+    uint32_t todo = warp_transpose32(lanes_rel, lane);
+#pragma unroll kFwdUnroll
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1u;
+      const float4 p = sw[j].p;
+      const float4 q = sw[j].q;
+      const uint2 mm = make_uint2(sw[j].m.x, sw[j].m.y);
+      const uint32_t mask = (mm.x >> lc) & 0xFFu;  // this lane's 8 columns
+      const uint32_t rows = (mm.y >> lr) & 3u;     // this lane's 2 rows
+      const float a0 = (rows & 1u) ? q.y : 0.f, a1 = (rows & 2u) ? q.y : 0.f;
+      const float du0 = p.x + flc;
+      const float dv0 = p.y + flr;
+      const f2_t DV = f2_pack(dv0, dv0 + 1.f);
+      const float bdu = p.w * du0, au2 = p.z * du0 * du0;
+      const f2_t CC = f2_pack(q.x, q.x);
+      f2_t h[8];
+      if (q.w != 0.f) {
+        const f2_t E0 = f2_fma(DV, f2_fma(CC, DV, f2_pack(bdu, bdu)), f2_pack(au2, au2));
+        const float a1e = p.z * fmaf(2.f, du0, 1.f);
+        const f2_t D = f2_fma(f2_pack(p.w, p.w), DV, f2_pack(a1e, a1e));
+        float e0, e1, d0, d1;
+        f2_unpack(E0, e0, e1);
+        f2_unpack(D, d0, d1);
+        h[0] = f2_pack(ex2_approx(e0), ex2_approx(e1));
+        f2_t rr = f2_pack(ex2_approx(d0), ex2_approx(d1));
+        const f2_t c2 = f2_pack(q.z, q.z);
+#pragma unroll
+        for (int k = 1; k < 8; ++k) {
+          h[k] = f2_mul(h[k - 1], rr);
+          if (k < 7) rr = f2_mul(rr, c2);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float duk = du0 + static_cast<float>(k);
+          const f2_t ek = f2_fma(DV, f2_fma(CC, DV, f2_pack(p.w * duk, p.w * duk)),
+                                 f2_pack(p.z * duk * duk, p.z * duk * duk));
+          float e0, e1;
+          f2_unpack(ek, e0, e1);
+          h[k] = f2_pack(ex2_approx(e0), ex2_approx(e1));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float hl, hh;
+        f2_unpack(h[k], hl, hh);
+        if (mask & (1u << k)) {
+          acc0[k] = fmaf(hl, a0, acc0[k]);
+          acc1[k] = fmaf(hh, a1, acc1[k]);
+        }
+      }
+    }
+    __syncwarp();
+    r_cur = r_next;
+  }
+  const int px0 = tx0 + lc;
+  if (px0 >= n_u) return;
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int py = ty0 + lr + hh;
+    if (py >= n_v) continue;
+    const float* v = hh ? acc1 : acc0;
+    float* rowp = images + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(py) * n_u;
+    if (((n_u & 3) == 0) && px0 + 8 <= n_u) {
+      reinterpret_cast<float4*>(rowp + px0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(rowp + px0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (px0 + k < n_u) rowp[px0 + k] = v[k];
+    }
+  }
+}
+
 // Lane-per-item backward (K4a). The per-(view, splat) pixel loop is small (hundreds of
 // pixels), so warp-cooperative schemes spend more instructions on lane mapping and the
 // cross-lane moment reduction than on pixels. Here ONE LANE owns one item end to end: it
@@ -552,7 +699,15 @@ void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const u
   const int n_stiles = stiles_u * stiles_v;
   dim3 grid(static_cast<unsigned>(n_stiles), static_cast<unsigned>(n_views));
   // (A/B: CTA-shared 128-record staging with block barriers was slower, 3.88 vs 3.63 ms)
-  k_raster_fwd2<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, images);
+#ifndef GSCT_FWD_HALF
+#define GSCT_FWD_HALF 1  // 1: warp per 32x16 half-super-tile, 2x8 lane blocks (k_raster_fwd4)
+#endif
+  if (GSCT_FWD_HALF) {
+    dim3 g4(static_cast<unsigned>((2 * n_stiles + 3) / 4), static_cast<unsigned>(n_views));
+    k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, images);
+  } else {
+    k_raster_fwd2<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, images);
+  }
   count_launch();
 }
 
