@@ -107,24 +107,24 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, ui
   end[k] = lower_bound_u32(keys, n_pairs, k + 1);
 }
 
-constexpr int kFwdWarps = 4;  // tiles per CTA (one warp per 16x16 tile of a 32x32 super-tile)
-
-// Forward (K3): one warp per 16x16 tile and view; lane l owns the 2 x 4 pixel block at
-// rows 2(l>>2) .. +1, columns 4(l&3) .. +3, the two rows held in the halves of packed f32x2
-// registers. Records of the 32x32 super-tile list containing the tile (ascending splat
-// index = the reference's per-pixel accumulation order) are staged 32 at a time in the
-// warp's shared-memory slice; the
-// staging lane also derives the per-splat ratio c = exp2(2A) and a "chain-safe" flag.
+// Forward (K3): one warp per 32x16 half of a 32x32 super-tile and view; lane l owns the
+// 2 x 8 pixel block at rows 2(l>>2), +1 and columns 8(l&3) .. +7, the two rows held in the
+// halves of packed f32x2 registers. Records of the super-tile list (ascending splat index =
+// the reference's per-pixel accumulation order) are staged 32 at a time in the warp's
+// shared-memory slice; the staging lane also derives the per-splat ratio c = exp2(2A), a
+// "chain-safe" flag and the 32-bit mask of lanes whose block the record's bbox meets. A
+// 5-step xor-shuffle 32x32 bit transpose turns those masks into each lane's own list of
+// records, so a lane only walks records that touch its block (in list order).
 // Along a row the Gaussian is evaluated multiplicatively: with e(k) = E0 + k D + k(k-1) A,
-//   g(k+1) = g(k) r(k),  r(k+1) = r(k) c,   g(0) = amp 2^E0,  r(0) = 2^D,
+//   g(k+1) = g(k) r(k),  r(k+1) = r(k) c,   g(0) = 2^E0,  r(0) = 2^D,
 // i.e. 2 packed FMULs per pixel pair instead of one MUFU.EX2 per pixel; the column mask
-// predicates the accumulation, row validity is folded into g(0). The chain is used when no
-// value in the tile's (4-column aligned) bbox window under/overflows fp32 (the flag);
+// predicates the accumulation, row validity is folded into the amplitude. The chain is used
+// when no value in the (8-column aligned) bbox window under/overflows fp32 (the flag);
 // otherwise the splat takes the direct MUFU path. Both give amp * exp(e) to a few ulps.
 struct __align__(16) StagedRec2 {
-  float4 p;  // du_t = (tx0 - u0) - mo_u, dv_t = (ty0 - v0) - mo_v (tile-origin offsets), A, B
+  float4 p;  // du_t = (tx0 - u0) - mo_u, dv_t = (ty0 - v0) - mo_v (block-origin offsets), A, B
   float4 q;  // C, amp, c = exp2(2A), chain-safe flag (1/0)
-  uint4 m;   // column mask (bit c: tile column c in the bbox) | row mask << 16, lane mask, -, -
+  uint4 m;   // column mask (32 columns), row mask (16 rows), lane mask, -
 };
 
 __device__ __forceinline__ float quad_e(float A, float B, float C, float du, float dv) {
@@ -146,164 +146,10 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 }
 
 #ifndef GSCT_FWD_UNROLL
-#define GSCT_FWD_UNROLL 4  // unroll factor of the per-lane record walk (A/B: 1 -> 3.50, 4 -> 3.15 ms)
+#define GSCT_FWD_UNROLL 4  // unroll factor of the per-lane record walk (A/B on 2x4 blocks: 1 -> 3.50, 4 -> 3.15 ms)
 #endif
 constexpr int kFwdUnroll = GSCT_FWD_UNROLL;
 
-#ifndef GSCT_FWD_FILTER
-#define GSCT_FWD_FILTER 1  // 1: each lane walks only the records touching its 2x4 block
-#endif
-
-__global__ void __launch_bounds__(kFwdWarps * 32) k_raster_fwd2(const RasterRec* __restrict__ rec,
-                                                                const uint32_t* __restrict__ vals,
-                                                                const uint32_t* __restrict__ start,
-                                                                const uint32_t* __restrict__ end, int64_t n,
-                                                                int n_u, int n_v, int stiles_u, int n_stiles,
-                                                                float* __restrict__ images) {
-  // one CTA per 32x32 super-tile list and view; warp w owns the 16x16 tile (w & 1, w >> 1)
-  // and walks the super-tile list independently (warp-private staging, no block barriers);
-  // records that miss its tile get an all-zero lane mask and cost one staging lane
-  __shared__ StagedRec2 s_rec[kFwdWarps][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int st = blockIdx.x, view = blockIdx.y;
-  const int tx0 = (st % stiles_u) * kBinTile + (warp & 1) * kTile;
-  const int ty0 = (st / stiles_u) * kBinTile + (warp >> 1) * kTile;
-  if (tx0 >= n_u || ty0 >= n_v) return;  // whole warp exits together
-  const int lr = 2 * (lane >> 2), lc = 4 * (lane & 3);  // lane block offset inside the tile
-  const float flr = static_cast<float>(lr), flc = static_cast<float>(lc);
-  const uint32_t key = static_cast<uint32_t>(view) * n_stiles + st;
-  const uint32_t b = start[key], e = end[key];
-  const RasterRec* __restrict__ vrec = rec + static_cast<int64_t>(view) * n;
-  StagedRec2* sw = s_rec[warp];
-  f2_t acc[4];  // column k of the block: (row lr, row lr + 1)
-#pragma unroll
-  for (int k = 0; k < 4; ++k) acc[k] = f2_pack(0.f, 0.f);
-
-  uint32_t idx_next = (b + 32 + lane < e) ? vals[b + 32 + lane] : 0u;
-  RasterRec r_cur;
-  if (b + lane < e) r_cur = vrec[vals[b + lane]];
-  for (uint32_t base = b; base < e; base += 32) {
-    const int cnt = min(32u, e - base);
-    const bool has_next = base + 32 + lane < e;
-    RasterRec r_next;
-    if (has_next) r_next = vrec[idx_next];
-    idx_next = (base + 64 + lane < e) ? vals[base + 64 + lane] : 0u;
-    uint32_t lanes_rel = 0u;  // lanes whose 2x4 block meets this record's bbox
-    if (lane < cnt) {
-      const RasterRec r = r_cur;
-      StagedRec2 s;
-      const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16, v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
-      const float du_t = (static_cast<float>(tx0) - static_cast<float>(u0)) - r.mo_u;
-      const float dv_t = (static_cast<float>(ty0) - static_cast<float>(v0)) - r.mo_v;
-      // bbox n tile in tile coordinates (may be empty: the list is the super-tile's)
-      const int c0 = max(u0 - tx0, 0), c1 = min(u1 - tx0, kTile - 1);
-      const int r0 = max(v0 - ty0, 0), r1 = min(v1 - ty0, kTile - 1);
-      if (c0 <= c1 && r0 <= r1) {
-      const uint32_t cm = ((2u << c1) - 1u) & ~((1u << c0) - 1u);
-      const uint32_t rm = ((2u << r1) - 1u) & ~((1u << r0) - 1u);
-      // lane mask: column quads c0/4..c1/4 x row pairs r0/2..r1/2 (lane = 4 * pair + quad)
-      const uint32_t quads = ((2u << (c1 >> 2)) - 1u) & ~((1u << (c0 >> 2)) - 1u);
-      const uint32_t pairs = (0x11111111u >> (4 * (7 - (r1 >> 1)))) & (0x11111111u << (4 * (r0 >> 1)));
-      lanes_rel = pairs * quads;
-      // chain-safety window: rows r0..r1 x 4-aligned columns; the exponent is concave (min at
-      // a corner), the ratio exponent D = A (2 du + 1) + B dv is linear (extremes at corners)
-      const float dua = du_t + static_cast<float>(c0 & ~3), dub = du_t + static_cast<float>(c1 | 3);
-      const float dva = dv_t + static_cast<float>(r0), dvb = dv_t + static_cast<float>(r1);
-      const float emin = fminf(fminf(quad_e(r.A, r.B, r.C, dua, dva), quad_e(r.A, r.B, r.C, dua, dvb)),
-                               fminf(quad_e(r.A, r.B, r.C, dub, dva), quad_e(r.A, r.B, r.C, dub, dvb)));
-      const float da = r.A * fmaf(2.f, dua, 1.f), db = r.A * fmaf(2.f, dub, 1.f);
-      const float dmax = fmaxf(fmaxf(fabsf(fmaf(r.B, dva, da)), fabsf(fmaf(r.B, dvb, da))),
-                               fmaxf(fabsf(fmaf(r.B, dva, db)), fabsf(fmaf(r.B, dvb, db))));
-      const bool safe = emin > -100.f && dmax < 100.f && r.A > -50.f;
-      s.p = make_float4(du_t, dv_t, r.A, r.B);
-      s.q = make_float4(r.C, r.amp, ex2_approx(2.f * r.A), safe ? 1.f : 0.f);
-      s.m = make_uint4(cm | (rm << 16), lanes_rel, 0u, 0u);
-      sw[lane] = s;
-      }
-    }
-    __syncwarp();
-#if GSCT_FWD_FILTER
-    uint32_t todo = warp_transpose32(lanes_rel, lane);  // records touching this lane's block
-#pragma unroll kFwdUnroll
-    while (todo) {
-      const int j = __ffs(todo) - 1;
-      todo &= todo - 1u;
-#else
-    for (int j = 0; j < cnt; ++j) {
-#endif
-      const float4 p = sw[j].p;
-      const float4 q = sw[j].q;
-      const uint32_t mm = sw[j].m.x;
-      const uint32_t mask = (mm >> lc) & 15u;        // this lane's 4 columns
-      const uint32_t rows = (mm >> (16 + lr)) & 3u;  // this lane's 2 rows
-      const f2_t AMP = f2_pack((rows & 1u) ? q.y : 0.f, (rows & 2u) ? q.y : 0.f);
-      const f2_t ZERO = f2_pack(0.f, 0.f);
-      const float du0 = p.x + flc;
-      const float dv0 = p.y + flr;
-      const f2_t DV = f2_pack(dv0, dv0 + 1.f);
-      const float bdu = p.w * du0, au2 = p.z * du0 * du0;
-      const f2_t CC = f2_pack(q.x, q.x);
-      f2_t h[4];  // exp2 of the exponent, without the amplitude
-      if (q.w != 0.f) {
-        // E0 = A du0^2 + B du0 dv + C dv^2;  D = A (2 du0 + 1) + B dv
-        const f2_t E0 = f2_fma(DV, f2_fma(CC, DV, f2_pack(bdu, bdu)), f2_pack(au2, au2));
-        const float a1 = p.z * fmaf(2.f, du0, 1.f);
-        const f2_t D = f2_fma(f2_pack(p.w, p.w), DV, f2_pack(a1, a1));
-        float e0, e1, d0, d1;
-        f2_unpack(E0, e0, e1);
-        f2_unpack(D, d0, d1);
-        h[0] = f2_pack(ex2_approx(e0), ex2_approx(e1));
-        f2_t rr = f2_pack(ex2_approx(d0), ex2_approx(d1));
-        const f2_t c2 = f2_pack(q.z, q.z);
-        h[1] = f2_mul(h[0], rr);
-        rr = f2_mul(rr, c2);
-        h[2] = f2_mul(h[1], rr);
-        rr = f2_mul(rr, c2);
-        h[3] = f2_mul(h[2], rr);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float duk = du0 + static_cast<float>(k);
-          const f2_t ek = f2_fma(DV, f2_fma(CC, DV, f2_pack(p.w * duk, p.w * duk)),
-                                 f2_pack(p.z * duk * duk, p.z * duk * duk));
-          float e0, e1;
-          f2_unpack(ek, e0, e1);
-          h[k] = f2_pack(ex2_approx(e0), ex2_approx(e1));
-        }
-      }
-      // columns outside the bbox get amplitude 0 (adds exact zeros; h is finite)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) f2_fma_acc(acc[k], h[k], (mask & (1u << k)) ? AMP : ZERO);
-    }
-    __syncwarp();
-    r_cur = r_next;
-  }
-  float acc0[4], acc1[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) f2_unpack(acc[k], acc0[k], acc1[k]);
-  const int px0 = tx0 + lc;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int py = ty0 + lr + h;
-    if (py >= n_v) continue;
-    const float* v = h ? acc1 : acc0;
-    float* row = images + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(py) * n_u;
-    if (((n_u & 3) == 0) && px0 + 4 <= n_u) {
-      reinterpret_cast<float4*>(row + px0)[0] = make_float4(v[0], v[1], v[2], v[3]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (px0 + k < n_u) row[px0 + k] = v[k];
-    }
-  }
-}
-
-// Forward v4 (K3): one warp per 32x16 half of a 32x32 super-tile; lane l owns a 2 x 8 pixel
-// block (rows 2(l>>2), +1; columns 8(l&3) .. +7), rows packed in f32x2 halves. Same
-// super-tile list walk, per-lane filtering and multiplicative row chains as k_raster_fwd2,
-// but twice the pixels per (lane, record): the per-record set-up (mask decode, exponent
-// origin, four MUFU) is amortised over 16 pixels instead of 8, and each super-tile list is
-// staged by 2 warps instead of 4.
 __global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict__ rec,
                                                      const uint32_t* __restrict__ vals,
                                                      const uint32_t* __restrict__ start,
@@ -697,17 +543,10 @@ void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const u
                              int stiles_v, float* images, cudaStream_t st) {
   if (n_views == 0) return;
   const int n_stiles = stiles_u * stiles_v;
-  dim3 grid(static_cast<unsigned>(n_stiles), static_cast<unsigned>(n_views));
-  // (A/B: CTA-shared 128-record staging with block barriers was slower, 3.88 vs 3.63 ms)
-#ifndef GSCT_FWD_HALF
-#define GSCT_FWD_HALF 1  // 1: warp per 32x16 half-super-tile, 2x8 lane blocks (k_raster_fwd4)
-#endif
-  if (GSCT_FWD_HALF) {
-    dim3 g4(static_cast<unsigned>((2 * n_stiles + 3) / 4), static_cast<unsigned>(n_views));
-    k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, images);
-  } else {
-    k_raster_fwd2<<<grid, kFwdWarps * 32, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, images);
-  }
+  // one warp per 32x16 half-super-tile (A/B at C2: 2x4-px lane blocks 3.65 ms, 2x8 2.96 ms,
+  // 4x8 3.34 ms; CTA-shared staging with block barriers was slower still)
+  dim3 g4(static_cast<unsigned>((2 * n_stiles + 3) / 4), static_cast<unsigned>(n_views));
+  k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, images);
   count_launch();
 }
 
