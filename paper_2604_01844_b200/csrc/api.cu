@@ -889,7 +889,7 @@ int gsct_voxelize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
     if (volume_location == GSCT_HOST) outv = ws<float>(c, S_VOLUME, static_cast<size_t>(nvox));
     const int nbx = (win.hi[0] - win.lo[0] + kBrick - 1) / kBrick;
     const int nby = (win.hi[1] - win.lo[1] + kBrick - 1) / kBrick;
-    const int nbz = (win.hi[2] - win.lo[2] + kBrick - 1) / kBrick;
+    const int nbz = (win.hi[2] - win.lo[2] + kBrickZ - 1) / kBrickZ;
     const uint64_t n_bricks = static_cast<uint64_t>(nbx) * nby * nbz;
     contract(n_bricks < (uint64_t(1) << 31), "voxelize: grid too large");
     if (n == 0) {

@@ -12,7 +12,8 @@ namespace gsct_dev {
 constexpr int kTile = 16;       // reference default tile (projector.hpp:67); the raster
                                 // kernel is specialised for it, other sizes are rejected
 constexpr int kBinTile = 32;   // forward binning granularity (32x32 super-tiles of 4 tiles)
-constexpr int kBrick = 8;       // voxel brick edge (8x8x8 voxels per CTA)
+constexpr int kBrick = 8;       // voxel brick edge in x and y
+constexpr int kBrickZ = 16;     // voxel brick depth (a brick = 8 x 8 x 16 voxels = one warp)
 constexpr float kLog2e = 1.4426950408889634f;
 
 // Device counters written by the set-up kernels (order-independent integer sums).

@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(256) k_voxel_preprocess(Cloud c, VoxGrid grid,
         cnt = 1;
 #pragma unroll
         for (int k = 0; k < 3; ++k)
-          cnt *= static_cast<uint32_t>((whi[k] - win.lo[k]) / kBrick - (wlo[k] - win.lo[k]) / kBrick + 1);
+          cnt *= static_cast<uint32_t>((whi[k] - win.lo[k]) / (k == 2 ? kBrickZ : kBrick) -
+                                       (wlo[k] - win.lo[k]) / (k == 2 ? kBrickZ : kBrick) + 1);
         n_pp = static_cast<unsigned long long>(whi[0] - wlo[0] + 1) *
                static_cast<unsigned long long>(whi[1] - wlo[1] + 1) *
                static_cast<unsigned long long>(whi[2] - wlo[2] + 1);

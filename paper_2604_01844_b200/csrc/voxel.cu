@@ -36,7 +36,7 @@ __global__ void k_emit_brick_pairs(const VoxelRec* __restrict__ rec,
   const int z0 = max(static_cast<int>(r.loz), win.lo[2]), z1 = min(static_cast<int>(r.hiz), win.hi[2] - 1);
   const int bx0 = (x0 - win.lo[0]) / kBrick, bx1 = (x1 - win.lo[0]) / kBrick;
   const int by0 = (y0 - win.lo[1]) / kBrick, by1 = (y1 - win.lo[1]) / kBrick;
-  const int bz0 = (z0 - win.lo[2]) / kBrick, bz1 = (z1 - win.lo[2]) / kBrick;
+  const int bz0 = (z0 - win.lo[2]) / kBrickZ, bz1 = (z1 - win.lo[2]) / kBrickZ;
   uint32_t off = offsets[i];
   for (int bz = bz0; bz <= bz1; ++bz)
     for (int by = by0; by <= by1; ++by)
@@ -97,16 +97,17 @@ struct __align__(16) StagedVox {
   uint4 m;   // x mask | y mask << 8, lane mask, lane of the exact-peak row (or ~0), bits of off_z
 };
 
-// Forward v2 (K7): one WARP per 8^3 brick (4 bricks per CTA); lane l owns the two x-rows
-// (y = 2(l & 3), +1; z = l >> 2) of 8 voxels, the rows in the halves of packed f32x2
-// registers. The brick's splat list (ascending index = the reference's per-voxel order) is
-// staged 32 records at a time in warp-private shared memory; each lane walks only the
-// records whose box meets its rows (32x32 warp bit transpose of the staged lane masks).
-// Along x the Gaussian is a 1-D quadratic in the exponent, evaluated multiplicatively
-// (g <- g r, r <- r c: 2 packed FMULs per voxel pair, one MUFU pair per row pair to start),
-// with a per-record safety flag (no fp32 under/overflow anywhere in the brick window)
-// falling back to direct exp2; the row holding an exactly-on-lattice centre also uses the
-// direct path so the peak voxel is rho * exp2(0) = rho exactly (test_voxelizer.cpp:16-22).
+// Forward (K7): one WARP per 8 x 8 x 16 brick (4 per CTA); lane l owns four x-rows of 8
+// voxels: y = 2(l & 3), +1 (the halves of packed f32x2 registers) at z = 2(l >> 2), +1. The
+// brick's splat list (ascending index = the reference's per-voxel order) is staged 32
+// records at a time in warp-private shared memory; each lane walks only the records whose
+// box meets its rows (32x32 warp bit transpose of the staged lane masks), so a staged
+// record's set-up is shared by up to 32 voxels of the lane. Along x the Gaussian is a 1-D
+// quadratic in the exponent, evaluated multiplicatively (g <- g r, r <- r c: 2 packed FMULs
+// per voxel pair, one MUFU pair per row pair to start), with a per-record safety flag (no
+// fp32 under/overflow anywhere in the brick window) falling back to direct exp2; the rows
+// holding an exactly-on-lattice centre also use the direct path so the peak voxel is
+// rho * exp2(0) = rho exactly (test_voxelizer.cpp:16-22).
 __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__ rec,
                                                    const uint32_t* __restrict__ vals,
                                                    const uint32_t* __restrict__ start,
@@ -118,14 +119,14 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
   const int brick = blockIdx.x * 4 + warp;
   if (brick >= n_bricks) return;
   const int bx = brick % nbx, by = (brick / nbx) % nby, bz = brick / (nbx * nby);
-  const int gx0 = win.lo[0] + bx * kBrick, gy0 = win.lo[1] + by * kBrick, gz0 = win.lo[2] + bz * kBrick;
-  const int yp = lane & 3, zl = lane >> 2;
-  const float fy = static_cast<float>(2 * yp) * sp, fzl = static_cast<float>(zl);
+  const int gx0 = win.lo[0] + bx * kBrick, gy0 = win.lo[1] + by * kBrick, gz0 = win.lo[2] + bz * kBrickZ;
+  const int yp = lane & 3, zp = lane >> 2;
+  const float fy = static_cast<float>(2 * yp) * sp;
   const uint32_t b = start[brick], e = end[brick];
   StagedVox* sw = s_rec[warp];
-  float acc0[8], acc1[8];
+  float acc[2][2][8];  // [z][y][x]
 #pragma unroll
-  for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.f;
+  for (int k = 0; k < 8; ++k) acc[0][0][k] = acc[0][1][k] = acc[1][0][k] = acc[1][1][k] = 0.f;
   for (uint32_t base = b; base < e; base += 32) {
     const int cnt = min(32u, e - base);
     uint32_t lanes_rel = 0u;
@@ -135,19 +136,20 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
       const int ilx = static_cast<int>(r.lox), ily = static_cast<int>(r.loy), ilz = static_cast<int>(r.loz);
       const int x_lo = max(ilx - gx0, 0), x_hi = min(static_cast<int>(r.hix) - gx0, kBrick - 1);
       const int y_lo = max(ily - gy0, 0), y_hi = min(static_cast<int>(r.hiy) - gy0, kBrick - 1);
-      const int z_lo = max(ilz - gz0, 0), z_hi = min(static_cast<int>(r.hiz) - gz0, kBrick - 1);
+      const int z_lo = max(ilz - gz0, 0), z_hi = min(static_cast<int>(r.hiz) - gz0, kBrickZ - 1);
       const uint32_t xm = ((2u << x_hi) - 1u) & ~((1u << x_lo) - 1u);
       const uint32_t ym = ((2u << y_hi) - 1u) & ~((1u << y_lo) - 1u);
-      const uint32_t pairs = ((2u << (y_hi >> 1)) - 1u) & ~((1u << (y_lo >> 1)) - 1u);
-      const uint32_t zs = (0x11111111u >> (4 * (7 - z_hi))) & (0x11111111u << (4 * z_lo));
-      lanes_rel = zs * pairs;
+      const uint32_t zm = ((2u << z_hi) - 1u) & ~((1u << z_lo) - 1u);
+      const uint32_t ypairs = ((2u << (y_hi >> 1)) - 1u) & ~((1u << (y_lo >> 1)) - 1u);
+      const uint32_t zpairs = (0x11111111u >> (4 * (7 - (z_hi >> 1)))) & (0x11111111u << (4 * (z_lo >> 1)));
+      lanes_rel = zpairs * ypairs;
       const float dxb = fmaf(static_cast<float>(gx0 - ilx), sp, -r.offx);
       const float dyb = fmaf(static_cast<float>(gy0 - ily), sp, -r.offy);
       // z offsets are formed per lane from the absolute slice index (fmaf(z - lo, sp, -off)),
       // and the safety window spans the whole box in z, so z-slab windows reproduce the
       // full-grid volume bit for bit
       const float fgz = static_cast<float>(gz0 - ilz);
-      // chain-safety window: x 0..7, rows (y_lo & ~1) .. (y_hi | 1), z_lo .. z_hi
+      // chain-safety window: x 0..7, rows (y_lo & ~1) .. (y_hi | 1), the whole box in z
       const float xa = dxb, xb = dxb + 7.f * sp, xc = dxb + 6.f * sp;
       const float ya = dyb + static_cast<float>(y_lo & ~1) * sp, yb = dyb + static_cast<float>(y_hi | 1) * sp;
       const float za = -r.offz, zb = fmaf(static_cast<float>(static_cast<int>(r.hiz) - ilz), sp, -r.offz);
@@ -166,19 +168,19 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
           }
       const float c2e = 2.f * r.Q00 * sp * sp;
       const bool safe = emin > -100.f && dmax < 100.f && c2e > -60.f;
-      // exactly-on-lattice centre inside this brick -> that row takes the direct path
+      // exactly-on-lattice centre inside this brick -> that lane takes the direct path
       uint32_t peak = 0xFFFFFFFFu;
       const float cxf = r.offx / sp, cyf = r.offy / sp, czf = r.offz / sp;
       if (cxf == rintf(cxf) && cyf == rintf(cyf) && czf == rintf(czf)) {
         const int px = ilx + static_cast<int>(cxf) - gx0, py = ily + static_cast<int>(cyf) - gy0,
                   pz = ilz + static_cast<int>(czf) - gz0;
-        if (px >= 0 && px < kBrick && py >= 0 && py < kBrick && pz >= 0 && pz < kBrick)
-          peak = static_cast<uint32_t>(pz * 4 + (py >> 1));  // the lane owning that row
+        if (px >= 0 && px < kBrick && py >= 0 && py < kBrick && pz >= 0 && pz < kBrickZ)
+          peak = static_cast<uint32_t>((pz >> 1) * 4 + (py >> 1));  // the lane owning that row
       }
       s.p = make_float4(dxb, dyb, fgz, r.rho);
       s.q = make_float4(r.Q00, r.Q11, r.Q22, r.Q01);
       s.r = make_float4(r.Q02, r.Q12, ex2_approx(c2e), safe ? 1.f : 0.f);
-      s.m = make_uint4(xm | (ym << 8), lanes_rel, peak, __float_as_uint(r.offz));
+      s.m = make_uint4(xm | (ym << 8) | (zm << 16), lanes_rel, peak, __float_as_uint(r.offz));
       sw[lane] = s;
     }
     __syncwarp();
@@ -193,65 +195,74 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
       const uint32_t xm = m.x & 0xFFu;
       const uint32_t rows = (m.x >> (8 + 2 * yp)) & 3u;
       const f2_t RHO = f2_pack((rows & 1u) ? p.w : 0.f, (rows & 2u) ? p.w : 0.f);
-      const float dy0 = p.y + fy, dz = fmaf(p.z + fzl, sp, -__uint_as_float(m.w)), dx0 = p.x;
+      const float dy0 = p.y + fy, dx0 = p.x;
       const f2_t DY = f2_pack(dy0, dy0 + sp);
-      // e(dx) = Q00 dx^2 + L dx + K,  L = Q01 dy + Q02 dz,  K = Q11 dy^2 + Q12 dy dz + Q22 dz^2
-      const f2_t L = f2_fma(f2_bc(q.w), DY, f2_bc(rr4.x * dz));
-      const f2_t K = f2_fma(DY, f2_fma(f2_bc(q.y), DY, f2_bc(rr4.y * dz)), f2_bc(q.z * dz * dz));
-      f2_t g[8];
-      if (rr4.w != 0.f && m.z != static_cast<uint32_t>(lane)) {
-        const f2_t E0 = f2_fma(L, f2_bc(dx0), f2_add(K, f2_bc(q.x * dx0 * dx0)));
-        const f2_t D0 = f2_fma(L, f2_bc(sp), f2_bc(q.x * fmaf(2.f * dx0, sp, sp * sp)));
-        float e0, e1, d0, d1;
-        f2_unpack(E0, e0, e1);
-        f2_unpack(D0, d0, d1);
-        g[0] = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
-        f2_t ratio = f2_pack(ex2_approx(d0), ex2_approx(d1));
-        const f2_t C2 = f2_bc(rr4.z);
+      const bool direct = rr4.w == 0.f || m.z == static_cast<uint32_t>(lane);
 #pragma unroll
-        for (int k = 1; k < 8; ++k) {
-          g[k] = f2_mul(g[k - 1], ratio);
-          if (k < 7) ratio = f2_mul(ratio, C2);
+      for (int zz = 0; zz < 2; ++zz) {
+        if (!((m.x >> (16 + 2 * zp + zz)) & 1u)) continue;
+        const float dz = fmaf(p.z + static_cast<float>(2 * zp + zz), sp, -__uint_as_float(m.w));
+        // e(dx) = Q00 dx^2 + L dx + K,  L = Q01 dy + Q02 dz,  K = Q11 dy^2 + Q12 dy dz + Q22 dz^2
+        const f2_t L = f2_fma(f2_bc(q.w), DY, f2_bc(rr4.x * dz));
+        const f2_t K = f2_fma(DY, f2_fma(f2_bc(q.y), DY, f2_bc(rr4.y * dz)), f2_bc(q.z * dz * dz));
+        f2_t g[8];
+        if (!direct) {
+          const f2_t E0 = f2_fma(L, f2_bc(dx0), f2_add(K, f2_bc(q.x * dx0 * dx0)));
+          const f2_t D0 = f2_fma(L, f2_bc(sp), f2_bc(q.x * fmaf(2.f * dx0, sp, sp * sp)));
+          float e0, e1, d0, d1;
+          f2_unpack(E0, e0, e1);
+          f2_unpack(D0, d0, d1);
+          g[0] = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
+          f2_t ratio = f2_pack(ex2_approx(d0), ex2_approx(d1));
+          const f2_t C2 = f2_bc(rr4.z);
+#pragma unroll
+          for (int k = 1; k < 8; ++k) {
+            g[k] = f2_mul(g[k - 1], ratio);
+            if (k < 7) ratio = f2_mul(ratio, C2);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float dx = fmaf(static_cast<float>(k), sp, dx0);
+            const f2_t ek = f2_fma(f2_add(f2_bc(q.x * dx), L), f2_bc(dx), K);
+            float e0, e1;
+            f2_unpack(ek, e0, e1);
+            g[k] = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
+          }
         }
-      } else {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const float dx = fmaf(static_cast<float>(k), sp, dx0);
-          const f2_t ek = f2_fma(f2_add(f2_bc(q.x * dx), L), f2_bc(dx), K);
-          float e0, e1;
-          f2_unpack(ek, e0, e1);
-          g[k] = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        float glo, ghi;
-        f2_unpack(g[k], glo, ghi);
-        if (xm & (1u << k)) {
-          acc0[k] += glo;
-          acc1[k] += ghi;
+          float glo, ghi;
+          f2_unpack(g[k], glo, ghi);
+          if (xm & (1u << k)) {
+            acc[zz][0][k] += glo;
+            acc[zz][1][k] += ghi;
+          }
         }
       }
     }
     __syncwarp();
   }
   const int wx = win.hi[0] - win.lo[0], wy = win.hi[1] - win.lo[1];
-  const int z = gz0 + zl;
-  if (z >= win.hi[2]) return;
   const int x0 = gx0 - win.lo[0];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int y = gy0 + 2 * yp + h;
-    if (y >= win.hi[1]) continue;
-    const float* v = h ? acc1 : acc0;
-    float* row = volume + (static_cast<int64_t>(z - win.lo[2]) * wy + (y - win.lo[1])) * wx;
-    if ((wx & 3) == 0 && x0 + 8 <= wx) {
-      reinterpret_cast<float4*>(row + x0)[0] = make_float4(v[0], v[1], v[2], v[3]);
-      reinterpret_cast<float4*>(row + x0)[1] = make_float4(v[4], v[5], v[6], v[7]);
-    } else {
+  for (int zz = 0; zz < 2; ++zz) {
+    const int z = gz0 + 2 * zp + zz;
+    if (z >= win.hi[2]) continue;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (x0 + k < wx) row[x0 + k] = v[k];
+    for (int h = 0; h < 2; ++h) {
+      const int y = gy0 + 2 * yp + h;
+      if (y >= win.hi[1]) continue;
+      const float* v = acc[zz][h];
+      float* row = volume + (static_cast<int64_t>(z - win.lo[2]) * wy + (y - win.lo[1])) * wx;
+      if ((wx & 3) == 0 && x0 + 8 <= wx) {
+        reinterpret_cast<float4*>(row + x0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(row + x0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (x0 + k < wx) row[x0 + k] = v[k];
+      }
     }
   }
 }
