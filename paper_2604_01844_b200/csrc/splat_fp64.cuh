@@ -355,16 +355,27 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
       p.degenerate = true;
       return;
     }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) p.d_ray[k] = rel[k] / p.dist;
     const double f = fr.focal;
-    p.mean2d[0] = f * p.t_cam[0] / (tz * g.s_u) + cu;
-    p.mean2d[1] = f * p.t_cam[1] / (tz * g.s_v) + cv;
     double* J = p.jac;
-    J[0] = f / (g.s_u * tz);
-    J[2] = -f * p.t_cam[0] / (g.s_u * tz * tz);
-    J[4] = f / (g.s_v * tz);
-    J[5] = -f * p.t_cam[1] / (g.s_v * tz * tz);
+    if (kBox) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) p.d_ray[k] = rel[k] / p.dist;
+      p.mean2d[0] = f * p.t_cam[0] / (tz * g.s_u) + cu;
+      p.mean2d[1] = f * p.t_cam[1] / (tz * g.s_v) + cv;
+      J[0] = f / (g.s_u * tz);
+      J[2] = -f * p.t_cam[0] / (g.s_u * tz * tz);
+      J[4] = f / (g.s_v * tz);
+      J[5] = -f * p.t_cam[1] / (g.s_v * tz * tz);
+    } else {  // backward tail: tolerance-level arithmetic, reciprocals instead of divisions
+      const double inv_dist = 1.0 / p.dist;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) p.d_ray[k] = rel[k] * inv_dist;
+      const double fu = f / (g.s_u * tz), fv = f / (g.s_v * tz), itz = 1.0 / tz;
+      J[0] = fu;
+      J[2] = -fu * p.t_cam[0] * itz;
+      J[4] = fv;
+      J[5] = -fv * p.t_cam[1] * itz;
+    }
     const double* rows[3] = {fr.u, fr.v, fr.d};
     double T[6], A[6];
 #pragma unroll
@@ -421,10 +432,18 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) p.cov2d[k] = cr[k];
-  p.conic[0] = cr[3] / dt2;
-  p.conic[1] = -cr[1] / dt2;
-  p.conic[2] = -cr[2] / dt2;
-  p.conic[3] = cr[0] / dt2;
+  if (kBox) {
+    p.conic[0] = cr[3] / dt2;
+    p.conic[1] = -cr[1] / dt2;
+    p.conic[2] = -cr[2] / dt2;
+    p.conic[3] = cr[0] / dt2;
+  } else {
+    const double idt = 1.0 / dt2;
+    p.conic[0] = cr[3] * idt;
+    p.conic[1] = -cr[1] * idt;
+    p.conic[2] = -cr[2] * idt;
+    p.conic[3] = cr[0] * idt;
+  }
   p.amplitude = p.mu * density * p.k;
   if (!kBox) {
     p.culled = false;
@@ -565,12 +584,13 @@ __device__ __forceinline__ void raster_chain_rule(const Frame& fr, const Geo& g,
     double gt[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) gt[k] = J[0 * 3 + k] * gm[0] + J[1 * 3 + k] * gm[1];
-    gt[0] += gJ[0 * 3 + 2] * (-f / (su * tz * tz));
-    gt[1] += gJ[1 * 3 + 2] * (-f / (sv * tz * tz));
-    gt[2] += gJ[0 * 3 + 0] * (-f / (su * tz * tz)) +
-             gJ[0 * 3 + 2] * (2.0 * f * p.t_cam[0] / (su * tz * tz * tz)) +
-             gJ[1 * 3 + 1] * (-f / (sv * tz * tz)) +
-             gJ[1 * 3 + 2] * (2.0 * f * p.t_cam[1] / (sv * tz * tz * tz));
+    // (tail-only code, tolerance-level: reciprocals instead of divisions)
+    const double itz = 1.0 / tz;
+    const double fu2 = -f / (su * tz * tz), fv2 = -f / (sv * tz * tz);
+    gt[0] += gJ[0 * 3 + 2] * fu2;
+    gt[1] += gJ[1 * 3 + 2] * fv2;
+    gt[2] += gJ[0 * 3 + 0] * fu2 + gJ[0 * 3 + 2] * (-2.0 * fu2 * p.t_cam[0] * itz) + gJ[1 * 3 + 1] * fv2 +
+             gJ[1 * 3 + 2] * (-2.0 * fv2 * p.t_cam[1] * itz);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       double acc = rows[0][k] * gt[0];
@@ -582,8 +602,9 @@ __device__ __forceinline__ void raster_chain_rule(const Frame& fr, const Geo& g,
 #pragma unroll
     for (int k = 0; k < 3; ++k) gd[k] = 2.0 * g_beta * p.ad[k];
     const double dd = dot3(p.d_ray, gd);
+    const double inv_dist = 1.0 / p.dist;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) gp[k] += (gd[k] - p.d_ray[k] * dd) / p.dist;
+    for (int k = 0; k < 3; ++k) gp[k] += (gd[k] - p.d_ray[k] * dd) * inv_dist;
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k) g_pos[k] = gp[k];
