@@ -611,7 +611,10 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       // host output: launch in view sub-ranges so each one's images go down while the next
       // computes (the kernel indexes keys/records/images by its own view range)
-      const int sub = images_location == GSCT_HOST ? std::max(1, (cv + 3) / 4) : cv;
+#ifndef GSCT_FWD_SPLIT
+#define GSCT_FWD_SPLIT 2  // host-output forward launched in this many view sub-ranges (A/B: 1 -> +1.74 ms, 2 -> +1.50, 4 -> +2.28)
+#endif
+      const int sub = images_location == GSCT_HOST ? std::max(1, (cv + GSCT_FWD_SPLIT - 1) / GSCT_FWD_SPLIT) : cv;
       for (int vs = 0; vs < cv; vs += sub) {
         const int nvs = std::min(sub, cv - vs);
         {
