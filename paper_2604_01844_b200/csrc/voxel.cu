@@ -267,6 +267,10 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
   }
 }
 
+#ifndef GSCT_VOX_LANES
+#define GSCT_VOX_LANES 4  // lanes per splat in the voxel backward (A/B at 512^3: 1 2.37, 2 2.02, 4 1.93, 8 2.05 ms)
+#endif
+constexpr int kVoxLanes = GSCT_VOX_LANES;
 #ifndef GSCT_VLD_NA
 #define GSCT_VLD_NA 1  // grad-volume row loads bypass L1 allocation (A/B: 2.36 vs 2.54 ms at 512^3)
 #endif
@@ -296,16 +300,20 @@ __global__ void __launch_bounds__(256, 4) k_voxel_bwd_lanes(const VoxelRec* __re
                                                             Window win, float sp, const float* __restrict__ grad,
                                                             float* __restrict__ mom) {
   constexpr int CW = VEC == 8 ? 8 : 4;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const int64_t i = order ? static_cast<int64_t>(__ldg(order + t)) : t;
+  // kVoxLanes lanes per splat (an aligned group): lane q walks the slices z = q, q + kVoxLanes,
+  // ... of the box; the group's ten sums are combined by a fixed xor tree at the end
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t t = tid / kVoxLanes;
+  const int q = static_cast<int>(tid % kVoxLanes);
+  const bool live = t < n;
+  const int64_t i = live ? (order ? static_cast<int64_t>(__ldg(order + t)) : t) : 0;
   const VoxelRec r = rec[i];
   const int x0 = max(static_cast<int>(r.lox), win.lo[0]), y0 = max(static_cast<int>(r.loy), win.lo[1]),
             z0 = max(static_cast<int>(r.loz), win.lo[2]);
   const int W = min(static_cast<int>(r.hix), win.hi[0] - 1) - x0 + 1,
             H = min(static_cast<int>(r.hiy), win.hi[1] - 1) - y0 + 1,
-            D = min(static_cast<int>(r.hiz), win.hi[2] - 1) - z0 + 1;
-  if (W <= 0 || H <= 0 || D <= 0) return;  // moments were zero-filled
+            D = live ? min(static_cast<int>(r.hiz), win.hi[2] - 1) - z0 + 1 : 0;
+  const bool empty = W <= 0 || H <= 0 || D <= 0;  // moments were zero-filled
   const int wx = win.hi[0] - win.lo[0], wy = win.hi[1] - win.lo[1];
   const int xa = VEC > 1 ? x0 - ((x0 - win.lo[0]) & (VEC - 1)) : x0;  // aligned first column
   const int lead = x0 - xa, ncol = lead + W, nch = (ncol + CW - 1) / CW;
@@ -323,7 +331,7 @@ __global__ void __launch_bounds__(256, 4) k_voxel_bwd_lanes(const VoxelRec* __re
   float m[10];
 #pragma unroll
   for (int k = 0; k < 10; ++k) m[k] = 0.f;
-  for (int zz = 0; zz < D; ++zz) {
+  for (int zz = q; zz < (empty ? 0 : D); zz += kVoxLanes) {
     const float dz = fmaf(static_cast<float>(z0 + zz) - r.loz, sp, -r.offz);
     const float* __restrict__ prow = gz + static_cast<int64_t>(zz) * wy * wx;
     for (int yy = 0; yy < H; ++yy, prow += wx) {
@@ -396,7 +404,14 @@ __global__ void __launch_bounds__(256, 4) k_voxel_bwd_lanes(const VoxelRec* __re
     }
   }
 #pragma unroll
-  for (int k = 0; k < 10; ++k) mom[static_cast<int64_t>(k) * n + i] = m[k];
+  for (int k = 0; k < 10; ++k) {
+#pragma unroll
+    for (int o = 1; o < kVoxLanes; o <<= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
+  }
+  if (live && !empty && q == 0) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) mom[static_cast<int64_t>(k) * n + i] = m[k];
+  }
 }
 
 // Walk order for the lane-per-splat backward: 64^3 region of the box corner (L2 locality of
@@ -472,9 +487,11 @@ void launch_voxel_bwd_lanes(const VoxelRec* rec, const uint32_t* order, int64_t 
                             float spacing, const float* grad_volume, float* moments, cudaStream_t st) {
   if (n == 0) return;
   if (voxel_bwd_vec(win, grad_volume) == 8)
-    k_voxel_bwd_lanes<8><<<blocks_for(n, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume, moments);
+    k_voxel_bwd_lanes<8><<<blocks_for(n * kVoxLanes, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume,
+                                                                        moments);
   else
-    k_voxel_bwd_lanes<1><<<blocks_for(n, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume, moments);
+    k_voxel_bwd_lanes<1><<<blocks_for(n * kVoxLanes, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume,
+                                                                        moments);
   count_launch();
 }
 
