@@ -56,27 +56,32 @@ __global__ void __launch_bounds__(128) k_splat_prepare(Cloud c, PreSplat* __rest
 #ifndef GSCT_PRE_MINB
 #define GSCT_PRE_MINB 8
 #endif
+#ifndef GSCT_PRE_VIEWS
+#define GSCT_PRE_VIEWS 8  // views per thread (the splat's set-up loaded once per thread)
+#endif
+constexpr int kPreViews = GSCT_PRE_VIEWS;
 __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const PreSplat* __restrict__ pre, int64_t n,
-                                                           const Frame* __restrict__ frames, Geo g,
+                                                           int n_views, const Frame* __restrict__ frames, Geo g,
                                                            RSet rs, int bin_ts,
                                                            RasterRec* __restrict__ rec,
                                                            uint32_t* __restrict__ tile_count,
                                                            DevStats* __restrict__ st) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y;
   unsigned long long n_culled = 0, n_degen = 0, n_tp = 0, n_pp = 0;
-  if (i < n) {
+  PreSplat s;
+  if (i < n) pre_load(pre, n, i, s);  // once per thread, reused for its kPreViews views
+  for (int vg = 0; vg < kPreViews; ++vg) {
+  const int v = blockIdx.y * kPreViews + vg;
+  if (i < n && v < n_views) {
     RasterRec r = empty_rec();
     uint32_t cnt = 0;
-    PreSplat s;
-    pre_load(pre, n, i, s);
     if (s.status == 0) {
       Proj p;
       project_full(frames[v], g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
       if (p.degenerate) {
-        n_degen = 1;
+        n_degen += 1;
       } else if (p.culled) {
-        n_culled = 1;
+        n_culled += 1;
       } else {
         const int u0 = p.rect[0], u1 = p.rect[1], v0 = p.rect[2], v1 = p.rect[3];
         r.urange = static_cast<uint32_t>(u0) | (static_cast<uint32_t>(u1) << 16);
@@ -90,14 +95,15 @@ __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const 
         // binning count at the kernel's tile size; stats at the requested tile size
         cnt = static_cast<uint32_t>((u1 / bin_ts - u0 / bin_ts + 1) * (v1 / bin_ts - v0 / bin_ts + 1));
         const int ts = rs.tile_size;
-        n_tp = static_cast<unsigned long long>((u1 / ts - u0 / ts + 1)) *
-               static_cast<unsigned long long>((v1 / ts - v0 / ts + 1));
-        n_pp = static_cast<unsigned long long>(u1 - u0 + 1) * static_cast<unsigned long long>(v1 - v0 + 1);
+        n_tp += static_cast<unsigned long long>((u1 / ts - u0 / ts + 1)) *
+                static_cast<unsigned long long>((v1 / ts - v0 / ts + 1));
+        n_pp += static_cast<unsigned long long>(u1 - u0 + 1) * static_cast<unsigned long long>(v1 - v0 + 1);
       }
     }
     const int64_t item = static_cast<int64_t>(v) * n + i;
     rec[item] = r;
     if (tile_count) tile_count[item] = cnt;
+  }
   }
   warp_add(&st->culled, n_culled);
   warp_add(&st->degenerate, n_degen);
@@ -285,8 +291,8 @@ void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frame
                               const RSet& rs, int bin_ts, RasterRec* rec, uint32_t* tile_count,
                               DevStats* stats, cudaStream_t st) {
   if (n == 0 || n_views == 0) return;
-  dim3 grid(blocks_for(n, 128), static_cast<unsigned>(n_views));
-  k_raster_preprocess<<<grid, 128, 0, st>>>(pre, n, frames_dev, g, rs, bin_ts, rec, tile_count, stats);
+  dim3 grid(blocks_for(n, 128), static_cast<unsigned>((n_views + kPreViews - 1) / kPreViews));
+  k_raster_preprocess<<<grid, 128, 0, st>>>(pre, n, n_views, frames_dev, g, rs, bin_ts, rec, tile_count, stats);
   count_launch();
 }
 
