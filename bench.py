@@ -388,7 +388,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     pairs_per_launch = stats.pixel_pairs / launches_per_step
     achieved_gbs = algo_bytes / (avg_ms / 1e3) / 1e9
     pair_rate = pairs_per_launch / (avg_ms / 1e3)
-    kernel = "k_raster_fwd2" if dom == "raster_fwd" else "k_raster_bwd_lanes"
+    kernel = "k_raster_fwd4" if dom == "raster_fwd" else "k_raster_bwd_lanes"
     traffic = None  # dram read+write bytes per launch from the committed ncu --set full capture
     measured = None  # the pipes that do bind (same capture): issue slots, L1/L2 throughput
     try:
