@@ -243,6 +243,48 @@ typedef struct {
 int gsct_adam_step(gsct_ctx ctx, gsct_cloud* params, gsct_adam_state* state, const gsct_grads* grads,
                    const gsct_learning_rates* lrs);
 
+/* Adaptive density control (optim.hpp:185-317) and its accumulators
+ * (accumulate_control_stats, optim.hpp:366-373): the OptimState arrays that track the cloud
+ * size besides the Adam moments. Device arrays. */
+typedef struct {
+  double* grad_norm; /* N: summed |dL/dmean2d| over visible view-steps (accum_grad_norm) */
+  double* grad_dir;  /* 3N: summed dL/dposition (accum_grad_dir) */
+  int64_t* count;    /* N: visible view-steps (accum_count) */
+} gsct_control_accum;
+/* std::mt19937_64 engine state of gsct::Rng (rng.hpp:18-69) in libstdc++'s layout: the 312
+ * state words then the position p -- the numbers Rng::save_state writes, in order. */
+typedef struct {
+  uint64_t x[312];
+  uint64_t p;
+} gsct_rng_state;
+/* TrainConfig's adaptive-control fields (optim.hpp:38-41) + OptimState::scene_extent. */
+typedef struct {
+  double grad_threshold, prune_density, split_scale_fraction, scene_extent;
+  int64_t max_gaussians;
+} gsct_control_config;
+typedef struct {
+  int64_t pruned, cloned, split; /* AdaptiveReport (optim.hpp:188-192) */
+  int64_t n_next;                /* rows written to the output cloud */
+} gsct_adaptive_report;
+/* accumulate_control_stats: for every splat with grads->visible set, grad_norm +=
+ * pos_grad_norm, grad_dir += grads->pos, count += 1. grads device-resident. */
+int gsct_accumulate_control_stats(gsct_ctx ctx, int64_t n, const gsct_grads* grads, gsct_control_accum* acc);
+/* adaptive_control: prune, then clone / split in index order under the max_gaussians cap;
+ * survivors, clones and split children are spliced in index order into out_cloud /
+ * out_state (device arrays of at least `capacity` rows, distinct from the inputs), fresh
+ * rows with zero moments; out_acc (capacity rows) is zeroed for the n_next rows; step and
+ * skipped_updates carry over. The split children draw 12 engine outputs each from rng
+ * (host) in index order; like the reference -- which draws from state.rng and then replaces
+ * the state with a copy taken before the draws (optim.hpp:244, 301, 315) -- the caller's
+ * engine state is left unchanged. The
+ * required capacity is max(n, max_gaussians); a smaller one that the result does not fit
+ * is a contract error. Non-finite parameters / zero quaternions are contract errors, as in
+ * activate (core.hpp:80-97). */
+int gsct_adaptive_control(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_adam_state* state,
+                          const gsct_control_accum* acc, const gsct_rng_state* rng,
+                          const gsct_control_config* cfg, int64_t capacity, gsct_cloud* out_cloud,
+                          gsct_adam_state* out_state, gsct_control_accum* out_acc, gsct_adaptive_report* report);
+
 /* ---- parity hooks (bit-exactness checks against the CPU oracle) ------------------ */
 /* Per splat for one view: rect[4N] (u_min,u_max,v_min,v_max), flags[N] (bit0 culled,
  * bit1 degenerate), mean2d[2N], conic[4N] (row-major), amplitude[N]; host outputs. */
@@ -271,6 +313,8 @@ void gsct_host_rng_destroy(void* rng);
 double gsct_host_rng_uniform(void* rng, double lo, double hi);
 double gsct_host_rng_normal(void* rng);
 int64_t gsct_host_rng_uniform_int(void* rng, int64_t n);
+void gsct_host_rng_get_state(void* rng, gsct_rng_state* out);
+void gsct_host_rng_set_state(void* rng, const gsct_rng_state* in);
 /* sample_subvolume (voxelizer.hpp:76-93): writes offset[3], dims[3]; returns 0 or 1 (error). */
 int gsct_host_sample_subvolume(const int parent_dims[3], const int sub_dims[3], void* rng,
                                int offset[3], int dims[3]);

@@ -335,6 +335,38 @@ class Ref:
         return int(st.value), int(sk.value)
 
 
+    def adaptive_control(self, params: dict, moments: dict, acc: dict, rng_state: np.ndarray, grad_threshold: float,
+                         prune_density: float, split_scale_fraction: float, scene_extent: float,
+                         max_gaussians: int):
+        """adaptive_control (optim.hpp:201-317) of the unchanged reference on flat fp64 arrays.
+        rng_state: uint64[313] = the engine's x[0..311], p (advanced in place). Returns
+        (params, moments, report {pruned, cloned, split, n_next}) of the output cloud."""
+        n = len(params["raw"])
+        cap = max(n, int(max_gaussians))
+        f = self.l.ref_adaptive_control
+        f.argtypes = [C.c_int64] + [C.c_void_p] * 4 + [C.c_void_p] * 4 + [C.c_void_p] * 2 + [C.c_int64, C.c_int64] + \
+                     [C.c_void_p] * 4 + [C.c_void_p, C.c_void_p]
+        keys = ("m_pos", "v_pos", "m_ls", "v_ls", "m_rot", "v_rot", "m_dens", "v_dens")
+        width = {"m_pos": 3, "v_pos": 3, "m_ls": 3, "v_ls": 3, "m_rot": 4, "v_rot": 4, "m_dens": 1, "v_dens": 1}
+        mv_in = [np.ascontiguousarray(moments[k], dtype=np.float64) for k in keys]
+        mv = (C.c_void_p * 8)(*[a.ctypes.data for a in mv_in])
+        out_m = {k: np.zeros((cap, width[k]) if width[k] > 1 else (cap,)) for k in keys}
+        omv = (C.c_void_p * 8)(*[out_m[k].ctypes.data for k in keys])
+        out_p = {"pos": np.zeros((cap, 3)), "ls": np.zeros((cap, 3)), "q": np.zeros((cap, 4)), "raw": np.zeros(cap)}
+        cfg = np.array([grad_threshold, prune_density, split_scale_fraction, scene_extent], dtype=np.float64)
+        rep = np.zeros(4, dtype=np.int64)
+        assert rng_state.dtype == np.uint64 and rng_state.shape == (313,)
+        ins = {k: np.ascontiguousarray(params[k], dtype=np.float64) for k in ("pos", "ls", "q", "raw")}
+        an = np.ascontiguousarray(acc["grad_norm"], dtype=np.float64)
+        ad = np.ascontiguousarray(acc["grad_dir"], dtype=np.float64)
+        ac = np.ascontiguousarray(acc["count"], dtype=np.int64)
+        self._chk(f(n, _p(ins["pos"]), _p(ins["ls"]), _p(ins["q"]), _p(ins["raw"]), mv, _p(an), _p(ad), ac.ctypes.data,
+                    rng_state.ctypes.data, _p(cfg), int(max_gaussians), cap, _p(out_p["pos"]), _p(out_p["ls"]),
+                    _p(out_p["q"]), _p(out_p["raw"]), omv, rep.ctypes.data))
+        m = int(rep[3])
+        return ({k: v[:m] for k, v in out_p.items()}, {k: v[:m] for k, v in out_m.items()},
+                {"pruned": int(rep[0]), "cloned": int(rep[1]), "split": int(rep[2]), "n_next": m})
+
     def total_loss_fit(self, rendered: np.ndarray, target: np.ndarray, alpha_ssim: float, streaming: bool = True):
         """(l1, ssim, total), grad for a [nz, ny, nx] volume (losses.hpp:648-664)."""
         r = np.ascontiguousarray(rendered, dtype=np.float64)

@@ -4,6 +4,7 @@
 // ctypes. Built by oracle/Makefile into oracle/_ref/libgsct_ref.so (git-ignored, travels
 // to the GPU box prebuilt). Array layouts match oracle/gsct_oracle.h.
 #include <cstdint>
+#include <sstream>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -423,6 +424,82 @@ int ref_raymarch_project(const double* volume, const int* dims, double spacing, 
     const std::size_t npx = static_cast<std::size_t>(g->n_u) * g->n_v;
     for (int k = 0; k < n_angles; ++k)
       std::memcpy(images + k * npx, P.images[static_cast<std::size_t>(k)].values.data(), npx * sizeof(double));
+  });
+}
+
+// adaptive_control (optim.hpp:201-317) of the unchanged reference on flat arrays. In:
+// n rows of params / moments / accumulators, rng = {x[312], p} (Rng::restore_state text),
+// cfg = {grad_threshold, prune_density, split_scale_fraction, scene_extent}, max_gaussians.
+// Out (capacity rows): params / moments, the report {pruned, cloned, split, n_next} and the
+// engine state after the call (in place; the reference leaves it unchanged, see the caller).
+int ref_adaptive_control(int64_t n, const double* pos, const double* ls, const double* q, const double* raw,
+                         const double* const* mv, const double* acc_norm, const double* acc_dir,
+                         const int64_t* acc_count, uint64_t* rng, const double* cfg, int64_t max_gaussians,
+                         int64_t capacity, double* opos, double* ols, double* oq, double* oraw, double* const* omv,
+                         int64_t* report) {
+  GUARD({
+    GaussianCloud c;
+    for (int64_t i = 0; i < n; ++i)
+      c.push_back(Vec3(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]), Vec3(ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]),
+                  Vec4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]), raw[i]);
+    OptimState st;
+    st.init(static_cast<std::size_t>(n), 0);
+    for (int64_t i = 0; i < n; ++i) {
+      for (int a = 0; a < 3; ++a) {
+        st.m_pos[i][a] = mv[0][3 * i + a];
+        st.v_pos[i][a] = mv[1][3 * i + a];
+        st.m_ls[i][a] = mv[2][3 * i + a];
+        st.v_ls[i][a] = mv[3][3 * i + a];
+        st.accum_grad_dir[i][a] = acc_dir[3 * i + a];
+      }
+      for (int a = 0; a < 4; ++a) {
+        st.m_rot[i][a] = mv[4][4 * i + a];
+        st.v_rot[i][a] = mv[5][4 * i + a];
+      }
+      st.m_dens[i] = mv[6][i];
+      st.v_dens[i] = mv[7][i];
+      st.accum_grad_norm[i] = acc_norm[i];
+      st.accum_count[i] = acc_count[i];
+    }
+    {
+      std::ostringstream os;
+      for (int k = 0; k < 312; ++k) os << rng[k] << ' ';
+      os << rng[312];
+      st.rng.restore_state(os.str());
+    }
+    st.scene_extent = cfg[3];
+    TrainConfig tc;
+    tc.grad_threshold = cfg[0];
+    tc.prune_density = cfg[1];
+    tc.split_scale_fraction = cfg[2];
+    tc.max_gaussians = static_cast<std::size_t>(max_gaussians);
+    const AdaptiveReport r = adaptive_control(c, st, tc);
+    const int64_t m = static_cast<int64_t>(c.size());
+    report[0] = static_cast<int64_t>(r.pruned);
+    report[1] = static_cast<int64_t>(r.cloned);
+    report[2] = static_cast<int64_t>(r.split);
+    report[3] = m;
+    if (m > capacity) return 2;
+    for (int64_t i = 0; i < m; ++i) {
+      for (int a = 0; a < 3; ++a) {
+        opos[3 * i + a] = c.positions[i][a];
+        ols[3 * i + a] = c.log_scales[i][a];
+        omv[0][3 * i + a] = st.m_pos[i][a];
+        omv[1][3 * i + a] = st.v_pos[i][a];
+        omv[2][3 * i + a] = st.m_ls[i][a];
+        omv[3][3 * i + a] = st.v_ls[i][a];
+      }
+      for (int a = 0; a < 4; ++a) {
+        oq[4 * i + a] = c.rotations[i][a];
+        omv[4][4 * i + a] = st.m_rot[i][a];
+        omv[5][4 * i + a] = st.v_rot[i][a];
+      }
+      oraw[i] = c.raw_densities[i];
+      omv[6][i] = st.m_dens[i];
+      omv[7][i] = st.v_dens[i];
+    }
+    std::istringstream in(st.rng.save_state());
+    for (int k = 0; k < 313; ++k) in >> rng[k];
   });
 }
 }  // extern "C"

@@ -24,7 +24,7 @@ namespace {
 enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
-  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR,
+  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG,
   S_COUNT_SLOTS
 };
 
@@ -53,7 +53,7 @@ struct gsct_ctx_s {
   Buf bufs[S_COUNT_SLOTS];
   DevStats* dstats = nullptr;   // device
   DevStats* hstats = nullptr;   // pinned host mirror
-  uint32_t* hscratch = nullptr; // pinned 2 x u32 for scan totals
+  uint32_t* hscratch = nullptr; // pinned 128 B: scan totals / small result words
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   gsct_stats pending{};          // async-mode stats accumulated at synchronize
   // per-phase event timing (gsct_ctx_set_profiling)
@@ -404,7 +404,7 @@ int gsct_ctx_create(int device, gsct_ctx* out) {
   if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&c->dstats, sizeof(DevStats)) != cudaSuccess ||
       cudaMallocHost(&c->hstats, sizeof(DevStats)) != cudaSuccess ||
-      cudaMallocHost(&c->hscratch, 4 * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMallocHost(&c->hscratch, 16 * sizeof(uint64_t)) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();
@@ -1251,6 +1251,85 @@ int gsct_adam_step(gsct_ctx c, gsct_cloud* params, gsct_adam_state* state, const
     CK(cudaStreamSynchronize(c->stream));
     std::memcpy(&h, c->hscratch, sizeof h);
     state->skipped_updates += static_cast<int64_t>(h);
+  });
+}
+
+int gsct_accumulate_control_stats(gsct_ctx c, int64_t n, const gsct_grads* grads, gsct_control_accum* acc) {
+  return run(c, [&] {
+    contract(grads && acc && n >= 0, "accumulate_control_stats: null argument");
+    contract(grads->location == GSCT_DEVICE, "accumulate_control_stats: gradients must be device-resident");
+    if (n == 0) return;
+    contract(grads->visible && grads->pos_grad_norm && grads->pos && acc->grad_norm && acc->grad_dir && acc->count,
+             "OptimState: arrays out of lockstep with the cloud");
+    launch_ctrl_accumulate(n, grads->visible, grads->pos_grad_norm, grads->pos, acc->grad_norm, acc->grad_dir,
+                           acc->count, c->stream);
+    CK(cudaGetLastError());
+    if (!c->async) CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int gsct_adaptive_control(gsct_ctx c, const gsct_cloud* cloud, const gsct_adam_state* state,
+                          const gsct_control_accum* acc, const gsct_rng_state* rng,
+                          const gsct_control_config* cfg, int64_t capacity, gsct_cloud* out_cloud,
+                          gsct_adam_state* out_state, gsct_control_accum* out_acc, gsct_adaptive_report* report) {
+  return run(c, [&] {
+    contract(cloud && state && acc && rng && cfg && out_cloud && out_state && out_acc && report,
+             "adaptive_control: null argument");
+    contract(cloud->location == GSCT_DEVICE && out_cloud->location == GSCT_DEVICE,
+             "adaptive_control: clouds must be device-resident");
+    contract(rng->p <= 312, "Rng::restore_state: malformed engine state");
+    const Cloud d = upload_cloud(c, cloud);
+    const int64_t n = d.n;
+    *report = gsct_adaptive_report{0, 0, 0, 0};
+    if (n == 0) return;
+    const size_t un = static_cast<size_t>(n);
+    void* scratch = ws<char>(c, S_CTRL, ctrl_scratch_bytes(n) + 512);
+    unsigned long long* small = reinterpret_cast<unsigned long long*>(c->hscratch);
+    CK(launch_ctrl_classify(d, cfg->prune_density, cfg->grad_threshold,
+                            cfg->split_scale_fraction * cfg->scene_extent, cfg->max_gaussians, acc->grad_norm,
+                            acc->count, scratch, small, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const unsigned long long err = small[1];
+    if (err != ~0ull) {
+      const int64_t i = static_cast<int64_t>(err >> 2);
+      contract(false, (err & 3) == 2 ? "activate: zero quaternion in splat " + std::to_string(i)
+                                     : "activate: non-finite parameter in splat " + std::to_string(i));
+    }
+    const int64_t survivors = static_cast<int64_t>(small[2]);
+    report->pruned = n - survivors;
+    report->cloned = static_cast<int64_t>(small[3]);
+    report->split = static_cast<int64_t>(small[4]);
+    report->n_next = survivors + report->cloned + report->split;
+    contract(report->n_next <= capacity, "adaptive_control: output capacity " + std::to_string(capacity) +
+                                             " < " + std::to_string(report->n_next) + " rows");
+    // the split children's engine draws, 12 per split, from a copy of the caller's state:
+    // the reference draws from state.rng and then replaces the state with next_state, whose
+    // rng was copied before the draws (optim.hpp:244, 301, 315), so the engine is unchanged
+    const int64_t n_draws = 12 * report->split;
+    unsigned long long* rs = ws<unsigned long long>(c, S_CTRL_RNG, 313 + static_cast<size_t>(n_draws));
+    static_assert(sizeof(gsct_rng_state) == 313 * sizeof(uint64_t), "gsct_rng_state layout");
+    if (n_draws > 0) {
+      CK(cudaMemcpyAsync(rs, rng, sizeof(gsct_rng_state), cudaMemcpyHostToDevice, c->stream));
+      launch_mt_generate(rs, rs + 313, n_draws, c->stream);
+      CK(cudaGetLastError());
+    }
+    const double* mv_in[8] = {state->m_pos, state->v_pos, state->m_ls, state->v_ls,
+                              state->m_rot, state->v_rot, state->m_dens, state->v_dens};
+    double* const mv_out[8] = {out_state->m_pos, out_state->v_pos, out_state->m_ls, out_state->v_ls,
+                               out_state->m_rot, out_state->v_rot, out_state->m_dens, out_state->v_dens};
+    launch_ctrl_write(d, mv_in, acc->grad_dir, scratch, rs + 313, std::log(1.6), const_cast<double*>(out_cloud->pos),
+                      const_cast<double*>(out_cloud->log_scale), const_cast<double*>(out_cloud->quat),
+                      const_cast<double*>(out_cloud->raw_density), mv_out, c->stream);
+    CK(cudaGetLastError());
+    const size_t nn = static_cast<size_t>(report->n_next);
+    CK(cudaMemsetAsync(out_acc->grad_norm, 0, nn * sizeof(double), c->stream));
+    CK(cudaMemsetAsync(out_acc->grad_dir, 0, 3 * nn * sizeof(double), c->stream));
+    CK(cudaMemsetAsync(out_acc->count, 0, nn * sizeof(int64_t), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    out_cloud->n = report->n_next;
+    out_state->step = state->step;
+    out_state->skipped_updates = state->skipped_updates;
+    (void)un;
   });
 }
 

@@ -138,6 +138,21 @@ void launch_adam_step(int64_t n, double* pos, double* ls, double* q, double* raw
                       const double* g_pos, const double* g_ls, const double* g_q, const double* g_raw,
                       const double* lrs, double bias1, double bias2, unsigned long long* skipped, cudaStream_t st);
 
+// (control.cu) adaptive control: accumulate_control_stats; classify (activate, max density,
+// prune / eligible flags, budget, clone / split, output rows -- small_host (pinned) receives
+// {max density bits, first activation error key, survivors, cloned, split}); the mt19937_64
+// draws (state_dev = {x[312], p}); the spliced output rows. mv = the 8 Adam moment arrays.
+void launch_ctrl_accumulate(int64_t n, const uint8_t* visible, const double* pgn, const double* g_pos,
+                            double* acc_norm, double* acc_dir, int64_t* acc_count, cudaStream_t st);
+size_t ctrl_scratch_bytes(int64_t n);
+cudaError_t launch_ctrl_classify(const Cloud& c, double prune_density, double grad_threshold, double split_below,
+                                 int64_t max_gaussians, const double* acc_norm, const int64_t* acc_count,
+                                 void* scratch, unsigned long long* small_host, cudaStream_t st);
+void launch_mt_generate(unsigned long long* state_dev, unsigned long long* out, int64_t count, cudaStream_t st);
+void launch_ctrl_write(const Cloud& c, const double* const* mv_in, const double* acc_dir, void* scratch,
+                       const unsigned long long* draws, double log_1p6, double* pos, double* ls, double* q,
+                       double* raw, double* const* mv_out, cudaStream_t st);
+
 // Launch accounting (gsct_ctx_launch_count).
 extern thread_local int64_t* g_launch_counter;
 inline void count_launch(int k = 1) {

@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <random>
+#include <sstream>
+#include <string>
 
 #include "../../include/gsct_cuda.h"
 
@@ -30,6 +32,15 @@ class Rng {
     const double u1 = 1.0 - uniform();
     const double u2 = uniform();
     return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+  }
+  std::string save_state() const {
+    std::ostringstream out;
+    out << engine_;
+    return out.str();
+  }
+  void restore_state(const std::string& s) {
+    std::istringstream in(s);
+    in >> engine_;
   }
 
  private:
@@ -116,6 +127,18 @@ double gsct_host_rng_normal(void* r) { return static_cast<Rng*>(r)->normal(); }
 int64_t gsct_host_rng_uniform_int(void* r, int64_t n) {
   if (n <= 0) return -1;
   return static_cast<Rng*>(r)->uniform_int(n);
+}
+// The engine's text form (Rng::save_state / restore_state): x[0..311] then p, libstdc++.
+void gsct_host_rng_get_state(void* r, gsct_rng_state* out) {
+  std::istringstream in(static_cast<Rng*>(r)->save_state());
+  for (auto& w : out->x) in >> w;
+  in >> out->p;
+}
+void gsct_host_rng_set_state(void* r, const gsct_rng_state* st) {
+  std::ostringstream os;
+  for (auto w : st->x) os << w << ' ';
+  os << st->p;
+  static_cast<Rng*>(r)->restore_state(os.str());
 }
 
 // voxelizer.hpp:76-93

@@ -97,6 +97,23 @@ class c_adam_state(C.Structure):
                [("step", C.c_int64), ("skipped_updates", C.c_int64)]
 
 
+class c_control_accum(C.Structure):
+    _fields_ = [("grad_norm", C.c_void_p), ("grad_dir", C.c_void_p), ("count", C.c_void_p)]
+
+
+class c_rng_state(C.Structure):
+    _fields_ = [("x", C.c_uint64 * 312), ("p", C.c_uint64)]
+
+
+class c_control_config(C.Structure):
+    _fields_ = [("grad_threshold", C.c_double), ("prune_density", C.c_double),
+                ("split_scale_fraction", C.c_double), ("scene_extent", C.c_double), ("max_gaussians", C.c_int64)]
+
+
+class c_adaptive_report(C.Structure):
+    _fields_ = [("pruned", C.c_int64), ("cloned", C.c_int64), ("split", C.c_int64), ("n_next", C.c_int64)]
+
+
 class c_grads(C.Structure):
     _fields_ = [("pos", C.c_void_p), ("log_scale", C.c_void_p), ("quat", C.c_void_p),
                 ("raw_density", C.c_void_p), ("pos_grad_norm", C.c_void_p), ("visible", C.c_void_p),
@@ -146,6 +163,10 @@ _SIGS = {
     "gsct_raymarch_project": (C.c_int, [C.c_void_p, C.c_void_p, _P(c_grid), C.c_int, _P(c_geometry), _P(C.c_double),
                                         C.c_int, C.c_void_p, C.c_int]),
     "gsct_adam_step": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_adam_state), _P(c_grads), _P(c_learning_rates)]),
+    "gsct_accumulate_control_stats": (C.c_int, [C.c_void_p, C.c_int64, _P(c_grads), _P(c_control_accum)]),
+    "gsct_adaptive_control": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_adam_state), _P(c_control_accum),
+                                        _P(c_rng_state), _P(c_control_config), C.c_int64, _P(c_cloud),
+                                        _P(c_adam_state), _P(c_control_accum), _P(c_adaptive_report)]),
     "gsct_host_view_frame": (None, [_P(c_geometry), C.c_double, _P(C.c_double)]),
     "gsct_host_default_geometry": (None, [_P(C.c_int), C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                           _P(c_geometry), _P(C.c_double)]),
@@ -154,6 +175,8 @@ _SIGS = {
     "gsct_host_rng_uniform": (C.c_double, [C.c_void_p, C.c_double, C.c_double]),
     "gsct_host_rng_normal": (C.c_double, [C.c_void_p]),
     "gsct_host_rng_uniform_int": (C.c_int64, [C.c_void_p, C.c_int64]),
+    "gsct_host_rng_get_state": (None, [C.c_void_p, _P(c_rng_state)]),
+    "gsct_host_rng_set_state": (None, [C.c_void_p, _P(c_rng_state)]),
     "gsct_host_sample_subvolume": (C.c_int, [_P(C.c_int), _P(C.c_int), C.c_void_p, _P(C.c_int), _P(C.c_int)]),
     "gsct_host_make_cloud": (C.c_int, [C.c_int, C.c_int64, C.c_uint64, _P(C.c_double), C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p]),
@@ -830,6 +853,15 @@ class Rng:
     def uniform_array(self, n: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
         return np.array([self.uniform(lo, hi) for _ in range(n)])
 
+    def state(self) -> c_rng_state:
+        """The engine state (Rng::save_state's numbers: x[0..311], p)."""
+        st = c_rng_state()
+        self._lib.gsct_host_rng_get_state(self._h, C.byref(st))
+        return st
+
+    def set_state(self, st: c_rng_state) -> None:
+        self._lib.gsct_host_rng_set_state(self._h, C.byref(st))
+
 
 def sample_subvolume(parent: GridSpec, sub_dims, rng: Rng) -> GridRegion:
     """gsct::sample_subvolume (voxelizer.hpp:76-93)."""
@@ -1015,3 +1047,108 @@ def adam_step(cloud: GaussianCloud, state: AdamState, grads: ParamGradients, lrs
     ctx.check(ctx._lib.gsct_adam_step(ctx.handle, C.byref(cc), C.byref(st), C.byref(gg), C.byref(lr)))
     state.step = int(st.step)
     state.skipped_updates = int(st.skipped_updates)
+
+
+# ---------------------------------------------------------------------------------------
+# Adaptive density control
+# ---------------------------------------------------------------------------------------
+@dataclass
+class ControlConfig:
+    """TrainConfig's adaptive-control fields (optim.hpp:38-41)."""
+    grad_threshold: float = 5e-5
+    prune_density: float = 5e-4
+    split_scale_fraction: float = 0.01
+    max_gaussians: int = 100000
+
+
+@dataclass
+class AdaptiveReport:
+    """optim.hpp:188-192"""
+    pruned: int = 0
+    cloned: int = 0
+    split: int = 0
+
+
+class OptimState(AdamState):
+    """OptimState (optim.hpp:84-125) on device: the Adam moments plus the densification
+    accumulators, all tracking the cloud size through adaptive control; the host Rng,
+    scene extent and normalisation factor."""
+
+    def __init__(self, n: int, seed: int = 0, device: int = 0):
+        import torch
+        super().__init__(n, device)
+        self.accum_grad_norm = torch.zeros(n, dtype=torch.float64, device=f"cuda:{device}")
+        self.accum_grad_dir = torch.zeros((n, 3), dtype=torch.float64, device=f"cuda:{device}")
+        self.accum_count = torch.zeros(n, dtype=torch.int64, device=f"cuda:{device}")
+        self.rng = Rng(seed)
+        self.scene_extent = 1.0
+        self.norm_factor = 1.0
+
+    def check_lockstep(self, n: int) -> None:
+        arrs = (self.m_pos, self.v_pos, self.m_ls, self.v_ls, self.m_rot, self.v_rot, self.m_dens, self.v_dens,
+                self.accum_grad_norm, self.accum_grad_dir, self.accum_count)
+        if any(a.shape[0] != n for a in arrs):
+            raise ContractError("OptimState: arrays out of lockstep with the cloud")
+
+    def _acc(self) -> c_control_accum:
+        return c_control_accum(self.accum_grad_norm.data_ptr(), self.accum_grad_dir.data_ptr(),
+                               self.accum_count.data_ptr())
+
+
+def accumulate_control_stats(state: OptimState, grads: ParamGradients, ctx: Optional[Context] = None) -> None:
+    """detail::accumulate_control_stats (optim.hpp:366-373) on device."""
+    if not _is_torch(grads.positions):
+        raise ContractError("accumulate_control_stats: gradients must be device-resident")
+    n = int(grads.positions.shape[0])
+    state.check_lockstep(n)
+    ctx = ctx or context(grads.positions.device.index or 0)
+    gg = grads._c()
+    acc = state._acc()
+    ctx.check(ctx._lib.gsct_accumulate_control_stats(ctx.handle, n, C.byref(gg), C.byref(acc)))
+
+
+def adaptive_control(cloud: GaussianCloud, state: OptimState, config: ControlConfig = ControlConfig(),
+                     ctx: Optional[Context] = None) -> AdaptiveReport:
+    """adaptive_control (optim.hpp:201-317) on a device-resident cloud: prunes, clones and
+    splits in place of `cloud` / `state` (their arrays are replaced) and returns the report.
+    The split children draw from state.rng, whose engine state is left unchanged -- as in the
+    reference, where the state is replaced by a copy taken before the draws (optim.hpp:244,
+    301, 315)."""
+    import torch
+    if not cloud.on_device:
+        raise ContractError("adaptive_control: clouds must be device-resident")
+    n = cloud.size()
+    state.check_lockstep(n)
+    ctx = _ctx_for(cloud, ctx)
+    dev = cloud.positions.device
+    cap = max(n, int(config.max_gaussians))
+    f64 = lambda *s: torch.empty(s, dtype=torch.float64, device=dev)
+    out = GaussianCloud(f64(cap, 3), f64(cap, 3), f64(cap, 4), f64(cap))
+    nxt = OptimState.__new__(OptimState)
+    nxt.m_pos, nxt.v_pos, nxt.m_ls, nxt.v_ls = f64(cap, 3), f64(cap, 3), f64(cap, 3), f64(cap, 3)
+    nxt.m_rot, nxt.v_rot, nxt.m_dens, nxt.v_dens = f64(cap, 4), f64(cap, 4), f64(cap), f64(cap)
+    nxt.accum_grad_norm, nxt.accum_grad_dir = f64(cap), f64(cap, 3)
+    nxt.accum_count = torch.empty(cap, dtype=torch.int64, device=dev)
+    keep: list = []
+    ci = cloud._c(keep)
+    co = c_cloud(cap, out.positions.data_ptr(), out.log_scales.data_ptr(), out.rotations.data_ptr(),
+                 out.raw_densities.data_ptr(), GSCT_DEVICE)
+    si = state._c()
+    nxt.step, nxt.skipped_updates = state.step, state.skipped_updates
+    so = c_adam_state(*[a.data_ptr() for a in (nxt.m_pos, nxt.v_pos, nxt.m_ls, nxt.v_ls, nxt.m_rot, nxt.v_rot,
+                                               nxt.m_dens, nxt.v_dens)], nxt.step, nxt.skipped_updates)
+    rs = state.rng.state()
+    cfg = c_control_config(config.grad_threshold, config.prune_density, config.split_scale_fraction,
+                           state.scene_extent, int(config.max_gaussians))
+    rep = c_adaptive_report()
+    acc_in, acc_out = state._acc(), nxt._acc()
+    ctx.check(ctx._lib.gsct_adaptive_control(ctx.handle, C.byref(ci), C.byref(si), C.byref(acc_in), C.byref(rs),
+                                             C.byref(cfg), cap, C.byref(co), C.byref(so), C.byref(acc_out),
+                                             C.byref(rep)))
+    m = int(rep.n_next)
+    cloud.positions, cloud.log_scales = out.positions[:m], out.log_scales[:m]
+    cloud.rotations, cloud.raw_densities = out.rotations[:m], out.raw_densities[:m]
+    for k in ("m_pos", "v_pos", "m_ls", "v_ls", "m_rot", "v_rot", "m_dens", "v_dens", "accum_grad_norm",
+              "accum_grad_dir", "accum_count"):
+        setattr(state, k, getattr(nxt, k)[:m])
+    return AdaptiveReport(int(rep.pruned), int(rep.cloned), int(rep.split))

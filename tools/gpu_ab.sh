@@ -1,1 +1,1 @@
-timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+timeout 600 python -m pytest tests/test_control.py -q -x 2>&1 | tail -15
