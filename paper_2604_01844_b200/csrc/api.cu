@@ -304,10 +304,15 @@ int bits_for(uint64_t n_keys) {
 
 // Exclusive scan of counts + pair emission + stable radix sort by key + key ranges.
 // Returns the number of pairs; sorted values end up in *vals_out, start/end per key.
+// sort_bits > 0: the emitted pairs are already ordered by the key bits above sort_bits
+// (view-major emission, key = view << sort_bits | tile), so a stable sort on the low
+// sort_bits alone leaves every (view, tile) run contiguous -- ordered (tile, view, splat)
+// rather than (view, tile, splat), with the splats of a run still ascending -- in one
+// radix pass instead of two or three; ranges are then marked at run boundaries.
 template <class Emit>
 int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32_t n_keys,
                      Emit&& emit, uint32_t** keys_out, uint32_t** vals_out, uint32_t** start,
-                     uint32_t** end) {
+                     uint32_t** end, int sort_bits = 0) {
   uint32_t* offsets = ws<uint32_t>(c, S_OFFSET, static_cast<size_t>(n_items));
   size_t tmp_bytes = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
@@ -328,14 +333,20 @@ int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32
   uint32_t* v2 = ws<uint32_t>(c, S_VALS2, total);
   emit(offsets, k1, v1);
   cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
-  const int end_bit = bits_for(n_keys);
+  const int end_bit = sort_bits > 0 ? sort_bits : bits_for(n_keys);
   tmp_bytes = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(total), 0, end_bit, c->stream));
   tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
   CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(total), 0, end_bit, c->stream));
   *keys_out = kb.Current();
   *vals_out = vb.Current();
-  launch_ranges(*keys_out, total, n_keys, *start, *end, c->stream);
+  if (sort_bits > 0) {
+    CK(cudaMemsetAsync(*start, 0, n_keys * sizeof(uint32_t), c->stream));
+    CK(cudaMemsetAsync(*end, 0, n_keys * sizeof(uint32_t), c->stream));
+    launch_mark_ranges(*keys_out, total, n_keys, *start, *end, c->stream);
+  } else {
+    launch_ranges(*keys_out, total, n_keys, *start, *end, c->stream);
+  }
   return total;
 }
 
@@ -599,15 +610,24 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       CK(cudaGetLastError());
       uint32_t *keys, *vals, *start, *end;
-      const uint32_t n_keys = static_cast<uint32_t>(cv) * static_cast<uint32_t>(n_tiles);
+#ifndef GSCT_BIN_ONEPASS
+#define GSCT_BIN_ONEPASS 1
+#endif
+      // key = view * stride + super-tile; stride a power of two for the one-pass sort, used
+      // when the tile bits fit one 8-bit radix pass (A/B: C2 bin 0.94 -> 0.74 ms; at C5,
+      // 12 tile bits, the two-pass tile-only sort was 1.1 ms slower than the full key)
+      const int tile_bits = bits_for(static_cast<uint32_t>(n_tiles));
+      const bool onepass = GSCT_BIN_ONEPASS && tile_bits <= 8;
+      const int stride = onepass ? (1 << tile_bits) : n_tiles;
+      const uint32_t n_keys = static_cast<uint32_t>(cv) * static_cast<uint32_t>(stride);
       {
         Phase ph(c, GSCT_PH_RASTER_BIN);
         bin_and_sort(
             c, cnt, n * cv, n_keys,
             [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
-              launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kBinTile, tiles_u, n_tiles, k, v, c->stream);
+              launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kBinTile, tiles_u, stride, k, v, c->stream);
             },
-            &keys, &vals, &start, &end);
+            &keys, &vals, &start, &end, onepass ? tile_bits : 0);
       }
       // host output: launch in view sub-ranges so each one's images go down while the next
       // computes (the kernel indexes keys/records/images by its own view range)
@@ -619,9 +639,9 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         const int nvs = std::min(sub, cv - vs);
         {
           Phase ph(c, GSCT_PH_RASTER_FWD);
-          launch_raster_fwd_super(rec + static_cast<int64_t>(vs) * n, vals, start + static_cast<int64_t>(vs) * n_tiles,
-                                  end + static_cast<int64_t>(vs) * n_tiles, n, nvs, geom->n_u, geom->n_v, tiles_u,
-                                  tiles_v, img + static_cast<int64_t>(vs) * npx, c->stream);
+          launch_raster_fwd_super(rec + static_cast<int64_t>(vs) * n, vals, start + static_cast<int64_t>(vs) * stride,
+                                  end + static_cast<int64_t>(vs) * stride, n, nvs, geom->n_u, geom->n_v, tiles_u,
+                                  tiles_v, stride, img + static_cast<int64_t>(vs) * npx, c->stream);
         }
         CK(cudaGetLastError());
         if (images_location == GSCT_HOST) {

@@ -89,10 +89,13 @@ void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets,
                             int n_tiles, uint32_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start,
                    uint32_t* end, cudaStream_t st);
+// equal keys contiguous, sequence not monotone; start / end must be zeroed first
+void launch_mark_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start,
+                        uint32_t* end, cudaStream_t st);
 // forward over 32x32 super-tile lists (keys = view * n_stiles + super-tile)
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
-                             int stiles_v, float* images, cudaStream_t st);
+                             int stiles_v, int key_stride, float* images, cudaStream_t st);
 // lane-per-item backward: shape sort keys, then the pixel walk in `order`
 int bwd_vec(int n_u, const float* grad_images);  // 8, 4 or 1 floats per row load
 // returns the number of key bits to sort on

@@ -107,6 +107,18 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, ui
   end[k] = lower_bound_u32(keys, n_pairs, k + 1);
 }
 
+// [start, end) of every key when equal keys are contiguous but the key sequence is not
+// monotone (the one-pass binning below): one thread per pair marks the run boundaries;
+// start / end of absent keys stay 0 (zeroed by the caller).
+__global__ void k_mark_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, uint32_t* __restrict__ start,
+                              uint32_t* __restrict__ end) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_pairs) return;
+  const uint32_t k = keys[i];
+  if (i == 0 || keys[i - 1] != k) start[k] = i;
+  if (i + 1 == n_pairs || keys[i + 1] != k) end[k] = i + 1;
+}
+
 // Forward (K3): one warp per 32x16 half of a 32x32 super-tile and view; lane l owns the
 // 2 x 8 pixel block at rows 2(l>>2), +1 and columns 8(l&3) .. +7, the two rows held in the
 // halves of packed f32x2 registers. Records of the super-tile list (ascending splat index =
@@ -154,7 +166,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict
                                                      const uint32_t* __restrict__ vals,
                                                      const uint32_t* __restrict__ start,
                                                      const uint32_t* __restrict__ end, int64_t n, int n_u,
-                                                     int n_v, int stiles_u, int n_stiles,
+                                                     int n_v, int stiles_u, int n_stiles, int key_stride,
                                                      float* __restrict__ images) {
   constexpr int kHW = 2 * kTile, kHH = kTile;  // half-tile: 32 wide, 16 tall
   __shared__ StagedRec2 s_rec[4][32];
@@ -167,7 +179,7 @@ __global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict
   if (ty0 >= n_v) return;
   const int lr = 2 * (lane >> 2), lc = 8 * (lane & 3);
   const float flr = static_cast<float>(lr), flc = static_cast<float>(lc);
-  const uint32_t key = static_cast<uint32_t>(view) * n_stiles + st;
+  const uint32_t key = static_cast<uint32_t>(view) * key_stride + st;
   const uint32_t b = start[key], e = end[key];
   const RasterRec* __restrict__ vrec = rec + static_cast<int64_t>(view) * n;
   StagedRec2* sw = s_rec[warp];
@@ -445,8 +457,11 @@ __global__ void __launch_bounds__(256, GSCT_LANES_MINB) k_raster_bwd_lanes(const
 // to 6 bits, so a warp's 32 items have near-identical loop trip counts. Empty items sort
 // last. Values = item index (the stable sort keeps index order inside a shape class).
 #ifndef GSCT_KEY_MODE
-#define GSCT_KEY_MODE 1  // 0: shape; 1: shape | view | detector region (L1 locality inside a warp)
+#define GSCT_KEY_MODE 1  // 0: shape; 1: shape | view | detector region (L1 locality inside a warp);
+                         // 2/3 (view dropped, 16/15 bits = 2 radix passes): C2 3.82/3.93 ms vs 3.61
 #endif
+// shape = chunks per row (5 bits) | rows (6 bits; 5 in mode 2)
+constexpr int kShapeBits = GSCT_KEY_MODE == 2 ? 10 : 11;
 __global__ void k_bwd_shape_keys(const RasterRec* __restrict__ rec, int64_t n_items, int64_t n, int vec,
                                  int region_shift, int region_bits, int view_bits,
                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
@@ -457,12 +472,13 @@ __global__ void k_bwd_shape_keys(const RasterRec* __restrict__ rec, int64_t n_it
   const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
   const int W = u1 - u0 + 1, H = v1 - v0 + 1;
   const int low_bits = region_bits + view_bits;
-  uint32_t key = (1u << (11 + low_bits)) - 1u;  // empty items sort last
+  uint32_t key = (1u << (kShapeBits + low_bits)) - 1u;  // empty items sort last
   if (W > 0 && H > 0) {
     const int cw = vec == 8 ? 8 : 4;
     const int lead = vec > 1 ? (u0 & (vec - 1)) : 0;
     const int nch = (lead + W + cw - 1) / cw;
-    const uint32_t shape = (static_cast<uint32_t>(min(nch, 31)) << 6) | static_cast<uint32_t>(min(H, 63));
+    constexpr int hb = kShapeBits - 5;
+    const uint32_t shape = (static_cast<uint32_t>(min(nch, 31)) << hb) | static_cast<uint32_t>(min(H, (1 << hb) - 1));
     const int half = region_bits / 2;
     const uint32_t ru = min(u0 >> region_shift, (1 << half) - 1), rv = min(v0 >> region_shift, (1 << half) - 1);
     const uint32_t view = static_cast<uint32_t>(i / n);
@@ -486,6 +502,14 @@ void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets, const
   count_launch();
 }
 
+void launch_mark_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start, uint32_t* end,
+                        cudaStream_t st) {
+  (void)n_keys;  // start / end zeroed by the caller
+  if (n_pairs == 0) return;
+  k_mark_ranges<<<blocks_for(n_pairs, 256), 256, 0, st>>>(keys, static_cast<uint32_t>(n_pairs), start, end);
+  count_launch();
+}
+
 void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start, uint32_t* end,
                    cudaStream_t st) {
   if (n_keys == 0) return;
@@ -506,18 +530,25 @@ int bwd_vec(int n_u, const float* grad_images) {
 int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v, int vec,
                           uint32_t* keys, uint32_t* vals, cudaStream_t st) {
   const int64_t n_items = n * n_views;
-  if (n_items == 0) return 11;
+  if (n_items == 0) return kShapeBits;
   int view_bits = 0, region_bits = 0, region_shift = 0;
+  const int side = n_u > n_v ? n_u : n_v;
 #if GSCT_KEY_MODE == 1
+  // (shape, view, region): 11 + view + 6 bits
   while ((1 << view_bits) < n_views) ++view_bits;
   region_bits = 6;  // 8 x 8 detector regions
-  const int side = n_u > n_v ? n_u : n_v;
   while ((side >> region_shift) > 8) ++region_shift;
+#elif GSCT_KEY_MODE == 2 || GSCT_KEY_MODE == 3
+  // view left out of the key: items are emitted view-major and the radix sort is stable,
+  // so the order is (shape, region, view, splat) with 16 / 15 key bits = two passes
+  region_bits = GSCT_KEY_MODE == 2 ? 6 : 4;
+  const int per_axis = 1 << (region_bits / 2);
+  while ((side >> region_shift) > per_axis) ++region_shift;
 #endif
   k_bwd_shape_keys<<<blocks_for(n_items, 256), 256, 0, st>>>(rec, n_items, n, vec, region_shift, region_bits,
                                                              view_bits, keys, vals);
   count_launch();
-  return 11 + view_bits + region_bits;  // key bits
+  return kShapeBits + view_bits + region_bits;  // key bits
 }
 
 void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_t n, int n_views, int n_u,
@@ -540,13 +571,13 @@ void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_
 
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
-                             int stiles_v, float* images, cudaStream_t st) {
+                             int stiles_v, int key_stride, float* images, cudaStream_t st) {
   if (n_views == 0) return;
   const int n_stiles = stiles_u * stiles_v;
   // one warp per 32x16 half-super-tile (A/B at C2: 2x4-px lane blocks 3.65 ms, 2x8 2.96 ms,
   // 4x8 3.34 ms; CTA-shared staging with block barriers was slower still)
   dim3 g4(static_cast<unsigned>((2 * n_stiles + 3) / 4), static_cast<unsigned>(n_views));
-  k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, images);
+  k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, key_stride, images);
   count_launch();
 }
 
