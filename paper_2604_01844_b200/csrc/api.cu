@@ -717,7 +717,10 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     }
     RasterRec* saved = reuse ? ws<RasterRec>(c, S_SAVED, un * n_views) : nullptr;
     const int tiles_u = (geom->n_u + kTile - 1) / kTile, tiles_v = (geom->n_v + kTile - 1) / kTile;
-    int chunk = views_per_chunk(n, n_views, static_cast<int64_t>(tiles_u) * tiles_v);
+#ifndef GSCT_BWD_ONECHUNK
+#define GSCT_BWD_ONECHUNK 1  // the lane backward has no tile keys: chunk by the item budget only
+#endif
+    int chunk = views_per_chunk(n, n_views, GSCT_BWD_ONECHUNK ? 0 : static_cast<int64_t>(tiles_u) * tiles_v);
     // host grad images: smaller chunks so only the first (~1/6 of the views) upload is
     // exposed before the pixel walk starts; the rest streams in behind the compute
     if (grad_location == GSCT_HOST && n_views >= 12) chunk = std::min(chunk, (n_views + 5) / 6);
