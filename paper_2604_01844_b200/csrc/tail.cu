@@ -18,6 +18,25 @@ namespace {
 // fixed 2-step xor tree inside the aligned group, so a splat's result depends only on its
 // own inputs (ParamGradients::add up to fp64 reassociation; duplicates stay identical).
 // acc layout [11][N]: g_pos(3), g_sigma(00,01,02,11,12,22), g_raw, sum |dL/dmean2d|.
+#ifndef GSCT_TAIL_PAD
+#define GSCT_TAIL_PAD 1
+#endif
+struct PaddedFrame {
+  Frame f;
+#if GSCT_TAIL_PAD
+  double pad[GSCT_TAIL_PAD];
+#endif
+};
+
+#ifndef GSCT_TAIL_SPRE
+#define GSCT_TAIL_SPRE 1
+#endif
+struct PaddedPre {
+  PreSplat p;
+  double pad;
+};
+static_assert(sizeof(PreSplat) % sizeof(double) == 0, "PreSplat: whole doubles");
+
 #ifndef GSCT_TAIL_MINB
 #define GSCT_TAIL_MINB 4  // 128 registers
 #endif
@@ -26,13 +45,26 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
                                                      Geo g, RSet rs, const float4* __restrict__ moments,
                                                      int frames_in_smem, double* __restrict__ acc,
                                                      uint8_t* __restrict__ visible) {
-  extern __shared__ Frame s_frames[];
-  const Frame* frames = frames_g;
-  if (frames_in_smem) {
-    for (int k = threadIdx.x; k < n_views; k += blockDim.x) s_frames[k] = frames_g[k];
-    __syncthreads();
-    frames = s_frames;
+  // smem frames padded to 17 doubles: the 4 lanes of a group read 4 different views, which
+  // at the natural 128 B stride would all hit the same banks (4-way conflicts)
+  extern __shared__ PaddedFrame s_frames[];
+  if (frames_in_smem)
+    for (int k = threadIdx.x; k < n_views; k += blockDim.x) s_frames[k].f = frames_g[k];
+#if GSCT_TAIL_SPRE
+  // the block's 32 splat set-ups staged in shared memory at a 200 B stride (8 distinct
+  // splats per warp access: conflict-free banks), instead of 8 L1 lines per field load
+  __shared__ PaddedPre s_pre[32];
+  {
+    const int64_t first = static_cast<int64_t>(blockIdx.x) * 32;
+    const int cnt = n - first < 32 ? static_cast<int>(n - first) : 32;
+    const double* src = reinterpret_cast<const double*>(pre + first);
+    constexpr int kD = sizeof(PreSplat) / sizeof(double);
+    for (int k = threadIdx.x; k < cnt * kD; k += blockDim.x)
+      reinterpret_cast<double*>(&s_pre[k / kD].p)[k % kD] = src[k];
   }
+#endif
+  __syncthreads();
+  const auto frame = [&](int vw) -> const Frame& { return frames_in_smem ? s_frames[vw].f : frames_g[vw]; };
   const int q = threadIdx.x & 3;
   const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 2;
   const bool live = i < n;
@@ -41,7 +73,11 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
   for (int k = 0; k < 11; ++k) v[k] = 0.0;
   bool vis = false;
   if (live) {
+#if GSCT_TAIL_SPRE
+    const PreSplat& s = s_pre[threadIdx.x >> 2].p;
+#else
     const PreSplat& s = pre[i];  // array-of-structs copy (fields re-read from L1 as needed)
+#endif
     if (s.status == 0) {
       for (int vw = q; vw < n_views; vw += 4) {
         const int64_t item = static_cast<int64_t>(vw) * n + i;
@@ -49,7 +85,8 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
         if (m1.z == 0.f) continue;  // culled or degenerate in this view
         const float4 m0 = moments[2 * item];
         Proj p;
-        project_full<false>(frames[vw], g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
+        const Frame& fr = frame(vw);
+        project_full<false>(fr, g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
         if (p.degenerate) continue;
         vis = true;
         // m0 = {sum t, sum t du, sum t dv, sum t du^2}, m1 = {sum t du dv, sum t dv^2, 1, -}
@@ -64,7 +101,7 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
         gc[2] = gc[1];
         gc[3] = -0.5 * amp * static_cast<double>(m1.y);
         double gp[3], gs[9], gr;
-        raster_chain_rule(frames[vw], g, rs, s.density, s.raw_density, s.sigma, p, static_cast<double>(m0.x), gm,
+        raster_chain_rule(fr, g, rs, s.density, s.raw_density, s.sigma, p, static_cast<double>(m0.x), gm,
                           gc, gp, gs, gr);
         v[0] += gp[0];
         v[1] += gp[1];
@@ -127,7 +164,7 @@ inline unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n +
 void launch_raster_tail(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views, const Geo& g,
                         const RSet& rs, const float* moments, double* acc, uint8_t* visible, cudaStream_t st) {
   if (n == 0) return;
-  const size_t smem = static_cast<size_t>(n_views) * sizeof(Frame);
+  const size_t smem = static_cast<size_t>(n_views) * sizeof(PaddedFrame);
   const bool in_smem = smem <= 24 * 1024;
   k_raster_tail<<<blocks_for(n * 4, 128), 128, in_smem ? smem : 0, st>>>(
       pre, n, frames_dev, n_views, g, rs, reinterpret_cast<const float4*>(moments), in_smem ? 1 : 0, acc, visible);
