@@ -161,11 +161,9 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 #define GSCT_FWD_UNROLL 4  // unroll factor of the per-lane record walk (A/B on 2x4 blocks: 1 -> 3.50, 4 -> 3.15 ms)
 #endif
 constexpr int kFwdUnroll = GSCT_FWD_UNROLL;
-#ifndef GSCT_FWD_PACKACC
-#define GSCT_FWD_PACKACC 1  // accumulate {row 0, row 1} per column with predicated packed FMAs
-                            // (__ffma2_rn: ptxas predicates it in place; inline-asm FFMA2 under an
-                            // `if` got temp + predicated MOV pairs). A/B C2 3.22 -> 2.92 ms
-#endif
+// Accumulation: {row 0, row 1} per column with predicated packed FMAs (__ffma2_rn, which
+// ptxas predicates in place; inline-asm FFMA2 under an `if` got a temporary + predicated MOV
+// pairs; scalar FFMAs per row: A/B C2 3.22 vs 2.92 ms).
 
 __global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict__ rec,
                                                      const uint32_t* __restrict__ vals,
@@ -188,15 +186,9 @@ __global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict
   const uint32_t b = start[key], e = end[key];
   const RasterRec* __restrict__ vrec = rec + static_cast<int64_t>(view) * n;
   StagedRec2* sw = s_rec[warp];
-#if GSCT_FWD_PACKACC
   float2 acc[8];  // per column {row 0, row 1}
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = make_float2(0.f, 0.f);
-#else
-  float acc0[8], acc1[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.f;
-#endif
 
   uint32_t idx_next = (b + 32 + lane < e) ? vals[b + 32 + lane] : 0u;
   RasterRec r_cur;
@@ -252,69 +244,48 @@ __global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict
       const float a0 = (rows & 1u) ? q.y : 0.f, a1 = (rows & 2u) ? q.y : 0.f;
       const float du0 = p.x + flc;
       const float dv0 = p.y + flr;
-      const f2_t DV = f2_pack(dv0, dv0 + 1.f);
       const float bdu = p.w * du0, au2 = p.z * du0 * du0;
-      const f2_t CC = f2_pack(q.x, q.x);
-      f2_t h[8];
+      const float2 A01 = make_float2(a0, a1);
+      const float2 DV2 = make_float2(dv0, dv0 + 1.f);
+      // accumulation inside each branch: no merge of the h registers after the branch
+      // (a merged h[8] cost ~10 register-pair MOVs per record)
       if (q.w != 0.f) {
-        const f2_t E0 = f2_fma(DV, f2_fma(CC, DV, f2_pack(bdu, bdu)), f2_pack(au2, au2));
+        const float2 E0 = __ffma2_rn(DV2, __ffma2_rn(make_float2(q.x, q.x), DV2, make_float2(bdu, bdu)),
+                                     make_float2(au2, au2));
         const float a1e = p.z * fmaf(2.f, du0, 1.f);
-        const f2_t D = f2_fma(f2_pack(p.w, p.w), DV, f2_pack(a1e, a1e));
-        float e0, e1, d0, d1;
-        f2_unpack(E0, e0, e1);
-        f2_unpack(D, d0, d1);
-        h[0] = f2_pack(ex2_approx(e0), ex2_approx(e1));
-        f2_t rr = f2_pack(ex2_approx(d0), ex2_approx(d1));
-        const f2_t c2 = f2_pack(q.z, q.z);
+        const float2 D = __ffma2_rn(make_float2(p.w, p.w), DV2, make_float2(a1e, a1e));
+        float2 h = make_float2(ex2_approx(E0.x), ex2_approx(E0.y));
+        float2 rr = make_float2(ex2_approx(D.x), ex2_approx(D.y));
+        const float2 c2 = make_float2(q.z, q.z);
 #pragma unroll
-        for (int k = 1; k < 8; ++k) {
-          h[k] = f2_mul(h[k - 1], rr);
-          if (k < 7) rr = f2_mul(rr, c2);
+        for (int k = 0; k < 8; ++k) {
+          if (mask & (1u << k)) acc[k] = __ffma2_rn(h, A01, acc[k]);
+          if (k < 7) h = __fmul2_rn(h, rr);
+          if (k < 6) rr = __fmul2_rn(rr, c2);
         }
       } else {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float duk = du0 + static_cast<float>(k);
-          const f2_t ek = f2_fma(DV, f2_fma(CC, DV, f2_pack(p.w * duk, p.w * duk)),
-                                 f2_pack(p.z * duk * duk, p.z * duk * duk));
-          float e0, e1;
-          f2_unpack(ek, e0, e1);
-          h[k] = f2_pack(ex2_approx(e0), ex2_approx(e1));
+          const float bk = p.w * duk, ak = p.z * duk * duk;
+          const float2 ek = __ffma2_rn(DV2, __ffma2_rn(make_float2(q.x, q.x), DV2, make_float2(bk, bk)),
+                                       make_float2(ak, ak));
+          const float2 h = make_float2(ex2_approx(ek.x), ex2_approx(ek.y));
+          if (mask & (1u << k)) acc[k] = __ffma2_rn(h, A01, acc[k]);
         }
       }
-#if GSCT_FWD_PACKACC
-      const float2 A01 = make_float2(a0, a1);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        float hl, hh;
-        f2_unpack(h[k], hl, hh);
-        if (mask & (1u << k)) acc[k] = __ffma2_rn(make_float2(hl, hh), A01, acc[k]);
-      }
-#else
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        float hl, hh;
-        f2_unpack(h[k], hl, hh);
-        if (mask & (1u << k)) {
-          acc0[k] = fmaf(hl, a0, acc0[k]);
-          acc1[k] = fmaf(hh, a1, acc1[k]);
-        }
-      }
-#endif
     }
     __syncwarp();
     r_cur = r_next;
   }
   const int px0 = tx0 + lc;
   if (px0 >= n_u) return;
-#if GSCT_FWD_PACKACC
   float acc0[8], acc1[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     acc0[k] = acc[k].x;
     acc1[k] = acc[k].y;
   }
-#endif
 #pragma unroll
   for (int hh = 0; hh < 2; ++hh) {
     const int py = ty0 + lr + hh;
