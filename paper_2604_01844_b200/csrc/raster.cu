@@ -460,6 +460,9 @@ __global__ void __launch_bounds__(256, GSCT_LANES_MINB) k_raster_bwd_lanes(const
 #define GSCT_KEY_MODE 1  // 0: shape; 1: shape | view | detector region (L1 locality inside a warp);
                          // 2/3 (view dropped, 16/15 bits = 2 radix passes): C2 3.82/3.93 ms vs 3.61
 #endif
+#ifndef GSCT_REGION_BITS
+#define GSCT_REGION_BITS 0  // 0: adaptive (below)
+#endif
 // shape = chunks per row (5 bits) | rows (6 bits; 5 in mode 2)
 constexpr int kShapeBits = GSCT_KEY_MODE == 2 ? 10 : 11;
 __global__ void k_bwd_shape_keys(const RasterRec* __restrict__ rec, int64_t n_items, int64_t n, int vec,
@@ -534,10 +537,17 @@ int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u,
   int view_bits = 0, region_bits = 0, region_shift = 0;
   const int side = n_u > n_v ? n_u : n_v;
 #if GSCT_KEY_MODE == 1
-  // (shape, view, region): 11 + view + 6 bits
+  // (shape, view, region): 11 + view + region bits
   while ((1 << view_bits) < n_views) ++view_bits;
-  region_bits = 6;  // 8 x 8 detector regions
-  while ((side >> region_shift) > 8) ++region_shift;
+  // 2^(bits/2) x 2^(bits/2) detector regions: the finest regions of >= 32 px that keep the
+  // key within 24 bits (three radix passes). A/B: C2 (512^2, 75 views) 6 bits 3.54 ms vs
+  // 8 bits 3.60; C5 (2048^2, 8 views) 6 bits 73.5 ms, 10 bits 67.7, 12 bits 66.4
+  region_bits = GSCT_REGION_BITS;
+  if (region_bits == 0) {
+    region_bits = 2;
+    while (region_bits + 2 <= 24 - 11 - view_bits && (side >> ((region_bits + 2) / 2)) >= 32) region_bits += 2;
+  }
+  while ((side >> region_shift) > (1 << (region_bits / 2))) ++region_shift;
 #elif GSCT_KEY_MODE == 2 || GSCT_KEY_MODE == 3
   // view left out of the key: items are emitted view-major and the radix sort is stable,
   // so the order is (shape, region, view, splat) with 16 / 15 key bits = two passes
