@@ -308,7 +308,7 @@ int bits_for(uint64_t n_keys) {
 // (view-major emission, key = view << sort_bits | tile), so a stable sort on the low
 // sort_bits alone leaves every (view, tile) run contiguous -- ordered (tile, view, splat)
 // rather than (view, tile, splat), with the splats of a run still ascending -- in one
-// radix pass instead of two or three; ranges are then marked at run boundaries.
+// radix pass instead of two or three; ranges by binary search in (tile, view) order.
 template <class Emit>
 int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32_t n_keys,
                      Emit&& emit, uint32_t** keys_out, uint32_t** vals_out, uint32_t** start,
@@ -341,9 +341,7 @@ int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32
   *keys_out = kb.Current();
   *vals_out = vb.Current();
   if (sort_bits > 0) {
-    CK(cudaMemsetAsync(*start, 0, n_keys * sizeof(uint32_t), c->stream));
-    CK(cudaMemsetAsync(*end, 0, n_keys * sizeof(uint32_t), c->stream));
-    launch_mark_ranges(*keys_out, total, n_keys, *start, *end, c->stream);
+    launch_ranges_swapped(*keys_out, total, n_keys, sort_bits, *start, *end, c->stream);
   } else {
     launch_ranges(*keys_out, total, n_keys, *start, *end, c->stream);
   }

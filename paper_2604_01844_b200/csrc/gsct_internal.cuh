@@ -89,9 +89,9 @@ void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets,
                             int n_tiles, uint32_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start,
                    uint32_t* end, cudaStream_t st);
-// equal keys contiguous, sequence not monotone; start / end must be zeroed first
-void launch_mark_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start,
-                        uint32_t* end, cudaStream_t st);
+// keys = view << tile_bits | tile, sorted by the tile bits only (view order < 2^16 kept)
+void launch_ranges_swapped(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, int tile_bits,
+                           uint32_t* start, uint32_t* end, cudaStream_t st);
 // forward over 32x32 super-tile lists (keys = view * n_stiles + super-tile)
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,

@@ -107,16 +107,31 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, ui
   end[k] = lower_bound_u32(keys, n_pairs, k + 1);
 }
 
-// [start, end) of every key when equal keys are contiguous but the key sequence is not
-// monotone (the one-pass binning below): one thread per pair marks the run boundaries;
-// start / end of absent keys stay 0 (zeroed by the caller).
-__global__ void k_mark_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, uint32_t* __restrict__ start,
-                              uint32_t* __restrict__ end) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_pairs) return;
-  const uint32_t k = keys[i];
-  if (i == 0 || keys[i - 1] != k) start[k] = i;
-  if (i + 1 == n_pairs || keys[i + 1] != k) end[k] = i + 1;
+// [start, end) of every key after the one-pass binning: keys = view << tile_bits | tile
+// sorted by tile only (stable), i.e. ascending in ord(key) = tile << 16 | view; binary
+// search in that order, one thread per key.
+__device__ __forceinline__ uint32_t swapped_ord(uint32_t key, int tile_bits) {
+  return ((key & ((1u << tile_bits) - 1u)) << 16) | (key >> tile_bits);
+}
+__device__ __forceinline__ uint32_t lower_bound_swapped(const uint32_t* __restrict__ a, uint32_t n, uint32_t x,
+                                                        int tile_bits) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (swapped_ord(__ldg(a + mid), tile_bits) < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+__global__ void k_ranges_swapped(const uint32_t* __restrict__ keys, uint32_t n_pairs, uint32_t n_keys, int tile_bits,
+                                 uint32_t* __restrict__ start, uint32_t* __restrict__ end) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_keys) return;
+  const uint32_t o = swapped_ord(k, tile_bits);
+  start[k] = lower_bound_swapped(keys, n_pairs, o, tile_bits);
+  end[k] = lower_bound_swapped(keys, n_pairs, o + 1, tile_bits);
 }
 
 // Forward (K3): one warp per 32x16 half of a 32x32 super-tile and view; lane l owns the
@@ -505,11 +520,11 @@ void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets, const
   count_launch();
 }
 
-void launch_mark_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint32_t* start, uint32_t* end,
-                        cudaStream_t st) {
-  (void)n_keys;  // start / end zeroed by the caller
-  if (n_pairs == 0) return;
-  k_mark_ranges<<<blocks_for(n_pairs, 256), 256, 0, st>>>(keys, static_cast<uint32_t>(n_pairs), start, end);
+void launch_ranges_swapped(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, int tile_bits, uint32_t* start,
+                          uint32_t* end, cudaStream_t st) {
+  if (n_keys == 0) return;
+  k_ranges_swapped<<<blocks_for(n_keys, 256), 256, 0, st>>>(keys, static_cast<uint32_t>(n_pairs), n_keys, tile_bits,
+                                                            start, end);
   count_launch();
 }
 
