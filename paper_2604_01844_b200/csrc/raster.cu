@@ -180,14 +180,60 @@ constexpr int kFwdUnroll = GSCT_FWD_UNROLL;
 // ptxas predicates in place; inline-asm FFMA2 under an `if` got a temporary + predicated MOV
 // pairs; scalar FFMAs per row: A/B C2 3.22 vs 2.92 ms).
 
-__global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict__ rec,
+#ifndef GSCT_FWD_GROUPS
+#define GSCT_FWD_GROUPS 2  // records staged per warp batch = 32 x groups (lane balance); A/B
+                           // C2 (min blocks 7/8): G1 2.65 ms, G2 2.56, G3 2.98, G4 3.23 -- the
+                           // refill logic and registers eat the balance gain beyond 2 groups
+#endif
+constexpr int kFwdGroups = GSCT_FWD_GROUPS;
+
+// Stages one record (the staging lane's work, see StagedRec2); returns the lane mask.
+__device__ __forceinline__ uint32_t stage_record(const RasterRec& r, int tx0, int ty0, StagedRec2* slot) {
+  constexpr int kHW = 2 * kTile, kHH = kTile;
+  const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16, v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+  const int c0 = max(u0 - tx0, 0), c1 = min(u1 - tx0, kHW - 1);
+  const int r0 = max(v0 - ty0, 0), r1 = min(v1 - ty0, kHH - 1);
+  if (c0 > c1 || r0 > r1) return 0u;
+  StagedRec2 s;
+  const float du_t = (static_cast<float>(tx0) - static_cast<float>(u0)) - r.mo_u;
+  const float dv_t = (static_cast<float>(ty0) - static_cast<float>(v0)) - r.mo_v;
+  const uint32_t cm = (c1 == 31 ? 0xFFFFFFFFu : ((2u << c1) - 1u)) & ~((1u << c0) - 1u);
+  const uint32_t rm = ((2u << r1) - 1u) & ~((1u << r0) - 1u);
+  // lane mask: column octets c0/8..c1/8 x row pairs r0/2..r1/2 (lane = 4 * pair + octet)
+  const uint32_t octs = ((2u << (c1 >> 3)) - 1u) & ~((1u << (c0 >> 3)) - 1u);
+  const uint32_t pairs = (0x11111111u >> (4 * (7 - (r1 >> 1)))) & (0x11111111u << (4 * (r0 >> 1)));
+  const uint32_t lanes_rel = pairs * octs;
+  // chain-safety window: rows r0..r1 x 8-aligned columns
+  const float dua = du_t + static_cast<float>(c0 & ~7), dub = du_t + static_cast<float>(c1 | 7);
+  const float dva = dv_t + static_cast<float>(r0 & ~1), dvb = dv_t + static_cast<float>(r1 | 1);
+  const float emin = fminf(fminf(quad_e(r.A, r.B, r.C, dua, dva), quad_e(r.A, r.B, r.C, dua, dvb)),
+                           fminf(quad_e(r.A, r.B, r.C, dub, dva), quad_e(r.A, r.B, r.C, dub, dvb)));
+  const float da = r.A * fmaf(2.f, dua, 1.f), db = r.A * fmaf(2.f, dub, 1.f);
+  const float dmax = fmaxf(fmaxf(fabsf(fmaf(r.B, dva, da)), fabsf(fmaf(r.B, dvb, da))),
+                           fmaxf(fabsf(fmaf(r.B, dva, db)), fabsf(fmaf(r.B, dvb, db))));
+  const bool safe = emin > -100.f && dmax < 100.f && r.A > -25.f;
+  s.p = make_float4(du_t, dv_t, r.A, r.B);
+  s.q = make_float4(r.C, r.amp, ex2_approx(2.f * r.A), safe ? 1.f : 0.f);
+  s.m = make_uint4(cm, rm, lanes_rel, 0u);
+  *slot = s;
+  return lanes_rel;
+}
+
+// Batches of 32 x kFwdGroups records: the warp's loop runs max over lanes of the lane's
+// record count in the batch, so bigger batches even out the per-lane counts (simulated on
+// the C2 lists: lane efficiency 61% at 32 records, 73% at 128, 85% over whole lists).
+#ifndef GSCT_FWD_MINB
+#define GSCT_FWD_MINB 7  // 72 registers (G=2) without spills
+#endif
+__global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const RasterRec* __restrict__ rec,
                                                      const uint32_t* __restrict__ vals,
                                                      const uint32_t* __restrict__ start,
                                                      const uint32_t* __restrict__ end, int64_t n, int n_u,
                                                      int n_v, int stiles_u, int n_stiles, int key_stride,
                                                      float* __restrict__ images) {
-  constexpr int kHW = 2 * kTile, kHH = kTile;  // half-tile: 32 wide, 16 tall
-  __shared__ StagedRec2 s_rec[4][32];
+  constexpr int kHH = kTile;  // half-tile: 32 wide, 16 tall
+  constexpr int kBatch = 32 * kFwdGroups;
+  __shared__ StagedRec2 s_rec[4][kBatch];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = blockIdx.x * 4 + warp;  // 2 halves per super-tile
   if (half >= 2 * n_stiles) return;
@@ -205,52 +251,63 @@ __global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = make_float2(0.f, 0.f);
 
-  uint32_t idx_next = (b + 32 + lane < e) ? vals[b + 32 + lane] : 0u;
-  RasterRec r_cur;
-  if (b + lane < e) r_cur = vrec[vals[b + lane]];
-  for (uint32_t base = b; base < e; base += 32) {
-    const int cnt = min(32u, e - base);
-    const bool has_next = base + 32 + lane < e;
-    RasterRec r_next;
-    if (has_next) r_next = vrec[idx_next];
-    idx_next = (base + 64 + lane < e) ? vals[base + 64 + lane] : 0u;
-    uint32_t lanes_rel = 0u;
-    if (lane < cnt) {
-      const RasterRec r = r_cur;
-      const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16, v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
-      const int c0 = max(u0 - tx0, 0), c1 = min(u1 - tx0, kHW - 1);
-      const int r0 = max(v0 - ty0, 0), r1 = min(v1 - ty0, kHH - 1);
-      if (c0 <= c1 && r0 <= r1) {
-        StagedRec2 s;
-        const float du_t = (static_cast<float>(tx0) - static_cast<float>(u0)) - r.mo_u;
-        const float dv_t = (static_cast<float>(ty0) - static_cast<float>(v0)) - r.mo_v;
-        const uint32_t cm = (c1 == 31 ? 0xFFFFFFFFu : ((2u << c1) - 1u)) & ~((1u << c0) - 1u);
-        const uint32_t rm = ((2u << r1) - 1u) & ~((1u << r0) - 1u);
-        // lane mask: column octets c0/8..c1/8 x row pairs r0/2..r1/2 (lane = 4 * pair + octet)
-        const uint32_t octs = ((2u << (c1 >> 3)) - 1u) & ~((1u << (c0 >> 3)) - 1u);
-        const uint32_t pairs = (0x11111111u >> (4 * (7 - (r1 >> 1)))) & (0x11111111u << (4 * (r0 >> 1)));
-        lanes_rel = pairs * octs;
-        // chain-safety window: rows r0..r1 x 8-aligned columns
-        const float dua = du_t + static_cast<float>(c0 & ~7), dub = du_t + static_cast<float>(c1 | 7);
-        const float dva = dv_t + static_cast<float>(r0 & ~1), dvb = dv_t + static_cast<float>(r1 | 1);
-        const float emin = fminf(fminf(quad_e(r.A, r.B, r.C, dua, dva), quad_e(r.A, r.B, r.C, dua, dvb)),
-                                 fminf(quad_e(r.A, r.B, r.C, dub, dva), quad_e(r.A, r.B, r.C, dub, dvb)));
-        const float da = r.A * fmaf(2.f, dua, 1.f), db = r.A * fmaf(2.f, dub, 1.f);
-        const float dmax = fmaxf(fmaxf(fabsf(fmaf(r.B, dva, da)), fabsf(fmaf(r.B, dvb, da))),
-                                 fmaxf(fabsf(fmaf(r.B, dva, db)), fabsf(fmaf(r.B, dvb, db))));
-        const bool safe = emin > -100.f && dmax < 100.f && r.A > -25.f;
-        s.p = make_float4(du_t, dv_t, r.A, r.B);
-        s.q = make_float4(r.C, r.amp, ex2_approx(2.f * r.A), safe ? 1.f : 0.f);
-        s.m = make_uint4(cm, rm, lanes_rel, 0u);
-        sw[lane] = s;
-      }
+  // records of the next batch and indices of the one after are prefetched across the
+  // current batch's walk (two dependent loads kept off the critical path)
+  uint32_t idx_next[kFwdGroups];
+  RasterRec recs[kFwdGroups];
+#pragma unroll
+  for (int g = 0; g < kFwdGroups; ++g) {
+    const uint32_t k = b + 32 * g + lane;
+    if (k < e) recs[g] = vrec[__ldg(vals + k)];
+    idx_next[g] = k + kBatch < e ? __ldg(vals + k + kBatch) : 0u;
+  }
+  for (uint32_t base = b; base < e; base += kBatch) {
+    uint32_t todo[kFwdGroups];
+#pragma unroll
+    for (int g = 0; g < kFwdGroups; ++g) {
+      const uint32_t rel = base + 32 * g + lane < e ? stage_record(recs[g], tx0, ty0, sw + 32 * g + lane) : 0u;
+      todo[g] = warp_transpose32(rel, lane);
     }
     __syncwarp();
-    uint32_t todo = warp_transpose32(lanes_rel, lane);
+#pragma unroll
+    for (int g = 0; g < kFwdGroups; ++g) {
+      const uint32_t k = base + kBatch + 32 * g + lane;
+      if (k < e) recs[g] = vrec[idx_next[g]];
+      idx_next[g] = k + kBatch < e ? __ldg(vals + k + kBatch) : 0u;
+    }
+    // one flat loop over the lane's records of the whole batch, so lanes do not wait for
+    // each other at group boundaries
+#if GSCT_FWD_GROUPS == 1
+    uint32_t cur = todo[0];
 #pragma unroll kFwdUnroll
-    while (todo) {
-      const int j = __ffs(todo) - 1;
-      todo &= todo - 1u;
+    while (cur) {
+      const int j = __ffs(cur) - 1;
+      cur &= cur - 1u;
+#else
+    // group words shifted in as they empty (a 64-bit find-first per record cost more)
+    uint32_t cur = todo[0];
+    int gbase = 0;
+#pragma unroll
+    for (int g = 1; g < kFwdGroups; ++g)
+      if (cur == 0u) {
+        cur = todo[g];
+        gbase = 32 * g;
+      }
+    int gnext = gbase / 32 + 1;
+#pragma unroll kFwdUnroll
+    while (cur) {
+      const int j = gbase + __ffs(cur) - 1;
+      cur &= cur - 1u;
+      if (cur == 0u) {
+#pragma unroll
+        for (int g = 1; g < kFwdGroups; ++g)
+          if (cur == 0u && g >= gnext) {
+            cur = todo[g];
+            gbase = 32 * g;
+            gnext = g + 1;
+          }
+      }
+#endif
       const float4 p = sw[j].p;
       const float4 q = sw[j].q;
       const uint2 mm = make_uint2(sw[j].m.x, sw[j].m.y);
@@ -291,7 +348,6 @@ __global__ void __launch_bounds__(128) k_raster_fwd4(const RasterRec* __restrict
       }
     }
     __syncwarp();
-    r_cur = r_next;
   }
   const int px0 = tx0 + lc;
   if (px0 >= n_u) return;
