@@ -49,7 +49,8 @@ enum gsct_status {
   GSCT_OK = 0,
   GSCT_ERR_CONTRACT = 1, /* maps to gsct::contract_error */
   GSCT_ERR_CUDA = 2,
-  GSCT_ERR_OOM = 3
+  GSCT_ERR_OOM = 3,
+  GSCT_ERR_PARSE = 4     /* maps to gsct::parse_error; the message ends "(byte offset N)" */
 };
 
 enum gsct_location { GSCT_HOST = 0, GSCT_DEVICE = 1 };
@@ -284,6 +285,19 @@ int gsct_adaptive_control(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_adam
                           const gsct_control_accum* acc, const gsct_rng_state* rng,
                           const gsct_control_config* cfg, int64_t capacity, gsct_cloud* out_cloud,
                           gsct_adam_state* out_state, gsct_control_accum* out_acc, gsct_adaptive_report* report);
+
+/* Compressed model (io.hpp:319-425): "FGSC", u32 version 1, u64 count, then 22 bytes per
+ * splat = 11 little-endian binary16 (half.hpp) of the ACTIVATED position, scales, unit
+ * quaternion (quantize-then-renormalise fixed point) and density. bytes: 16 + 22 N, at
+ * `location` (2-byte aligned). *saturated = values clipped to +-65504 (CompressStats); like
+ * the reference, a warning goes to stderr when any were. Non-finite parameters / zero
+ * quaternions are contract errors (activate). */
+int gsct_compress_model(gsct_ctx ctx, const gsct_cloud* cloud, uint8_t* bytes, int location, int64_t* saturated);
+/* decompress_model: header errors (truncation, magic, version, size) are GSCT_ERR_PARSE with
+ * the reference's messages. out->n must equal the header's count (bytes 8..15, little
+ * endian); out arrays (pos, log_scale, quat, raw_density) at out->location. Log-scales of
+ * scales floored at 2^-24; unit quaternions (zero -> identity); densities clamped at 0. */
+int gsct_decompress_model(gsct_ctx ctx, const uint8_t* bytes, int64_t n_bytes, int location, gsct_cloud* out);
 
 /* ---- parity hooks (bit-exactness checks against the CPU oracle) ------------------ */
 /* Per splat for one view: rect[4N] (u_min,u_max,v_min,v_max), flags[N] (bit0 culled,

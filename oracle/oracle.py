@@ -367,6 +367,29 @@ class Ref:
         return ({k: v[:m] for k, v in out_p.items()}, {k: v[:m] for k, v in out_m.items()},
                 {"pruned": int(rep[0]), "cloned": int(rep[1]), "split": int(rep[2]), "n_next": m})
 
+    def compress_model(self, params: dict):
+        """compress_model (io.hpp:323-385): (bytes, saturated)."""
+        n = len(params["raw"])
+        out = np.zeros(16 + 22 * n, dtype=np.uint8)
+        sat = C.c_int64(0)
+        f = self.l.ref_compress_model
+        f.argtypes = [C.c_int64] + [C.c_void_p] * 5 + [C.c_void_p]
+        ins = {k: np.ascontiguousarray(params[k], dtype=np.float64) for k in ("pos", "ls", "q", "raw")}
+        self._chk(f(n, _p(ins["pos"]), _p(ins["ls"]), _p(ins["q"]), _p(ins["raw"]), out.ctypes.data, C.byref(sat)))
+        return out, int(sat.value)
+
+    def decompress_model(self, data: np.ndarray, capacity: int = 1 << 16):
+        """decompress_model (io.hpp:387-419): dict of pos / ls / q / raw."""
+        data = np.ascontiguousarray(data, dtype=np.uint8)
+        cap = max(int(capacity), 1)
+        out = {"pos": np.zeros((cap, 3)), "ls": np.zeros((cap, 3)), "q": np.zeros((cap, 4)), "raw": np.zeros(cap)}
+        m = C.c_int64(0)
+        f = self.l.ref_decompress_model
+        f.argtypes = [C.c_void_p, C.c_int64, C.c_int64] + [C.c_void_p] * 4 + [C.c_void_p]
+        self._chk(f(data.ctypes.data if data.size else None, data.size, cap, _p(out["pos"]), _p(out["ls"]),
+                    _p(out["q"]), _p(out["raw"]), C.byref(m)))
+        return {k: v[:m.value] for k, v in out.items()}
+
     def total_loss_fit(self, rendered: np.ndarray, target: np.ndarray, alpha_ssim: float, streaming: bool = True):
         """(l1, ssim, total), grad for a [nz, ny, nx] volume (losses.hpp:648-664)."""
         r = np.ascontiguousarray(rendered, dtype=np.float64)

@@ -11,6 +11,7 @@
 
 #include "gsct/bench.hpp"
 #include "gsct/core.hpp"
+#include "gsct/io.hpp"
 #include "gsct/losses.hpp"
 #include "gsct/optim.hpp"
 #include "gsct/parallel.hpp"
@@ -500,6 +501,42 @@ int ref_adaptive_control(int64_t n, const double* pos, const double* ls, const d
     }
     std::istringstream in(st.rng.save_state());
     for (int k = 0; k < 313; ++k) in >> rng[k];
+  });
+}
+
+// compress_model / decompress_model (io.hpp:319-425) of the unchanged reference. compress:
+// out must hold 16 + 22 n bytes; *saturated (CompressStats). decompress: arrays of
+// capacity rows; *n_out = decoded count (error 2 if it exceeds the capacity).
+int ref_compress_model(int64_t n, const double* pos, const double* ls, const double* q, const double* raw,
+                       uint8_t* out, int64_t* saturated) {
+  GUARD({
+    GaussianCloud c;
+    for (int64_t i = 0; i < n; ++i)
+      c.push_back(Vec3(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]), Vec3(ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]),
+                  Vec4(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]), raw[i]);
+    CompressStats st;
+    const std::vector<std::uint8_t> b = compress_model(c, &st);
+    std::memcpy(out, b.data(), b.size());
+    *saturated = static_cast<int64_t>(st.saturated);
+  });
+}
+
+int ref_decompress_model(const uint8_t* bytes, int64_t n_bytes, int64_t capacity, double* pos, double* ls, double* q,
+                         double* raw, int64_t* n_out) {
+  GUARD({
+    const std::vector<std::uint8_t> b(bytes, bytes + n_bytes);
+    const GaussianCloud c = decompress_model(b);
+    const int64_t m = static_cast<int64_t>(c.size());
+    *n_out = m;
+    if (m > capacity) return 2;
+    for (int64_t i = 0; i < m; ++i) {
+      for (int a = 0; a < 3; ++a) {
+        pos[3 * i + a] = c.positions[i][a];
+        ls[3 * i + a] = c.log_scales[i][a];
+      }
+      for (int a = 0; a < 4; ++a) q[4 * i + a] = c.rotations[i][a];
+      raw[i] = c.raw_densities[i];
+    }
   });
 }
 }  // extern "C"

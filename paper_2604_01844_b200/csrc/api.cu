@@ -24,7 +24,7 @@ namespace {
 enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
-  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG,
+  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG, S_FGSC, S_FGSC_LOG, S_FGSC_CNT,
   S_COUNT_SLOTS
 };
 
@@ -70,6 +70,7 @@ struct gsct_ctx_s {
   bool save_fb = false;
   bool saved_valid = false;
   std::string saved_key;
+  bool fgsc_table_ready = false;  // S_FGSC_LOG holds the binary16 log table
 };
 
 namespace gsct_dev {
@@ -1360,6 +1361,136 @@ int gsct_adaptive_control(gsct_ctx c, const gsct_cloud* cloud, const gsct_adam_s
     out_state->step = state->step;
     out_state->skipped_updates = state->skipped_updates;
     (void)un;
+  });
+}
+
+namespace {
+[[noreturn]] void parse_fail(const std::string& msg, size_t offset) {
+  throw CallError{GSCT_ERR_PARSE, msg + " (byte offset " + std::to_string(offset) + ")"};
+}
+constexpr int kFgscHalfs = 0x7c00;  // binary16 patterns 0 .. 0x7bff (positive finite + zero)
+}  // namespace
+
+int gsct_compress_model(gsct_ctx c, const gsct_cloud* cloud, uint8_t* bytes, int location, int64_t* saturated) {
+  return run(c, [&] {
+    contract(cloud && bytes && saturated, "compress_model: null argument");
+    contract((reinterpret_cast<uintptr_t>(bytes) & 1) == 0, "compress_model: byte buffer must be 2-byte aligned");
+    const Cloud d = upload_cloud(c, cloud);
+    const int64_t n = d.n;
+    uint8_t header[16] = {'F', 'G', 'S', 'C', 1, 0, 0, 0};
+    for (int k = 0; k < 8; ++k) header[8 + k] = static_cast<uint8_t>(static_cast<uint64_t>(n) >> (8 * k));
+    const size_t body_bytes = 22 * static_cast<size_t>(n);
+    unsigned long long* cnt = ws<unsigned long long>(c, S_FGSC_CNT, 2);
+    const unsigned long long init[2] = {0ull, ~0ull};
+    CK(cudaMemcpyAsync(cnt, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+    uint16_t* body = location == GSCT_DEVICE ? reinterpret_cast<uint16_t*>(bytes + 16)
+                                             : ws<uint16_t>(c, S_FGSC, 11 * static_cast<size_t>(n) + 1);
+    launch_fgsc_encode(d, body, cnt, c->stream);
+    CK(cudaGetLastError());
+    if (location == GSCT_DEVICE) {
+      CK(cudaMemcpyAsync(bytes, header, 16, cudaMemcpyHostToDevice, c->stream));
+    } else {
+      std::memcpy(bytes, header, 16);
+      if (n) CK(cudaMemcpyAsync(bytes + 16, body, body_bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(c->hscratch);
+    CK(cudaMemcpyAsync(h, cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (h[1] != ~0ull) {
+      const int64_t i = static_cast<int64_t>(h[1] >> 2);
+      contract(false, (h[1] & 3) == 2 ? "activate: zero quaternion in splat " + std::to_string(i)
+                                      : "activate: non-finite parameter in splat " + std::to_string(i));
+    }
+    *saturated = static_cast<int64_t>(h[0]);
+    if (h[0]) std::fprintf(stderr, "gsct: warning: values saturated to the binary16 range\n");
+  });
+}
+
+int gsct_decompress_model(gsct_ctx c, const uint8_t* bytes, int64_t n_bytes, int location, gsct_cloud* out) {
+  return run(c, [&] {
+    contract(out != nullptr && n_bytes >= 0 && (bytes || n_bytes == 0), "decompress_model: null argument");
+    const std::string src = "compressed model";
+    uint8_t hdr[16] = {};
+    const size_t have = static_cast<size_t>(std::min<int64_t>(n_bytes, 16));
+    if (have) {
+      if (location == GSCT_DEVICE)
+        CK(cudaMemcpy(hdr, bytes, have, cudaMemcpyDeviceToHost));
+      else
+        std::memcpy(hdr, bytes, have);
+    }
+    // ByteReader (io.hpp:56-135) order: magic, version, count, then the size check
+    const auto need = [&](size_t off, size_t k, const char* what) {
+      if (static_cast<size_t>(n_bytes) < off + k)
+        parse_fail(src + ": truncated while reading " + what + ", need " + std::to_string(k) + " bytes, have " +
+                       std::to_string(static_cast<size_t>(n_bytes) - off),
+                   off);
+    };
+    need(0, 4, "compressed model header");
+    if (std::memcmp(hdr, "FGSC", 4) != 0)
+      parse_fail(src + ": bad magic for compressed model header, expected 'FGSC' got '" +
+                     std::string(reinterpret_cast<const char*>(hdr), 4) + "'",
+                 0);
+    need(4, 4, "format version");
+    uint32_t version = 0;
+    for (int k = 0; k < 4; ++k) version |= static_cast<uint32_t>(hdr[4 + k]) << (8 * k);
+    if (version != 1) parse_fail(src + ": unsupported version " + std::to_string(version), 4);
+    need(8, 8, "splat count");
+    uint64_t count = 0;
+    for (int k = 0; k < 8; ++k) count |= static_cast<uint64_t>(hdr[8 + k]) << (8 * k);
+    const size_t expected = 16 + 22 * static_cast<size_t>(count);
+    if (static_cast<size_t>(n_bytes) != expected)
+      parse_fail(src + ": file is " + std::to_string(n_bytes) + " bytes, header requires " + std::to_string(expected),
+                 static_cast<size_t>(n_bytes));
+    contract(out->n == static_cast<int64_t>(count), "decompress_model: output holds " + std::to_string(out->n) +
+                                                        " splats, the model " + std::to_string(count));
+    const int64_t n = static_cast<int64_t>(count);
+    if (n == 0) return;
+    contract(out->pos && out->log_scale && out->quat && out->raw_density, "decompress_model: null output array");
+    // std::log over the positive binary16 values (glibc, exact reference arithmetic), once
+    double* table = ws<double>(c, S_FGSC_LOG, kFgscHalfs);
+    if (!c->fgsc_table_ready) {
+      std::vector<double> t(kFgscHalfs, 0.0);
+      for (int hb = 1; hb < kFgscHalfs; ++hb) {
+        const int e = (hb >> 10) & 0x1f, m = hb & 0x3ff;
+        const double v = e == 0 ? std::ldexp(static_cast<double>(m), -24) : std::ldexp(static_cast<double>(1024 + m), e - 25);
+        t[static_cast<size_t>(hb)] = std::log(v);
+      }
+      CK(cudaMemcpy(table, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice));
+      c->fgsc_table_ready = true;
+    }
+    const uint16_t* body;
+    if (location == GSCT_DEVICE) {
+      contract((reinterpret_cast<uintptr_t>(bytes) & 1) == 0, "decompress_model: byte buffer must be 2-byte aligned");
+      body = reinterpret_cast<const uint16_t*>(bytes + 16);
+    } else {
+      uint16_t* b = ws<uint16_t>(c, S_FGSC, 11 * static_cast<size_t>(n));
+      CK(cudaMemcpyAsync(b, bytes + 16, 22 * static_cast<size_t>(n), cudaMemcpyHostToDevice, c->stream));
+      body = b;
+    }
+    const size_t un = static_cast<size_t>(n);
+    double *p, *l, *q, *r;
+    if (out->location == GSCT_DEVICE) {
+      p = const_cast<double*>(out->pos);
+      l = const_cast<double*>(out->log_scale);
+      q = const_cast<double*>(out->quat);
+      r = const_cast<double*>(out->raw_density);
+    } else {
+      p = ws<double>(c, S_POS, 3 * un);
+      l = ws<double>(c, S_LS, 3 * un);
+      q = ws<double>(c, S_Q, 4 * un);
+      r = ws<double>(c, S_RAW, un);
+    }
+    launch_fgsc_decode(body, n, table, p, l, q, r, c->stream);
+    CK(cudaGetLastError());
+    if (out->location == GSCT_HOST) {
+      CK(cudaMemcpyAsync(const_cast<double*>(out->pos), p, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(const_cast<double*>(out->log_scale), l, 3 * un * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream));
+      CK(cudaMemcpyAsync(const_cast<double*>(out->quat), q, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(const_cast<double*>(out->raw_density), r, un * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 

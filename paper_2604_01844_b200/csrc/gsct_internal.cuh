@@ -156,6 +156,11 @@ void launch_ctrl_write(const Cloud& c, const double* const* mv_in, const double*
                        const unsigned long long* draws, double log_1p6, double* pos, double* ls, double* q,
                        double* raw, double* const* mv_out, cudaStream_t st);
 
+// (codec.cu) FGSC body: 11 binary16 words per splat; counters = {saturated, error key}
+void launch_fgsc_encode(const Cloud& c, uint16_t* body, unsigned long long* counters, cudaStream_t st);
+void launch_fgsc_decode(const uint16_t* body, int64_t n, const double* log_table, double* pos, double* ls, double* q,
+                        double* raw, cudaStream_t st);
+
 // Launch accounting (gsct_ctx_launch_count).
 extern thread_local int64_t* g_launch_counter;
 inline void count_launch(int k = 1) {

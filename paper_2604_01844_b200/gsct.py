@@ -29,7 +29,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "libgsct_b200.so"
 if os.environ.get("GSCT_LIB_PATH"):  # A/B experiments with alternative builds (tools/)
     _LIB_PATH = Path(os.environ["GSCT_LIB_PATH"]).resolve()
 
-GSCT_OK, GSCT_ERR_CONTRACT, GSCT_ERR_CUDA, GSCT_ERR_OOM = 0, 1, 2, 3
+GSCT_OK, GSCT_ERR_CONTRACT, GSCT_ERR_CUDA, GSCT_ERR_OOM, GSCT_ERR_PARSE = 0, 1, 2, 3, 4
 # enum gsct_phase (include/gsct_cuda.h)
 PHASES = ("raster_setup", "raster_bin", "raster_fwd", "raster_bwd", "raster_tail",
           "voxel_setup", "voxel_bin", "voxel_fwd", "voxel_bwd", "voxel_tail")
@@ -38,6 +38,16 @@ GSCT_HOST, GSCT_DEVICE = 0, 1
 
 class GsctError(RuntimeError):
     """Base error (gsct::error)."""
+
+
+class ParseError(GsctError):
+    """gsct::parse_error (common.hpp:23-27); .offset = the byte offset in the message."""
+
+    @property
+    def offset(self) -> int:
+        import re
+        m = re.search(r"\(byte offset (\d+)\)$", str(self))
+        return int(m.group(1)) if m else -1
 
 
 class ContractError(GsctError):
@@ -167,6 +177,8 @@ _SIGS = {
     "gsct_adaptive_control": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_adam_state), _P(c_control_accum),
                                         _P(c_rng_state), _P(c_control_config), C.c_int64, _P(c_cloud),
                                         _P(c_adam_state), _P(c_control_accum), _P(c_adaptive_report)]),
+    "gsct_compress_model": (C.c_int, [C.c_void_p, _P(c_cloud), C.c_void_p, C.c_int, _P(C.c_int64)]),
+    "gsct_decompress_model": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, _P(c_cloud)]),
     "gsct_host_view_frame": (None, [_P(c_geometry), C.c_double, _P(C.c_double)]),
     "gsct_host_default_geometry": (None, [_P(C.c_int), C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                           _P(c_geometry), _P(C.c_double)]),
@@ -456,6 +468,8 @@ class Context:
             raise ContractError(msg)
         if status == GSCT_ERR_OOM:
             raise OutOfMemoryError(msg)
+        if status == GSCT_ERR_PARSE:
+            raise ParseError(msg)
         raise CudaError(msg)
 
     def set_stream(self, stream_ptr: int) -> None:
@@ -1152,3 +1166,56 @@ def adaptive_control(cloud: GaussianCloud, state: OptimState, config: ControlCon
               "accum_grad_dir", "accum_count"):
         setattr(state, k, getattr(nxt, k)[:m])
     return AdaptiveReport(int(rep.pruned), int(rep.cloned), int(rep.split))
+
+
+# ---------------------------------------------------------------------------------------
+# Compressed model codec (FGSC, 22 bytes per splat)
+# ---------------------------------------------------------------------------------------
+def compress_model(cloud: GaussianCloud, ctx: Optional[Context] = None):
+    """compress_model (io.hpp:323-385): (bytes, saturated). Host cloud -> numpy uint8 bytes;
+    device cloud -> torch uint8 CUDA tensor (16 + 22 N)."""
+    ctx = _ctx_for(cloud, ctx)
+    keep: list = []
+    cc = cloud._c(keep)
+    n = cloud.size()
+    sat = C.c_int64(0)
+    if cloud.on_device:
+        import torch
+        out = torch.empty(16 + 22 * n, dtype=torch.uint8, device=cloud.positions.device)
+        ctx.check(ctx._lib.gsct_compress_model(ctx.handle, C.byref(cc), C.c_void_p(out.data_ptr()), GSCT_DEVICE,
+                                               C.byref(sat)))
+    else:
+        out = np.empty(16 + 22 * n, dtype=np.uint8)
+        ctx.check(ctx._lib.gsct_compress_model(ctx.handle, C.byref(cc), C.c_void_p(out.ctypes.data), GSCT_HOST,
+                                               C.byref(sat)))
+    return out, int(sat.value)
+
+
+def decompress_model(data, ctx: Optional[Context] = None) -> GaussianCloud:
+    """decompress_model (io.hpp:387-419). numpy bytes -> host cloud; a torch uint8 CUDA
+    tensor -> device cloud. Header errors raise ParseError with the reference's messages."""
+    ctx = ctx or context(0)
+    if _is_torch(data):
+        import torch
+        nb = int(data.numel())
+        head = data[:16].cpu().numpy() if nb else np.zeros(0, dtype=np.uint8)
+        ptr, loc, dev = data.data_ptr(), GSCT_DEVICE, data.device
+    else:
+        data = np.ascontiguousarray(data, dtype=np.uint8)
+        nb = int(data.size)
+        head = data[:16]
+        ptr, loc, dev = (data.ctypes.data if nb else None), GSCT_HOST, None
+    count = int.from_bytes(bytes(head[8:16]), "little") if len(head) >= 16 else 0
+    n = count if nb == 16 + 22 * count else 0  # a size mismatch is reported by the call
+    if dev is not None:
+        import torch
+        f = lambda *s: torch.empty(s, dtype=torch.float64, device=dev)
+        cloud = GaussianCloud(f(n, 3), f(n, 3), f(n, 4), f(n))
+        arrs = [cloud.positions, cloud.log_scales, cloud.rotations, cloud.raw_densities]
+        co = c_cloud(count, *[a.data_ptr() for a in arrs], GSCT_DEVICE)
+    else:
+        cloud = GaussianCloud(np.empty((n, 3)), np.empty((n, 3)), np.empty((n, 4)), np.empty(n))
+        arrs = [cloud.positions, cloud.log_scales, cloud.rotations, cloud.raw_densities]
+        co = c_cloud(count, *[a.ctypes.data if a.size else None for a in arrs], GSCT_HOST)
+    ctx.check(ctx._lib.gsct_decompress_model(ctx.handle, C.c_void_p(ptr) if ptr else None, nb, loc, C.byref(co)))
+    return cloud
