@@ -255,6 +255,24 @@ Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl, cudaStream_t st, bool copy)
   return d;
 }
 
+// Device address of a page-locked, device-mapped host buffer (cudaHostAlloc'd / registered
+// memory under UVA, e.g. torch pinned tensors), else nullptr. Host outputs in such memory are
+// written by the kernels directly over PCIe ("zero-copy"): the transfer overlaps the kernel
+// instead of following it as a D2H copy.
+#ifndef GSCT_ZEROCOPY
+#define GSCT_ZEROCOPY 1
+#endif
+template <class T>
+T* mapped_host(T* host) {
+  if (!GSCT_ZEROCOPY || host == nullptr) return nullptr;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer ? static_cast<T*>(a.devicePointer) : nullptr;
+}
+
 void reset_stats(gsct_ctx c) {
   if (c->async) return;  // async: accumulate until gsct_ctx_synchronize
   DevStats z{0, 0, 0, 0, ~0ull};
@@ -576,7 +594,12 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (n_views)
       CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
     float* out = images;
-    if (images_location == GSCT_HOST && n_views) out = ws<float>(c, S_IMAGES, static_cast<size_t>(npx) * n_views);
+    float* zc_images = images_location == GSCT_HOST && n > 0 ? mapped_host(images) : nullptr;
+    if (zc_images)
+      out = zc_images;  // the forward kernel stores straight into the pinned host images
+    else if (images_location == GSCT_HOST && n_views)
+      out = ws<float>(c, S_IMAGES, static_cast<size_t>(npx) * n_views);
+    const bool stage_images = images_location == GSCT_HOST && !zc_images;
     const Geo g = make_geo(geom);
     const RSet r = make_rs(rs);
     c->saved_valid = false;
@@ -633,9 +656,16 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
 #ifndef GSCT_FWD_SPLIT
 #define GSCT_FWD_SPLIT 2  // host-output forward launched in this many view sub-ranges (A/B: 1 -> +1.74 ms, 2 -> +1.50, 4 -> +2.28)
 #endif
-      const int sub = images_location == GSCT_HOST ? std::max(1, (cv + GSCT_FWD_SPLIT - 1) / GSCT_FWD_SPLIT) : cv;
-      for (int vs = 0; vs < cv; vs += sub) {
-        const int nvs = std::min(sub, cv - vs);
+#ifndef GSCT_FWD_MINPIECE
+#define GSCT_FWD_MINPIECE 0  // > 0: halving sub-ranges (38, 19, 9, ...) down to this many views
+#endif
+      const int sub = stage_images ? std::max(1, (cv + GSCT_FWD_SPLIT - 1) / GSCT_FWD_SPLIT) : cv;
+      for (int vs = 0, nvs = 0; vs < cv; vs += nvs) {
+        const int rem = cv - vs;
+        if (stage_images && GSCT_FWD_MINPIECE > 0)
+          nvs = rem <= 2 * GSCT_FWD_MINPIECE ? rem : (rem + 1) / 2;
+        else
+          nvs = std::min(sub, rem);
         {
           Phase ph(c, GSCT_PH_RASTER_FWD);
           launch_raster_fwd_super(rec + static_cast<int64_t>(vs) * n, vals, start + static_cast<int64_t>(vs) * stride,
@@ -643,14 +673,14 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
                                   tiles_v, stride, img + static_cast<int64_t>(vs) * npx, c->stream);
         }
         CK(cudaGetLastError());
-        if (images_location == GSCT_HOST) {
+        if (stage_images) {
           stream_after(c, c->copy_stream, c->stream);
           CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0 + vs) * npx, img + static_cast<int64_t>(vs) * npx,
                              static_cast<size_t>(npx) * nvs * sizeof(float), cudaMemcpyDeviceToHost, c->copy_stream));
         }
       }
     }
-    if (images_location == GSCT_HOST && n_views) stream_after(c, c->stream, c->copy_stream);
+    if (stage_images && n_views) stream_after(c, c->stream, c->copy_stream);
     finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
     if (saved) {
       c->saved_key = raster_call_key(cloud, geom, angles, n_views, rs);
@@ -684,7 +714,23 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     const int64_t npx = static_cast<int64_t>(geom->n_u) * geom->n_v;
     double *gp = out->pos, *gl = out->log_scale, *gq = out->quat, *gr = out->raw_density, *gn = out->pos_grad_norm;
     uint8_t* gv = out->visible;
-    if (out->location == GSCT_HOST) {
+    // host gradients in mapped pinned memory: the tail / finalize kernels store into them
+    // directly (no trailing D2H); otherwise staged in the workspace and copied down
+#ifndef GSCT_ZEROCOPY_GRADS
+#define GSCT_ZEROCOPY_GRADS 0  // A/B C2 e2e: the strided per-splat stores of the tail / finalize
+                               // over PCIe cost +1.9 ms vs a 0.4 ms staged D2H
+#endif
+    bool zc_grads = false;
+    if (GSCT_ZEROCOPY_GRADS && out->location == GSCT_HOST && n > 0 && n_views > 0) {
+      double *mp = mapped_host(out->pos), *ml = mapped_host(out->log_scale), *mq = mapped_host(out->quat),
+             *mr = mapped_host(out->raw_density), *mn = mapped_host(out->pos_grad_norm);
+      uint8_t* mv = mapped_host(out->visible);
+      if (mp && ml && mq && mr && mn && mv) {
+        gp = mp, gl = ml, gq = mq, gr = mr, gn = mn, gv = mv;
+        zc_grads = true;
+      }
+    }
+    if (out->location == GSCT_HOST && !zc_grads) {
       gp = ws<double>(c, S_GPOS, 3 * un);
       gl = ws<double>(c, S_GLS, 3 * un);
       gq = ws<double>(c, S_GQ, 4 * un);
@@ -794,7 +840,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));  // also when n_views == 0
       c->event_pool.push_back(cloud_up);
     }
-    if (out->location == GSCT_HOST && n > 0) {
+    if (out->location == GSCT_HOST && n > 0 && !zc_grads) {
       CK(cudaMemcpyAsync(out->pos, gp, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaMemcpyAsync(out->log_scale, gl, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaMemcpyAsync(out->quat, gq, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));

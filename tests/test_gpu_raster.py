@@ -256,6 +256,38 @@ def test_device_resident_matches_host(ctx):
         assert np.array_equal(getattr(gd, k).cpu().numpy(), getattr(gh, k)), k
 
 
+def test_pinned_host_buffers_zero_copy(ctx):
+    """Pinned (device-mapped) host images / gradients are written by the kernels directly
+    (zero-copy); results are bit-identical to the device-resident and pageable paths, with
+    and without save-for-backward, and for a view count that spans several chunks."""
+    import torch
+
+    geom = cone_geometry(64, 0.5, np.linspace(0, 2 * np.pi, 7, endpoint=False))
+    cloud = gsct.make_cloud("random", 300, seed=12, pos_range=8.0)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    pcloud = gsct.GaussianCloud(pin(cloud.positions), pin(cloud.log_scales), pin(cloud.rotations),
+                                pin(cloud.raw_densities))
+    dev = gsct.rasterize_views(cloud.to_device(0), geom, None, ctx=ctx).cpu().numpy()
+    img = torch.full((7, 64, 64), np.nan, dtype=torch.float32).pin_memory().numpy()
+    gsct.rasterize_views(pcloud, geom, None, out=img, ctx=ctx)
+    assert np.array_equal(img, dev)
+    gi = pin(np.random.default_rng(5).uniform(-1, 1, size=img.shape).astype(np.float32))
+    pageable = gsct.rasterize_backward_views(cloud, geom, None, np.array(gi), ctx=ctx)
+    n = cloud.size()
+    z = lambda *s: torch.full(s, np.nan, dtype=torch.float64).pin_memory().numpy()
+    for sfb in (False, True):
+        gh = gsct.ParamGradients(z(n, 3), z(n, 3), z(n, 4), z(n), z(n),
+                                 torch.full((n,), 7, dtype=torch.uint8).pin_memory().numpy())
+        try:
+            ctx.set_save_for_backward(sfb)
+            gsct.rasterize_views(pcloud, geom, None, out=img, ctx=ctx)
+            gsct.rasterize_backward_views(pcloud, geom, None, gi, out=gh, ctx=ctx)
+        finally:
+            ctx.set_save_for_backward(False)
+        for k in ("positions", "log_scales", "rotations", "raw_densities", "pos_grad_norm", "visible"):
+            assert np.array_equal(getattr(gh, k), getattr(pageable, k)), (sfb, k)
+
+
 def test_save_for_backward_is_exact(ctx):
     """Reusing the forward's set-up gives bit-identical gradients; a call that does not match
     the saved forward (other views) recomputes."""

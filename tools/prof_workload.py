@@ -28,6 +28,39 @@ def main() -> None:
     ctx = gsct.context(0)
     ctx.set_async(True)
     ctx.set_profiling(True)
+    if what == "e2e":  # C-ABI host-buffer fwd / fwd+bwd wall times (sync calls), ms
+        import time
+
+        import numpy as np
+        cloud, geom = bench.make_workload(cfg)
+        n, nv = cloud.size(), len(geom.angles)
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        hc = gsct.GaussianCloud(pin(cloud.positions), pin(cloud.log_scales), pin(cloud.rotations),
+                                pin(cloud.raw_densities))
+        img = torch.empty((nv, geom.n_v, geom.n_u), dtype=torch.float32).pin_memory().numpy()
+        gi = torch.ones((nv, geom.n_v, geom.n_u), dtype=torch.float32).pin_memory().numpy()
+        z = lambda *s: torch.zeros(s, dtype=torch.float64).pin_memory().numpy()
+        gh = gsct.ParamGradients(z(n, 3), z(n, 3), z(n, 4), z(n), z(n),
+                                 torch.zeros(n, dtype=torch.uint8).pin_memory().numpy())
+        ctx.set_async(False)
+        ctx.set_profiling(False)
+        ctx.set_save_for_backward(True)
+        rs = gsct.RasterSettings()
+
+        def med(fn, k=int(reps) * 3):
+            fn()
+            ts = []
+            for _ in range(k):
+                t0 = time.perf_counter()
+                fn()
+                ts.append((time.perf_counter() - t0) * 1e3)
+            return round(float(np.median(ts)), 3)
+
+        fwd = med(lambda: gsct.rasterize_views(hc, geom, None, rs, out=img, ctx=ctx))
+        both = med(lambda: (gsct.rasterize_views(hc, geom, None, rs, out=img, ctx=ctx),
+                            gsct.rasterize_backward_views(hc, geom, None, gi, rs, out=gh, ctx=ctx)))
+        print(json.dumps({"fwd_host_ms": fwd, "fwdbwd_host_ms": both, "proj_per_s": round(nv / both * 1e3, 1)}))
+        return
     if what == "raster":
         cloud, geom = bench.make_workload(cfg)
         step = bench.DeviceStep(ctx, cloud, geom, list(range(len(geom.angles))), 1)
