@@ -830,17 +830,45 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       CK(cudaGetLastError());
     }
+#ifndef GSCT_TAIL_PIECES
+#define GSCT_TAIL_PIECES 4  // staged host gradients: tail + finalize in splat ranges, each range's
+                            // D2H overlapping the next range's tail
+#endif
+    const bool stage_grads = out->location == GSCT_HOST && n > 0 && !zc_grads;
+    const int pieces = stage_grads && n_views > 0 && n >= 4096 ? GSCT_TAIL_PIECES : 1;
+    bool grads_down = false;
     if (n > 0 && n_views > 0) {
       Phase ph(c, GSCT_PH_RASTER_TAIL);
-      launch_raster_tail(pre_aos, n, dframes, n_views, g, r, mom, acc, gv, c->stream);
       if (cloud_up) CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));
-      launch_raster_finalize(d, acc, gp, gl, gq, gr, gn, c->stream);
+      for (int k = 0; k < pieces; ++k) {
+        const int64_t i0 = n * k / pieces, i1 = n * (k + 1) / pieces;
+        launch_raster_tail(pre_aos, n, i0, i1, dframes, n_views, g, r, mom, acc, gv, c->stream);
+        launch_raster_finalize(d, i0, i1, acc, gp, gl, gq, gr, gn, c->stream);
+        if (pieces > 1) {
+          const size_t a = static_cast<size_t>(i0), m = static_cast<size_t>(i1 - i0);
+          stream_after(c, c->copy_stream, c->stream);
+          CK(cudaMemcpyAsync(out->pos + 3 * a, gp + 3 * a, 3 * m * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->copy_stream));
+          CK(cudaMemcpyAsync(out->log_scale + 3 * a, gl + 3 * a, 3 * m * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->copy_stream));
+          CK(cudaMemcpyAsync(out->quat + 4 * a, gq + 4 * a, 4 * m * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->copy_stream));
+          CK(cudaMemcpyAsync(out->raw_density + a, gr + a, m * sizeof(double), cudaMemcpyDeviceToHost, c->copy_stream));
+          CK(cudaMemcpyAsync(out->pos_grad_norm + a, gn + a, m * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->copy_stream));
+          CK(cudaMemcpyAsync(out->visible + a, gv + a, m, cudaMemcpyDeviceToHost, c->copy_stream));
+        }
+      }
+      if (pieces > 1) {
+        stream_after(c, c->stream, c->copy_stream);
+        grads_down = true;
+      }
     }
     if (cloud_up) {
       CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));  // also when n_views == 0
       c->event_pool.push_back(cloud_up);
     }
-    if (out->location == GSCT_HOST && n > 0 && !zc_grads) {
+    if (stage_grads && !grads_down) {
       CK(cudaMemcpyAsync(out->pos, gp, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaMemcpyAsync(out->log_scale, gl, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaMemcpyAsync(out->quat, gq, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));

@@ -67,11 +67,11 @@ void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frame
 // (tail.cu) acc: fp64 [11][N] view sum (g_pos 3, g_sigma 6, g_raw, sum |dL/dmean2d|);
 // moments: view-major [n_views][N] x 8 fp32 {t, t du, t dv, t du^2, t du dv, t dv^2,
 // visible, 0} covering every view of the call
-void launch_raster_tail(const PreSplat* pre_aos, int64_t n, const Frame* frames_dev, int n_views,
-                        const Geo& g, const RSet& rs, const float* moments, double* acc,
-                        uint8_t* visible, cudaStream_t st);
-void launch_raster_finalize(const Cloud& c, const double* acc, double* g_pos, double* g_ls,
-                            double* g_q, double* g_raw, double* g_pgn, cudaStream_t st);
+void launch_raster_tail(const PreSplat* pre_aos, int64_t n, int64_t i0, int64_t i1, const Frame* frames_dev,
+                        int n_views, const Geo& g, const RSet& rs, const float* moments, double* acc,
+                        uint8_t* visible, cudaStream_t st);  // splats [i0, i1)
+void launch_raster_finalize(const Cloud& c, int64_t i0, int64_t i1, const double* acc, double* g_pos,
+                            double* g_ls, double* g_q, double* g_raw, double* g_pgn, cudaStream_t st);
 void launch_debug_project(const PreSplat* pre, int64_t n, const Frame* frame_dev, const Geo& g,
                           const RSet& rs, int32_t* rect, uint8_t* flags, double* mean2d,
                           double* conic, double* amplitude, cudaStream_t st);

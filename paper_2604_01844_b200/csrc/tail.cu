@@ -41,6 +41,7 @@ static_assert(sizeof(PreSplat) % sizeof(double) == 0, "PreSplat: whole doubles")
 #define GSCT_TAIL_MINB 4  // 128 registers
 #endif
 __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSplat* __restrict__ pre /* AoS */, int64_t n,
+                                                     int64_t i0, int64_t i1,
                                                      const Frame* __restrict__ frames_g, int n_views,
                                                      Geo g, RSet rs, const float4* __restrict__ moments,
                                                      int frames_in_smem, double* __restrict__ acc,
@@ -55,8 +56,8 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
   // splats per warp access: conflict-free banks), instead of 8 L1 lines per field load
   __shared__ PaddedPre s_pre[32];
   {
-    const int64_t first = static_cast<int64_t>(blockIdx.x) * 32;
-    const int cnt = n - first < 32 ? static_cast<int>(n - first) : 32;
+    const int64_t first = i0 + static_cast<int64_t>(blockIdx.x) * 32;
+    const int cnt = i1 - first < 32 ? static_cast<int>(i1 - first) : 32;
     const double* src = reinterpret_cast<const double*>(pre + first);
     constexpr int kD = sizeof(PreSplat) / sizeof(double);
     for (int k = threadIdx.x; k < cnt * kD; k += blockDim.x)
@@ -66,8 +67,8 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
   __syncthreads();
   const auto frame = [&](int vw) -> const Frame& { return frames_in_smem ? s_frames[vw].f : frames_g[vw]; };
   const int q = threadIdx.x & 3;
-  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 2;
-  const bool live = i < n;
+  const int64_t i = i0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 2);
+  const bool live = i < i1;
   double v[11];
 #pragma unroll
   for (int k = 0; k < 11; ++k) v[k] = 0.0;
@@ -131,12 +132,13 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
 }
 
 // Per-splat finalize: covariance_backward (core.hpp:170-191) of the summed dL/dSigma.
-__global__ void __launch_bounds__(128) k_raster_finalize(Cloud c, const double* __restrict__ acc,
+__global__ void __launch_bounds__(128) k_raster_finalize(Cloud c, int64_t i0, int64_t i1,
+                                                         const double* __restrict__ acc,
                                                          double* __restrict__ g_pos, double* __restrict__ g_ls,
                                                          double* __restrict__ g_q, double* __restrict__ g_raw,
                                                          double* __restrict__ g_pgn) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= c.n) return;
+  const int64_t i = i0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= i1) return;
   const int64_t n = c.n;
   double gl[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0};
   Act a;
@@ -161,20 +163,22 @@ inline unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n +
 
 }  // namespace
 
-void launch_raster_tail(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views, const Geo& g,
-                        const RSet& rs, const float* moments, double* acc, uint8_t* visible, cudaStream_t st) {
-  if (n == 0) return;
+void launch_raster_tail(const PreSplat* pre, int64_t n, int64_t i0, int64_t i1, const Frame* frames_dev,
+                        int n_views, const Geo& g, const RSet& rs, const float* moments, double* acc,
+                        uint8_t* visible, cudaStream_t st) {
+  if (i1 <= i0) return;
   const size_t smem = static_cast<size_t>(n_views) * sizeof(PaddedFrame);
   const bool in_smem = smem <= 24 * 1024;
-  k_raster_tail<<<blocks_for(n * 4, 128), 128, in_smem ? smem : 0, st>>>(
-      pre, n, frames_dev, n_views, g, rs, reinterpret_cast<const float4*>(moments), in_smem ? 1 : 0, acc, visible);
+  k_raster_tail<<<blocks_for((i1 - i0) * 4, 128), 128, in_smem ? smem : 0, st>>>(
+      pre, n, i0, i1, frames_dev, n_views, g, rs, reinterpret_cast<const float4*>(moments), in_smem ? 1 : 0, acc,
+      visible);
   count_launch();
 }
 
-void launch_raster_finalize(const Cloud& c, const double* acc, double* g_pos, double* g_ls, double* g_q,
-                            double* g_raw, double* g_pgn, cudaStream_t st) {
-  if (c.n == 0) return;
-  k_raster_finalize<<<blocks_for(c.n, 128), 128, 0, st>>>(c, acc, g_pos, g_ls, g_q, g_raw, g_pgn);
+void launch_raster_finalize(const Cloud& c, int64_t i0, int64_t i1, const double* acc, double* g_pos, double* g_ls,
+                            double* g_q, double* g_raw, double* g_pgn, cudaStream_t st) {
+  if (i1 <= i0) return;
+  k_raster_finalize<<<blocks_for(i1 - i0, 128), 128, 0, st>>>(c, i0, i1, acc, g_pos, g_ls, g_q, g_raw, g_pgn);
   count_launch();
 }
 

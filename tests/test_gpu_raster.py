@@ -256,14 +256,16 @@ def test_device_resident_matches_host(ctx):
         assert np.array_equal(getattr(gd, k).cpu().numpy(), getattr(gh, k)), k
 
 
-def test_pinned_host_buffers_zero_copy(ctx):
-    """Pinned (device-mapped) host images / gradients are written by the kernels directly
-    (zero-copy); results are bit-identical to the device-resident and pageable paths, with
-    and without save-for-backward, and for a view count that spans several chunks."""
+@pytest.mark.parametrize("n", [300, 5000])
+def test_pinned_host_buffers_zero_copy(ctx, n):
+    """Pinned (device-mapped) host images are written by the forward kernel directly
+    (zero-copy); host gradients of >= 4096 splats come down in splat-range pieces behind the
+    tail. Results are bit-identical to the device-resident and pageable paths, with and
+    without save-for-backward."""
     import torch
 
     geom = cone_geometry(64, 0.5, np.linspace(0, 2 * np.pi, 7, endpoint=False))
-    cloud = gsct.make_cloud("random", 300, seed=12, pos_range=8.0)
+    cloud = gsct.make_cloud("random", n, seed=12, pos_range=8.0)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
     pcloud = gsct.GaussianCloud(pin(cloud.positions), pin(cloud.log_scales), pin(cloud.rotations),
                                 pin(cloud.raw_densities))
@@ -273,7 +275,10 @@ def test_pinned_host_buffers_zero_copy(ctx):
     assert np.array_equal(img, dev)
     gi = pin(np.random.default_rng(5).uniform(-1, 1, size=img.shape).astype(np.float32))
     pageable = gsct.rasterize_backward_views(cloud, geom, None, np.array(gi), ctx=ctx)
-    n = cloud.size()
+    dgrad = gsct.rasterize_backward_views(cloud.to_device(0), geom, None, torch.from_numpy(np.array(gi)).cuda(),
+                                          ctx=ctx)
+    for k in ("positions", "log_scales", "rotations", "raw_densities", "pos_grad_norm", "visible"):
+        assert np.array_equal(getattr(dgrad, k).cpu().numpy(), getattr(pageable, k)), k
     z = lambda *s: torch.full(s, np.nan, dtype=torch.float64).pin_memory().numpy()
     for sfb in (False, True):
         gh = gsct.ParamGradients(z(n, 3), z(n, 3), z(n, 4), z(n), z(n),
