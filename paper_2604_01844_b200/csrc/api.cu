@@ -582,7 +582,34 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     contract(images != nullptr || n_views == 0, "rasterize: null image buffer");
     if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
     reset_stats(c);
-    const Cloud d = upload_cloud(c, cloud);
+#ifndef GSCT_CLOUD_PIECES
+#define GSCT_CLOUD_PIECES 4  // host cloud uploaded in splat ranges, each range's set-up starting
+                             // as soon as its bytes are in (single view chunk only)
+#endif
+    const int64_t n_in = cloud ? cloud->n : 0;
+    const int cloud_pieces = cloud && cloud->location == GSCT_HOST && n_in >= 16384 && n_views > 0 &&
+                                     views_per_chunk(n_in, n_views, 0) >= n_views
+                                 ? GSCT_CLOUD_PIECES
+                                 : 1;
+    const Cloud d = upload_cloud(c, cloud, c->stream, cloud_pieces == 1);
+    std::vector<cudaEvent_t> piece_up;
+    if (cloud_pieces > 1) {
+      stream_after(c, c->copy_stream, c->stream);  // after the (re)allocation and prior readers
+      for (int k = 0; k < cloud_pieces; ++k) {
+        const size_t a = static_cast<size_t>(n_in * k / cloud_pieces), b = static_cast<size_t>(n_in * (k + 1) / cloud_pieces);
+        const size_t m = b - a;
+        CK(cudaMemcpyAsync(const_cast<double*>(d.pos) + 3 * a, cloud->pos + 3 * a, 3 * m * sizeof(double),
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaMemcpyAsync(const_cast<double*>(d.ls) + 3 * a, cloud->log_scale + 3 * a, 3 * m * sizeof(double),
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaMemcpyAsync(const_cast<double*>(d.q) + 4 * a, cloud->quat + 4 * a, 4 * m * sizeof(double),
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaMemcpyAsync(const_cast<double*>(d.raw) + a, cloud->raw_density + a, m * sizeof(double),
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        piece_up.push_back(pooled_event(c));
+        CK(cudaEventRecord(piece_up.back(), c->copy_stream));
+      }
+    }
     const int64_t n = d.n;
     const int64_t npx = static_cast<int64_t>(geom->n_u) * geom->n_v;
     // binned at 32x32 super-tiles (kBinTile); RenderStats::tile_pairs stays at rs->tile_size
@@ -605,7 +632,7 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     c->saved_valid = false;
     PreSplat* pre = ws<PreSplat>(c, S_PRE, static_cast<size_t>(n) + 1);
     PreSplat* pre_aos = ws<PreSplat>(c, S_PRE_AOS, static_cast<size_t>(n) + 1);
-    if (n > 0) {
+    if (n > 0 && cloud_pieces == 1) {
       Phase ph(c, GSCT_PH_RASTER_SETUP);
       launch_splat_prepare(d, pre, pre_aos, c->dstats, c->stream);
     }
@@ -628,7 +655,19 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * cv);
       {
         Phase ph(c, GSCT_PH_RASTER_SETUP);
-        launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream);
+        if (cloud_pieces > 1) {  // one view chunk: per splat range, wait for its bytes, set up
+          for (int k = 0; k < cloud_pieces; ++k) {
+            const int64_t i0 = n * k / cloud_pieces, i1 = n * (k + 1) / cloud_pieces;
+            CK(cudaStreamWaitEvent(c->stream, piece_up[static_cast<size_t>(k)], 0));
+            launch_splat_prepare(d, pre, pre_aos, c->dstats, c->stream, i0, i1);
+            launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream, i0,
+                                     i1);
+          }
+          for (cudaEvent_t e : piece_up) c->event_pool.push_back(e);
+          piece_up.clear();
+        } else {
+          launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream);
+        }
       }
       CK(cudaGetLastError());
       uint32_t *keys, *vals, *start, *end;

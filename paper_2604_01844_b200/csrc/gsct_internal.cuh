@@ -60,10 +60,12 @@ struct Window {
 
 // ---- launch wrappers (defined in preprocess.cu / raster.cu / voxel.cu) ----
 // pre: structure-of-arrays set-up (pre_store/pre_load); pre_aos: the same, array-of-structs
-void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevStats* stats, cudaStream_t st);
+void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevStats* stats, cudaStream_t st,
+                          int64_t i0 = 0, int64_t i1 = -1);  // splats [i0, i1), -1 = n
 void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
                               const Geo& g, const RSet& rs, int bin_ts, RasterRec* rec,
-                              uint32_t* tile_count, DevStats* stats, cudaStream_t st);
+                              uint32_t* tile_count, DevStats* stats, cudaStream_t st, int64_t i0 = 0,
+                              int64_t i1 = -1);
 // (tail.cu) acc: fp64 [11][N] view sum (g_pos 3, g_sigma 6, g_raw, sum |dL/dmean2d|);
 // moments: view-major [n_views][N] x 8 fp32 {t, t du, t dv, t du^2, t du dv, t dv^2,
 // visible, 0} covering every view of the call

@@ -37,11 +37,11 @@ __device__ __forceinline__ RasterRec empty_rec() {
 // Writes the set-up twice: structure-of-arrays for the per-(view, splat) set-up kernel
 // (coalesced field loads) and array-of-structs for the backward tail (lazy L1 re-reads
 // keep its register pressure down).
-__global__ void __launch_bounds__(128) k_splat_prepare(Cloud c, PreSplat* __restrict__ pre,
+__global__ void __launch_bounds__(128) k_splat_prepare(Cloud c, int64_t i0, int64_t i1, PreSplat* __restrict__ pre,
                                                        PreSplat* __restrict__ pre_aos,
                                                        DevStats* __restrict__ st) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= c.n) return;
+  const int64_t i = i0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= i1) return;
   PreSplat s;
   prepare_splat(c.pos, c.ls, c.q, c.raw, i, s);
   if (s.status) flag_error(st, i, s.status);
@@ -61,18 +61,18 @@ __global__ void __launch_bounds__(128) k_splat_prepare(Cloud c, PreSplat* __rest
 #endif
 constexpr int kPreViews = GSCT_PRE_VIEWS;
 __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const PreSplat* __restrict__ pre, int64_t n,
-                                                           int n_views, const Frame* __restrict__ frames, Geo g,
+                                                           int64_t i0, int64_t i1, int n_views, const Frame* __restrict__ frames, Geo g,
                                                            RSet rs, int bin_ts,
                                                            RasterRec* __restrict__ rec,
                                                            uint32_t* __restrict__ tile_count,
                                                            DevStats* __restrict__ st) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = i0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   unsigned long long n_culled = 0, n_degen = 0, n_tp = 0, n_pp = 0;
   PreSplat s;
-  if (i < n) pre_load(pre, n, i, s);  // once per thread, reused for its kPreViews views
+  if (i < i1) pre_load(pre, n, i, s);  // once per thread, reused for its kPreViews views
   for (int vg = 0; vg < kPreViews; ++vg) {
   const int v = blockIdx.y * kPreViews + vg;
-  if (i < n && v < n_views) {
+  if (i < i1 && v < n_views) {
     RasterRec r = empty_rec();
     uint32_t cnt = 0;
     if (s.status == 0) {
@@ -281,18 +281,22 @@ inline unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n +
 
 }  // namespace
 
-void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevStats* stats, cudaStream_t st) {
-  if (c.n == 0) return;
-  k_splat_prepare<<<blocks_for(c.n, 128), 128, 0, st>>>(c, pre, pre_aos, stats);
+void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevStats* stats, cudaStream_t st,
+                          int64_t i0, int64_t i1) {
+  if (i1 < 0) i1 = c.n;
+  if (i1 <= i0) return;
+  k_splat_prepare<<<blocks_for(i1 - i0, 128), 128, 0, st>>>(c, i0, i1, pre, pre_aos, stats);
   count_launch();
 }
 
 void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views, const Geo& g,
                               const RSet& rs, int bin_ts, RasterRec* rec, uint32_t* tile_count,
-                              DevStats* stats, cudaStream_t st) {
-  if (n == 0 || n_views == 0) return;
-  dim3 grid(blocks_for(n, 128), static_cast<unsigned>((n_views + kPreViews - 1) / kPreViews));
-  k_raster_preprocess<<<grid, 128, 0, st>>>(pre, n, n_views, frames_dev, g, rs, bin_ts, rec, tile_count, stats);
+                              DevStats* stats, cudaStream_t st, int64_t i0, int64_t i1) {
+  if (i1 < 0) i1 = n;
+  if (i1 <= i0 || n_views == 0) return;
+  dim3 grid(blocks_for(i1 - i0, 128), static_cast<unsigned>((n_views + kPreViews - 1) / kPreViews));
+  k_raster_preprocess<<<grid, 128, 0, st>>>(pre, n, i0, i1, n_views, frames_dev, g, rs, bin_ts, rec, tile_count,
+                                            stats);
   count_launch();
 }
 

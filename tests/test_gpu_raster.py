@@ -256,11 +256,12 @@ def test_device_resident_matches_host(ctx):
         assert np.array_equal(getattr(gd, k).cpu().numpy(), getattr(gh, k)), k
 
 
-@pytest.mark.parametrize("n", [300, 5000])
+@pytest.mark.parametrize("n", [300, 5000, 20000])
 def test_pinned_host_buffers_zero_copy(ctx, n):
     """Pinned (device-mapped) host images are written by the forward kernel directly
     (zero-copy); host gradients of >= 4096 splats come down in splat-range pieces behind the
-    tail. Results are bit-identical to the device-resident and pageable paths, with and
+    tail; a host cloud of >= 16384 splats goes up in pieces, each piece's set-up starting
+    behind its bytes. Results are bit-identical to the device-resident and pageable paths, with and
     without save-for-backward."""
     import torch
 
