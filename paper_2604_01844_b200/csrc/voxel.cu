@@ -124,9 +124,9 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
   const float fy = static_cast<float>(2 * yp) * sp;
   const uint32_t b = start[brick], e = end[brick];
   StagedVox* sw = s_rec[warp];
-  float acc[2][2][8];  // [z][y][x]
+  float2 acc[2][8];  // [z][x] {y row 0, y row 1}
 #pragma unroll
-  for (int k = 0; k < 8; ++k) acc[0][0][k] = acc[0][1][k] = acc[1][0][k] = acc[1][1][k] = 0.f;
+  for (int k = 0; k < 8; ++k) acc[0][k] = acc[1][k] = make_float2(0.f, 0.f);
   for (uint32_t base = b; base < e; base += 32) {
     const int cnt = min(32u, e - base);
     uint32_t lanes_rel = 0u;
@@ -198,6 +198,16 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
       const float dy0 = p.y + fy, dx0 = p.x;
       const f2_t DY = f2_pack(dy0, dy0 + sp);
       const bool direct = rr4.w == 0.f || m.z == static_cast<uint32_t>(lane);
+      // the exponent / chain arithmetic stays in inline-asm packed ops (never contracted, so a
+      // voxel's value does not depend on which lane or unrolled z step computes it: z-slab
+      // windows stay bit-identical); only the accumulation uses the __fadd2_rn builtin, which
+      // ptxas predicates in place per x bit (a C-level `if` around an asm add left a
+      // temporary + predicated MOV pairs)
+      const auto accum = [&](float2& a, f2_t g) {
+        float lo, hi;
+        f2_unpack(g, lo, hi);
+        a = __fadd2_rn(a, make_float2(lo, hi));
+      };
 #pragma unroll
       for (int zz = 0; zz < 2; ++zz) {
         if (!((m.x >> (16 + 2 * zp + zz)) & 1u)) continue;
@@ -205,20 +215,20 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
         // e(dx) = Q00 dx^2 + L dx + K,  L = Q01 dy + Q02 dz,  K = Q11 dy^2 + Q12 dy dz + Q22 dz^2
         const f2_t L = f2_fma(f2_bc(q.w), DY, f2_bc(rr4.x * dz));
         const f2_t K = f2_fma(DY, f2_fma(f2_bc(q.y), DY, f2_bc(rr4.y * dz)), f2_bc(q.z * dz * dz));
-        f2_t g[8];
         if (!direct) {
           const f2_t E0 = f2_fma(L, f2_bc(dx0), f2_add(K, f2_bc(q.x * dx0 * dx0)));
           const f2_t D0 = f2_fma(L, f2_bc(sp), f2_bc(q.x * fmaf(2.f * dx0, sp, sp * sp)));
           float e0, e1, d0, d1;
           f2_unpack(E0, e0, e1);
           f2_unpack(D0, d0, d1);
-          g[0] = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
+          f2_t g = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
           f2_t ratio = f2_pack(ex2_approx(d0), ex2_approx(d1));
           const f2_t C2 = f2_bc(rr4.z);
 #pragma unroll
-          for (int k = 1; k < 8; ++k) {
-            g[k] = f2_mul(g[k - 1], ratio);
-            if (k < 7) ratio = f2_mul(ratio, C2);
+          for (int k = 0; k < 8; ++k) {
+            if (xm & (1u << k)) accum(acc[zz][k], g);
+            if (k < 7) g = f2_mul(g, ratio);
+            if (k < 6) ratio = f2_mul(ratio, C2);
           }
         } else {
 #pragma unroll
@@ -227,16 +237,8 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
             const f2_t ek = f2_fma(f2_add(f2_bc(q.x * dx), L), f2_bc(dx), K);
             float e0, e1;
             f2_unpack(ek, e0, e1);
-            g[k] = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          float glo, ghi;
-          f2_unpack(g[k], glo, ghi);
-          if (xm & (1u << k)) {
-            acc[zz][0][k] += glo;
-            acc[zz][1][k] += ghi;
+            const f2_t g = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), RHO);
+            if (xm & (1u << k)) accum(acc[zz][k], g);
           }
         }
       }
@@ -253,7 +255,9 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
     for (int h = 0; h < 2; ++h) {
       const int y = gy0 + 2 * yp + h;
       if (y >= win.hi[1]) continue;
-      const float* v = acc[zz][h];
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = h ? acc[zz][k].y : acc[zz][k].x;
       float* row = volume + (static_cast<int64_t>(z - win.lo[2]) * wy + (y - win.lo[1])) * wx;
       if ((wx & 3) == 0 && x0 + 8 <= wx) {
         reinterpret_cast<float4*>(row + x0)[0] = make_float4(v[0], v[1], v[2], v[3]);

@@ -1,4 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_raster.py tests/test_gpu_fullsize.py tests/test_dropin.py -q -x 2>&1 | tail -2
-timeout 600 python tools/ab_variants.py run e2e c2 3
-timeout 600 python tools/ab_variants.py run e2e c2 3
-timeout 600 python tools/ab_variants.py run e2e c5 1
+timeout 900 python -m pytest tests/test_gpu_voxel.py tests/test_gpu_fullsize.py tests/test_golden.py -q -x 2>&1 | tail -2
