@@ -131,3 +131,13 @@ def test_compress_contract(ctx):
     c.rotations[7] = 0.0
     with pytest.raises(gsct.ContractError, match="zero quaternion in splat 7"):
         gsct.compress_model(c, ctx=ctx)
+
+
+@pytest.mark.gpu
+def test_empty_model_roundtrip(ref, ctx):
+    """test_io.cpp:152-161: an empty cloud is exactly the 16-byte header."""
+    b, sat = gsct.compress_model(gsct.GaussianCloud.empty(), ctx=ctx)
+    want, _ = ref.compress_model({"pos": np.zeros((0, 3)), "ls": np.zeros((0, 3)), "q": np.zeros((0, 4)),
+                                  "raw": np.zeros(0)})
+    assert sat == 0 and len(b) == 16 and np.array_equal(b, want) and bytes(b[:4]) == b"FGSC"
+    assert gsct.decompress_model(b, ctx=ctx).size() == 0

@@ -253,3 +253,22 @@ def test_adaptive_control_contract(ctx):
     st.accum_count = torch.zeros(5, dtype=torch.int64, device="cuda")
     with pytest.raises(gsct.ContractError, match="lockstep"):
         gsct.adaptive_control(cloud, st, ctx=ctx)
+
+
+@pytest.mark.gpu
+def test_adaptive_control_empty_and_all_pruned(ctx):
+    import torch
+    cloud, st = _device_inputs({"pos": np.zeros((0, 3)), "ls": np.zeros((0, 3)), "q": np.zeros((0, 4)),
+                                "raw": np.zeros(0)},
+                               {k: np.zeros((0, WIDTH[k]) if WIDTH[k] > 1 else (0,)) for k in KEYS},
+                               {"grad_norm": np.zeros(0), "grad_dir": np.zeros((0, 3)),
+                                "count": np.zeros(0, dtype=np.int64)})
+    rep = gsct.adaptive_control(cloud, st, ctx=ctx)
+    assert (rep.pruned, rep.cloned, rep.split) == (0, 0, 0) and cloud.size() == 0
+    # every activated density zero: max density 0, prune_below 0, nothing is < 0 -> all kept
+    p, mom, acc, cfg, seed, pre = _case("calm")
+    p["raw"][:] = 0.0
+    cloud, st = _device_inputs(p, mom, acc)
+    rep = gsct.adaptive_control(cloud, st, ctx=ctx)
+    assert rep.pruned == 0 and cloud.size() == len(p["raw"])
+    assert torch.equal(cloud.positions.cpu(), torch.from_numpy(p["pos"]))

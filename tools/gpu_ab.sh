@@ -1,2 +1,1 @@
-timeout 600 python tools/ab_variants.py run raster c2 5
-timeout 600 python tools/ab_variants.py run raster c5 2
+timeout 600 python -m pytest tests/test_codec.py tests/test_control.py -q 2>&1 | tail -3
