@@ -10,16 +10,11 @@
 #include <cuda_runtime.h>
 
 #include "gsct_internal.cuh"
+#include "packed_f32.cuh"
 
 namespace gsct_dev {
 
 namespace {
-
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 __global__ void k_emit_brick_pairs(const VoxelRec* __restrict__ rec,
                                    const uint32_t* __restrict__ offsets,
@@ -47,43 +42,7 @@ __global__ void k_emit_brick_pairs(const VoxelRec* __restrict__ rec,
       }
 }
 
-typedef unsigned long long f2_t;  // two packed fp32 values (lo, hi)
-__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
-  f2_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void f2_unpack(f2_t v, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
-  f2_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
-  f2_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
-  f2_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2_t f2_bc(float x) { return f2_pack(x, x); }
 
-// 32 x 32 bit-matrix transpose across a warp (see raster.cu): lane j's row -> lane l's column.
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
-  const uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-  for (int t = 0; t < 5; ++t) {
-    const int s = 16 >> t;
-    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
-    x = (lane & s) ? ((x & ~M[t]) | ((y >> s) & M[t])) : ((x & M[t]) | ((y << s) & ~M[t]));
-  }
-  return x;
-}
 
 __device__ __forceinline__ float vox_e(const VoxelRec& r, float dx, float dy, float dz) {
   // Q00 dx^2 + Q11 dy^2 + Q22 dz^2 + Q01 dx dy + Q02 dx dz + Q12 dy dz

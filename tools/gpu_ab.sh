@@ -1,1 +1,2 @@
-timeout 600 python -m pytest tests/test_codec.py tests/test_control.py -q 2>&1 | tail -3
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+timeout 600 python tools/prof_workload.py raster c2 3
