@@ -30,7 +30,8 @@ struct __align__(16) RasterRec {
   uint32_t urange;  // u_min | u_max << 16   (empty: u_min > u_max)
   uint32_t vrange;  // v_min | v_max << 16
   float mo_u, mo_v; // mean2d - (u_min, v_min)
-  float A, B, C, amp;
+  float A, B, C, amp;  // amp's sign bit set: the forward's exp chain is not safe over the
+                       // record's aligned bbox (raster_chain_safe) -> direct exp2 path
 };
 static_assert(sizeof(RasterRec) == 32, "RasterRec must be 32 B");
 
@@ -45,6 +46,26 @@ struct __align__(16) VoxelRec {
   float Q22, Q01, Q02, Q12;
 };
 static_assert(sizeof(VoxelRec) == 64, "VoxelRec must be 64 B");
+
+// Chain safety of a raster record over a window of offsets du in [dua, dub] (8-column
+// aligned), dv in [dva, dvb] (row-pair aligned): the multiplicative exp chain of the forward
+// (g <- g r, r <- r c) stays finite and normal when no exponent in the window is below -100
+// and no per-column step exceeds 100 in magnitude. The exponent A du^2 + B du dv + C dv^2
+// is negative semi-definite, so its minimum over a box is at a corner; the step
+// A (2 du + 1) + B dv is linear, so its extremes are at corners too -- a flag computed over
+// a box holds for every sub-box.
+__device__ __forceinline__ float raster_quad_e(float A, float B, float C, float du, float dv) {
+  return fmaf(fmaf(A, du, B * dv), du, C * dv * dv);
+}
+__device__ __forceinline__ bool raster_chain_safe(float A, float B, float C, float dua, float dub, float dva,
+                                                  float dvb) {
+  const float emin = fminf(fminf(raster_quad_e(A, B, C, dua, dva), raster_quad_e(A, B, C, dua, dvb)),
+                           fminf(raster_quad_e(A, B, C, dub, dva), raster_quad_e(A, B, C, dub, dvb)));
+  const float da = A * fmaf(2.f, dua, 1.f), db = A * fmaf(2.f, dub, 1.f);
+  const float dmax = fmaxf(fmaxf(fabsf(fmaf(B, dva, da)), fabsf(fmaf(B, dvb, da))),
+                           fmaxf(fabsf(fmaf(B, dva, db)), fabsf(fmaf(B, dvb, db))));
+  return emin > -100.f && dmax < 100.f && A > -25.f;
+}
 
 struct Cloud {
   int64_t n;

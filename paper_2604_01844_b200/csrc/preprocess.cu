@@ -92,6 +92,13 @@ __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const 
         r.B = static_cast<float>(-kLog2eD * p.conic[1]);
         r.C = static_cast<float>(-0.5 * kLog2eD * p.conic[3]);
         r.amp = static_cast<float>(p.amplitude);
+        {  // chain safety over the 8-column / row-pair aligned bbox, carried in amp's sign
+          const float dua = static_cast<float>((u0 & ~7) - u0) - r.mo_u;
+          const float dub = static_cast<float>((u1 | 7) - u0) - r.mo_u;
+          const float dva = static_cast<float>((v0 & ~1) - v0) - r.mo_v;
+          const float dvb = static_cast<float>((v1 | 1) - v0) - r.mo_v;
+          if (!raster_chain_safe(r.A, r.B, r.C, dua, dub, dva, dvb)) r.amp = copysignf(r.amp, -1.f);
+        }
         // binning count at the kernel's tile size; stats at the requested tile size
         cnt = static_cast<uint32_t>((u1 / bin_ts - u0 / bin_ts + 1) * (v1 / bin_ts - v0 / bin_ts + 1));
         const int ts = rs.tile_size;

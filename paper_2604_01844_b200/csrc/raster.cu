@@ -114,9 +114,9 @@ struct __align__(16) StagedRec2 {
   uint4 m;   // column mask (32 columns), row mask (16 rows), lane mask, -
 };
 
-__device__ __forceinline__ float quad_e(float A, float B, float C, float du, float dv) {
-  return fmaf(fmaf(A, du, B * dv), du, C * dv * dv);
-}
+#ifndef GSCT_FWD_PREFLAG
+#define GSCT_FWD_PREFLAG 1  // chain-safety flag from the set-up instead of per staged record
+#endif
 
 #ifndef GSCT_FWD_UNROLL
 #define GSCT_FWD_UNROLL 4  // unroll factor of the per-lane record walk (A/B on 2x4 blocks: 1 -> 3.50, 4 -> 3.15 ms)
@@ -149,17 +149,17 @@ __device__ __forceinline__ uint32_t stage_record(const RasterRec& r, int tx0, in
   const uint32_t octs = ((2u << (c1 >> 3)) - 1u) & ~((1u << (c0 >> 3)) - 1u);
   const uint32_t pairs = (0x11111111u >> (4 * (7 - (r1 >> 1)))) & (0x11111111u << (4 * (r0 >> 1)));
   const uint32_t lanes_rel = pairs * octs;
+#if GSCT_FWD_PREFLAG
+  // chain safety from the set-up (over the whole aligned bbox, amp's sign bit)
+  const bool safe = !signbit(r.amp);
+#else
   // chain-safety window: rows r0..r1 x 8-aligned columns
-  const float dua = du_t + static_cast<float>(c0 & ~7), dub = du_t + static_cast<float>(c1 | 7);
-  const float dva = dv_t + static_cast<float>(r0 & ~1), dvb = dv_t + static_cast<float>(r1 | 1);
-  const float emin = fminf(fminf(quad_e(r.A, r.B, r.C, dua, dva), quad_e(r.A, r.B, r.C, dua, dvb)),
-                           fminf(quad_e(r.A, r.B, r.C, dub, dva), quad_e(r.A, r.B, r.C, dub, dvb)));
-  const float da = r.A * fmaf(2.f, dua, 1.f), db = r.A * fmaf(2.f, dub, 1.f);
-  const float dmax = fmaxf(fmaxf(fabsf(fmaf(r.B, dva, da)), fabsf(fmaf(r.B, dvb, da))),
-                           fmaxf(fabsf(fmaf(r.B, dva, db)), fabsf(fmaf(r.B, dvb, db))));
-  const bool safe = emin > -100.f && dmax < 100.f && r.A > -25.f;
+  const bool safe = raster_chain_safe(r.A, r.B, r.C, du_t + static_cast<float>(c0 & ~7),
+                                      du_t + static_cast<float>(c1 | 7), dv_t + static_cast<float>(r0 & ~1),
+                                      dv_t + static_cast<float>(r1 | 1));
+#endif
   s.p = make_float4(du_t, dv_t, r.A, r.B);
-  s.q = make_float4(r.C, r.amp, ex2_approx(2.f * r.A), safe ? 1.f : 0.f);
+  s.q = make_float4(r.C, fabsf(r.amp), ex2_approx(2.f * r.A), safe ? 1.f : 0.f);
   s.m = make_uint4(cm, rm, lanes_rel, 0u);
   *slot = s;
   return lanes_rel;
