@@ -263,14 +263,17 @@ Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl, cudaStream_t st, bool copy)
 #define GSCT_ZEROCOPY 1
 #endif
 template <class T>
-T* mapped_host(T* host) {
+T* mapped_host(gsct_ctx c, T* host) {
   if (!GSCT_ZEROCOPY || host == nullptr) return nullptr;
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
-  return a.type == cudaMemoryTypeHost && a.devicePointer ? static_cast<T*>(a.devicePointer) : nullptr;
+  // only memory pinned under this context's device (portable allocations made elsewhere
+  // take the staged path: their mapping into this device cannot be told from here)
+  return a.type == cudaMemoryTypeHost && a.devicePointer && a.device == c->device ? static_cast<T*>(a.devicePointer)
+                                                                                   : nullptr;
 }
 
 void reset_stats(gsct_ctx c) {
@@ -621,7 +624,7 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (n_views)
       CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
     float* out = images;
-    float* zc_images = images_location == GSCT_HOST && n > 0 ? mapped_host(images) : nullptr;
+    float* zc_images = images_location == GSCT_HOST && n > 0 ? mapped_host(c, images) : nullptr;
     if (zc_images)
       out = zc_images;  // the forward kernel stores straight into the pinned host images
     else if (images_location == GSCT_HOST && n_views)
@@ -761,9 +764,9 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
 #endif
     bool zc_grads = false;
     if (GSCT_ZEROCOPY_GRADS && out->location == GSCT_HOST && n > 0 && n_views > 0) {
-      double *mp = mapped_host(out->pos), *ml = mapped_host(out->log_scale), *mq = mapped_host(out->quat),
-             *mr = mapped_host(out->raw_density), *mn = mapped_host(out->pos_grad_norm);
-      uint8_t* mv = mapped_host(out->visible);
+      double *mp = mapped_host(c, out->pos), *ml = mapped_host(c, out->log_scale), *mq = mapped_host(c, out->quat),
+             *mr = mapped_host(c, out->raw_density), *mn = mapped_host(c, out->pos_grad_norm);
+      uint8_t* mv = mapped_host(c, out->visible);
       if (mp && ml && mq && mr && mn && mv) {
         gp = mp, gl = ml, gq = mq, gr = mr, gn = mn, gv = mv;
         zc_grads = true;
