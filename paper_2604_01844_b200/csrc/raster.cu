@@ -119,7 +119,8 @@ struct __align__(16) StagedRec2 {
 #endif
 
 #ifndef GSCT_FWD_UNROLL
-#define GSCT_FWD_UNROLL 4  // unroll factor of the per-lane record walk (A/B on 2x4 blocks: 1 -> 3.50, 4 -> 3.15 ms)
+#define GSCT_FWD_UNROLL 2  // unroll factor of the per-lane record walk (A/B on 2x4 blocks: 1 -> 3.50, 4 -> 3.15 ms;
+                           // current kernel: 1 / 2 / 4 / 8 -> 2.51 / 2.50 / 2.53 / 2.54 ms)
 #endif
 constexpr int kFwdUnroll = GSCT_FWD_UNROLL;
 // Accumulation: {row 0, row 1} per column with predicated packed FMAs (__ffma2_rn, which
