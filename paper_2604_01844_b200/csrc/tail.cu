@@ -37,6 +37,12 @@ struct PaddedPre {
 };
 static_assert(sizeof(PreSplat) % sizeof(double) == 0, "PreSplat: whole doubles");
 
+#ifndef GSCT_TAIL_LANES
+#define GSCT_TAIL_LANES 4  // lanes per splat (each takes every L-th view); A/B C2 2/4/8: 0.737/0.731/0.810 ms
+#endif
+constexpr int kTL = GSCT_TAIL_LANES, kTLog = kTL == 8 ? 3 : (kTL == 4 ? 2 : (kTL == 2 ? 1 : 0));
+constexpr int kTSplats = 128 / kTL;  // splats per 128-thread block
+
 #ifndef GSCT_TAIL_MINB
 #define GSCT_TAIL_MINB 4  // 128 registers
 #endif
@@ -54,10 +60,10 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
 #if GSCT_TAIL_SPRE
   // the block's 32 splat set-ups staged in shared memory at a 200 B stride (8 distinct
   // splats per warp access: conflict-free banks), instead of 8 L1 lines per field load
-  __shared__ PaddedPre s_pre[32];
+  __shared__ PaddedPre s_pre[kTSplats];
   {
-    const int64_t first = i0 + static_cast<int64_t>(blockIdx.x) * 32;
-    const int cnt = i1 - first < 32 ? static_cast<int>(i1 - first) : 32;
+    const int64_t first = i0 + static_cast<int64_t>(blockIdx.x) * kTSplats;
+    const int cnt = i1 - first < kTSplats ? static_cast<int>(i1 - first) : kTSplats;
     const double* src = reinterpret_cast<const double*>(pre + first);
     constexpr int kD = sizeof(PreSplat) / sizeof(double);
     for (int k = threadIdx.x; k < cnt * kD; k += blockDim.x)
@@ -66,8 +72,8 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
 #endif
   __syncthreads();
   const auto frame = [&](int vw) -> const Frame& { return frames_in_smem ? s_frames[vw].f : frames_g[vw]; };
-  const int q = threadIdx.x & 3;
-  const int64_t i = i0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 2);
+  const int q = threadIdx.x & (kTL - 1);
+  const int64_t i = i0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> kTLog);
   const bool live = i < i1;
   double v[11];
 #pragma unroll
@@ -75,12 +81,12 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
   bool vis = false;
   if (live) {
 #if GSCT_TAIL_SPRE
-    const PreSplat& s = s_pre[threadIdx.x >> 2].p;
+    const PreSplat& s = s_pre[threadIdx.x >> kTLog].p;
 #else
     const PreSplat& s = pre[i];  // array-of-structs copy (fields re-read from L1 as needed)
 #endif
     if (s.status == 0) {
-      for (int vw = q; vw < n_views; vw += 4) {
+      for (int vw = q; vw < n_views; vw += kTL) {
         const int64_t item = static_cast<int64_t>(vw) * n + i;
         const float4 m1 = moments[2 * item + 1];
         if (m1.z == 0.f) continue;  // culled or degenerate in this view
@@ -120,14 +126,14 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
   }
 #pragma unroll
   for (int k = 0; k < 11; ++k) {
-    v[k] += __shfl_xor_sync(0xffffffffu, v[k], 1);
-    v[k] += __shfl_xor_sync(0xffffffffu, v[k], 2);
+#pragma unroll
+    for (int o = 1; o < kTL; o <<= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
   }
   const unsigned ball = __ballot_sync(0xffffffffu, vis);
   if (live && q == 0) {
 #pragma unroll
     for (int k = 0; k < 11; ++k) acc[k * n + i] = v[k];
-    visible[i] = static_cast<uint8_t>(((ball >> (threadIdx.x & 31)) & 15u) != 0u);
+    visible[i] = static_cast<uint8_t>(((ball >> (threadIdx.x & 31)) & ((1u << kTL) - 1u)) != 0u);
   }
 }
 
@@ -169,7 +175,7 @@ void launch_raster_tail(const PreSplat* pre, int64_t n, int64_t i0, int64_t i1, 
   if (i1 <= i0) return;
   const size_t smem = static_cast<size_t>(n_views) * sizeof(PaddedFrame);
   const bool in_smem = smem <= 24 * 1024;
-  k_raster_tail<<<blocks_for((i1 - i0) * 4, 128), 128, in_smem ? smem : 0, st>>>(
+  k_raster_tail<<<blocks_for((i1 - i0) * kTL, 128), 128, in_smem ? smem : 0, st>>>(
       pre, n, i0, i1, frames_dev, n_views, g, rs, reinterpret_cast<const float4*>(moments), in_smem ? 1 : 0, acc,
       visible);
   count_launch();
