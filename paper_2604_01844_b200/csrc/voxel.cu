@@ -67,7 +67,14 @@ struct __align__(16) StagedVox {
 // fp32 under/overflow anywhere in the brick window) falling back to direct exp2; the rows
 // holding an exactly-on-lattice centre also use the direct path so the peak voxel is
 // rho * exp2(0) = rho exactly (test_voxelizer.cpp:16-22).
-__global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__ rec,
+#ifndef GSCT_VFWD_MINB
+#define GSCT_VFWD_MINB 6  // 80 registers, 6 CTAs/SM (A/B 512^3: 5 CTAs 1.011 ms, 6 0.976, 7 1.001, 8 1.096)
+#endif
+#ifndef GSCT_VFWD_UNROLL
+#define GSCT_VFWD_UNROLL 1  // (2: 0.985 ms with 6 CTAs)
+#endif
+constexpr int kVfwdUnroll = GSCT_VFWD_UNROLL;
+__global__ void __launch_bounds__(128, GSCT_VFWD_MINB) k_voxel_fwd2(const VoxelRec* __restrict__ rec,
                                                    const uint32_t* __restrict__ vals,
                                                    const uint32_t* __restrict__ start,
                                                    const uint32_t* __restrict__ end, Window win,
@@ -144,6 +151,7 @@ __global__ void __launch_bounds__(128) k_voxel_fwd2(const VoxelRec* __restrict__
     }
     __syncwarp();
     uint32_t todo = warp_transpose32(lanes_rel, lane);
+#pragma unroll kVfwdUnroll
     while (todo) {
       const int j = __ffs(todo) - 1;
       todo &= todo - 1u;
