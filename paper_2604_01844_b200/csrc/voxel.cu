@@ -266,7 +266,10 @@ __device__ __forceinline__ void ldg_v8(const float* p, float (&w)[8]) {
 // splat's sums depend only on its own inputs. Splats run in `order` (detector-region major,
 // then box shape) so warps see uniform trip counts and the grad volume stays L2-resident.
 template <int VEC>
-__global__ void __launch_bounds__(256, 4) k_voxel_bwd_lanes(const VoxelRec* __restrict__ rec,
+#ifndef GSCT_VBWD_MINB
+#define GSCT_VBWD_MINB 4
+#endif
+__global__ void __launch_bounds__(256, GSCT_VBWD_MINB) k_voxel_bwd_lanes(const VoxelRec* __restrict__ rec,
                                                             const uint32_t* __restrict__ order, int64_t n,
                                                             Window win, float sp, const float* __restrict__ grad,
                                                             float* __restrict__ mom) {

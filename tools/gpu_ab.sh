@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_voxel.py tests/test_gpu_fullsize.py -q -x 2>&1 | tail -2
+timeout 600 python tools/ab_variants.py run voxel c3 5
