@@ -397,7 +397,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         if hit and args.config == "c2":
             traffic = int(np.mean([d["dram_bytes"] for d in hit]))
             measured = {"kernel": kernel, "source": "profiles/r1/raster/summary.json (ncu --set full, C2)"}
-            for key in ("issue_active_pct", "l1tex_throughput_pct", "l2_throughput_pct", "xu_pipe_pct",
+            for key in ("issue_active_pct", "l1tex_throughput_pct", "l1_lsu_wavefronts_pct", "l2_throughput_pct", "xu_pipe_pct",
                         "fma_pipe_pct", "warps_active_pct"):
                 if key in hit[0]:
                     measured[key] = round(float(np.mean([d[key] for d in hit])), 1)
