@@ -371,3 +371,16 @@ def test_forward_extreme_shapes(ctx, orc, gname):
         acc = g if acc is None else {k: (acc[k] | g[k]) if k == "visible" else acc[k] + g[k] for k in g}
     errs = grad_class_errors(grads, acc)
     assert all(e <= GRAD_TOL for e in errs.values()), errs
+
+
+def test_pinned_ragged_detector(ctx):
+    """Zero-copy host images on a detector whose width is not a multiple of 4 (scalar-store
+    edge path) and whose height is not a multiple of 16: identical to the device path."""
+    import torch
+
+    geom = gsct.ScanGeometry("cone", 50, 37, 0.6, 0.6, [0.2, 1.9, 4.4], 50.0, 25.0)
+    cloud = gsct.make_cloud("random", 400, seed=21, pos_range=7.0)
+    dev = gsct.rasterize_views(cloud.to_device(0), geom, None, ctx=ctx).cpu().numpy()
+    img = torch.full((3, 37, 50), np.nan, dtype=torch.float32).pin_memory().numpy()
+    gsct.rasterize_views(cloud, geom, None, out=img, ctx=ctx)
+    assert np.array_equal(img, dev)

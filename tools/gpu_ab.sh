@@ -1,1 +1,1 @@
-timeout 600 python tools/ab_variants.py run voxel c3 5
+timeout 600 python -m pytest tests/test_gpu_raster.py -q -x -k "pinned" 2>&1 | tail -2
