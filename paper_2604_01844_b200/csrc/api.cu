@@ -46,6 +46,9 @@ struct gsct_ctx_s {
   // host<->device image traffic of the C-ABI host-buffer path runs here, chunk by chunk,
   // overlapped with the compute stream (event-ordered both ways)
   cudaStream_t copy_stream = nullptr;
+  // second compute stream: the host-image forward alternates its view sub-ranges between
+  // this and `stream`, so consecutive sub-range kernels fill each other's tails
+  cudaStream_t aux_stream = nullptr;
   bool own_stream = false;
   bool async = false;
   std::string err;
@@ -437,7 +440,8 @@ int gsct_ctx_create(int device, gsct_ctx* out) {
       cudaMallocHost(&c->hstats, sizeof(DevStats)) != cudaSuccess ||
       cudaMallocHost(&c->hscratch, 16 * sizeof(uint64_t)) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();
     delete c;
     return GSCT_ERR_CUDA;
@@ -469,6 +473,7 @@ void gsct_ctx_destroy(gsct_ctx c) {
   if (c->copy_stream) {
     cudaStreamSynchronize(c->copy_stream);
     cudaStreamDestroy(c->copy_stream);
+    if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
   }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -696,31 +701,40 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       // host output: launch in view sub-ranges so each one's images go down while the next
       // computes (the kernel indexes keys/records/images by its own view range)
 #ifndef GSCT_FWD_SPLIT
-#define GSCT_FWD_SPLIT 2  // host-output forward launched in this many view sub-ranges (A/B: 1 -> +1.74 ms, 2 -> +1.50, 4 -> +2.28)
+#define GSCT_FWD_SPLIT 4  // staged host images: view sub-ranges (single stream A/B: 1 -> +1.74 ms, 2 -> +1.50,
+                          // 4 -> +2.28; alternating two streams: 2/4/6/8 -> fwd 4.82/4.65/4.79/5.15 ms
+                          // at C2, zero-copy 4.61)
 #endif
 #ifndef GSCT_FWD_MINPIECE
 #define GSCT_FWD_MINPIECE 0  // > 0: halving sub-ranges (38, 19, 9, ...) down to this many views
 #endif
+#ifndef GSCT_FWD_DUAL
+#define GSCT_FWD_DUAL 1  // staged host images: sub-range kernels alternate between two streams
+#endif
+      const bool dual = stage_images && GSCT_FWD_DUAL && GSCT_FWD_SPLIT > 1;
+      if (dual) stream_after(c, c->aux_stream, c->stream);  // after the binning
       const int sub = stage_images ? std::max(1, (cv + GSCT_FWD_SPLIT - 1) / GSCT_FWD_SPLIT) : cv;
-      for (int vs = 0, nvs = 0; vs < cv; vs += nvs) {
+      for (int vs = 0, nvs = 0, k = 0; vs < cv; vs += nvs, ++k) {
         const int rem = cv - vs;
         if (stage_images && GSCT_FWD_MINPIECE > 0)
           nvs = rem <= 2 * GSCT_FWD_MINPIECE ? rem : (rem + 1) / 2;
         else
           nvs = std::min(sub, rem);
+        cudaStream_t fs = dual && (k & 1) ? c->aux_stream : c->stream;
         {
           Phase ph(c, GSCT_PH_RASTER_FWD);
           launch_raster_fwd_super(rec + static_cast<int64_t>(vs) * n, vals, start + static_cast<int64_t>(vs) * stride,
                                   end + static_cast<int64_t>(vs) * stride, n, nvs, geom->n_u, geom->n_v, tiles_u,
-                                  tiles_v, stride, img + static_cast<int64_t>(vs) * npx, c->stream);
+                                  tiles_v, stride, img + static_cast<int64_t>(vs) * npx, fs);
         }
         CK(cudaGetLastError());
         if (stage_images) {
-          stream_after(c, c->copy_stream, c->stream);
+          stream_after(c, c->copy_stream, fs);
           CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0 + vs) * npx, img + static_cast<int64_t>(vs) * npx,
                              static_cast<size_t>(npx) * nvs * sizeof(float), cudaMemcpyDeviceToHost, c->copy_stream));
         }
       }
+      if (dual) stream_after(c, c->stream, c->aux_stream);
     }
     if (stage_images && n_views) stream_after(c, c->stream, c->copy_stream);
     finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
