@@ -708,6 +708,9 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
 #ifndef GSCT_FWD_MINPIECE
 #define GSCT_FWD_MINPIECE 0  // > 0: halving sub-ranges (38, 19, 9, ...) down to this many views
 #endif
+#ifndef GSCT_FWD_BULKSTORE
+#define GSCT_FWD_BULKSTORE 1  // zero-copy images leave the forward kernel as TMA bulk row stores
+#endif
 #ifndef GSCT_FWD_DUAL
 #define GSCT_FWD_DUAL 1  // staged host images: sub-range kernels alternate between two streams
 #endif
@@ -725,7 +728,8 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
           Phase ph(c, GSCT_PH_RASTER_FWD);
           launch_raster_fwd_super(rec + static_cast<int64_t>(vs) * n, vals, start + static_cast<int64_t>(vs) * stride,
                                   end + static_cast<int64_t>(vs) * stride, n, nvs, geom->n_u, geom->n_v, tiles_u,
-                                  tiles_v, stride, img + static_cast<int64_t>(vs) * npx, fs);
+                                  tiles_v, stride, img + static_cast<int64_t>(vs) * npx, fs,
+                                  zc_images && GSCT_FWD_BULKSTORE ? 1 : 0);
         }
         CK(cudaGetLastError());
         if (stage_images) {

@@ -118,7 +118,8 @@ void launch_ranges_swapped(const uint32_t* keys, int64_t n_pairs, uint32_t n_key
 // forward over 32x32 super-tile lists (keys = view * n_stiles + super-tile)
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
-                             int stiles_v, int key_stride, float* images, cudaStream_t st);
+                             int stiles_v, int key_stride, float* images, cudaStream_t st,
+                             int bulk_out = 0);  // 1: images are host-mapped (TMA bulk row stores)
 // lane-per-item backward: shape sort keys, then the pixel walk in `order`
 int bwd_vec(int n_u, const float* grad_images);  // 8, 4 or 1 floats per row load
 // returns the number of key bits to sort on

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
                                                      const uint32_t* __restrict__ start,
                                                      const uint32_t* __restrict__ end, int64_t n, int n_u,
                                                      int n_v, int stiles_u, int n_stiles, int key_stride,
-                                                     float* __restrict__ images) {
+                                                     float* __restrict__ images, int bulk_out) {
   constexpr int kHH = kTile;  // half-tile: 32 wide, 16 tall
   constexpr int kBatch = 32 * kFwdGroups;
   __shared__ StagedRec2 s_rec[4][kBatch];
@@ -297,6 +297,32 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
     __syncwarp();
   }
   const int px0 = tx0 + lc;
+  if (bulk_out && tx0 + 2 * kTile <= n_u && (n_u & 3) == 0) {
+    // host-mapped output: the half-tile goes through the warp's (now idle) staging smem and
+    // leaves as one 128 B TMA bulk store per row (cp.async.bulk, async proxy); the warp only
+    // waits until its smem has been read, not for the PCIe writes, so plain stores' PCIe
+    // back-pressure no longer stalls the warp's exit
+    float* so = reinterpret_cast<float*>(sw);  // 16 rows x 32 floats = 2 KB of the 3 KB slice
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      so[lr * 32 + lc + k] = acc[k].x;
+      so[(lr + 1) * 32 + lc + k] = acc[k].y;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(so));
+      for (int rr = 0; rr < kHH && ty0 + rr < n_v; ++rr) {
+        float* dst = images + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(ty0 + rr) * n_u + tx0;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;" ::"l"(dst),
+                     "r"(sbase + rr * 128u)
+                     : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    return;
+  }
   if (px0 >= n_u) return;
   float acc0[8], acc1[8];
 #pragma unroll
@@ -599,13 +625,14 @@ void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_
 
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
-                             int stiles_v, int key_stride, float* images, cudaStream_t st) {
+                             int stiles_v, int key_stride, float* images, cudaStream_t st, int bulk_out) {
   if (n_views == 0) return;
   const int n_stiles = stiles_u * stiles_v;
   // one warp per 32x16 half-super-tile (A/B at C2: 2x4-px lane blocks 3.65 ms, 2x8 2.96 ms,
   // 4x8 3.34 ms; CTA-shared staging with block barriers was slower still)
   dim3 g4(static_cast<unsigned>((2 * n_stiles + 3) / 4), static_cast<unsigned>(n_views));
-  k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, key_stride, images);
+  k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, key_stride, images,
+                                    bulk_out);
   count_launch();
 }
 
