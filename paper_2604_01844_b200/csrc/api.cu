@@ -777,26 +777,29 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     // host gradients in mapped pinned memory: the tail / finalize kernels store into them
     // directly (no trailing D2H); otherwise staged in the workspace and copied down
 #ifndef GSCT_ZEROCOPY_GRADS
-#define GSCT_ZEROCOPY_GRADS 0  // A/B C2 e2e: the strided per-splat stores of the tail / finalize
-                               // over PCIe cost +1.9 ms vs a 0.4 ms staged D2H
+#define GSCT_ZEROCOPY_GRADS 0  // 1: the finalize leaves host-mapped gradients as TMA bulk stores
+                               // (A/B C2 e2e 9.46 ms vs 9.28 for the staged 4-piece D2H, which
+                               // overlaps the tail; plain strided stores over PCIe: +1.9 ms)
 #endif
     bool zc_grads = false;
     if (GSCT_ZEROCOPY_GRADS && out->location == GSCT_HOST && n > 0 && n_views > 0) {
       double *mp = mapped_host(c, out->pos), *ml = mapped_host(c, out->log_scale), *mq = mapped_host(c, out->quat),
              *mr = mapped_host(c, out->raw_density), *mn = mapped_host(c, out->pos_grad_norm);
-      uint8_t* mv = mapped_host(c, out->visible);
-      if (mp && ml && mq && mr && mn && mv) {
-        gp = mp, gl = ml, gq = mq, gr = mr, gn = mn, gv = mv;
+      const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+      if (mp && ml && mq && mr && mn && a16(mp) && a16(ml) && a16(mq) && a16(mr) && a16(mn)) {
+        gp = mp, gl = ml, gq = mq, gr = mr, gn = mn;
         zc_grads = true;
       }
     }
-    if (out->location == GSCT_HOST && !zc_grads) {
-      gp = ws<double>(c, S_GPOS, 3 * un);
-      gl = ws<double>(c, S_GLS, 3 * un);
-      gq = ws<double>(c, S_GQ, 4 * un);
-      gr = ws<double>(c, S_GRAW, un);
-      gn = ws<double>(c, S_GPGN, un);
-      gv = ws<uint8_t>(c, S_GVIS, un);
+    if (out->location == GSCT_HOST) {
+      if (!zc_grads) {
+        gp = ws<double>(c, S_GPOS, 3 * un);
+        gl = ws<double>(c, S_GLS, 3 * un);
+        gq = ws<double>(c, S_GQ, 4 * un);
+        gr = ws<double>(c, S_GRAW, un);
+        gn = ws<double>(c, S_GPGN, un);
+      }
+      gv = ws<uint8_t>(c, S_GVIS, un);  // visibility bytes always staged (N bytes)
     }
     if (n > 0 && n_views == 0) {
       CK(cudaMemsetAsync(gp, 0, 3 * un * sizeof(double), c->stream));
@@ -929,7 +932,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       for (int k = 0; k < pieces; ++k) {
         const int64_t i0 = n * k / pieces, i1 = n * (k + 1) / pieces;
         launch_raster_tail(pre_aos, n, i0, i1, dframes, n_views, g, r, mom, acc, gv, c->stream);
-        launch_raster_finalize(d, i0, i1, acc, gp, gl, gq, gr, gn, c->stream);
+        launch_raster_finalize(d, i0, i1, acc, gp, gl, gq, gr, gn, c->stream, zc_grads ? 1 : 0);
         if (pieces > 1) {
           const size_t a = static_cast<size_t>(i0), m = static_cast<size_t>(i1 - i0);
           stream_after(c, c->copy_stream, c->stream);
@@ -954,6 +957,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));  // also when n_views == 0
       c->event_pool.push_back(cloud_up);
     }
+    if (zc_grads) CK(cudaMemcpyAsync(out->visible, gv, un, cudaMemcpyDeviceToHost, c->stream));
     if (stage_grads && !grads_down) {
       CK(cudaMemcpyAsync(out->pos, gp, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaMemcpyAsync(out->log_scale, gl, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));

@@ -94,7 +94,8 @@ void launch_raster_tail(const PreSplat* pre_aos, int64_t n, int64_t i0, int64_t 
                         int n_views, const Geo& g, const RSet& rs, const float* moments, double* acc,
                         uint8_t* visible, cudaStream_t st);  // splats [i0, i1)
 void launch_raster_finalize(const Cloud& c, int64_t i0, int64_t i1, const double* acc, double* g_pos,
-                            double* g_ls, double* g_q, double* g_raw, double* g_pgn, cudaStream_t st);
+                            double* g_ls, double* g_q, double* g_raw, double* g_pgn, cudaStream_t st,
+                            int bulk_out = 0);  // 1: gradient arrays host-mapped, 16 B aligned
 void launch_debug_project(const PreSplat* pre, int64_t n, const Frame* frame_dev, const Geo& g,
                           const RSet& rs, int32_t* rect, uint8_t* flags, double* mean2d,
                           double* conic, double* amplitude, cudaStream_t st);

@@ -138,31 +138,77 @@ __global__ void __launch_bounds__(128, GSCT_TAIL_MINB) k_raster_tail(const PreSp
 }
 
 // Per-splat finalize: covariance_backward (core.hpp:170-191) of the summed dL/dSigma.
+// bulk_out (host-mapped gradients): the block's 128 splats are staged in shared memory and
+// leave as five contiguous TMA bulk stores (cp.async.bulk), so the strided per-splat stores
+// do not cross PCIe one by one (a block whose byte counts are not 16-byte multiples --
+// only an odd-sized last block -- stores directly).
 __global__ void __launch_bounds__(128) k_raster_finalize(Cloud c, int64_t i0, int64_t i1,
                                                          const double* __restrict__ acc,
                                                          double* __restrict__ g_pos, double* __restrict__ g_ls,
                                                          double* __restrict__ g_q, double* __restrict__ g_raw,
-                                                         double* __restrict__ g_pgn) {
-  const int64_t i = i0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= i1) return;
+                                                         double* __restrict__ g_pgn, int bulk_out) {
+  __shared__ double s_out[128 * 12];
+  const int64_t b0 = i0 + static_cast<int64_t>(blockIdx.x) * blockDim.x;
+  const int64_t i = b0 + threadIdx.x;
+  const int cnt = i1 - b0 < 128 ? static_cast<int>(i1 - b0) : 128;
+  const bool bulk = bulk_out && (cnt % 2) == 0;
   const int64_t n = c.n;
-  double gl[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0};
-  Act a;
-  if (activate(c.pos, c.ls, c.q, c.raw, i, a) == 0) {
-    const double s00 = acc[3 * n + i], s01 = acc[4 * n + i], s02 = acc[5 * n + i];
-    const double s11 = acc[6 * n + i], s12 = acc[7 * n + i], s22 = acc[8 * n + i];
-    const double gsig[9] = {s00, s01, s02, s01, s11, s12, s02, s12, s22};
-    covariance_backward(a.scales, a.uq, a.raw_q, gsig, gl, gq);
-  }
+  if (i < i1) {
+    double gl[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0};
+    Act a;
+    if (activate(c.pos, c.ls, c.q, c.raw, i, a) == 0) {
+      const double s00 = acc[3 * n + i], s01 = acc[4 * n + i], s02 = acc[5 * n + i];
+      const double s11 = acc[6 * n + i], s12 = acc[7 * n + i], s22 = acc[8 * n + i];
+      const double gsig[9] = {s00, s01, s02, s01, s11, s12, s02, s12, s22};
+      covariance_backward(a.scales, a.uq, a.raw_q, gsig, gl, gq);
+    }
+    if (bulk) {
+      const int t = threadIdx.x;
+      double* sp = s_out;                // pos   [cnt][3]
+      double* sl = s_out + 3 * cnt;      // ls    [cnt][3]
+      double* sq = s_out + 6 * cnt;      // quat  [cnt][4]
+      double* sr = s_out + 10 * cnt;     // raw   [cnt]
+      double* sn = s_out + 11 * cnt;     // |dL/dmean2d| [cnt]
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    g_pos[3 * i + k] = acc[k * n + i];
-    g_ls[3 * i + k] = gl[k];
-  }
+      for (int k = 0; k < 3; ++k) {
+        sp[3 * t + k] = acc[k * n + i];
+        sl[3 * t + k] = gl[k];
+      }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) g_q[4 * i + k] = gq[k];
-  g_raw[i] = acc[9 * n + i];
-  g_pgn[i] = acc[10 * n + i];
+      for (int k = 0; k < 4; ++k) sq[4 * t + k] = gq[k];
+      sr[t] = acc[9 * n + i];
+      sn[t] = acc[10 * n + i];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        g_pos[3 * i + k] = acc[k * n + i];
+        g_ls[3 * i + k] = gl[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) g_q[4 * i + k] = gq[k];
+      g_raw[i] = acc[9 * n + i];
+      g_pgn[i] = acc[10 * n + i];
+    }
+  }
+  if (!bulk) return;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(s_out));
+    const uint32_t c8 = static_cast<uint32_t>(cnt) * 8u;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g_pos + 3 * b0), "r"(sb),
+                 "r"(3u * c8) : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g_ls + 3 * b0),
+                 "r"(sb + 3u * c8), "r"(3u * c8) : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g_q + 4 * b0),
+                 "r"(sb + 6u * c8), "r"(4u * c8) : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g_raw + b0),
+                 "r"(sb + 10u * c8), "r"(c8) : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g_pgn + b0),
+                 "r"(sb + 11u * c8), "r"(c8) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
 }
 
 inline unsigned blocks_for(int64_t n, int b) { return static_cast<unsigned>((n + b - 1) / b); }
@@ -182,9 +228,10 @@ void launch_raster_tail(const PreSplat* pre, int64_t n, int64_t i0, int64_t i1, 
 }
 
 void launch_raster_finalize(const Cloud& c, int64_t i0, int64_t i1, const double* acc, double* g_pos, double* g_ls,
-                            double* g_q, double* g_raw, double* g_pgn, cudaStream_t st) {
+                            double* g_q, double* g_raw, double* g_pgn, cudaStream_t st, int bulk_out) {
   if (i1 <= i0) return;
-  k_raster_finalize<<<blocks_for(i1 - i0, 128), 128, 0, st>>>(c, i0, i1, acc, g_pos, g_ls, g_q, g_raw, g_pgn);
+  k_raster_finalize<<<blocks_for(i1 - i0, 128), 128, 0, st>>>(c, i0, i1, acc, g_pos, g_ls, g_q, g_raw, g_pgn,
+                                                              bulk_out);
   count_launch();
 }
 
