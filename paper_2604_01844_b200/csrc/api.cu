@@ -890,6 +890,28 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       cloud_up = pooled_event(c);
       CK(cudaEventRecord(cloud_up, c->copy_stream));
     }
+    // with the forward's records of every view at hand (save-for-backward) and several chunks,
+    // the walk order of all views is sorted once up front (view-major keys: each chunk is a
+    // contiguous range) instead of once per chunk
+    const bool one_sort = reuse && n > 0 && cb.size() > 2 && bwd_keys_view_major();
+    const uint32_t* all_order = nullptr;
+    if (one_sort) {
+      Phase ph(c, GSCT_PH_RASTER_BWD);
+      const int64_t items = n * n_views;
+      uint32_t* k1 = ws<uint32_t>(c, S_KEYS, static_cast<size_t>(items));
+      uint32_t* v1 = ws<uint32_t>(c, S_VALS, static_cast<size_t>(items));
+      uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, static_cast<size_t>(items));
+      uint32_t* v2 = ws<uint32_t>(c, S_VALS2, static_cast<size_t>(items));
+      const float* gbase = gdev ? gdev : grad_images;
+      const int kbits = launch_bwd_shape_keys(saved, n, n_views, geom->n_u, geom->n_v, bwd_vec(geom->n_u, gbase), k1, v1,
+                                              c->stream);
+      cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
+      size_t tmp_bytes = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
+      void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+      CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
+      all_order = vb.Current();
+    }
     for (int ci = 0; ci + 1 < static_cast<int>(cb.size()) && n > 0; ++ci) {
       const int v0 = cb[static_cast<size_t>(ci)], cv = cb[static_cast<size_t>(ci) + 1] - v0;
       const float* gimg = gdev ? gdev + static_cast<int64_t>(v0) * npx : grad_images + static_cast<int64_t>(v0) * npx;
@@ -900,6 +922,15 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       {
         Phase ph(c, GSCT_PH_RASTER_BWD);
+        if (one_sort) {  // walk this chunk's contiguous range of the all-view order
+          if (gdev) {
+            CK(cudaStreamWaitEvent(c->stream, up_done[static_cast<size_t>(ci)], 0));
+            c->event_pool.push_back(up_done[static_cast<size_t>(ci)]);
+          }
+          launch_raster_bwd_lanes(saved, all_order + static_cast<int64_t>(v0) * n, n, cv, geom->n_u, geom->n_v,
+                                  gdev ? gdev : grad_images, mom, 0, c->stream);
+          continue;
+        }
         const int64_t items = n * cv;
         uint32_t* k1 = ws<uint32_t>(c, S_KEYS, static_cast<size_t>(items));
         uint32_t* v1 = ws<uint32_t>(c, S_VALS, static_cast<size_t>(items));
