@@ -893,7 +893,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     // with the forward's records of every view at hand (save-for-backward) and several chunks,
     // the walk order of all views is sorted once up front (view-major keys: each chunk is a
     // contiguous range) instead of once per chunk
-    const bool one_sort = reuse && n > 0 && cb.size() > 2 && bwd_keys_view_major();
+    const bool one_sort = reuse && n > 0 && cb.size() > 2 && bwd_view_major(geom->n_u, geom->n_v);
     const uint32_t* all_order = nullptr;
     if (one_sort) {
       Phase ph(c, GSCT_PH_RASTER_BWD);

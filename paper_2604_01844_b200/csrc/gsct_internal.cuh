@@ -123,8 +123,9 @@ void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const u
                              int bulk_out = 0);  // 1: images are host-mapped (TMA bulk row stores)
 // lane-per-item backward: shape sort keys, then the pixel walk in `order`
 int bwd_vec(int n_u, const float* grad_images);  // 8, 4 or 1 floats per row load
-// true when the walk-order keys are view-major (each view a contiguous range of the order)
-bool bwd_keys_view_major();
+// true when the walk-order keys of an n_u x n_v detector are view-major (each view a
+// contiguous range of the order)
+bool bwd_view_major(int n_u, int n_v);
 // returns the number of key bits to sort on
 int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v, int vec,
                           uint32_t* keys, uint32_t* vals, cudaStream_t st);

@@ -500,19 +500,20 @@ __global__ void __launch_bounds__(256, GSCT_LANES_MINB) k_raster_bwd_lanes(const
 // Bbox-shape sort keys for the lane-per-item backward: (chunks per row, rows), each clamped
 // to 6 bits, so a warp's 32 items have near-identical loop trip counts. Empty items sort
 // last. Values = item index (the stable sort keeps index order inside a shape class).
-#ifndef GSCT_KEY_MODE
-#define GSCT_KEY_MODE 5  // 0: shape; 1: shape | view | detector region (L1 locality inside a warp);
-                         // 2/3 (view dropped, 16/15 bits = 2 radix passes): C2 3.82/3.93 ms vs 3.61;
-                         // 5: view | shape | region -- a warp's lanes walk one image (C2 3.44 vs
-                         // 3.55 ms for mode 1) and every view is a contiguous range of the order
-#endif
+// Walk-order keys, two layouts chosen per call (bwd_view_major):
+//   shape-major (shape, view, region): a shape class of all views at a time;
+//   view-major (view, shape, region): a warp's lanes walk one image and every view is one
+//     contiguous range of the order (so chunked host grad images can share one sort).
+// A/B: C2 (512^2 images) view-major 3.44 ms vs 3.55; C5 (2048^2) 72.9 vs 67.7 ms.
+// Rejected: dropping the view from the key (16 / 15 bits, 2 radix passes; C2 3.82 / 3.93 ms)
+// and coarse-shape row-band orders (3.81 ms).
 #ifndef GSCT_REGION_BITS
 #define GSCT_REGION_BITS 0  // 0: adaptive (below)
 #endif
-// shape = chunks per row (5 bits) | rows (6 bits; 5 in mode 2)
-constexpr int kShapeBits = GSCT_KEY_MODE == 2 ? 10 : 11;
+// shape = chunks per row (5 bits) | rows (6 bits)
+constexpr int kShapeBits = 11;
 __global__ void k_bwd_shape_keys(const RasterRec* __restrict__ rec, int64_t n_items, int64_t n, int vec,
-                                 int region_shift, int region_bits, int view_bits,
+                                 int region_shift, int region_bits, int view_bits, int view_major,
                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_items) return;
@@ -520,13 +521,11 @@ __global__ void k_bwd_shape_keys(const RasterRec* __restrict__ rec, int64_t n_it
   const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
   const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
   const int W = u1 - u0 + 1, H = v1 - v0 + 1;
-  const int low_bits = region_bits + view_bits;
-#if GSCT_KEY_MODE == 5
-  // empty items last within their own view (each view's n items stay one contiguous range)
-  uint32_t key = (static_cast<uint32_t>(i / n) << (kShapeBits + region_bits)) | ((1u << (kShapeBits + region_bits)) - 1u);
-#else
-  uint32_t key = (1u << (kShapeBits + low_bits)) - 1u;  // empty items sort last
-#endif
+  const uint32_t view = static_cast<uint32_t>(i / n);
+  const int sr_bits = kShapeBits + region_bits;
+  // empty items sort last (view-major: last within their own view, so each view's n items
+  // stay one contiguous range)
+  uint32_t key = view_major ? (view << sr_bits) | ((1u << sr_bits) - 1u) : (1u << (sr_bits + view_bits)) - 1u;
   if (W > 0 && H > 0) {
     const int cw = vec == 8 ? 8 : 4;
     const int lead = vec > 1 ? (u0 & (vec - 1)) : 0;
@@ -535,13 +534,9 @@ __global__ void k_bwd_shape_keys(const RasterRec* __restrict__ rec, int64_t n_it
     const uint32_t shape = (static_cast<uint32_t>(min(nch, 31)) << hb) | static_cast<uint32_t>(min(H, (1 << hb) - 1));
     const int half = region_bits / 2;
     const uint32_t ru = min(u0 >> region_shift, (1 << half) - 1), rv = min(v0 >> region_shift, (1 << half) - 1);
-    const uint32_t view = static_cast<uint32_t>(i / n);
-#if GSCT_KEY_MODE == 5
-    // (view, shape, region): each view's items contiguous in the walk order
-    key = (view << (kShapeBits + region_bits)) | (shape << region_bits) | (rv << half) | ru;
-#else
-    key = (shape << low_bits) | (view << region_bits) | (rv << half) | ru;
-#endif
+    const uint32_t region = (rv << half) | ru;
+    key = view_major ? (view << sr_bits) | (shape << region_bits) | region
+                     : (shape << (view_bits + region_bits)) | (view << region_bits) | region;
   }
   keys[i] = key;
   vals[i] = static_cast<uint32_t>(i);
@@ -586,7 +581,10 @@ int bwd_vec(int n_u, const float* grad_images) {
   return 1;
 }
 
-bool bwd_keys_view_major() { return GSCT_KEY_MODE == 5; }
+#ifndef GSCT_VIEW_MAJOR_MAX_PX
+#define GSCT_VIEW_MAJOR_MAX_PX (1 << 20)  // view-major walk order up to 1M-pixel (4 MB) images
+#endif
+bool bwd_view_major(int n_u, int n_v) { return static_cast<int64_t>(n_u) * n_v <= GSCT_VIEW_MAJOR_MAX_PX; }
 
 int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v, int vec,
                           uint32_t* keys, uint32_t* vals, cudaStream_t st) {
@@ -594,27 +592,20 @@ int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u,
   if (n_items == 0) return kShapeBits;
   int view_bits = 0, region_bits = 0, region_shift = 0;
   const int side = n_u > n_v ? n_u : n_v;
-#if GSCT_KEY_MODE == 1 || GSCT_KEY_MODE == 5
-  // (shape, view, region) / (view, shape, region): 11 + view + region bits
   while ((1 << view_bits) < n_views) ++view_bits;
   // 2^(bits/2) x 2^(bits/2) detector regions: the finest regions of >= 32 px that keep the
-  // key within 24 bits (three radix passes). A/B: C2 (512^2, 75 views) 6 bits 3.54 ms vs
-  // 8 bits 3.60; C5 (2048^2, 8 views) 6 bits 73.5 ms, 10 bits 67.7, 12 bits 66.4
+  // key within 24 bits (three radix passes). A/B (shape-major): C2 (512^2, 75 views) 6 bits
+  // 3.54 ms vs 8 bits 3.60; C5 (2048^2, 8 views) 6 bits 73.5 ms, 10 bits 67.7, 12 bits 66.4;
+  // (view-major, C2) 2 / 4 / 6 / 8 bits: 3.63 / 3.55 / 3.44 / 3.53 ms
   region_bits = GSCT_REGION_BITS;
   if (region_bits == 0) {
     region_bits = 2;
-    while (region_bits + 2 <= 24 - 11 - view_bits && (side >> ((region_bits + 2) / 2)) >= 32) region_bits += 2;
+    while (region_bits + 2 <= 24 - kShapeBits - view_bits && (side >> ((region_bits + 2) / 2)) >= 32) region_bits += 2;
   }
   while ((side >> region_shift) > (1 << (region_bits / 2))) ++region_shift;
-#elif GSCT_KEY_MODE == 2 || GSCT_KEY_MODE == 3
-  // view left out of the key: items are emitted view-major and the radix sort is stable,
-  // so the order is (shape, region, view, splat) with 16 / 15 key bits = two passes
-  region_bits = GSCT_KEY_MODE == 2 ? 6 : 4;
-  const int per_axis = 1 << (region_bits / 2);
-  while ((side >> region_shift) > per_axis) ++region_shift;
-#endif
   k_bwd_shape_keys<<<blocks_for(n_items, 256), 256, 0, st>>>(rec, n_items, n, vec, region_shift, region_bits,
-                                                             view_bits, keys, vals);
+                                                             view_bits, bwd_view_major(n_u, n_v) ? 1 : 0, keys,
+                                                             vals);
   count_launch();
   return kShapeBits + view_bits + region_bits;  // key bits
 }
