@@ -955,7 +955,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
                             // D2H overlapping the next range's tail
 #endif
     const bool stage_grads = out->location == GSCT_HOST && n > 0 && !zc_grads;
-    const int pieces = stage_grads && n_views > 0 && n >= 4096 ? GSCT_TAIL_PIECES : 1;
+    const int pieces = (stage_grads || zc_grads) && n_views > 0 && n >= 4096 ? GSCT_TAIL_PIECES : 1;
     bool grads_down = false;
     if (n > 0 && n_views > 0) {
       Phase ph(c, GSCT_PH_RASTER_TAIL);
@@ -964,7 +964,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         const int64_t i0 = n * k / pieces, i1 = n * (k + 1) / pieces;
         launch_raster_tail(pre_aos, n, i0, i1, dframes, n_views, g, r, mom, acc, gv, c->stream);
         launch_raster_finalize(d, i0, i1, acc, gp, gl, gq, gr, gn, c->stream, zc_grads ? 1 : 0);
-        if (pieces > 1) {
+        if (pieces > 1 && stage_grads) {
           const size_t a = static_cast<size_t>(i0), m = static_cast<size_t>(i1 - i0);
           stream_after(c, c->copy_stream, c->stream);
           CK(cudaMemcpyAsync(out->pos + 3 * a, gp + 3 * a, 3 * m * sizeof(double), cudaMemcpyDeviceToHost,
@@ -979,7 +979,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
           CK(cudaMemcpyAsync(out->visible + a, gv + a, m, cudaMemcpyDeviceToHost, c->copy_stream));
         }
       }
-      if (pieces > 1) {
+      if (pieces > 1 && stage_grads) {
         stream_after(c, c->stream, c->copy_stream);
         grads_down = true;
       }
