@@ -252,7 +252,7 @@ def secondary_2k(ctx, n_views_measured: int = 8, k: int = 3) -> dict:
             f"cone 2048^2, fwd+bwd of {n_views_measured} of 75 views per step (per-view rate)", "ms_per_step": ms}
 
 
-def secondary_train(ctx, k: int = 3) -> dict:
+def secondary_train(ctx, k: int = 5) -> dict:
     """BASELINE configs[1] as a device-resident training iteration: render the 75 C2 views,
     fused L1 + 0.25 SSIM2D image loss against measured projections (rendered from the
     unperturbed cloud), backward to the Gaussians, one Adam step (batched-gradient data
