@@ -432,12 +432,9 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) p.cov2d[k] = cr[k];
-  if (kBox) {
-    p.conic[0] = cr[3] / dt2;
-    p.conic[1] = -cr[1] / dt2;
-    p.conic[2] = -cr[2] / dt2;
-    p.conic[3] = cr[0] / dt2;
-  } else {
+  {
+    // the conic feeds only the fp32 record and the gradients (never the integer box), so one
+    // reciprocal replaces the reference's four divisions (<= 1 ulp apart)
     const double idt = 1.0 / dt2;
     p.conic[0] = cr[3] * idt;
     p.conic[1] = -cr[1] * idt;
