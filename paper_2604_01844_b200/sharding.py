@@ -16,7 +16,7 @@ tests) and only move data that the path must exchange.
 """
 from __future__ import annotations
 
-from typing import Optional, Sequence
+from typing import Sequence
 
 
 def shard_views(n_views: int, rank: int, world: int) -> list[int]:

@@ -2,7 +2,6 @@
 everything else runs on CPU (oracle vs reference, golden vectors, host logic, gloo)."""
 from __future__ import annotations
 
-import os
 import sys
 from pathlib import Path
 

@@ -14,7 +14,6 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import has_gpu
 from paper_2604_01844_b200 import gsct
 
 

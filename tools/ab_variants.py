@@ -8,7 +8,6 @@ a fresh process running tools/prof_workload.py, so per-phase device times are co
 """
 from __future__ import annotations
 
-import json
 import os
 import subprocess
 import sys
