@@ -894,6 +894,9 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     // the walk order of all views is sorted once up front (view-major keys: each chunk is a
     // contiguous range) instead of once per chunk
     const bool one_sort = reuse && n > 0 && cb.size() > 2 && bwd_view_major(geom->n_u, geom->n_v);
+#ifndef GSCT_BWD_DUAL
+#define GSCT_BWD_DUAL 1  // chunk walks alternate between two streams
+#endif
     const uint32_t* all_order = nullptr;
     if (one_sort) {
       Phase ph(c, GSCT_PH_RASTER_BWD);
@@ -911,6 +914,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
       CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
       all_order = vb.Current();
+      if (GSCT_BWD_DUAL) stream_after(c, c->aux_stream, c->stream);  // after the sort
     }
     for (int ci = 0; ci + 1 < static_cast<int>(cb.size()) && n > 0; ++ci) {
       const int v0 = cb[static_cast<size_t>(ci)], cv = cb[static_cast<size_t>(ci) + 1] - v0;
@@ -923,12 +927,14 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       {
         Phase ph(c, GSCT_PH_RASTER_BWD);
         if (one_sort) {  // walk this chunk's contiguous range of the all-view order
+          // chunks alternate between two streams so a chunk's walk fills the previous one's tail
+          cudaStream_t ws_ = GSCT_BWD_DUAL && (ci & 1) ? c->aux_stream : c->stream;
           if (gdev) {
-            CK(cudaStreamWaitEvent(c->stream, up_done[static_cast<size_t>(ci)], 0));
+            CK(cudaStreamWaitEvent(ws_, up_done[static_cast<size_t>(ci)], 0));
             c->event_pool.push_back(up_done[static_cast<size_t>(ci)]);
           }
           launch_raster_bwd_lanes(saved, all_order + static_cast<int64_t>(v0) * n, n, cv, geom->n_u, geom->n_v,
-                                  gdev ? gdev : grad_images, mom, 0, c->stream);
+                                  gdev ? gdev : grad_images, mom, 0, ws_);
           continue;
         }
         const int64_t items = n * cv;
@@ -950,6 +956,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       CK(cudaGetLastError());
     }
+    if (one_sort && GSCT_BWD_DUAL) stream_after(c, c->stream, c->aux_stream);
 #ifndef GSCT_TAIL_PIECES
 #define GSCT_TAIL_PIECES 4  // staged host gradients: tail + finalize in splat ranges, each range's
                             // D2H overlapping the next range's tail
