@@ -967,13 +967,19 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (n > 0 && n_views > 0) {
       Phase ph(c, GSCT_PH_RASTER_TAIL);
       if (cloud_up) CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));
+#ifndef GSCT_TAIL_DUAL
+#define GSCT_TAIL_DUAL 1  // tail pieces alternate between two streams
+#endif
+      const bool tdual = GSCT_TAIL_DUAL && pieces > 1;
+      if (tdual) stream_after(c, c->aux_stream, c->stream);
       for (int k = 0; k < pieces; ++k) {
         const int64_t i0 = n * k / pieces, i1 = n * (k + 1) / pieces;
-        launch_raster_tail(pre_aos, n, i0, i1, dframes, n_views, g, r, mom, acc, gv, c->stream);
-        launch_raster_finalize(d, i0, i1, acc, gp, gl, gq, gr, gn, c->stream, zc_grads ? 1 : 0);
+        cudaStream_t ts = tdual && (k & 1) ? c->aux_stream : c->stream;
+        launch_raster_tail(pre_aos, n, i0, i1, dframes, n_views, g, r, mom, acc, gv, ts);
+        launch_raster_finalize(d, i0, i1, acc, gp, gl, gq, gr, gn, ts, zc_grads ? 1 : 0);
         if (pieces > 1 && stage_grads) {
           const size_t a = static_cast<size_t>(i0), m = static_cast<size_t>(i1 - i0);
-          stream_after(c, c->copy_stream, c->stream);
+          stream_after(c, c->copy_stream, ts);
           CK(cudaMemcpyAsync(out->pos + 3 * a, gp + 3 * a, 3 * m * sizeof(double), cudaMemcpyDeviceToHost,
                              c->copy_stream));
           CK(cudaMemcpyAsync(out->log_scale + 3 * a, gl + 3 * a, 3 * m * sizeof(double), cudaMemcpyDeviceToHost,
@@ -986,6 +992,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
           CK(cudaMemcpyAsync(out->visible + a, gv + a, m, cudaMemcpyDeviceToHost, c->copy_stream));
         }
       }
+      if (tdual) stream_after(c, c->stream, c->aux_stream);
       if (pieces > 1 && stage_grads) {
         stream_after(c, c->stream, c->copy_stream);
         grads_down = true;
