@@ -646,7 +646,10 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     }
     // save-for-backward keeps every view's records in one buffer for the backward call
     RasterRec* saved = c->save_fb && n > 0 ? ws<RasterRec>(c, S_SAVED, static_cast<size_t>(n) * n_views) : nullptr;
-    int chunk = views_per_chunk(n, n_views, n_tiles);
+#ifndef GSCT_FWD_TILECAP
+#define GSCT_FWD_TILECAP 1  // 1: <= 65536 (view, tile) keys per forward chunk (16-bit sorts)
+#endif
+    int chunk = views_per_chunk(n, n_views, GSCT_FWD_TILECAP ? n_tiles : 0);
     for (int v0 = 0; v0 < n_views; v0 += chunk) {
       const int cv = std::min(chunk, n_views - v0);
       float* img = out + static_cast<int64_t>(v0) * npx;
