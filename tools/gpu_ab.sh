@@ -1,2 +1,1 @@
-timeout 600 python tools/ab_variants.py run raster c5 2
-timeout 600 python tools/ab_variants.py run raster c5 2
+timeout 600 python -m pytest tests/test_gpu_raster.py -q -x -k "chunked or pinned" 2>&1 | tail -3
