@@ -174,8 +174,11 @@ def timed_steps(step, stream, k: int, flush) -> list[float]:
     return times
 
 
-def run_e2e(ctx, cloud, geom, views, k: int, w: int) -> dict:
-    """Same step through the C ABI with pinned host buffers; copies inside the timed region."""
+def run_e2e(ctx, cloud, geom, views, k: int, w: int, world: int = 1) -> dict:
+    """Same step through the C ABI with pinned host buffers; copies inside the timed region.
+    With several ranks each rank runs its view shard and the summed gradients are formed by
+    an all-reduce of the packed fp64 gradient buffer (host -> device -> all-reduce -> host,
+    inside the step); per-step time = max over ranks."""
     import torch
     from paper_2604_01844_b200 import gsct
 
@@ -187,26 +190,46 @@ def run_e2e(ctx, cloud, geom, views, k: int, w: int) -> dict:
     n = cloud.size()
     images = torch.empty((nv, geom.n_v, geom.n_u), dtype=torch.float32).pin_memory().numpy()
     gimg = torch.ones((nv, geom.n_v, geom.n_u), dtype=torch.float32).pin_memory().numpy()
-    z = lambda *s: torch.zeros(s, dtype=torch.float64).pin_memory().numpy()
-    grads = gsct.ParamGradients(z(n, 3), z(n, 3), z(n, 4), z(n), z(n),
-                                torch.zeros(n, dtype=torch.uint8).pin_memory().numpy())
+    # one pinned fp64 buffer holding every gradient class (pos 3N, ls 3N, q 4N, raw N, |g2d| N)
+    flat_h = torch.zeros(12 * n, dtype=torch.float64).pin_memory()
+    f = flat_h.numpy()
+    grads = gsct.ParamGradients(f[:3 * n].reshape(n, 3), f[3 * n:6 * n].reshape(n, 3), f[6 * n:10 * n].reshape(n, 4),
+                                f[10 * n:11 * n], f[11 * n:], torch.zeros(n, dtype=torch.uint8).pin_memory().numpy())
     rs = gsct.RasterSettings()
+    dev = torch.device(f"cuda:{ctx.device}")
+    flat_d = torch.empty(12 * n, dtype=torch.float64, device=dev) if world > 1 else None
 
     def step():
         gsct.rasterize_views(hcloud, geom, views, rs, out=images, ctx=ctx)
         gsct.rasterize_backward_views(hcloud, geom, views, gimg, rs, out=grads, ctx=ctx)
+        if world > 1:
+            import torch.distributed as dist
+
+            flat_d.copy_(flat_h, non_blocking=True)
+            dist.all_reduce(flat_d)
+            flat_h.copy_(flat_d)  # device->host: the summed gradients
         return float(grads.raw_densities[0])  # device->host result read
 
     for _ in range(w):
         step()
     ts = []
     for _ in range(k):
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
         t0 = time.perf_counter()
         step()
         ts.append((time.perf_counter() - t0) * 1e3)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor(ts, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ts = t.cpu().tolist()
     cloud_bytes = n * 11 * 8
-    h2d = 2 * cloud_bytes + gimg.nbytes  # the cloud is uploaded by both calls
-    d2h = images.nbytes + n * (12 * 8 + 1)
+    h2d = 2 * cloud_bytes + gimg.nbytes + (flat_h.numel() * 8 if world > 1 else 0)  # cloud up in both calls
+    d2h = images.nbytes + n * (12 * 8 + 1) + (flat_h.numel() * 8 if world > 1 else 0)
     return {"ms": ts, "h2d": h2d, "d2h": d2h}
 
 
@@ -363,6 +386,17 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     n_views_total = len(geom.angles)
     value = n_views_total * args.steps / (total_ms / 1e3)
 
+    # e2e through the C ABI with pinned host buffers (every rank: its shard + the all-reduce)
+    e2e = None
+    if not args.no_e2e:
+        e = run_e2e(ctx, cloud, geom, views, max(3, min(args.steps, 5)), 2, world)
+        e_ms = float(np.mean(e["ms"]))
+        e2e = {"value": round(n_views_total / (e_ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": e["h2d"],
+               "d2h_bytes_per_step": e["d2h"], "ms_per_step": round(e_ms, 3),
+               "path": "gsct_rasterize_fwd + gsct_rasterize_bwd (C ABI, GSCT_HOST pinned buffers, sync)"
+                       + (" + all-reduce of the packed gradients, max over ranks" if world > 1 else "")}
+        ctx.set_async(True)
+
     if rank != 0:
         return
 
@@ -432,13 +466,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "phase_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
-    if not args.no_e2e and world == 1:
-        e = run_e2e(ctx, cloud, geom, views, max(2, min(args.steps, 5)), 1)
-        e_ms = float(np.mean(e["ms"]))
-        out["e2e"] = {"value": round(n_views_total / (e_ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": e["h2d"],
-                      "d2h_bytes_per_step": e["d2h"], "ms_per_step": round(e_ms, 3),
-                      "path": "gsct_rasterize_fwd + gsct_rasterize_bwd (C ABI, GSCT_HOST pinned buffers, sync)"}
-        ctx.set_async(True)
+    if e2e is not None:
+        out["e2e"] = e2e
     if not args.no_secondary and world == 1:
         try:
             out["secondary"] = {"raster_2048": secondary_2k(ctx), "voxel_512": secondary_voxel(ctx),

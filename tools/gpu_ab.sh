@@ -1,1 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_raster.py -q -x -k "chunked or pinned" 2>&1 | tail -3
+timeout 900 python bench.py > gpurun_out/bench1.json 2>/dev/null; python -c "
+import json; d=json.loads(open('gpurun_out/bench1.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e'])"
+timeout 900 python bench.py --steps 3 --warmup 3 --no-secondary > gpurun_out/bench1.json 2>/dev/null; python -c "
+import json; d=json.loads(open('gpurun_out/bench1.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e'])"
