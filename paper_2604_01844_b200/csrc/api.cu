@@ -24,7 +24,7 @@ namespace {
 enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
-  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG, S_FGSC, S_FGSC_LOG, S_FGSC_CNT,
+  S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG, S_FGSC, S_FGSC_LOG, S_FGSC_CNT, S_VTCOUNT,
   S_COUNT_SLOTS
 };
 
@@ -373,6 +373,42 @@ int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32
   return total;
 }
 
+// Packed keys-only forward binning (see k_emit_tile_keys): scan of the per-item counts,
+// emission of tile << 24 | splat with (view, tile) counts, ONE stable radix pass over the tile
+// bits (4 bytes per pair moved), ranges from the counts. Returns the number of pairs.
+int64_t bin_packed(gsct_ctx c, const RasterRec* rec, const uint32_t* counts, int64_t n, int n_views, int tiles_u,
+                   int n_tiles, int tile_bits, int key_stride, uint32_t** keys_out, uint32_t** start, uint32_t** end) {
+  const int64_t n_items = n * n_views;
+  uint32_t* offsets = ws<uint32_t>(c, S_OFFSET, static_cast<size_t>(n_items));
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
+  void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
+  const uint32_t total = read_scan_total(c, offsets, counts, n_items);
+  const uint32_t n_keys = static_cast<uint32_t>(n_views) * static_cast<uint32_t>(key_stride);
+  *start = ws<uint32_t>(c, S_START, n_keys);
+  *end = ws<uint32_t>(c, S_END, n_keys);
+  if (total == 0) {
+    CK(cudaMemsetAsync(*start, 0, n_keys * sizeof(uint32_t), c->stream));
+    CK(cudaMemsetAsync(*end, 0, n_keys * sizeof(uint32_t), c->stream));
+    *keys_out = nullptr;
+    return 0;
+  }
+  uint32_t* k1 = ws<uint32_t>(c, S_KEYS, total);
+  uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, total);
+  uint32_t* vt = ws<uint32_t>(c, S_VTCOUNT, static_cast<size_t>(n_views) * n_tiles);
+  CK(cudaMemsetAsync(vt, 0, static_cast<size_t>(n_views) * n_tiles * sizeof(uint32_t), c->stream));
+  launch_emit_tile_keys(rec, offsets, counts, n, n_views, kBinTile, tiles_u, n_tiles, k1, vt, c->stream);
+  cub::DoubleBuffer<uint32_t> kb(k1, k2);
+  tmp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, kb, static_cast<int>(total), 24, 24 + tile_bits, c->stream));
+  tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+  CK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, kb, static_cast<int>(total), 24, 24 + tile_bits, c->stream));
+  *keys_out = kb.Current();
+  launch_ranges_from_counts(vt, n_views, n_tiles, key_stride, *start, *end, c->stream);
+  return total;
+}
+
 // Identity of a rasterizer call for save-for-backward: cloud buffers and size, geometry,
 // angles and settings, field by field (no struct padding).
 std::string raster_call_key(const gsct_cloud* cl, const gsct_geometry* g, const double* angles, int n_views,
@@ -692,15 +728,25 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       const bool onepass = GSCT_BIN_ONEPASS && tile_bits <= 8;
       const int stride = onepass ? (1 << tile_bits) : n_tiles;
       const uint32_t n_keys = static_cast<uint32_t>(cv) * static_cast<uint32_t>(stride);
+#ifndef GSCT_BIN_PACKED
+#define GSCT_BIN_PACKED 1  // keys-only packed binning when it applies (see bin_packed)
+#endif
+      const bool packed = GSCT_BIN_PACKED && onepass && n >= 256 && n < (int64_t(1) << 24) && n_tiles <= 256;
       {
         Phase ph(c, GSCT_PH_RASTER_BIN);
-        bin_and_sort(
-            c, cnt, n * cv, n_keys,
-            [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
-              launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kBinTile, tiles_u, stride, k, v, c->stream);
-            },
-            &keys, &vals, &start, &end, onepass ? tile_bits : 0);
+        if (packed) {
+          bin_packed(c, rec, cnt, n, cv, tiles_u, n_tiles, tile_bits, stride, &vals, &start, &end);
+          keys = nullptr;
+        } else {
+          bin_and_sort(
+              c, cnt, n * cv, n_keys,
+              [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
+                launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kBinTile, tiles_u, stride, k, v, c->stream);
+              },
+              &keys, &vals, &start, &end, onepass ? tile_bits : 0);
+        }
       }
+      const uint32_t vmask = packed ? 0x00FFFFFFu : 0xFFFFFFFFu;
       // host output: launch in view sub-ranges so each one's images go down while the next
       // computes (the kernel indexes keys/records/images by its own view range)
 #ifndef GSCT_FWD_SPLIT
@@ -736,7 +782,7 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
           launch_raster_fwd_super(rec + static_cast<int64_t>(vs) * n, vals, start + static_cast<int64_t>(vs) * stride,
                                   end + static_cast<int64_t>(vs) * stride, n, nvs, geom->n_u, geom->n_v, tiles_u,
                                   tiles_v, stride, img + static_cast<int64_t>(vs) * npx, fs,
-                                  (zc_images || GSCT_FWD_BULK_DEVICE) && GSCT_FWD_BULKSTORE ? 1 : 0);
+                                  (zc_images || GSCT_FWD_BULK_DEVICE) && GSCT_FWD_BULKSTORE ? 1 : 0, vmask);
         }
         CK(cudaGetLastError());
         if (stage_images) {

@@ -120,7 +120,14 @@ void launch_ranges_swapped(const uint32_t* keys, int64_t n_pairs, uint32_t n_key
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
                              int stiles_v, int key_stride, float* images, cudaStream_t st,
-                             int bulk_out = 0);  // 1: images are host-mapped (TMA bulk row stores)
+                             int bulk_out = 0,             // 1: images are host-mapped (TMA bulk row stores)
+                             uint32_t vmask = 0xFFFFFFFFu);  // splat = vals[k] & vmask (packed keys)
+// packed keys-only binning (tile << 24 | splat) with (view, tile) counts, and its ranges
+void launch_emit_tile_keys(const RasterRec* rec, const uint32_t* offsets, const uint32_t* counts, int64_t n,
+                           int n_views, int ts, int tiles_u, int n_tiles, uint32_t* keys, uint32_t* vt_count,
+                           cudaStream_t st);
+void launch_ranges_from_counts(const uint32_t* vt_count, int n_views, int n_tiles, int key_stride, uint32_t* start,
+                               uint32_t* end, cudaStream_t st);
 // lane-per-item backward: shape sort keys, then the pixel walk in `order`
 int bwd_vec(int n_u, const float* grad_images);  // 8, 4 or 1 floats per row load
 // true when the walk-order keys of an n_u x n_v detector are view-major (each view a

@@ -67,6 +67,75 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, uint32_t n_pairs, ui
   end[k] = lower_bound_u32(keys, n_pairs, k + 1);
 }
 
+// Packed keys-only binning (one view chunk, <= 256 super-tiles per view, < 2^24 splats):
+// each pair is ONE u32 = super-tile << 24 | splat, emitted view-major in splat order, so a
+// stable radix pass over bits 24..31 orders them (tile, view, splat) while moving 4 bytes per
+// pair instead of a key + value. The (view, tile) counts the ranges need are histogrammed
+// here (per-CTA shared-memory bins, flushed with integer atomics: order-free).
+__global__ void __launch_bounds__(256) k_emit_tile_keys(const RasterRec* __restrict__ rec,
+                                                        const uint32_t* __restrict__ offsets,
+                                                        const uint32_t* __restrict__ counts, int64_t n, int n_views,
+                                                        int tiles_u, int n_tiles, int ts, uint32_t* __restrict__ keys,
+                                                        uint32_t* __restrict__ vt_count) {
+  __shared__ uint32_t h[2][256];  // a CTA's 256 items span at most two views (n >= 256)
+  const int64_t item0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+  const int vbase = static_cast<int>(item0 / n);
+  for (int k = threadIdx.x; k < 512; k += blockDim.x) (&h[0][0])[k] = 0u;
+  __syncthreads();
+  const int64_t item = item0 + threadIdx.x;
+  if (item < n * n_views) {
+    const uint32_t cnt = counts[item];
+    if (cnt) {
+      const int v = static_cast<int>(item / n);
+      const uint32_t i = static_cast<uint32_t>(item - static_cast<int64_t>(v) * n);
+      const RasterRec r = rec[item];
+      const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
+      const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+      uint32_t off = offsets[item];
+      for (int tv = v0 / ts; tv <= v1 / ts; ++tv)
+        for (int tu = u0 / ts; tu <= u1 / ts; ++tu) {
+          const uint32_t t = static_cast<uint32_t>(tv * tiles_u + tu);
+          keys[off++] = (t << 24) | i;
+          atomicAdd(&h[v - vbase][t], 1u);
+        }
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 2 * n_tiles; k += blockDim.x) {
+    const int vv = vbase + k / n_tiles, t = k % n_tiles;
+    const uint32_t c = h[k / n_tiles][t];
+    if (c && vv < n_views) atomicAdd(&vt_count[vv * n_tiles + t], c);
+  }
+}
+
+// [start, end) per (view, tile) of the (tile, view, splat)-ordered packed keys, from the
+// counts: one CTA, thread t owns tile t (block scan of the tile totals, then the views).
+__global__ void __launch_bounds__(256) k_ranges_from_counts(const uint32_t* __restrict__ vt_count, int n_views,
+                                                            int n_tiles, int key_stride, uint32_t* __restrict__ start,
+                                                            uint32_t* __restrict__ end) {
+  __shared__ uint32_t tot[256];
+  const int t = threadIdx.x;
+  uint32_t sum = 0;
+  if (t < n_tiles)
+    for (int v = 0; v < n_views; ++v) sum += vt_count[v * n_tiles + t];
+  tot[t] = sum;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {  // inclusive Hillis-Steele scan
+    const uint32_t x = t >= o ? tot[t - o] : 0u;
+    __syncthreads();
+    tot[t] += x;
+    __syncthreads();
+  }
+  if (t >= n_tiles) return;
+  uint32_t base = tot[t] - sum;  // exclusive
+  for (int v = 0; v < n_views; ++v) {
+    const uint32_t c = vt_count[v * n_tiles + t];
+    start[v * key_stride + t] = base;
+    end[v * key_stride + t] = base + c;
+    base += c;
+  }
+}
+
 // [start, end) of every key after the one-pass binning: keys = view << tile_bits | tile
 // sorted by tile only (stable), i.e. ascending in ord(key) = tile << 16 | view; binary
 // search in that order, one thread per key.
@@ -177,7 +246,7 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
                                                      const uint32_t* __restrict__ start,
                                                      const uint32_t* __restrict__ end, int64_t n, int n_u,
                                                      int n_v, int stiles_u, int n_stiles, int key_stride,
-                                                     float* __restrict__ images, int bulk_out) {
+                                                     float* __restrict__ images, int bulk_out, uint32_t vmask) {
   constexpr int kHH = kTile;  // half-tile: 32 wide, 16 tall
   constexpr int kBatch = 32 * kFwdGroups;
   __shared__ StagedRec2 s_rec[4][kBatch];
@@ -205,8 +274,8 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
 #pragma unroll
   for (int g = 0; g < kFwdGroups; ++g) {
     const uint32_t k = b + 32 * g + lane;
-    if (k < e) recs[g] = vrec[__ldg(vals + k)];
-    idx_next[g] = k + kBatch < e ? __ldg(vals + k + kBatch) : 0u;
+    if (k < e) recs[g] = vrec[__ldg(vals + k) & vmask];
+    idx_next[g] = k + kBatch < e ? __ldg(vals + k + kBatch) & vmask : 0u;
   }
   for (uint32_t base = b; base < e; base += kBatch) {
     uint32_t todo[kFwdGroups];
@@ -220,7 +289,7 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
     for (int g = 0; g < kFwdGroups; ++g) {
       const uint32_t k = base + kBatch + 32 * g + lane;
       if (k < e) recs[g] = vrec[idx_next[g]];
-      idx_next[g] = k + kBatch < e ? __ldg(vals + k + kBatch) : 0u;
+      idx_next[g] = k + kBatch < e ? __ldg(vals + k + kBatch) & vmask : 0u;
     }
     // one flat loop over the lane's records of the whole batch, so lanes do not wait for
     // each other at group boundaries
@@ -556,6 +625,22 @@ void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets, const
   count_launch();
 }
 
+void launch_emit_tile_keys(const RasterRec* rec, const uint32_t* offsets, const uint32_t* counts, int64_t n,
+                           int n_views, int ts, int tiles_u, int n_tiles, uint32_t* keys, uint32_t* vt_count,
+                           cudaStream_t st) {
+  const int64_t items = n * n_views;
+  if (items == 0) return;
+  k_emit_tile_keys<<<blocks_for(items, 256), 256, 0, st>>>(rec, offsets, counts, n, n_views, tiles_u, n_tiles, ts,
+                                                           keys, vt_count);
+  count_launch();
+}
+
+void launch_ranges_from_counts(const uint32_t* vt_count, int n_views, int n_tiles, int key_stride, uint32_t* start,
+                               uint32_t* end, cudaStream_t st) {
+  k_ranges_from_counts<<<1, 256, 0, st>>>(vt_count, n_views, n_tiles, key_stride, start, end);
+  count_launch();
+}
+
 void launch_ranges_swapped(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, int tile_bits, uint32_t* start,
                           uint32_t* end, cudaStream_t st) {
   if (n_keys == 0) return;
@@ -630,14 +715,15 @@ void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_
 
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
-                             int stiles_v, int key_stride, float* images, cudaStream_t st, int bulk_out) {
+                             int stiles_v, int key_stride, float* images, cudaStream_t st, int bulk_out,
+                             uint32_t vmask) {
   if (n_views == 0) return;
   const int n_stiles = stiles_u * stiles_v;
   // one warp per 32x16 half-super-tile (A/B at C2: 2x4-px lane blocks 3.65 ms, 2x8 2.96 ms,
   // 4x8 3.34 ms; CTA-shared staging with block barriers was slower still)
   dim3 g4(static_cast<unsigned>((2 * n_stiles + 3) / 4), static_cast<unsigned>(n_views));
   k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, key_stride, images,
-                                    bulk_out);
+                                    bulk_out, vmask);
   count_launch();
 }
 
