@@ -1,3 +1,1 @@
-timeout 600 python tools/bitcmp_raster.py
-timeout 600 python tools/ab_variants.py run raster c2 5
-timeout 600 python tools/ab_variants.py run raster c2 5
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
