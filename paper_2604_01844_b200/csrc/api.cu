@@ -398,14 +398,23 @@ int64_t bin_packed(gsct_ctx c, const RasterRec* rec, const uint32_t* counts, int
   uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, total);
   uint32_t* vt = ws<uint32_t>(c, S_VTCOUNT, static_cast<size_t>(n_views) * n_tiles);
   CK(cudaMemsetAsync(vt, 0, static_cast<size_t>(n_views) * n_tiles * sizeof(uint32_t), c->stream));
-  launch_emit_tile_keys(rec, offsets, counts, n, n_views, kBinTile, tiles_u, n_tiles, k1, vt, c->stream);
+  const bool wide = n_tiles > 256;
+  const int shift = wide ? 32 - tile_bits : 24;
+  if (wide)
+    launch_emit_tile_keys_wide(rec, offsets, counts, n, n_views, kBinTile, tiles_u, n_tiles, shift, k1, vt, c->stream);
+  else
+    launch_emit_tile_keys(rec, offsets, counts, n, n_views, kBinTile, tiles_u, n_tiles, k1, vt, c->stream);
   cub::DoubleBuffer<uint32_t> kb(k1, k2);
   tmp_bytes = 0;
-  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, kb, static_cast<int>(total), 24, 24 + tile_bits, c->stream));
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, kb, static_cast<int>(total), shift, shift + tile_bits,
+                                    c->stream));
   tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
-  CK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, kb, static_cast<int>(total), 24, 24 + tile_bits, c->stream));
+  CK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, kb, static_cast<int>(total), shift, shift + tile_bits, c->stream));
   *keys_out = kb.Current();
-  launch_ranges_from_counts(vt, n_views, n_tiles, key_stride, *start, *end, c->stream);
+  if (wide)
+    launch_ranges_from_counts_wide(vt, n_views, n_tiles, key_stride, *start, *end, c->stream);
+  else
+    launch_ranges_from_counts(vt, n_views, n_tiles, key_stride, *start, *end, c->stream);
   return total;
 }
 
@@ -731,7 +740,13 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
 #ifndef GSCT_BIN_PACKED
 #define GSCT_BIN_PACKED 1  // keys-only packed binning when it applies (see bin_packed)
 #endif
-      const bool packed = GSCT_BIN_PACKED && onepass && n >= 256 && n < (int64_t(1) << 24) && n_tiles <= 256;
+#ifndef GSCT_BIN_PACKED_WIDE
+#define GSCT_BIN_PACKED_WIDE 1  // packed keys also beyond 8 tile bits (2048^2: tile << 20 | splat)
+#endif
+      const bool packed_narrow = onepass && n >= 256 && n < (int64_t(1) << 24) && n_tiles <= 256;
+      const bool packed_wide = GSCT_BIN_PACKED_WIDE && !packed_narrow && tile_bits <= 12 && n >= kWideMinItems &&
+                               n < (int64_t(1) << (32 - tile_bits)) && n_tiles <= 4096;
+      const bool packed = GSCT_BIN_PACKED && (packed_narrow || packed_wide);
       {
         Phase ph(c, GSCT_PH_RASTER_BIN);
         if (packed) {
@@ -746,7 +761,7 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
               &keys, &vals, &start, &end, onepass ? tile_bits : 0);
         }
       }
-      const uint32_t vmask = packed ? 0x00FFFFFFu : 0xFFFFFFFFu;
+      const uint32_t vmask = !packed ? 0xFFFFFFFFu : (packed_wide ? (0xFFFFFFFFu >> tile_bits) : 0x00FFFFFFu);
       // host output: launch in view sub-ranges so each one's images go down while the next
       // computes (the kernel indexes keys/records/images by its own view range)
 #ifndef GSCT_FWD_SPLIT

@@ -128,6 +128,15 @@ void launch_emit_tile_keys(const RasterRec* rec, const uint32_t* offsets, const 
                            cudaStream_t st);
 void launch_ranges_from_counts(const uint32_t* vt_count, int n_views, int n_tiles, int key_stride, uint32_t* start,
                                uint32_t* end, cudaStream_t st);
+// > 256 tiles per view (key = tile << shift | splat, CTA-level shared-memory counts); a CTA
+// emits kWideItems consecutive items, so n >= kWideItems keeps it within two views
+constexpr int kWideItems = 4096;
+constexpr int kWideMinItems = kWideItems;
+void launch_emit_tile_keys_wide(const RasterRec* rec, const uint32_t* offsets, const uint32_t* counts, int64_t n,
+                                int n_views, int ts, int tiles_u, int n_tiles, int shift, uint32_t* keys,
+                                uint32_t* vt_count, cudaStream_t st);
+void launch_ranges_from_counts_wide(const uint32_t* vt_count, int n_views, int n_tiles, int key_stride,
+                                    uint32_t* start, uint32_t* end, cudaStream_t st);
 // lane-per-item backward: shape sort keys, then the pixel walk in `order`
 int bwd_vec(int n_u, const float* grad_images);  // 8, 4 or 1 floats per row load
 // true when the walk-order keys of an n_u x n_v detector are view-major (each view a

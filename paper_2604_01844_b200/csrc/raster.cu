@@ -108,6 +108,86 @@ __global__ void __launch_bounds__(256) k_emit_tile_keys(const RasterRec* __restr
   }
 }
 
+// Wide variant for > 256 tiles per view (2048^2: 4096 super-tiles, key = tile << 20 | splat):
+// each CTA emits kWideItems consecutive items (so it still spans at most two views) into
+// shared-memory bins of 2 x n_tiles counts, flushed once per CTA with integer atomics.
+__global__ void __launch_bounds__(256) k_emit_tile_keys_wide(const RasterRec* __restrict__ rec,
+                                                             const uint32_t* __restrict__ offsets,
+                                                             const uint32_t* __restrict__ counts, int64_t n,
+                                                             int n_views, int tiles_u, int n_tiles, int ts, int shift,
+                                                             uint32_t* __restrict__ keys,
+                                                             uint32_t* __restrict__ vt_count) {
+  extern __shared__ uint32_t hw[];  // [2][n_tiles]
+  const int64_t item0 = static_cast<int64_t>(blockIdx.x) * kWideItems;
+  const int vbase = static_cast<int>(item0 / n);
+  for (int k = threadIdx.x; k < 2 * n_tiles; k += blockDim.x) hw[k] = 0u;
+  __syncthreads();
+  const int64_t n_items = n * n_views;
+  for (int it = threadIdx.x; it < kWideItems; it += blockDim.x) {
+    const int64_t item = item0 + it;
+    if (item >= n_items) break;
+    const uint32_t cnt = counts[item];
+    if (!cnt) continue;
+    const int v = static_cast<int>(item / n);
+    const uint32_t i = static_cast<uint32_t>(item - static_cast<int64_t>(v) * n);
+    const RasterRec r = rec[item];
+    const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
+    const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+    uint32_t off = offsets[item];
+    uint32_t* hv = hw + (v - vbase) * n_tiles;
+    for (int tv = v0 / ts; tv <= v1 / ts; ++tv)
+      for (int tu = u0 / ts; tu <= u1 / ts; ++tu) {
+        const uint32_t t = static_cast<uint32_t>(tv * tiles_u + tu);
+        keys[off++] = (t << shift) | i;
+        atomicAdd(&hv[t], 1u);
+      }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 2 * n_tiles; k += blockDim.x) {
+    const int vv = vbase + k / n_tiles, t = k % n_tiles;
+    const uint32_t c = hw[k];
+    if (c && vv < n_views) atomicAdd(&vt_count[vv * n_tiles + t], c);
+  }
+}
+
+// Ranges for > 256 tiles: one CTA of 1024 threads, tiles in rounds of 1024 with a running base.
+__global__ void __launch_bounds__(1024) k_ranges_from_counts_wide(const uint32_t* __restrict__ vt_count, int n_views,
+                                                                  int n_tiles, int key_stride,
+                                                                  uint32_t* __restrict__ start,
+                                                                  uint32_t* __restrict__ end) {
+  __shared__ uint32_t tot[1024];
+  __shared__ uint32_t round_base;
+  if (threadIdx.x == 0) round_base = 0u;
+  for (int r0 = 0; r0 < n_tiles; r0 += 1024) {
+    const int t = r0 + threadIdx.x;
+    uint32_t sum = 0;
+    if (t < n_tiles)
+      for (int v = 0; v < n_views; ++v) sum += vt_count[v * n_tiles + t];
+    __syncthreads();
+    tot[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const uint32_t x = threadIdx.x >= static_cast<unsigned>(o) ? tot[threadIdx.x - o] : 0u;
+      __syncthreads();
+      tot[threadIdx.x] += x;
+      __syncthreads();
+    }
+    const uint32_t rb = round_base;
+    if (t < n_tiles) {
+      uint32_t base = rb + tot[threadIdx.x] - sum;
+      for (int v = 0; v < n_views; ++v) {
+        const uint32_t c = vt_count[v * n_tiles + t];
+        start[v * key_stride + t] = base;
+        end[v * key_stride + t] = base + c;
+        base += c;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) round_base = rb + tot[1023];
+    __syncthreads();
+  }
+}
+
 // [start, end) per (view, tile) of the (tile, view, splat)-ordered packed keys, from the
 // counts: one CTA, thread t owns tile t (block scan of the tile totals, then the views).
 __global__ void __launch_bounds__(256) k_ranges_from_counts(const uint32_t* __restrict__ vt_count, int n_views,
@@ -638,6 +718,23 @@ void launch_emit_tile_keys(const RasterRec* rec, const uint32_t* offsets, const 
 void launch_ranges_from_counts(const uint32_t* vt_count, int n_views, int n_tiles, int key_stride, uint32_t* start,
                                uint32_t* end, cudaStream_t st) {
   k_ranges_from_counts<<<1, 256, 0, st>>>(vt_count, n_views, n_tiles, key_stride, start, end);
+  count_launch();
+}
+
+void launch_emit_tile_keys_wide(const RasterRec* rec, const uint32_t* offsets, const uint32_t* counts, int64_t n,
+                                int n_views, int ts, int tiles_u, int n_tiles, int shift, uint32_t* keys,
+                                uint32_t* vt_count, cudaStream_t st) {
+  const int64_t items = n * n_views;
+  if (items == 0) return;
+  const size_t smem = 2 * static_cast<size_t>(n_tiles) * sizeof(uint32_t);
+  k_emit_tile_keys_wide<<<blocks_for(items, kWideItems), 256, smem, st>>>(rec, offsets, counts, n, n_views, tiles_u,
+                                                                          n_tiles, ts, shift, keys, vt_count);
+  count_launch();
+}
+
+void launch_ranges_from_counts_wide(const uint32_t* vt_count, int n_views, int n_tiles, int key_stride,
+                                    uint32_t* start, uint32_t* end, cudaStream_t st) {
+  k_ranges_from_counts_wide<<<1, 1024, 0, st>>>(vt_count, n_views, n_tiles, key_stride, start, end);
   count_launch();
 }
 
