@@ -691,10 +691,18 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     }
     // save-for-backward keeps every view's records in one buffer for the backward call
     RasterRec* saved = c->save_fb && n > 0 ? ws<RasterRec>(c, S_SAVED, static_cast<size_t>(n) * n_views) : nullptr;
+#ifndef GSCT_BIN_PACKED
+#define GSCT_BIN_PACKED 1  // keys-only packed binning when it applies (see bin_packed)
+#endif
 #ifndef GSCT_FWD_TILECAP
 #define GSCT_FWD_TILECAP 1  // 1: <= 65536 (view, tile) keys per forward chunk (16-bit sorts)
 #endif
-    int chunk = views_per_chunk(n, n_views, GSCT_FWD_TILECAP ? n_tiles : 0);
+    // the packed keys-only binning has no per-chunk key limit; the key + value fallback keeps
+    // (view, tile) keys within 16 bits (A/B at C5 with packed keys: uncapped 25-view chunks
+    // bin + forward 42.2 ms vs 43.2 capped)
+    const int tbits = bits_for(static_cast<uint32_t>(n_tiles));
+    const bool packable = GSCT_BIN_PACKED && tbits <= 12 && n >= kWideMinItems && n < (int64_t(1) << (32 - tbits));
+    int chunk = views_per_chunk(n, n_views, GSCT_FWD_TILECAP && !packable ? n_tiles : 0);
     for (int v0 = 0; v0 < n_views; v0 += chunk) {
       const int cv = std::min(chunk, n_views - v0);
       float* img = out + static_cast<int64_t>(v0) * npx;
@@ -737,9 +745,6 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       const bool onepass = GSCT_BIN_ONEPASS && tile_bits <= 8;
       const int stride = onepass ? (1 << tile_bits) : n_tiles;
       const uint32_t n_keys = static_cast<uint32_t>(cv) * static_cast<uint32_t>(stride);
-#ifndef GSCT_BIN_PACKED
-#define GSCT_BIN_PACKED 1  // keys-only packed binning when it applies (see bin_packed)
-#endif
 #ifndef GSCT_BIN_PACKED_WIDE
 #define GSCT_BIN_PACKED_WIDE 1  // packed keys also beyond 8 tile bits (2048^2: tile << 20 | splat)
 #endif
