@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-timeout 600 python tools/prof_workload.py raster c5 2
-timeout 600 python tools/prof_workload.py raster c2 5
+# scratch driver for one-off GPU A/B runs (edited per experiment; see tools/ab_variants.py)
+timeout 600 python tools/ab_variants.py run raster c2 5
