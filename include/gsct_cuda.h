@@ -152,6 +152,7 @@ enum gsct_phase {
   GSCT_PH_VOXEL_FWD,        /* K7 */
   GSCT_PH_VOXEL_BWD,        /* K8a */
   GSCT_PH_VOXEL_TAIL,       /* K8b */
+  GSCT_PH_RASTER_ORDER,     /* K4a walk order: keys + radix sort (split from RASTER_BWD) */
   GSCT_NUM_PHASES
 };
 int gsct_ctx_set_profiling(gsct_ctx ctx, int on);

@@ -975,7 +975,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
 #endif
     const uint32_t* all_order = nullptr;
     if (one_sort) {
-      Phase ph(c, GSCT_PH_RASTER_BWD);
+      Phase ph(c, GSCT_PH_RASTER_ORDER);
       const int64_t items = n * n_views;
       uint32_t* k1 = ws<uint32_t>(c, S_KEYS, static_cast<size_t>(items));
       uint32_t* v1 = ws<uint32_t>(c, S_VALS, static_cast<size_t>(items));
@@ -1001,8 +1001,8 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kTile, rec, nullptr, c->dstats, c->stream);
       }
       {
-        Phase ph(c, GSCT_PH_RASTER_BWD);
         if (one_sort) {  // walk this chunk's contiguous range of the all-view order
+          Phase ph(c, GSCT_PH_RASTER_BWD);
           // chunks alternate between two streams so a chunk's walk fills the previous one's tail
           cudaStream_t ws_ = GSCT_BWD_DUAL && (ci & 1) ? c->aux_stream : c->stream;
           if (gdev) {
@@ -1018,16 +1018,22 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         uint32_t* v1 = ws<uint32_t>(c, S_VALS, static_cast<size_t>(items));
         uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, static_cast<size_t>(items));
         uint32_t* v2 = ws<uint32_t>(c, S_VALS2, static_cast<size_t>(items));
-        const int kbits = launch_bwd_shape_keys(rec, n, cv, geom->n_u, geom->n_v, bwd_vec(geom->n_u, gimg), k1, v1, c->stream);
         cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
-        size_t tmp_bytes = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
-        void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
-        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
+        {
+          Phase po(c, GSCT_PH_RASTER_ORDER);
+          const int kbits =
+              launch_bwd_shape_keys(rec, n, cv, geom->n_u, geom->n_v, bwd_vec(geom->n_u, gimg), k1, v1, c->stream);
+          size_t tmp_bytes = 0;
+          CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits,
+                                             c->stream));
+          void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+          CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
+        }
         if (gdev) {
           CK(cudaStreamWaitEvent(c->stream, up_done[static_cast<size_t>(ci)], 0));
           c->event_pool.push_back(up_done[static_cast<size_t>(ci)]);
         }
+        Phase ph(c, GSCT_PH_RASTER_BWD);
         launch_raster_bwd_lanes(rec, vb.Current(), n, cv, geom->n_u, geom->n_v, gimg, mom, v0, c->stream);
       }
       CK(cudaGetLastError());

@@ -14,6 +14,8 @@
 // with shape-sorted work in the backward). See DESIGN.md section 4.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "gsct_internal.cuh"
 #include "packed_f32.cuh"
 
@@ -646,6 +648,220 @@ __global__ void __launch_bounds__(256, GSCT_LANES_MINB) k_raster_bwd_lanes(const
   dst[1] = make_float4(muv, mvv, 1.f, 0.f);
 }
 
+// Chain variant of K4a (the default for 32 B-aligned rows). Same ownership (one lane per
+// (view, splat) item, bbox rows walked as 32 B chunks of 8 columns, edge columns zeroed),
+// but the exponent along a row is a multiplicative chain over column PAIRS instead of one
+// MUFU.EX2 per pixel: with the packed pair g = (2^e(k), 2^e(k+1)),
+//   g(k+2) = g(k) r(k),  r(k+2) = r(k) c,  r(k) = 2^(e(k+2) - e(k)),  c = 2^(8A),
+// (e(k+2) - e(k) = A (4 du + 4) + 2 B dv is linear in k), so a row costs 4 MUFU for its
+// seeds and two packed FMULs per column pair. The per-chunk sums use compile-time column
+// offsets (Y0 = sum t, Y1 = sum t k, Y2 = sum t k^2 for k = 0..7 in the chunk), folded into
+// the row sums around the centred column k' = k - round(kappa) once per chunk. A record whose
+// chain could leave the normal fp32 range over its walked window takes the direct path.
+__device__ __forceinline__ bool raster_chain2_safe(float A, float B, float C, float dua, float dub, float dva,
+                                                   float dvb) {
+  const float emin = fminf(fminf(raster_quad_e(A, B, C, dua, dva), raster_quad_e(A, B, C, dua, dvb)),
+                           fminf(raster_quad_e(A, B, C, dub, dva), raster_quad_e(A, B, C, dub, dvb)));
+  const float da = A * fmaf(4.f, dua, 4.f), db = A * fmaf(4.f, dub, 4.f);
+  const float b2a = 2.f * B * dva, b2b = 2.f * B * dvb;
+  const float dmax = fmaxf(fmaxf(fabsf(da + b2a), fabsf(da + b2b)), fmaxf(fabsf(db + b2a), fabsf(db + b2b)));
+  return emin > -100.f && dmax < 100.f && A > -12.f;
+}
+
+#ifndef GSCT_CHAIN_MINB
+#define GSCT_CHAIN_MINB 3
+#endif
+#ifndef GSCT_CHAIN_UNROLL
+#define GSCT_CHAIN_UNROLL 1
+#endif
+constexpr int kChainUnroll = GSCT_CHAIN_UNROLL;
+__global__ void __launch_bounds__(256, GSCT_CHAIN_MINB) k_raster_bwd_chain(const RasterRec* __restrict__ rec,
+                                                                           const uint32_t* __restrict__ order,
+                                                                           int64_t n_items, int64_t n, int n_u,
+                                                                           int n_v, const float* __restrict__ grad,
+                                                                           float* __restrict__ moments, double inv_n,
+                                                                           int view_offset) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n_items) return;
+  const int64_t item = order ? static_cast<int64_t>(__ldg(order + t)) : t;
+  const RasterRec r = rec[item];
+  const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
+  const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+  const int W = u1 - u0 + 1, H = v1 - v0 + 1;
+  float4* dst = reinterpret_cast<float4*>(moments + (static_cast<int64_t>(view_offset) * n + item) * 8);
+  if (W <= 0 || H <= 0) {
+    dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int view = static_cast<int>((static_cast<double>(item) + 0.5) * inv_n);
+  const int ua = u0 & ~7;
+  const int lead = u0 - ua;
+  const int ncol = lead + W;
+  const int nch = (ncol + 7) >> 3;
+  // walked column k = 0 .. 8 nch - 1 (absolute ua + k); du = k - kap
+  const float kap = static_cast<float>(lead) + r.mo_u;
+  const float kr = rintf(kap);
+  const float dl = kap - kr;  // du = k' - dl, k' = k - kr
+  const float* __restrict__ prow = grad + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(v0) * n_u + ua;
+  const float A = r.A, B = r.B, C = r.C;
+  const bool safe = raster_chain2_safe(A, B, C, -kap, static_cast<float>(8 * nch + 1) - kap, -r.mo_v,
+                                       static_cast<float>(H - 1) - r.mo_v);
+  float m0 = 0.f, mu = 0.f, mv = 0.f, muu = 0.f, muv = 0.f, mvv = 0.f;
+  float dv = -r.mo_v;
+  const f2_t c2 = f2_bc(ex2_approx(8.f * A));
+  const f2_t KO0 = f2_pack(0.f, 1.f);
+  // edge-column masks of the first and last chunk as packed 0/1 pairs (per item, all rows)
+  f2_t MF[4], ML[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const int q0 = 2 * h, q1 = 2 * h + 1, last = 8 * (nch - 1);
+    const bool f0 = q0 >= lead && (nch > 1 || q0 < ncol), f1 = q1 >= lead && (nch > 1 || q1 < ncol);
+    MF[h] = f2_pack(f0 ? 1.f : 0.f, f1 ? 1.f : 0.f);
+    ML[h] = f2_pack(last + q0 < ncol ? 1.f : 0.f, last + q1 < ncol ? 1.f : 0.f);
+  }
+  for (int row = 0; row < H; ++row, prow += n_u, dv += 1.f) {
+    f2_t X0 = f2_bc(0.f), X1 = X0, X2 = X0;
+    if (safe) {
+      const float du0 = -kap;
+      const float bdv = B * dv, cdv2 = C * dv * dv;
+      const float e0 = fmaf(fmaf(A, du0, bdv), du0, cdv2);
+      const float e1 = fmaf(fmaf(A, du0 + 1.f, bdv), du0 + 1.f, cdv2);
+      const float d0 = fmaf(A, fmaf(4.f, du0, 4.f), 2.f * bdv);
+      const float d1 = fmaf(4.f, A, d0);
+      f2_t g = f2_pack(ex2_approx(e0), ex2_approx(e1));
+      f2_t rr = f2_pack(ex2_approx(d0), ex2_approx(d1));
+      // BE = (k'(col 0 of the chunk), k'(col 1)); per chunk, with tt_h the pair (2h, 2h+1):
+      //   Y0 = sum_h tt_h, Z = sum_h h tt_h, Q = sum_h h^2 tt_h
+      //   sum t k' = BE Y0 + 2 Z,  sum t k'^2 = BE (BE Y0 + 4 Z) + 4 Q
+      f2_t BE = f2_add(f2_bc(-kr), KO0);
+      // one 8-column chunk; kMask: first / last chunk (edge columns zeroed by the 0/1 pairs)
+      auto chunk = [&](const float* __restrict__ p, const f2_t* M, auto masked) {
+        float w[8];
+        ldg_v8(p, w);
+        f2_t W0 = f2_pack(w[0], w[1]), W1 = f2_pack(w[2], w[3]), W2 = f2_pack(w[4], w[5]),
+             W3 = f2_pack(w[6], w[7]);
+        if constexpr (decltype(masked)::value) {
+          W0 = f2_mul(W0, M[0]), W1 = f2_mul(W1, M[1]), W2 = f2_mul(W2, M[2]), W3 = f2_mul(W3, M[3]);
+        }
+        const f2_t t0 = f2_mul(g, W0);
+        g = f2_mul(g, rr);
+        rr = f2_mul(rr, c2);
+        const f2_t t1 = f2_mul(g, W1);
+        g = f2_mul(g, rr);
+        rr = f2_mul(rr, c2);
+        const f2_t t2 = f2_mul(g, W2);
+        g = f2_mul(g, rr);
+        rr = f2_mul(rr, c2);
+        const f2_t t3 = f2_mul(g, W3);
+        g = f2_mul(g, rr);
+        rr = f2_mul(rr, c2);
+        const f2_t Y0 = f2_add(f2_add(t0, t1), f2_add(t2, t3));
+        const f2_t Z = f2_fma(t3, f2_bc(3.f), f2_fma(t2, f2_bc(2.f), t1));
+        const f2_t Q = f2_fma(t3, f2_bc(9.f), f2_fma(t2, f2_bc(4.f), t1));
+        X0 = f2_add(X0, Y0);
+        X1 = f2_fma(BE, Y0, f2_fma(Z, f2_bc(2.f), X1));
+        X2 = f2_fma(BE, f2_fma(Z, f2_bc(4.f), f2_mul(BE, Y0)), f2_fma(Q, f2_bc(4.f), X2));
+        BE = f2_add(BE, f2_bc(8.f));
+      };
+      using yes = std::integral_constant<bool, true>;
+      using no = std::integral_constant<bool, false>;
+      chunk(prow, MF, yes{});
+#pragma unroll kChainUnroll
+      for (int j = 1; j < nch - 1; ++j) chunk(prow + 8 * j, nullptr, no{});
+      if (nch > 1) chunk(prow + 8 * (nch - 1), ML, yes{});
+    } else {
+      // direct path: one exp2 per pixel (the quadratic in k' evaluated per column pair)
+      float b = -kr;
+      const f2_t A2 = f2_bc(A);
+      const float bp = fmaf(B, dv, -2.f * A * dl), cp = fmaf(dv, fmaf(C, dv, -B * dl), A * dl * dl);
+      const f2_t BP2 = f2_bc(bp), CP2 = f2_bc(cp);
+#pragma unroll 1
+      for (int j = 0; j < nch; ++j, b += 8.f) {
+        float w[8];
+        ldg_v8(prow + 8 * j, w);
+        f2_t kA = f2_add(f2_bc(b), KO0);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          // E(k') = A k'^2 + B' k' + C'  (du = k' - dl)
+          const f2_t e = f2_fma(f2_fma(A2, kA, BP2), kA, CP2);
+          float e0, e1;
+          f2_unpack(e, e0, e1);
+          f2_t wp = f2_pack(w[2 * h], w[2 * h + 1]);
+          if (j == 0)
+            wp = f2_mul(wp, MF[h]);
+          else if (j == nch - 1)
+            wp = f2_mul(wp, ML[h]);
+          const f2_t tt = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), wp);
+          X0 = f2_add(X0, tt);
+          const f2_t tk = f2_mul(tt, kA);
+          X1 = f2_add(X1, tk);
+          X2 = f2_fma(tk, kA, X2);
+          kA = f2_add(kA, f2_bc(2.f));
+        }
+      }
+    }
+    float t0, t1, t2;
+    {
+      float a, c;
+      f2_unpack(X0, a, c);
+      t0 = a + c;
+      f2_unpack(X1, a, c);
+      t1 = a + c;
+      f2_unpack(X2, a, c);
+      t2 = a + c;
+    }
+    // sum t du = t1 - dl t0;  sum t du^2 = t2 - 2 dl t1 + dl^2 t0
+    const float su = fmaf(-dl, t0, t1);
+    const float suu = fmaf(dl, fmaf(dl, t0, -2.f * t1), t2);
+    m0 += t0;
+    mu += su;
+    mv = fmaf(dv, t0, mv);
+    muu += suu;
+    muv = fmaf(dv, su, muv);
+    mvv = fmaf(dv * dv, t0, mvv);
+  }
+  dst[0] = make_float4(m0, mu, mv, muu);
+  dst[1] = make_float4(muv, mvv, 1.f, 0.f);
+}
+
+// Spatial walk-order keys for the chain backward: a coarse shape class (chunks per row
+// clamped to 4, rows / 4 clamped to 15: near-uniform trip counts in a warp) then the bbox's
+// top row and left column, so the 32 lanes of a warp walk items whose rows coincide and whose
+// 32 B row chunks share 128 B lines (simulated on C2 records: L1 wavefronts per row-chunk load
+// 28.7 -> 7.9 at near-equal trip-count uniformity; the top row must be exact, the column can be
+// coarse: 24 key bits at C2 and C5). Layouts as k_bwd_shape_keys (view-major or shape-major);
+// pos = (v0 >> vs) << ub | (u0 >> us).
+#ifndef GSCT_BWD_KEY24
+#define GSCT_BWD_KEY24 1  // 1: 6-bit shape class, 24-bit keys at C2/C5; 0: 8-bit class, 32-bit keys
+#endif
+constexpr int kShape2Bits = GSCT_BWD_KEY24 ? 6 : 8;
+__global__ void k_bwd_spatial_keys(const RasterRec* __restrict__ rec, int64_t n_items, int64_t n, int vs, int us,
+                                   int ub, int pos_bits, int view_bits, int view_major, uint32_t* __restrict__ keys,
+                                   uint32_t* __restrict__ vals) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  const RasterRec r = rec[i];
+  const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
+  const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+  const int W = u1 - u0 + 1, H = v1 - v0 + 1;
+  const uint32_t view = static_cast<uint32_t>(i / n);
+  const int sp_bits = kShape2Bits + pos_bits;
+  uint32_t key = view_major ? (view << sp_bits) | ((1u << sp_bits) - 1u)
+                            : (sp_bits + view_bits >= 32 ? 0xFFFFFFFFu : (1u << (sp_bits + view_bits)) - 1u);
+  if (W > 0 && H > 0) {
+    const int nch = ((u0 & 7) + W + 7) >> 3;
+    const uint32_t shape = GSCT_BWD_KEY24
+                               ? (static_cast<uint32_t>(min(nch, 4) - 1) << 4) | static_cast<uint32_t>(min(H >> 2, 15))
+                               : (static_cast<uint32_t>(min(nch, 7)) << 5) | static_cast<uint32_t>(min(H >> 1, 31));
+    const uint32_t pos = (static_cast<uint32_t>(v0 >> vs) << ub) | static_cast<uint32_t>(u0 >> us);
+    key = view_major ? (view << sp_bits) | (shape << pos_bits) | pos
+                     : (shape << (view_bits + pos_bits)) | (view << pos_bits) | pos;
+  }
+  keys[i] = key;
+  vals[i] = static_cast<uint32_t>(i);
+}
+
 // Bbox-shape sort keys for the lane-per-item backward: (chunks per row, rows), each clamped
 // to 6 bits, so a warp's 32 items have near-identical loop trip counts. Empty items sort
 // last. Values = item index (the stable sort keeps index order inside a shape class).
@@ -779,6 +995,31 @@ int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u,
   // key within 24 bits (three radix passes). A/B (shape-major): C2 (512^2, 75 views) 6 bits
   // 3.54 ms vs 8 bits 3.60; C5 (2048^2, 8 views) 6 bits 73.5 ms, 10 bits 67.7, 12 bits 66.4;
   // (view-major, C2) 2 / 4 / 6 / 8 bits: 3.63 / 3.55 / 3.44 / 3.53 ms
+#ifndef GSCT_BWD_CHAIN
+#define GSCT_BWD_CHAIN 1  // chain backward + spatial walk order for 32 B-aligned rows
+#endif
+  if (GSCT_BWD_CHAIN && vec == 8) {
+    auto bits_of = [](int x) {
+      int b = 0;
+      while (x > 0) ++b, x >>= 1;
+      return b;
+    };
+    // 24 key bits (three radix passes) when the exact top row and >= 1 column bit fit
+    int budget = (GSCT_BWD_KEY24 ? 24 : 32) - kShape2Bits - view_bits;
+    if (budget < bits_of(n_v - 1) + 1) budget = 32 - kShape2Bits - view_bits;
+    int vs = 0, us = 0;
+    while (bits_of((n_v - 1) >> vs) + bits_of((n_u - 1) >> us) > budget) {
+      if (bits_of((n_u - 1) >> us) > 2)
+        ++us;
+      else
+        ++vs;
+    }
+    const int ub = bits_of((n_u - 1) >> us), pos_bits = bits_of((n_v - 1) >> vs) + ub;
+    k_bwd_spatial_keys<<<blocks_for(n_items, 256), 256, 0, st>>>(rec, n_items, n, vs, us, ub, pos_bits, view_bits,
+                                                                 bwd_view_major(n_u, n_v) ? 1 : 0, keys, vals);
+    count_launch();
+    return kShape2Bits + view_bits + pos_bits;
+  }
   region_bits = GSCT_REGION_BITS;
   if (region_bits == 0) {
     region_bits = 2;
@@ -798,7 +1039,10 @@ void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_
   const int64_t items = n * n_views;
   if (items == 0) return;
   const int vec = bwd_vec(n_u, grad_images);
-  if (vec == 8)
+  if (GSCT_BWD_CHAIN && vec == 8)
+    k_raster_bwd_chain<<<blocks_for(items, 256), 256, 0, st>>>(rec, order, items, n, n_u, n_v, grad_images, moments,
+                                                               1.0 / static_cast<double>(n), view_offset);
+  else if (vec == 8)
     k_raster_bwd_lanes<8><<<blocks_for(items, 256), 256, 0, st>>>(rec, order, items, n, n_u, n_v, grad_images,
                                                                   moments, 1.0 / static_cast<double>(n), view_offset);
   else if (vec == 4)

@@ -32,7 +32,7 @@ if os.environ.get("GSCT_LIB_PATH"):  # A/B experiments with alternative builds (
 GSCT_OK, GSCT_ERR_CONTRACT, GSCT_ERR_CUDA, GSCT_ERR_OOM, GSCT_ERR_PARSE = 0, 1, 2, 3, 4
 # enum gsct_phase (include/gsct_cuda.h)
 PHASES = ("raster_setup", "raster_bin", "raster_fwd", "raster_bwd", "raster_tail",
-          "voxel_setup", "voxel_bin", "voxel_fwd", "voxel_bwd", "voxel_tail")
+          "voxel_setup", "voxel_bin", "voxel_fwd", "voxel_bwd", "voxel_tail", "raster_order")
 GSCT_HOST, GSCT_DEVICE = 0, 1
 
 
