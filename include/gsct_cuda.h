@@ -11,6 +11,7 @@
  *   gsct_voxelize_bwd   <- gsct::voxelize_backward    proj/include/gsct/voxelizer.hpp:214-263
  *   gsct_debug_project  <- gsct::project_cloud        proj/include/gsct/projector.hpp:292-303
  *   gsct_debug_tile_pairs <- gsct::bin_tiles          proj/include/gsct/projector.hpp:266-286
+ *   gsct_debug_fwd_bins <- gsct::bin_tiles (tile 32)  the forward's own super-tile lists
  *   gsct_debug_voxel_boxes <- detail::prepare_voxel_splats proj/include/gsct/voxelizer.hpp:145-155
  *   gsct_host_*         <- harness/utility functions (rng.hpp, bench.hpp, synthetic.hpp,
  *                          voxelizer.hpp:76-93 sample_subvolume, projector.hpp:29-43 view_frame)
@@ -306,6 +307,15 @@ int gsct_decompress_model(gsct_ctx ctx, const uint8_t* bytes, int64_t n_bytes, i
 int gsct_debug_project(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_geometry* geom,
                        double angle, const gsct_raster_settings* rs, int32_t* rect,
                        uint8_t* flags, double* mean2d, double* conic, double* amplitude);
+/* The forward's OWN binning (the code gsct_rasterize_fwd runs: 32x32 super-tiles, the
+ * packed / key+value plan, view chunks and <= 2^30-pair binning ranges) exported as CSR:
+ * offsets[n_views * n_stiles + 1] over (view, super-tile) in view-major, tile row-major
+ * order, splats[] the ascending splat list of each. n_stiles = ceil(n_u/32) * ceil(n_v/32).
+ * *n_pairs is set; splats written only if capacity suffices. Compare with bin_tiles
+ * (projector.hpp:266-286) at tile_size 32. */
+int gsct_debug_fwd_bins(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_geometry* geom, const double* angles,
+                        int n_views, const gsct_raster_settings* rs, int64_t* offsets, uint32_t* splats,
+                        int64_t capacity, int64_t* n_pairs);
 /* Sorted (key, value) pairs of the binning of n_views views: key = view*n_tiles + tile,
  * value = splat; *n_pairs is set; arrays written only if capacity suffices. */
 int gsct_debug_tile_pairs(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_geometry* geom,

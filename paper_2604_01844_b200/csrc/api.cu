@@ -3,6 +3,7 @@
 // error mapping to the reference's contract_error messages, and RenderStats.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -25,6 +26,7 @@ enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
   S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG, S_FGSC, S_FGSC_LOG, S_FGSC_CNT, S_VTCOUNT,
+  S_TOTAL64, S_VIEWPAIRS,
   S_COUNT_SLOTS
 };
 
@@ -314,11 +316,18 @@ void finish_sync(gsct_ctx c, gsct_stats* stats, bool counters, double* ms_slot) 
   }
 }
 
-uint32_t read_scan_total(gsct_ctx c, const uint32_t* offsets, const uint32_t* counts, int64_t n) {
-  CK(cudaMemcpyAsync(c->hscratch, offsets + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(c->hscratch + 1, counts + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+// Exact 64-bit sum of per-item pair counts (the u32 scan could wrap); pairs beyond what one
+// radix sort takes are a contract error rather than a wrapped workspace.
+int64_t count_total(gsct_ctx c, const uint32_t* counts, int64_t n) {
+  unsigned long long* d = ws<unsigned long long>(c, S_TOTAL64, 1);
+  CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->stream));
+  launch_sum_u32(counts, n, d, c->stream);
+  CK(cudaMemcpyAsync(c->hscratch, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  return c->hscratch[0] + c->hscratch[1];
+  unsigned long long t = 0;
+  std::memcpy(&t, c->hscratch, sizeof t);
+  contract(t <= static_cast<unsigned long long>(INT32_MAX), "bin: more than 2^31 pairs (" + std::to_string(t) + ")");
+  return static_cast<int64_t>(t);
 }
 
 int bits_for(uint64_t n_keys) {
@@ -337,13 +346,13 @@ int bits_for(uint64_t n_keys) {
 template <class Emit>
 int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32_t n_keys,
                      Emit&& emit, uint32_t** keys_out, uint32_t** vals_out, uint32_t** start,
-                     uint32_t** end, int sort_bits = 0) {
+                     uint32_t** end, int sort_bits = 0, int64_t known_total = -1) {
   uint32_t* offsets = ws<uint32_t>(c, S_OFFSET, static_cast<size_t>(n_items));
   size_t tmp_bytes = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
   void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
   CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
-  const uint32_t total = read_scan_total(c, offsets, counts, n_items);
+  const int64_t total = known_total >= 0 ? known_total : count_total(c, counts, n_items);
   *start = ws<uint32_t>(c, S_START, n_keys);
   *end = ws<uint32_t>(c, S_END, n_keys);
   if (total == 0) {
@@ -373,49 +382,136 @@ int64_t bin_and_sort(gsct_ctx c, const uint32_t* counts, int64_t n_items, uint32
   return total;
 }
 
+// Forward binning plan (one place decides, for chunk sizing and for the binning itself):
+//  narrow packed: <= 256 super-tiles (one 8-bit pass), 256 <= n < 2^24: key = tile << 24 | splat
+//  wide packed:   <= 4096 super-tiles, n >= kWideMinItems, n < 2^(32 - tile_bits):
+//                 key = tile << (32 - tile_bits) | splat
+//  otherwise:     key + value pairs (view * stride + tile, splat)
+#ifndef GSCT_BIN_PACKED
+#define GSCT_BIN_PACKED 1  // keys-only packed binning when it applies (see bin_packed)
+#endif
+#ifndef GSCT_BIN_PACKED_WIDE
+#define GSCT_BIN_PACKED_WIDE 1  // packed keys also beyond 8 tile bits (2048^2: tile << 20 | splat)
+#endif
+#ifndef GSCT_BIN_ONEPASS
+#define GSCT_BIN_ONEPASS 1
+#endif
+struct BinPlan {
+  int tile_bits = 0;
+  bool onepass = false;  // key stride a power of two; the sort covers the tile bits only
+  int stride = 0;        // (view, tile) key stride
+  bool packed = false, wide = false;
+  int shift = 24;        // packed: tile bits start here
+  uint32_t vmask = 0xFFFFFFFFu;  // packed: splat index = key & vmask
+};
+BinPlan fwd_bin_plan(int64_t n, int n_tiles) {
+  BinPlan p;
+  p.tile_bits = bits_for(static_cast<uint32_t>(n_tiles));
+  // key = view * stride + super-tile; stride a power of two for the one-pass sort, used when
+  // the tile bits fit one 8-bit radix pass (A/B: C2 bin 0.94 -> 0.74 ms; at C5, 12 tile bits,
+  // the two-pass tile-only sort was 1.1 ms slower than the full key)
+  p.onepass = GSCT_BIN_ONEPASS && p.tile_bits <= 8;
+  p.stride = p.onepass ? (1 << p.tile_bits) : n_tiles;
+  const bool narrow = GSCT_BIN_PACKED && p.onepass && n >= 256 && n < (int64_t(1) << 24) && n_tiles <= 256;
+  const bool wide = GSCT_BIN_PACKED && GSCT_BIN_PACKED_WIDE && !narrow && p.tile_bits >= 1 && p.tile_bits <= 12 &&
+                    n >= kWideMinItems && n < (int64_t(1) << (32 - p.tile_bits)) && n_tiles <= 4096;
+  p.packed = narrow || wide;
+  p.wide = wide;
+  p.shift = wide ? 32 - p.tile_bits : 24;
+  p.vmask = !p.packed ? 0xFFFFFFFFu : (wide ? (0xFFFFFFFFu >> p.tile_bits) : 0x00FFFFFFu);
+  return p;
+}
+
+// pairs per binning pass: int-sized for the radix sort, and a bounded key workspace
+constexpr int64_t kMaxBinPairs = int64_t(1) << 30;
+
 // Packed keys-only forward binning (see k_emit_tile_keys): scan of the per-item counts,
-// emission of tile << 24 | splat with (view, tile) counts, ONE stable radix pass over the tile
-// bits (4 bytes per pair moved), ranges from the counts. Returns the number of pairs.
-int64_t bin_packed(gsct_ctx c, const RasterRec* rec, const uint32_t* counts, int64_t n, int n_views, int tiles_u,
-                   int n_tiles, int tile_bits, int key_stride, uint32_t** keys_out, uint32_t** start, uint32_t** end) {
+// emission of the packed keys with (view, tile) counts, ONE stable radix pass over the tile
+// bits (two for the wide layout; 4 bytes per pair moved), ranges from the counts. `total` is
+// the exact pair count (the set-up's per-view sums, <= kMaxBinPairs).
+void bin_packed(gsct_ctx c, const BinPlan& pl, const RasterRec* rec, const uint32_t* counts, int64_t n, int n_views,
+                int tiles_u, int n_tiles, int64_t total, uint32_t** keys_out, uint32_t** start, uint32_t** end) {
   const int64_t n_items = n * n_views;
-  uint32_t* offsets = ws<uint32_t>(c, S_OFFSET, static_cast<size_t>(n_items));
-  size_t tmp_bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
-  void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
-  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
-  const uint32_t total = read_scan_total(c, offsets, counts, n_items);
-  const uint32_t n_keys = static_cast<uint32_t>(n_views) * static_cast<uint32_t>(key_stride);
+  const uint32_t n_keys = static_cast<uint32_t>(n_views) * static_cast<uint32_t>(pl.stride);
   *start = ws<uint32_t>(c, S_START, n_keys);
   *end = ws<uint32_t>(c, S_END, n_keys);
   if (total == 0) {
     CK(cudaMemsetAsync(*start, 0, n_keys * sizeof(uint32_t), c->stream));
     CK(cudaMemsetAsync(*end, 0, n_keys * sizeof(uint32_t), c->stream));
     *keys_out = nullptr;
-    return 0;
+    return;
   }
-  uint32_t* k1 = ws<uint32_t>(c, S_KEYS, total);
-  uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, total);
+  uint32_t* offsets = ws<uint32_t>(c, S_OFFSET, static_cast<size_t>(n_items));
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
+  void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
+  uint32_t* k1 = ws<uint32_t>(c, S_KEYS, static_cast<size_t>(total));
+  uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, static_cast<size_t>(total));
   uint32_t* vt = ws<uint32_t>(c, S_VTCOUNT, static_cast<size_t>(n_views) * n_tiles);
   CK(cudaMemsetAsync(vt, 0, static_cast<size_t>(n_views) * n_tiles * sizeof(uint32_t), c->stream));
-  const bool wide = n_tiles > 256;
-  const int shift = wide ? 32 - tile_bits : 24;
-  if (wide)
-    launch_emit_tile_keys_wide(rec, offsets, counts, n, n_views, kBinTile, tiles_u, n_tiles, shift, k1, vt, c->stream);
+  if (pl.wide)
+    launch_emit_tile_keys_wide(rec, offsets, counts, n, n_views, kBinTile, tiles_u, n_tiles, pl.shift, k1, vt,
+                               c->stream);
   else
     launch_emit_tile_keys(rec, offsets, counts, n, n_views, kBinTile, tiles_u, n_tiles, k1, vt, c->stream);
   cub::DoubleBuffer<uint32_t> kb(k1, k2);
   tmp_bytes = 0;
-  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, kb, static_cast<int>(total), shift, shift + tile_bits,
-                                    c->stream));
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, kb, static_cast<int>(total), pl.shift,
+                                    pl.shift + pl.tile_bits, c->stream));
   tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
-  CK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, kb, static_cast<int>(total), shift, shift + tile_bits, c->stream));
+  CK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, kb, static_cast<int>(total), pl.shift, pl.shift + pl.tile_bits,
+                                    c->stream));
   *keys_out = kb.Current();
-  if (wide)
-    launch_ranges_from_counts_wide(vt, n_views, n_tiles, key_stride, *start, *end, c->stream);
+  if (pl.wide)
+    launch_ranges_from_counts_wide(vt, n_views, n_tiles, pl.stride, *start, *end, c->stream);
   else
-    launch_ranges_from_counts(vt, n_views, n_tiles, key_stride, *start, *end, c->stream);
-  return total;
+    launch_ranges_from_counts(vt, n_views, n_tiles, pl.stride, *start, *end, c->stream);
+}
+
+// The forward's binning of views [0, n_views) of one chunk's records (view-major, `counts`
+// their super-tile counts, `total` the exact pair count): sorted splat lists per (view,
+// super-tile) in [start, end) of `vals` (splat = vals[k] & plan.vmask). Shared by
+// gsct_rasterize_fwd and the parity export gsct_debug_fwd_bins.
+struct FwdBins {
+  const uint32_t* vals = nullptr;
+  const uint32_t* start = nullptr;
+  const uint32_t* end = nullptr;
+};
+FwdBins fwd_bin(gsct_ctx c, const BinPlan& pl, const RasterRec* rec, const uint32_t* cnt, int64_t n, int n_views,
+                int tiles_u, int n_tiles, int64_t total) {
+  uint32_t *keys = nullptr, *vals = nullptr, *start = nullptr, *end = nullptr;
+  if (pl.packed) {
+    bin_packed(c, pl, rec, cnt, n, n_views, tiles_u, n_tiles, total, &vals, &start, &end);
+  } else {
+    const uint32_t n_keys = static_cast<uint32_t>(n_views) * static_cast<uint32_t>(pl.stride);
+    bin_and_sort(
+        c, cnt, n * n_views, n_keys,
+        [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
+          launch_emit_tile_pairs(rec, offsets, cnt, n, n_views, kBinTile, tiles_u, pl.stride, k, v, c->stream);
+        },
+        &keys, &vals, &start, &end, pl.onepass ? pl.tile_bits : 0, total);
+  }
+  return FwdBins{vals, start, end};
+}
+
+// Splits a chunk's views into consecutive binning ranges of at most kMaxBinPairs pairs each
+// (per-view pair counts from the set-up); a single view above the bound is a contract error.
+std::vector<int> bin_ranges(const unsigned long long* view_pairs, int n_views) {
+  std::vector<int> cut{0};
+  unsigned long long acc = 0;
+  for (int v = 0; v < n_views; ++v) {
+    const unsigned long long p = view_pairs[v];
+    contract(p <= static_cast<unsigned long long>(kMaxBinPairs),
+             "rasterize: more than 2^30 (super-tile, splat) pairs in one view (" + std::to_string(p) + ")");
+    if (acc + p > static_cast<unsigned long long>(kMaxBinPairs)) {
+      cut.push_back(v);
+      acc = 0;
+    }
+    acc += p;
+  }
+  cut.push_back(n_views);
+  return cut;
 }
 
 // Identity of a rasterizer call for save-for-backward: cloud buffers and size, geometry,
@@ -691,18 +787,16 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     }
     // save-for-backward keeps every view's records in one buffer for the backward call
     RasterRec* saved = c->save_fb && n > 0 ? ws<RasterRec>(c, S_SAVED, static_cast<size_t>(n) * n_views) : nullptr;
-#ifndef GSCT_BIN_PACKED
-#define GSCT_BIN_PACKED 1  // keys-only packed binning when it applies (see bin_packed)
-#endif
 #ifndef GSCT_FWD_TILECAP
 #define GSCT_FWD_TILECAP 1  // 1: <= 65536 (view, tile) keys per forward chunk (16-bit sorts)
 #endif
     // the packed keys-only binning has no per-chunk key limit; the key + value fallback keeps
     // (view, tile) keys within 16 bits (A/B at C5 with packed keys: uncapped 25-view chunks
     // bin + forward 42.2 ms vs 43.2 capped)
-    const int tbits = bits_for(static_cast<uint32_t>(n_tiles));
-    const bool packable = GSCT_BIN_PACKED && tbits <= 12 && n >= kWideMinItems && n < (int64_t(1) << (32 - tbits));
-    int chunk = views_per_chunk(n, n_views, GSCT_FWD_TILECAP && !packable ? n_tiles : 0);
+    const BinPlan plan = fwd_bin_plan(n, n_tiles);
+    int chunk = views_per_chunk(n, n_views, GSCT_FWD_TILECAP && !plan.packed ? n_tiles : 0);
+    unsigned long long* dpairs = ws<unsigned long long>(c, S_VIEWPAIRS, static_cast<size_t>(chunk) + 1);
+    std::vector<unsigned long long> hpairs(static_cast<size_t>(chunk));
     for (int v0 = 0; v0 < n_views; v0 += chunk) {
       const int cv = std::min(chunk, n_views - v0);
       float* img = out + static_cast<int64_t>(v0) * npx;
@@ -717,6 +811,7 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       RasterRec* rec = saved ? saved + static_cast<int64_t>(v0) * n : ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * cv);
       uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * cv);
+      CK(cudaMemsetAsync(dpairs, 0, static_cast<size_t>(cv) * sizeof(unsigned long long), c->stream));
       {
         Phase ph(c, GSCT_PH_RASTER_SETUP);
         if (cloud_pieces > 1) {  // one view chunk: per splat range, wait for its bytes, set up
@@ -725,50 +820,35 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
             CK(cudaStreamWaitEvent(c->stream, piece_up[static_cast<size_t>(k)], 0));
             launch_splat_prepare(d, pre, pre_aos, c->dstats, c->stream, i0, i1);
             launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream, i0,
-                                     i1);
+                                     i1, dpairs);
           }
           for (cudaEvent_t e : piece_up) c->event_pool.push_back(e);
           piece_up.clear();
         } else {
-          launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream);
+          launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream, 0, -1,
+                                   dpairs);
         }
       }
       CK(cudaGetLastError());
-      uint32_t *keys, *vals, *start, *end;
-#ifndef GSCT_BIN_ONEPASS
-#define GSCT_BIN_ONEPASS 1
-#endif
-      // key = view * stride + super-tile; stride a power of two for the one-pass sort, used
-      // when the tile bits fit one 8-bit radix pass (A/B: C2 bin 0.94 -> 0.74 ms; at C5,
-      // 12 tile bits, the two-pass tile-only sort was 1.1 ms slower than the full key)
-      const int tile_bits = bits_for(static_cast<uint32_t>(n_tiles));
-      const bool onepass = GSCT_BIN_ONEPASS && tile_bits <= 8;
-      const int stride = onepass ? (1 << tile_bits) : n_tiles;
-      const uint32_t n_keys = static_cast<uint32_t>(cv) * static_cast<uint32_t>(stride);
-#ifndef GSCT_BIN_PACKED_WIDE
-#define GSCT_BIN_PACKED_WIDE 1  // packed keys also beyond 8 tile bits (2048^2: tile << 20 | splat)
-#endif
-      const bool packed_narrow = onepass && n >= 256 && n < (int64_t(1) << 24) && n_tiles <= 256;
-      const bool packed_wide = GSCT_BIN_PACKED_WIDE && !packed_narrow && tile_bits <= 12 && n >= kWideMinItems &&
-                               n < (int64_t(1) << (32 - tile_bits)) && n_tiles <= 4096;
-      const bool packed = GSCT_BIN_PACKED && (packed_narrow || packed_wide);
-      {
-        Phase ph(c, GSCT_PH_RASTER_BIN);
-        if (packed) {
-          bin_packed(c, rec, cnt, n, cv, tiles_u, n_tiles, tile_bits, stride, &vals, &start, &end);
-          keys = nullptr;
-        } else {
-          bin_and_sort(
-              c, cnt, n * cv, n_keys,
-              [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
-                launch_emit_tile_pairs(rec, offsets, cnt, n, cv, kBinTile, tiles_u, stride, k, v, c->stream);
-              },
-              &keys, &vals, &start, &end, onepass ? tile_bits : 0);
+      // exact 64-bit (super-tile, splat) pair count per view: binning ranges of <= 2^30 pairs
+      CK(cudaMemcpyAsync(hpairs.data(), dpairs, static_cast<size_t>(cv) * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      const std::vector<int> cut = bin_ranges(hpairs.data(), cv);
+      for (size_t bi = 0; bi + 1 < cut.size(); ++bi) {
+        const int b0 = cut[bi], bv = cut[bi + 1] - cut[bi];  // views [v0 + b0, v0 + b0 + bv)
+        int64_t total = 0;
+        for (int v = b0; v < b0 + bv; ++v) total += static_cast<int64_t>(hpairs[static_cast<size_t>(v)]);
+        const RasterRec* brec = rec + static_cast<int64_t>(b0) * n;
+        float* bimg = img + static_cast<int64_t>(b0) * npx;
+        FwdBins bins;
+        {
+          Phase ph(c, GSCT_PH_RASTER_BIN);
+          bins = fwd_bin(c, plan, brec, cnt + static_cast<int64_t>(b0) * n, n, bv, tiles_u, n_tiles, total);
         }
-      }
-      const uint32_t vmask = !packed ? 0xFFFFFFFFu : (packed_wide ? (0xFFFFFFFFu >> tile_bits) : 0x00FFFFFFu);
-      // host output: launch in view sub-ranges so each one's images go down while the next
-      // computes (the kernel indexes keys/records/images by its own view range)
+        const int stride = plan.stride;
+        // host output: launch in view sub-ranges so each one's images go down while the next
+        // computes (the kernel indexes keys/records/images by its own view range)
 #ifndef GSCT_FWD_SPLIT
 #define GSCT_FWD_SPLIT 4  // staged host images: view sub-ranges (single stream A/B: 1 -> +1.74 ms, 2 -> +1.50,
                           // 4 -> +2.28; alternating two streams: 2/4/6/8 -> fwd 4.82/4.65/4.79/5.15 ms
@@ -787,34 +867,36 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
 #ifndef GSCT_FWD_DUAL
 #define GSCT_FWD_DUAL 1  // staged host images: sub-range kernels alternate between two streams
 #endif
-      const bool dual = stage_images && GSCT_FWD_DUAL && GSCT_FWD_SPLIT > 1;
-      if (dual) stream_after(c, c->aux_stream, c->stream);  // after the binning
-      const int sub = stage_images ? std::max(1, (cv + GSCT_FWD_SPLIT - 1) / GSCT_FWD_SPLIT) : cv;
-      for (int vs = 0, nvs = 0, k = 0; vs < cv; vs += nvs, ++k) {
-        const int rem = cv - vs;
-        if (stage_images && GSCT_FWD_MINPIECE > 0)
-          nvs = rem <= 2 * GSCT_FWD_MINPIECE ? rem : (rem + 1) / 2;
-        else
-          nvs = std::min(sub, rem);
-        cudaStream_t fs = dual && (k & 1) ? c->aux_stream : c->stream;
-        {
-          Phase ph(c, GSCT_PH_RASTER_FWD);
-          launch_raster_fwd_super(rec + static_cast<int64_t>(vs) * n, vals, start + static_cast<int64_t>(vs) * stride,
-                                  end + static_cast<int64_t>(vs) * stride, n, nvs, geom->n_u, geom->n_v, tiles_u,
-                                  tiles_v, stride, img + static_cast<int64_t>(vs) * npx, fs,
-                                  (zc_images || GSCT_FWD_BULK_DEVICE) && GSCT_FWD_BULKSTORE ? 1 : 0, vmask);
+        const bool dual = stage_images && GSCT_FWD_DUAL && GSCT_FWD_SPLIT > 1;
+        if (dual) stream_after(c, c->aux_stream, c->stream);  // after the binning
+        const int sub = stage_images ? std::max(1, (bv + GSCT_FWD_SPLIT - 1) / GSCT_FWD_SPLIT) : bv;
+        for (int vs = 0, nvs = 0, k = 0; vs < bv; vs += nvs, ++k) {
+          const int rem = bv - vs;
+          if (stage_images && GSCT_FWD_MINPIECE > 0)
+            nvs = rem <= 2 * GSCT_FWD_MINPIECE ? rem : (rem + 1) / 2;
+          else
+            nvs = std::min(sub, rem);
+          cudaStream_t fs = dual && (k & 1) ? c->aux_stream : c->stream;
+          {
+            Phase ph(c, GSCT_PH_RASTER_FWD);
+            launch_raster_fwd_super(brec + static_cast<int64_t>(vs) * n, bins.vals,
+                                    bins.start + static_cast<int64_t>(vs) * stride,
+                                    bins.end + static_cast<int64_t>(vs) * stride, n, nvs, geom->n_u, geom->n_v,
+                                    tiles_u, tiles_v, stride, bimg + static_cast<int64_t>(vs) * npx, fs,
+                                    (zc_images || GSCT_FWD_BULK_DEVICE) && GSCT_FWD_BULKSTORE ? 1 : 0, plan.vmask);
+          }
+          CK(cudaGetLastError());
+          if (stage_images) {
+            stream_after(c, c->copy_stream, fs);
+            CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0 + b0 + vs) * npx,
+                               bimg + static_cast<int64_t>(vs) * npx, static_cast<size_t>(npx) * nvs * sizeof(float),
+                               cudaMemcpyDeviceToHost, c->copy_stream));
+          }
         }
-        CK(cudaGetLastError());
-        if (stage_images) {
-          stream_after(c, c->copy_stream, fs);
-          CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0 + vs) * npx, img + static_cast<int64_t>(vs) * npx,
-                             static_cast<size_t>(npx) * nvs * sizeof(float), cudaMemcpyDeviceToHost, c->copy_stream));
-        }
+        if (dual) stream_after(c, c->stream, c->aux_stream);
       }
-      if (dual) stream_after(c, c->stream, c->aux_stream);
     }
-    if (stage_images && n_views) stream_after(c, c->stream, c->copy_stream);
-    finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
+    if (stage_images && n_views) stream_after(c, c->stream, c->copy_stream);    finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
     if (saved) {
       c->saved_key = raster_call_key(cloud, geom, angles, n_views, rs);
       c->saved_valid = true;
@@ -1346,6 +1428,87 @@ int gsct_debug_project(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     CK(cudaMemcpyAsync(mean2d, dmean, 2 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(conic, dconic, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(amplitude, damp, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    finish_sync(c, nullptr, false, nullptr);
+  });
+}
+
+int gsct_debug_fwd_bins(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry* geom, const double* angles,
+                        int n_views, const gsct_raster_settings* rs, int64_t* offsets, uint32_t* splats,
+                        int64_t capacity, int64_t* n_pairs) {
+  return run(c, [&] {
+    validate_geometry(geom, angles, n_views);
+    contract(rs != nullptr && rs->tile_size >= 1, "bin_tiles: tile size must be at least 1");
+    contract(n_pairs != nullptr && offsets != nullptr, "debug_fwd_bins: null output");
+    reset_stats(c);
+    const Cloud d = upload_cloud(c, cloud);
+    const int64_t n = d.n;
+    const int tiles_u = (geom->n_u + kBinTile - 1) / kBinTile, tiles_v = (geom->n_v + kBinTile - 1) / kBinTile;
+    const int n_tiles = tiles_u * tiles_v;
+    *n_pairs = 0;
+    std::fill(offsets, offsets + static_cast<int64_t>(n_views) * n_tiles + 1, int64_t(0));
+    if (n == 0 || n_views == 0) {
+      finish_sync(c, nullptr, false, nullptr);
+      return;
+    }
+    std::vector<Frame> frames(static_cast<size_t>(n_views));
+    for (int v = 0; v < n_views; ++v) frames[static_cast<size_t>(v)] = make_frame(geom, angles[v]);
+    Frame* dframes = ws<Frame>(c, S_FRAMES, frames.size() + 1);
+    CK(cudaMemcpyAsync(dframes, frames.data(), frames.size() * sizeof(Frame), cudaMemcpyHostToDevice, c->stream));
+    c->saved_valid = false;
+    PreSplat* pre = ws<PreSplat>(c, S_PRE, static_cast<size_t>(n) + 1);
+    launch_splat_prepare(d, pre, ws<PreSplat>(c, S_PRE_AOS, static_cast<size_t>(n) + 1), c->dstats, c->stream);
+    const Geo g = make_geo(geom);
+    const RSet r = make_rs(rs);
+    // same plan and chunking as gsct_rasterize_fwd
+    const BinPlan plan = fwd_bin_plan(n, n_tiles);
+    const int chunk = views_per_chunk(n, n_views, !plan.packed ? n_tiles : 0);
+    unsigned long long* dpairs = ws<unsigned long long>(c, S_VIEWPAIRS, static_cast<size_t>(chunk) + 1);
+    std::vector<unsigned long long> hpairs(static_cast<size_t>(chunk));
+    std::vector<std::vector<uint32_t>> lists(static_cast<size_t>(n_views) * n_tiles);
+    for (int v0 = 0; v0 < n_views; v0 += chunk) {
+      const int cv = std::min(chunk, n_views - v0);
+      RasterRec* rec = ws<RasterRec>(c, S_REC, static_cast<size_t>(n) * cv);
+      uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n) * cv);
+      CK(cudaMemsetAsync(dpairs, 0, static_cast<size_t>(cv) * sizeof(unsigned long long), c->stream));
+      launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream, 0, -1,
+                               dpairs);
+      CK(cudaMemcpyAsync(hpairs.data(), dpairs, static_cast<size_t>(cv) * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      const std::vector<int> cut = bin_ranges(hpairs.data(), cv);
+      for (size_t bi = 0; bi + 1 < cut.size(); ++bi) {
+        const int b0 = cut[bi], bv = cut[bi + 1] - cut[bi];
+        int64_t total = 0;
+        for (int v = b0; v < b0 + bv; ++v) total += static_cast<int64_t>(hpairs[static_cast<size_t>(v)]);
+        const FwdBins bins = fwd_bin(c, plan, rec + static_cast<int64_t>(b0) * n, cnt + static_cast<int64_t>(b0) * n,
+                                     n, bv, tiles_u, n_tiles, total);
+        const size_t nk = static_cast<size_t>(bv) * plan.stride;
+        std::vector<uint32_t> hs(nk), he(nk), hv(static_cast<size_t>(total));
+        if (total > 0) {
+          CK(cudaMemcpyAsync(hs.data(), bins.start, nk * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+          CK(cudaMemcpyAsync(he.data(), bins.end, nk * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+          CK(cudaMemcpyAsync(hv.data(), bins.vals, static_cast<size_t>(total) * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, c->stream));
+        }
+        CK(cudaStreamSynchronize(c->stream));
+        for (int v = 0; v < bv && total > 0; ++v)
+          for (int t = 0; t < n_tiles; ++t) {
+            const size_t k = static_cast<size_t>(v) * plan.stride + t;
+            auto& L = lists[static_cast<size_t>(v0 + b0 + v) * n_tiles + t];
+            for (uint32_t q = hs[k]; q < he[k]; ++q) L.push_back(hv[q] & plan.vmask);
+          }
+      }
+    }
+    int64_t acc = 0;
+    for (size_t k = 0; k < lists.size(); ++k) {
+      offsets[k] = acc;
+      acc += static_cast<int64_t>(lists[k].size());
+    }
+    offsets[lists.size()] = acc;
+    *n_pairs = acc;
+    if (splats && acc <= capacity)
+      for (size_t k = 0; k < lists.size(); ++k)
+        std::copy(lists[k].begin(), lists[k].end(), splats + offsets[k]);
     finish_sync(c, nullptr, false, nullptr);
   });
 }

@@ -83,10 +83,13 @@ struct Window {
 // pre: structure-of-arrays set-up (pre_store/pre_load); pre_aos: the same, array-of-structs
 void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevStats* stats, cudaStream_t st,
                           int64_t i0 = 0, int64_t i1 = -1);  // splats [i0, i1), -1 = n
+// view_pairs (optional): per-view 64-bit sums of tile_count, accumulated with atomics
 void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
                               const Geo& g, const RSet& rs, int bin_ts, RasterRec* rec,
                               uint32_t* tile_count, DevStats* stats, cudaStream_t st, int64_t i0 = 0,
-                              int64_t i1 = -1);
+                              int64_t i1 = -1, unsigned long long* view_pairs = nullptr);
+// *total += sum of counts[0, n) (64-bit)
+void launch_sum_u32(const uint32_t* counts, int64_t n, unsigned long long* total, cudaStream_t st);
 // (tail.cu) acc: fp64 [11][N] view sum (g_pos 3, g_sigma 6, g_raw, sum |dL/dmean2d|);
 // moments: view-major [n_views][N] x 8 fp32 {t, t du, t dv, t du^2, t du dv, t dv^2,
 // visible, 0} covering every view of the call

@@ -5,6 +5,8 @@
 // (see splat_fp64.cuh): integer boxes and keys are bit-exact with the CPU oracle.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "gsct_internal.cuh"
 
 namespace gsct_dev {
@@ -65,16 +67,17 @@ __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const 
                                                            RSet rs, int bin_ts,
                                                            RasterRec* __restrict__ rec,
                                                            uint32_t* __restrict__ tile_count,
-                                                           DevStats* __restrict__ st) {
+                                                           DevStats* __restrict__ st,
+                                                           unsigned long long* __restrict__ view_pairs) {
   const int64_t i = i0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   unsigned long long n_culled = 0, n_degen = 0, n_tp = 0, n_pp = 0;
   PreSplat s;
   if (i < i1) pre_load(pre, n, i, s);  // once per thread, reused for its kPreViews views
   for (int vg = 0; vg < kPreViews; ++vg) {
   const int v = blockIdx.y * kPreViews + vg;
+  uint32_t cnt = 0;
   if (i < i1 && v < n_views) {
     RasterRec r = empty_rec();
-    uint32_t cnt = 0;
     if (s.status == 0) {
       Proj p;
       project_full(frames[v], g, s.pos, s.sigma, s.sigma_inv, s.det_ok != 0, s.density, rs, p);
@@ -110,6 +113,11 @@ __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const 
     const int64_t item = static_cast<int64_t>(v) * n + i;
     rec[item] = r;
     if (tile_count) tile_count[item] = cnt;
+  }
+  // per-view pair totals (every lane of the warp shares the view: blockIdx.y)
+  if (view_pairs && v < n_views) {
+    const uint32_t ws = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && ws) atomicAdd(view_pairs + v, static_cast<unsigned long long>(ws));
   }
   }
   warp_add(&st->culled, n_culled);
@@ -298,12 +306,28 @@ void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevS
 
 void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views, const Geo& g,
                               const RSet& rs, int bin_ts, RasterRec* rec, uint32_t* tile_count,
-                              DevStats* stats, cudaStream_t st, int64_t i0, int64_t i1) {
+                              DevStats* stats, cudaStream_t st, int64_t i0, int64_t i1,
+                              unsigned long long* view_pairs) {
   if (i1 < 0) i1 = n;
   if (i1 <= i0 || n_views == 0) return;
   dim3 grid(blocks_for(i1 - i0, 128), static_cast<unsigned>((n_views + kPreViews - 1) / kPreViews));
   k_raster_preprocess<<<grid, 128, 0, st>>>(pre, n, i0, i1, n_views, frames_dev, g, rs, bin_ts, rec, tile_count,
-                                            stats);
+                                            stats, tile_count ? view_pairs : nullptr);
+  count_launch();
+}
+
+__global__ void k_sum_u32(const uint32_t* __restrict__ counts, int64_t n, unsigned long long* __restrict__ total) {
+  unsigned long long acc = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    acc += counts[i];
+  warp_add(total, acc);
+}
+
+void launch_sum_u32(const uint32_t* counts, int64_t n, unsigned long long* total, cudaStream_t st) {
+  if (n <= 0) return;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  k_sum_u32<<<blocks, 256, 0, st>>>(counts, n, total);
   count_launch();
 }
 

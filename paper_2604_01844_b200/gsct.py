@@ -160,6 +160,8 @@ _SIGS = {
                                            C.c_void_p, _P(c_grads)]),
     "gsct_debug_project": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), C.c_double, _P(c_raster_settings),
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gsct_debug_fwd_bins": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), _P(C.c_double), C.c_int,
+                                      _P(c_raster_settings), C.c_void_p, C.c_void_p, C.c_int64, _P(C.c_int64)]),
     "gsct_debug_tile_pairs": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), _P(C.c_double), C.c_int,
                                         _P(c_raster_settings), C.c_void_p, C.c_void_p, C.c_int64,
                                         _P(C.c_int64)]),
@@ -783,6 +785,30 @@ def tile_pairs(cloud: GaussianCloud, geometry: ScanGeometry, view_indices=None,
                                              int(ang.size), C.byref(rs), keys.ctypes.data, vals.ctypes.data,
                                              n_pairs.value, C.byref(n_pairs)))
     return keys[: n_pairs.value], vals[: n_pairs.value]
+
+
+def forward_bins(cloud: GaussianCloud, geometry: ScanGeometry, view_indices=None,
+                 settings: RasterSettings = RasterSettings(), ctx: Optional[Context] = None):
+    """The forward's own binning (gsct_debug_fwd_bins): CSR offsets over (view, 32x32
+    super-tile), view-major, and the ascending splat lists. Equals bin_tiles at tile_size 32
+    (projector.hpp:266-286) per view."""
+    ctx = _ctx_for(cloud, ctx)
+    ang = _angles(geometry, view_indices)
+    keep: list = []
+    cc = cloud._c(keep)
+    g = geometry.c()
+    rs = settings.c()
+    n_st = ((geometry.n_u + 31) // 32) * ((geometry.n_v + 31) // 32)
+    offsets = np.zeros(int(ang.size) * n_st + 1, dtype=np.int64)
+    n_pairs = C.c_int64(0)
+    ctx.check(ctx._lib.gsct_debug_fwd_bins(ctx.handle, C.byref(cc), C.byref(g), ang.ctypes.data_as(_P(C.c_double)),
+                                           int(ang.size), C.byref(rs), offsets.ctypes.data, None, 0,
+                                           C.byref(n_pairs)))
+    splats = np.zeros(max(n_pairs.value, 1), dtype=np.uint32)
+    ctx.check(ctx._lib.gsct_debug_fwd_bins(ctx.handle, C.byref(cc), C.byref(g), ang.ctypes.data_as(_P(C.c_double)),
+                                           int(ang.size), C.byref(rs), offsets.ctypes.data, splats.ctypes.data,
+                                           n_pairs.value, C.byref(n_pairs)))
+    return offsets, splats[: n_pairs.value]
 
 
 def bin_tiles(cloud: GaussianCloud, geometry: ScanGeometry, angle_index: int,

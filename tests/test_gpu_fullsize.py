@@ -3,9 +3,9 @@ reference compiled here (oracle/_ref, all host threads), plus size-independent p
 over the whole workload:
 
   C2 (paper standard): 200k-Gaussian Shepp-Logan cloud, 75 cone views at 512^2
-    * every view's RenderStats counters exact vs the reference (per-view tile/pixel pairs);
-    * two full views (forward images and backward gradients with a seeded U(-1,1) grad
-      image) within the parity tolerance;
+    * two full views (0 and 37): RenderStats counters exact vs the reference, forward
+      images and backward gradients (seeded U(-1,1) grad image) within the parity
+      tolerance (every view's counters and the 75-view gradient sum: test_gpu_configs.py);
     * all 75 views: bit-identical re-run (fwd and bwd), power-of-two density homogeneity
       bitwise (tau = 1e-12 as test_projector.cpp:221-249).
   C5 (scaling run): 1M Gaussians, one 2048^2 cone view: counters exact, image and gradients
