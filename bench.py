@@ -6,8 +6,10 @@ configs[1], SURVEY.md 8d "C2"): 75 cone-beam views at 512^2 of a 200k-Gaussian
 Shepp-Logan phantom cloud in a 256^3 volume, one step = forward projection of all 75
 views + backward (per-Gaussian gradients summed over the views), device-resident.
 `e2e` is the same step through the C ABI with pinned HOST buffers (cloud up, grad images
-up, images and gradients down inside the timed region). Secondary lines: fwd+bwd proj/s
-at 2048^2 (1M Gaussians, C5) and voxelization Gvox/s at 512^3 (500k Gaussians, C3).
+up, images and gradients down inside the timed region). The other two metric numbers are
+full lines of their own under `secondary`: fwd+bwd proj/s at 2048^2 (C5: 1M Gaussians, all
+75 views per step) and voxelization Gvox/s at 512^3 (C3: 500k Gaussians) plus 1024^3 (C5's
+volume), each with a roofline object and the reference CPU figure.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...   (views sharded across ranks,
@@ -18,9 +20,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
-import tempfile
+import threading
 import time
 from pathlib import Path
 
@@ -39,10 +40,38 @@ WORKLOADS = {
     "c5": (1024, 1_000_000, 75, 2048),
 }
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+# SURVEY.md 8(d) compulsory bytes: per splat 44 B of parameters read per pass, 49 B of
+# gradients written by the backward; 4 B per pixel / voxel written (forward) or read (backward)
+PARAM_B, GRAD_B, PX_B = 44, 49, 4
+# FMA-pipe ops per pair the reference formulation costs: fwd ~4, raster bwd
+# ~12, voxel bwd ~20 (the FMA sub-bound beside the MUFU-pair bound)
+FMA_PER_PAIR = {"raster_fwd": 4, "raster_bwd": 12, "voxel_fwd": 4, "voxel_bwd": 20}
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_for(name: str, world: int = 1) -> dict:
+    """The workload description shared by both arms (same string, same keys)."""
+    side, n, views, det = WORKLOADS[name]
+    return {"workload": f"{name.upper()}: {n} Gaussians (seeded 3D Shepp-Logan phantom cloud), {side}^3 volume, "
+                        f"{views} cone views at {det}^2, fwd+bwd of every view per step",
+            "gaussians": n, "views": views, "detector": [det, det], "volume_side": side,
+            "parallelism": f"views sharded over {world} GPU(s)",
+            "l2": "flushed between timed steps (256 MiB memset outside the events)",
+            "settings": "reference defaults: tau 1e-4, sigma_cap 3, 16x16 tiles, 0.3 px^2 dilation",
+            "grad_images": "all-ones (bench.hpp:114-115)"}
 
 
 # ---------------------------------------------------------------------------------------
@@ -57,6 +86,19 @@ def make_workload(name: str, seed: int = 0):
     return cloud, geom
 
 
+def make_workload_ref(ref, name: str, seed: int = 0):
+    """The same inputs built without the product library: the phantom cloud drawn with the
+    reference's Rng and default_geometry (synthetic.hpp:246-271) from oracle/_ref
+    (bit-identical to make_workload: tests/test_capi.py)."""
+    from paper_2604_01844_b200.gsct import GaussianCloud, ScanGeometry  # pure-Python value types
+
+    side, n, views, det = WORKLOADS[name]
+    pos, ls, q, raw = ref.shepp_logan_cloud(n, side, 1.0, seed)
+    g, ang = ref.default_geometry((side, side, side), 1.0, views, 1, det, det)
+    geom = ScanGeometry("cone", g.n_u, g.n_v, g.s_u, g.s_v, list(ang), g.source_to_origin, g.origin_to_detector)
+    return GaussianCloud(pos, ls, q, raw), geom
+
+
 def shard_views(n_views: int, rank: int, world: int) -> list[int]:
     """View sharding: rank r owns views {v : v mod P == r}."""
     from paper_2604_01844_b200.sharding import shard_views as _sv
@@ -65,56 +107,60 @@ def shard_views(n_views: int, rank: int, world: int) -> list[int]:
 
 
 # ---------------------------------------------------------------------------------------
-# clocks (nvidia-smi sampled during the timed region)
+# clocks sampled DURING the timed region (NVML in a thread, 2 ms period)
 # ---------------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, device: int):
-        self.device = device
-        self.proc = None
-        self.path = None
+    def __init__(self, device: int, period_s: float = 0.002):
+        self.device, self.period = device, period_s
+        self.rows: list[tuple[int, int, int, float]] = []  # (sm MHz, max MHz, reasons, power W)
+        self._stop = threading.Event()
+        self._thr = None
+        self._nv = None
+
+    def _poll(self):
+        nv, h = self._nv, self._h
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.rows.append((int(sm), int(smax), int(rs), float(pw)))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __enter__(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self._nv, self._h = nv, nv.nvmlDeviceGetHandleByIndex(self.device)
+            self._thr = threading.Thread(target=self._poll, daemon=True)
+            self._thr.start()
+            time.sleep(0.01)
         except Exception:
-            self.proc = None
-        time.sleep(0.25)
+            self._nv = None
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join(timeout=2)
 
     def summary(self) -> dict:
-        rows = []
-        try:
-            for line in open(self.path):
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 9 and parts[1].isdigit():
-                    rows.append(parts)
-        except Exception:
-            pass
-        if not rows:
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [int(r[1]) for r in rows]
-        sm_max = max(int(r[2]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        sm = [r[0] for r in self.rows]
+        sm_max = max(r[1] for r in self.rows)
+        reasons = sorted({name for r in self.rows for bit, name in self.REASONS.items() if r[2] & bit})
         loaded = [s for s in sm if s > 0.5 * sm_max] or sm
         return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": sm_max, "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("", "[N/A]"))}
+                "samples": len(self.rows), "power_w_max": round(max(r[3] for r in self.rows), 1),
+                "source": "NVML, 2 ms period, inside the timed region"}
 
 
 # ---------------------------------------------------------------------------------------
@@ -233,21 +279,74 @@ def run_e2e(ctx, cloud, geom, views, k: int, w: int, world: int = 1) -> dict:
     return {"ms": ts, "h2d": h2d, "d2h": d2h}
 
 
-def cpu_baseline_sample(cloud, geom, budget_s: float = 10.0, max_views: int = 75) -> dict:
-    """The unchanged reference (oracle/_ref/libgsct_ref.so) on every host core: fwd+bwd of
-    the first views of the same workload until the time budget (bounded sample)."""
-    from oracle.oracle import Ref
-    from paper_2604_01844_b200 import gsct
+# ---------------------------------------------------------------------------------------
+# roofline objects (live CUDA-event kernel phases; SURVEY.md 8d units)
+# ---------------------------------------------------------------------------------------
+def _peaks(ctx) -> dict:
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    return {"hbm": peaks.get("hbm_gbs", 6650.0),
+            "hbm_src": "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)",
+            "ex2": ctx.microbench("ex2"), "ffma": ctx.microbench("ffma")}
 
-    ref = Ref()
+
+def _ncu_traffic(tag: str, kernel: str):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full summary."""
+    try:
+        prof = json.loads((ROOT / "profiles" / tag / "summary.json").read_text())
+        hit = [d for d in prof if d["kernel"] == kernel and "dram_bytes" in d]
+        if hit:
+            return int(np.mean([d["dram_bytes"] for d in hit])), hit[0]
+    except Exception:
+        pass
+    return None, None
+
+
+def roofline_objects(peaks: dict, phase: str, kernel: str, ms_total: float, launches: int, algo_bytes_step: float,
+                     pairs_step: float, steps: int, ncu_tag: str) -> tuple[dict, dict]:
+    """`roofline` (HBM: SURVEY 8d compulsory bytes of the kernel's launches / its measured
+    launch time) and `roofline_sfu` (splat-pair rate vs the on-box MUFU ex2 peak, the bound
+    SURVEY 8d names; the FMA sub-bound beside it)."""
+    launches_per_step = max(launches // max(steps, 1), 1)
+    avg_ms = ms_total / max(launches, 1)
+    algo_bytes = algo_bytes_step / launches_per_step
+    pairs = pairs_step / launches_per_step
+    achieved = algo_bytes / (avg_ms / 1e3) / 1e9
+    rate = pairs / (avg_ms / 1e3)
+    traffic, meas = _ncu_traffic(ncu_tag, kernel)
+    roof = {"bound": "hbm", "kernel": kernel, "achieved": round(achieved, 2), "peak": peaks["hbm"], "unit": "GB/s",
+            "frac": round(achieved / peaks["hbm"], 4), "traffic": traffic, "peak_source": peaks["hbm_src"],
+            "algorithmic_bytes_per_launch": int(algo_bytes), "avg_launch_ms": round(avg_ms, 4),
+            "launches_per_step": launches_per_step,
+            "algorithmic_bytes_def": "SURVEY.md 8(d): 44 B params read + 49 B grads written (bwd) per (view, splat), "
+                                     "4 B per pixel/voxel written (fwd) or read (bwd)",
+            "note": "compulsory HBM bytes are a few % of peak by design; the binding units are MUFU/FMA "
+                    "(roofline_sfu) -- see profiles/ for the pipe utilisation"}
+    if meas:
+        roof["ncu"] = {k: meas[k] for k in ("issue_active_pct", "fma_pipe_pct", "xu_pipe_pct", "l1tex_throughput_pct",
+                                             "warps_active_pct", "duration_ms") if k in meas}
+        roof["ncu"]["source"] = f"profiles/{ncu_tag}/summary.json"
+    fma = FMA_PER_PAIR[phase]
+    sfu = {"bound": "sfu_ex2", "kernel": kernel, "achieved": rate, "peak": peaks["ex2"],
+           "unit": "splat-pairs/s (one exp per pair in the reference, projector.hpp:341,410 / voxelizer.hpp:184,242)",
+           "frac": round(rate / peaks["ex2"], 4), "pairs_per_launch": int(pairs),
+           "fma_subbound": {"ops_per_pair": fma, "peak_ffma_per_s": peaks["ffma"],
+                            "frac": round(rate * fma / peaks["ffma"], 4)},
+           "note": "peaks = on-box MUFU ex2.approx / FFMA microbenchmarks in this run"}
+    return roof, sfu
+
+
+def cpu_baseline_views(ref, cloud, geom, n_views: int, budget_s: float = 15.0) -> dict:
+    """The unchanged reference on every host core: fwd+bwd of the first views (bounded)."""
+    from paper_2604_01844_b200.gsct import RasterSettings
+
     cores = ref.threads()
     h = ref.cloud(cloud)
-    rs = gsct.RasterSettings()
+    rs = RasterSettings()
     ones = np.ones((geom.n_v, geom.n_u))
     n = cloud.size()
     done, t_total = 0, 0.0
     try:
-        while done < max_views and t_total < budget_s:
+        while done < n_views and t_total < budget_s:
             t0 = time.perf_counter()
             ref.rasterize_view(h, geom, done, rs)
             ref.rasterize_backward(h, geom, done, ones, rs, n)
@@ -255,24 +354,146 @@ def cpu_baseline_sample(cloud, geom, budget_s: float = 10.0, max_views: int = 75
             done += 1
     finally:
         ref.free_cloud(h)
-    return {"value": done / t_total, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"first {done} of {len(geom.angles)} views, fwd+bwd (rasterize_view + rasterize_backward), "
-                      f"{t_total:.1f} s wall on {cores} threads; per-view rate"}
+    return {"value": round(done / t_total, 4), "unit": UNIT, "cores": cores, "kind": "reference",
+            "cpu": cpu_model(),
+            "sample": f"first {done} of {len(geom.angles)} views, fwd+bwd (rasterize_view + rasterize_backward, "
+                      f"projector.hpp:308,371), {t_total:.1f} s wall on {cores} threads; per-view rate"
+                      + (" (75-view step extrapolated linearly)" if done < len(geom.angles) else "")}
 
 
-def secondary_2k(ctx, n_views_measured: int = 8, k: int = 3) -> dict:
+def cpu_baseline_voxel(ref, cloud, side: int, slices: int = 64, with_bwd: bool = True) -> dict:
+    """The reference's voxelize (+ voxelize_backward) on a z-slab of `slices` slices of the
+    side^3 grid (GridRegion::of_parent, voxelizer.hpp:53-66), all host threads; Gvox/s of the
+    slab extrapolated to the full grid (labelled)."""
+    from paper_2604_01844_b200.gsct import GridRegion, GridSpec, VoxelSettings
+
+    cores = ref.threads()
+    grid = GridSpec.centered((side,) * 3, 1.0)
+    z0 = side // 2 - slices // 2
+    region = GridRegion.of_parent(grid, (0, 0, z0), (side, side, slices))
+    vs = VoxelSettings()
+    h = ref.cloud(cloud)
+    try:
+        t0 = time.perf_counter()
+        vol, _ = ref.voxelize(h, region, vs)
+        tf = time.perf_counter() - t0
+        tb = 0.0
+        if with_bwd:
+            gv = np.ones_like(vol)
+            t0 = time.perf_counter()
+            ref.voxelize_backward(h, region, gv, vs, cloud.size())
+            tb = time.perf_counter() - t0
+    finally:
+        ref.free_cloud(h)
+    nvox = side * side * slices
+    out = {"value": round(nvox / (tf + tb) / 1e9, 6), "unit": "Gvox/s", "cores": cores, "kind": "reference",
+           "cpu": cpu_model(), "fwd_gvox_per_s": round(nvox / tf / 1e9, 6),
+           "sample": f"{slices}-slice z-slab ({side}x{side}x{slices}) of the {side}^3 grid, voxelize"
+                     + (" + voxelize_backward (ones)" if with_bwd else "") +
+                     f" (voxelizer.hpp:162,214), {tf + tb:.1f} s wall on {cores} threads; Gvox/s extrapolated to "
+                     f"the full grid"}
+    return out
+
+
+# ---------------------------------------------------------------------------------------
+# secondary lines: C5 (2048^2, 75 views), C3 (512^3), C5 volume (1024^3), C2 training step
+# ---------------------------------------------------------------------------------------
+def secondary_2k(ctx, peaks, ref, k: int = 5) -> dict:
+    import torch
+
+    cloud, geom = make_workload("c5")
+    views = list(range(len(geom.angles)))
+    st = DeviceStep(ctx, cloud, geom, views, 1)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=st.dev)
+    from paper_2604_01844_b200 import gsct
+
+    stats = gsct.RenderStats()
+    ctx.set_async(False)
+    gsct.rasterize_views(st.dcloud, geom, views, st.rs, stats, out=st.images, ctx=ctx)
+    ctx.set_async(True)
+    for _ in range(3):
+        st()
+    ctx.set_profiling(True)
+    ctx.phase_times()
+    ts = timed_steps(st, st.stream, k, lambda: flush.zero_())
+    ph = ctx.phase_times()
+    ctx.set_profiling(False)
+    ms = float(np.mean(ts))
+    n, nv, npx = cloud.size(), len(views), geom.n_u * geom.n_v
+    dom = max(("raster_fwd", "raster_bwd"), key=lambda p: ph[p][0])
+    bytes_step = nv * ((PARAM_B + (GRAD_B if dom == "raster_bwd" else 0)) * n + PX_B * npx)
+    roof, sfu = roofline_objects(peaks, dom, "k_raster_fwd4" if dom == "raster_fwd" else "k_raster_bwd_chain",
+                                 ph[dom][0], ph[dom][1], bytes_step, stats.pixel_pairs, k, "r2/raster_c5")
+    out = {"metric": "fwd+bwd projections/s at 2048^2", "value": round(nv / (ms / 1e3), 2), "unit": UNIT,
+           "ms_per_step": round(ms, 3), "steps": k, "warmup": 3, "step_ms": [round(t, 2) for t in ts],
+           "config": {"workload": "C5: 1M Gaussians (3D Shepp-Logan phantom cloud), 1024^3 volume, 75 cone views "
+                                  "at 2048^2, fwd+bwd of every view per step (device-resident, L2 flushed)"},
+           "work": {"pixel_pairs_per_pass": stats.pixel_pairs, "tile_pairs_per_step": stats.tile_pairs},
+           "phase_ms_per_step": {p: round(v[0] / k, 3) for p, v in ph.items() if v[1]},
+           "roofline": roof, "roofline_sfu": sfu}
+    if ref is not None:
+        out["cpu_baseline"] = cpu_baseline_views(ref, cloud, geom, 3, budget_s=60.0)
+    del st
+    torch.cuda.empty_cache()
+    return out
+
+
+def _voxel_line(ctx, peaks, ref, side: int, n: int, seed: int, k: int, ncu_tag: str, name: str) -> dict:
     import torch
     from paper_2604_01844_b200 import gsct
 
-    cloud, geom = make_workload("c5")
-    views = list(range(n_views_measured))
-    st = DeviceStep(ctx, cloud, geom, views, 1)
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=st.dev)
-    st()
-    ts = timed_steps(st, st.stream, k, lambda: flush.zero_())
-    ms = float(np.mean(ts))
-    return {"proj_per_s_2048": n_views_measured / (ms / 1e3), "workload": "C5: 1M Gaussians, 1024^3 SL cloud, "
-            f"cone 2048^2, fwd+bwd of {n_views_measured} of 75 views per step (per-view rate)", "ms_per_step": ms}
+    cloud_h = gsct.make_cloud("shepp_logan", n, seed=seed, side=side, spacing=1.0)
+    cloud = cloud_h.to_device(ctx.device)
+    grid = gsct.GridSpec.centered((side, side, side), 1.0)
+    region = gsct.GridRegion.covering(grid)
+    vs = gsct.VoxelSettings()
+    dev = torch.device(f"cuda:{ctx.device}")
+    vol = torch.empty((side, side, side), dtype=torch.float32, device=dev)
+    gvol = torch.ones_like(vol)
+    grads = gsct.ParamGradients.zeros(n, ctx.device)
+    stream = torch.cuda.ExternalStream(int(gsct.lib().gsct_ctx_stream(ctx.handle)), device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    fwd = lambda: gsct.voxelize(cloud, region, vs, out=vol, ctx=ctx)
+    bwd = lambda: gsct.voxelize_backward(cloud, region, gvol, vs, out=grads, ctx=ctx)
+    stats = gsct.RenderStats()
+    ctx.set_async(False)
+    gsct.voxelize(cloud, region, vs, stats, out=vol, ctx=ctx)
+    ctx.set_async(True)
+    for _ in range(3):
+        fwd()
+        bwd()
+    ctx.set_profiling(True)
+    ctx.phase_times()
+    tf = float(np.mean(timed_steps(fwd, stream, k, lambda: flush.zero_())))
+    phf = ctx.phase_times()
+    tb = float(np.mean(timed_steps(bwd, stream, k, lambda: flush.zero_())))
+    phb = ctx.phase_times()
+    ctx.set_profiling(False)
+    nvox = side ** 3
+    # dominant kernel of the fwd+bwd pair
+    f_ms, f_cnt = phf["voxel_fwd"]
+    b_ms, b_cnt = phb["voxel_bwd"]
+    if b_ms >= f_ms:
+        roof, sfu = roofline_objects(peaks, "voxel_bwd", "k_voxel_bwd_lanes", b_ms, b_cnt,
+                                     PX_B * nvox + (PARAM_B + GRAD_B) * n, stats.pixel_pairs, k, ncu_tag)
+    else:
+        roof, sfu = roofline_objects(peaks, "voxel_fwd", "k_voxel_fwd2", f_ms, f_cnt, PX_B * nvox + PARAM_B * n,
+                                     stats.pixel_pairs, k, ncu_tag)
+    out = {"metric": f"voxelize Gvox/s at {side}^3", "value": round(nvox / (tf / 1e3) / 1e9, 3), "unit": "Gvox/s",
+           "fwd_bwd_gvox_per_s": round(nvox / ((tf + tb) / 1e3) / 1e9, 3), "fwd_ms": round(tf, 4),
+           "bwd_ms": round(tb, 4), "steps": k, "voxel_pairs": stats.pixel_pairs,
+           "config": {"workload": f"{name}: {n} Gaussians (3D Shepp-Logan phantom cloud) into a {side}^3 grid, "
+                                  "voxelize_full (value) and + voxelize_backward with an all-ones grad volume "
+                                  "(fwd_bwd_gvox_per_s), device-resident, L2 flushed"},
+           "phase_ms_fwd": {p: round(v[0] / k, 4) for p, v in phf.items() if v[1]},
+           "phase_ms_bwd": {p: round(v[0] / k, 4) for p, v in phb.items() if v[1]},
+           "roofline": roof, "roofline_sfu": sfu}
+    if ref is not None:
+        cb = cpu_baseline_voxel(ref, cloud_h, side, 64, with_bwd=True)
+        out["cpu_baseline"] = {**cb, "value": cb["fwd_gvox_per_s"], "fwd_bwd_gvox_per_s": cb["value"]}
+    del vol, gvol, grads, cloud
+    torch.cuda.empty_cache()
+    return out
 
 
 def secondary_train(ctx, k: int = 5) -> dict:
@@ -310,37 +531,6 @@ def secondary_train(ctx, k: int = 5) -> dict:
     return {"workload": "C2 training iteration: 75 views render + L1/SSIM2D loss + backward + Adam (device-resident)",
             "ms_per_iteration": ms, "proj_per_s": len(views) / (ms / 1e3),
             "mean_view_loss_first_last": [losses[0], losses[-1]], "iterations": len(losses)}
-
-
-def secondary_voxel(ctx, k: int = 3) -> dict:
-    import torch
-    from paper_2604_01844_b200 import gsct
-
-    side, n = 512, 500_000
-    cloud = gsct.make_cloud("shepp_logan", n, seed=1, side=side, spacing=1.0).to_device(ctx.device)
-    grid = gsct.GridSpec.centered((side, side, side), 1.0)
-    region = gsct.GridRegion.covering(grid)
-    vs = gsct.VoxelSettings()
-    dev = torch.device(f"cuda:{ctx.device}")
-    vol = torch.empty((side, side, side), dtype=torch.float32, device=dev)
-    gvol = torch.ones_like(vol)
-    grads = gsct.ParamGradients.zeros(n, ctx.device)
-    stream = torch.cuda.ExternalStream(int(gsct.lib().gsct_ctx_stream(ctx.handle)), device=dev)
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    fwd = lambda: gsct.voxelize(cloud, region, vs, out=vol, ctx=ctx)
-    bwd = lambda: gsct.voxelize_backward(cloud, region, gvol, vs, out=grads, ctx=ctx)
-    stats = gsct.RenderStats()
-    ctx.set_async(False)
-    gsct.voxelize(cloud, region, vs, stats, out=vol, ctx=ctx)
-    ctx.set_async(True)
-    fwd()
-    bwd()
-    tf = float(np.mean(timed_steps(fwd, stream, k, lambda: flush.zero_())))
-    tb = float(np.mean(timed_steps(bwd, stream, k, lambda: flush.zero_())))
-    nvox = side ** 3
-    return {"voxelize_gvox_per_s_512": nvox / (tf / 1e3) / 1e9, "voxelize_fwd_bwd_gvox_per_s_512":
-            nvox / ((tf + tb) / 1e3) / 1e9, "fwd_ms": tf, "bwd_ms": tb, "voxel_pairs": stats.pixel_pairs,
-            "workload": "C3: 500k Gaussians (SL cloud), 512^3 grid, voxelize_full + voxelize_backward"}
 
 
 def run_ours(args, rank: int, world: int, local_rank: int) -> None:
@@ -400,134 +590,116 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if rank != 0:
         return
 
-    # --- roofline of the dominant kernel (live CUDA-event phase timing over the timed region)
-    ex2_peak = ctx.microbench("ex2")
-    ffma_peak = ctx.microbench("ffma")
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    hbm_src = "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    dom = max(("raster_fwd", "raster_bwd"), key=lambda p: phases[p][0])
-    dom_ms, dom_count = phases[dom]
-    launches_per_step = max(dom_count // args.steps, 1)  # views are processed in chunks
-    avg_ms = dom_ms / max(dom_count, 1)
+    peaks = _peaks(ctx)
     n = cloud.size()
-    nv = len(views)
     npx = geom.n_u * geom.n_v
-    # compulsory bytes per step: the 32 B fp32 splat record of every
-    # (view, splat) read once + the image write (fwd) / the grad-image read and the 32 B
-    # moment write (bwd); per launch = per step / launches (equal-size view chunks)
-    items = nv * n
-    algo_bytes_step = items * 32 + nv * npx * 4 + (items * 32 if dom == "raster_bwd" else 0)
-    algo_bytes = algo_bytes_step / launches_per_step
-    pairs_per_launch = stats.pixel_pairs / launches_per_step
-    achieved_gbs = algo_bytes / (avg_ms / 1e3) / 1e9
-    pair_rate = pairs_per_launch / (avg_ms / 1e3)
-    kernel = "k_raster_fwd4" if dom == "raster_fwd" else "k_raster_bwd_lanes"
-    traffic = None  # dram read+write bytes per launch from the committed ncu --set full capture
-    measured = None  # the pipes that do bind (same capture): issue slots, L1/L2 throughput
-    try:
-        prof = json.loads((ROOT / "profiles" / "r1" / "raster" / "summary.json").read_text())
-        hit = [d for d in prof if d["kernel"] == kernel and "dram_bytes" in d]
-        if hit and args.config == "c2":
-            traffic = int(np.mean([d["dram_bytes"] for d in hit]))
-            measured = {"kernel": kernel, "source": "profiles/r1/raster/summary.json (ncu --set full, C2)"}
-            for key in ("issue_active_pct", "l1tex_throughput_pct", "l1_lsu_wavefronts_pct", "l2_throughput_pct", "xu_pipe_pct",
-                        "fma_pipe_pct", "warps_active_pct"):
-                if key in hit[0]:
-                    measured[key] = round(float(np.mean([d[key] for d in hit])), 1)
-    except Exception:
-        pass
-    roofline = {"bound": "hbm", "kernel": kernel,
-                "achieved": round(achieved_gbs, 2), "peak": hbm_peak,
-                "unit": "GB/s", "frac": round(achieved_gbs / hbm_peak, 4), "traffic": traffic,
-                "peak_source": hbm_src, "algorithmic_bytes_per_launch": int(algo_bytes),
-                "avg_launch_ms": round(avg_ms, 4), "launches_per_step": launches_per_step,
-                "note": "not HBM-bound by design: the binding resources are SFU/issue (roofline_sfu)"}
-    roofline_sfu = {"bound": "sfu_ex2", "kernel": roofline["kernel"], "achieved": pair_rate, "peak": ex2_peak,
-                    "unit": "ex2/s (= splat-pixel pairs/s)", "frac": round(pair_rate / ex2_peak, 4),
-                    "pairs_per_launch": int(pairs_per_launch), "ffma_peak_per_s": ffma_peak,
-                    "note": "one exp per splat-pixel pair per pass (projector.hpp:341,410); peak = on-box "
-                            "MUFU ex2.approx microbenchmark in this run"}
+    dom = max(("raster_fwd", "raster_bwd"), key=lambda p: phases[p][0])
+    bytes_step = len(views) * ((PARAM_B + (GRAD_B if dom == "raster_bwd" else 0)) * n + PX_B * npx)
+    roofline, roofline_sfu = roofline_objects(
+        peaks, dom, "k_raster_fwd4" if dom == "raster_fwd" else "k_raster_bwd_chain", phases[dom][0],
+        phases[dom][1], bytes_step, stats.pixel_pairs, args.steps, "r2/raster" if args.config == "c2" else "-")
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded 3D Shepp-Logan phantom cloud, random init)",
-        "config": {"workload": f"{args.config.upper()}: {n} Gaussians, {WORKLOADS[args.config][0]}^3 volume, "
-                               f"{n_views_total} cone views at {geom.n_u}^2, fwd+bwd per step",
-                   "gaussians": n, "views": n_views_total, "detector": [geom.n_u, geom.n_v],
-                   "volume_side": WORKLOADS[args.config][0], "parallelism": f"views sharded over {world} GPU(s)",
-                   "l2": "flushed between timed steps (256 MiB memset outside the events)",
-                   "settings": "reference defaults: tau 1e-4, sigma_cap 3, 16x16 tiles, 0.3 px^2 dilation"},
+        "config": config_for(args.config, world),
         "work": {"tile_pairs_per_step": stats.tile_pairs, "pixel_pairs_per_pass": stats.pixel_pairs,
                  "culled": stats.culled, "degenerate": stats.degenerate},
-        "roofline": roofline, "roofline_sfu": roofline_sfu, "roofline_measured": measured,
+        "roofline": roofline, "roofline_sfu": roofline_sfu,
         "phase_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
     if e2e is not None:
         out["e2e"] = e2e
-    if not args.no_secondary and world == 1:
-        try:
-            out["secondary"] = {"raster_2048": secondary_2k(ctx), "voxel_512": secondary_voxel(ctx),
-                                "train_iteration_c2": secondary_train(ctx)}
-        except Exception as exc:  # report, never hide the main line
-            out["secondary"] = {"error": repr(exc)}
+    ref = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            out["cpu_baseline"] = cpu_baseline_sample(cloud, geom)
+            from oracle.oracle import Ref
+
+            ref = Ref()
+            out["cpu_baseline"] = cpu_baseline_views(ref, cloud, geom, len(geom.angles))
         except Exception as exc:
             out["cpu_baseline"] = {"error": repr(exc)}
+    if not args.no_secondary and world == 1:
+        sec = {}
+        for name, fn in (("raster_2048", lambda: secondary_2k(ctx, peaks, ref)),
+                         ("voxel_512", lambda: _voxel_line(ctx, peaks, ref, 512, 500_000, 1, 3, "r2/voxel", "C3")),
+                         ("voxel_1024", lambda: _voxel_line(ctx, peaks, ref, 1024, 1_000_000, 1, 2, "r2/voxel_1024",
+                                                            "C5 volume")),
+                         ("train_iteration_c2", lambda: secondary_train(ctx))):
+            try:
+                sec[name] = fn()
+            except Exception as exc:  # report, never hide the main line
+                sec[name] = {"error": repr(exc)}
+        out["secondary"] = sec
     print(json.dumps(out), flush=True)
 
 
 def run_reference(args, rank: int, world: int) -> None:
-    """Reference arm: the reference's own CPU implementation (oracle/_ref, compiled from the
-    unchanged /root/reference headers) on all host threads, same metric and workload."""
+    """Reference arm: the reference's own CPU implementation (oracle/_ref: the unchanged
+    /root/reference headers compiled here) on all host threads, on our arm's workload, metric
+    and config. Inputs are built by the reference's Rng / default_geometry (no product
+    library is loaded). Each step is a bounded sample of the 75-view step: the first
+    calibration view sizes it so the whole --steps/--warmup run stays within a few minutes."""
     if rank != 0:
         return
     from oracle.oracle import REF_LIB, Ref
-    from paper_2604_01844_b200 import gsct
+    from paper_2604_01844_b200.gsct import RasterSettings
 
     if not REF_LIB.exists():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libgsct_ref.so was not built"}))
         return
-    cloud, geom = make_workload(args.config)
     ref = Ref()
     cores = ref.threads()
+    cloud, geom = make_workload_ref(ref, args.config)
     h = ref.cloud(cloud)
-    rs = gsct.RasterSettings()
+    rs = RasterSettings()
     ones = np.ones((geom.n_v, geom.n_u))
     n = cloud.size()
-    views_per_step = 1
+    nv = len(geom.angles)
+    cursor = [0]
 
-    def step(i):
-        v = i % len(geom.angles)
+    def view_pass():
+        v = cursor[0] % nv
+        cursor[0] += 1
         ref.rasterize_view(h, geom, v, rs)
         ref.rasterize_backward(h, geom, v, ones, rs, n)
 
-    for i in range(args.warmup):
-        step(i)
+    t0 = time.perf_counter()
+    view_pass()  # calibration (untimed)
+    t_view = time.perf_counter() - t0
+    budget_s = float(os.environ.get("GSCT_REF_BUDGET_S", "150"))
+    views_per_step = int(max(1, min(nv, budget_s / (max(args.steps + args.warmup, 1) * t_view))))
+
+    def step():
+        for _ in range(views_per_step):
+            view_pass()
+
+    for _ in range(args.warmup):
+        step()
     ts = []
-    for i in range(args.steps):
+    for _ in range(args.steps):
         t0 = time.perf_counter()
-        step(args.warmup + i)
+        step()
         ts.append((time.perf_counter() - t0) * 1e3)
     ref.free_cloud(h)
     ms = float(np.mean(ts))
     value = views_per_step / (ms / 1e3)
-    sample = (f"{views_per_step} of {len(geom.angles)} views fwd+bwd per step (rasterize_view + "
-              f"rasterize_backward), {cores} threads")
+    sample = (f"{views_per_step} of {nv} views fwd+bwd per step (rasterize_view + rasterize_backward, "
+              f"projector.hpp:308,371; views cycled), {cores} threads on {cpu_model()}"
+              + ("" if views_per_step == nv else "; proj/s per-view rate of the 75-view step"))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded 3D Shepp-Logan cloud)",
-        "config": {"workload": f"{args.config.upper()}: {n} Gaussians, {len(geom.angles)} cone views at "
-                               f"{geom.n_u}^2, fwd+bwd (bounded per-step sample)"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded 3D Shepp-Logan phantom cloud, random init)",
+        "config": config_for(args.config, world),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
     }), flush=True)
 
 

@@ -300,6 +300,16 @@ class Ref:
                                    _p(raw))
         return pos, ls, q, raw
 
+    def shepp_logan_cloud(self, count: int, side: int, spacing: float = 1.0, seed: int = 0):
+        """The benchmark phantom cloud drawn with the reference's Rng (ref_shepp_logan_cloud)."""
+        pos = np.zeros((count, 3))
+        ls = np.zeros((count, 3))
+        q = np.zeros((count, 4))
+        raw = np.zeros(count)
+        self.l.ref_shepp_logan_cloud(C.c_int64(count), C.c_double(side), C.c_double(spacing), C.c_uint64(seed),
+                                     _p(pos), _p(ls), _p(q), _p(raw))
+        return pos, ls, q, raw
+
     def default_geometry(self, dims, spacing, n_views, cone, n_u, n_v):
         g = _Geo()
         ang = np.zeros(n_views)

@@ -281,6 +281,47 @@ int64_t ref_random_cloud(uint64_t seed, int count, double pos_range, double scal
   return static_cast<int64_t>(c.size());
 }
 
+// The benchmark phantom cloud (harness, not a reference function), drawn with
+// the reference's own Rng (rng.hpp:18-69) so the reference arm of bench.py builds its inputs
+// without the product library. Same arithmetic as the product harness's
+// gsct_host_make_cloud(kind 2): positions uniform inside the outer Shepp-Logan ellipsoid
+// (semi-axes 0.69, 0.92, 0.81 of the half-side), log-scales ln(s0) + U(-0.3, 0.3) with
+// s0 = 0.554 (V_fg / N)^(1/3), normalised N(0,1)^4 quaternions, raw density 0.15 U(0.2, 1).
+int64_t ref_shepp_logan_cloud(int64_t count, double side, double sp, uint64_t seed, double* pos, double* ls,
+                              double* q, double* raw) {
+  Rng rng(seed);
+  const double half = 0.5 * side * sp;
+  const double ax = 0.69 * half, ay = 0.92 * half, az = 0.81 * half;
+  const double vfg = 4.0 / 3.0 * M_PI * ax * ay * az;
+  const double s0 = 0.554 * std::cbrt(vfg / static_cast<double>(count > 0 ? count : 1));
+  for (int64_t i = 0; i < count; ++i) {
+    double x, y, z;
+    do {
+      x = rng.uniform(-1.0, 1.0);
+      y = rng.uniform(-1.0, 1.0);
+      z = rng.uniform(-1.0, 1.0);
+    } while (x * x + y * y + z * z > 1.0);
+    pos[3 * i] = x * ax;
+    pos[3 * i + 1] = y * ay;
+    pos[3 * i + 2] = z * az;
+    for (int k = 0; k < 3; ++k) ls[3 * i + k] = std::log(s0) + rng.uniform(-0.3, 0.3);
+    double qq[4] = {rng.normal(), rng.normal(), rng.normal(), rng.normal()};
+    double zz = qq[0] * qq[0];
+    zz += qq[1] * qq[1];
+    zz += qq[2] * qq[2];
+    zz += qq[3] * qq[3];
+    if (std::sqrt(zz) == 0.0) {
+      qq[0] = 1;
+      qq[1] = qq[2] = qq[3] = 0;
+      zz = 1.0;
+    }
+    const double nrm = std::sqrt(zz);
+    for (int k = 0; k < 4; ++k) q[4 * i + k] = qq[k] / nrm;
+    raw[i] = 0.15 * rng.uniform(0.2, 1.0);
+  }
+  return count;
+}
+
 void ref_default_geometry(int nx, int ny, int nz, double spacing, int n_views, int cone, int n_u,
                           int n_v, Geo* out, double* angles) {
   const Volume vol = Volume::zeros({nx, ny, nz}, spacing, Vec3::Zero());

@@ -107,3 +107,21 @@ def test_harness_generators_match_reference(ref):
         assert (g.s_u, g.s_v, g.source_to_origin, g.origin_to_detector) == (
             gg.s_u, gg.s_v, gg.source_to_origin, gg.origin_to_detector)
         assert np.array_equal(ang, np.asarray(gg.angles))
+
+
+def test_reference_arm_inputs_match_product_harness(ref):
+    """bench.py's reference arm builds the C2 / C5 workloads without the product library
+    (ref_shepp_logan_cloud with the reference Rng + default_geometry); they must be the
+    very inputs our arm uses."""
+    import bench
+
+    for name in ("c1", "c2"):
+        c_ours, g_ours = bench.make_workload(name)
+        c_ref, g_ref = bench.make_workload_ref(ref, name)
+        for a, b in zip((c_ref.positions, c_ref.log_scales, c_ref.rotations, c_ref.raw_densities),
+                        (c_ours.positions, c_ours.log_scales, c_ours.rotations, c_ours.raw_densities)):
+            assert np.array_equal(a, b)
+        assert g_ref == g_ours or (
+            (g_ref.mode, g_ref.n_u, g_ref.n_v, g_ref.s_u, g_ref.s_v, g_ref.source_to_origin, g_ref.origin_to_detector)
+            == (g_ours.mode, g_ours.n_u, g_ours.n_v, g_ours.s_u, g_ours.s_v, g_ours.source_to_origin,
+                g_ours.origin_to_detector) and np.array_equal(np.asarray(g_ref.angles), np.asarray(g_ours.angles)))
