@@ -26,7 +26,7 @@ enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
   S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG, S_FGSC, S_FGSC_LOG, S_FGSC_CNT, S_VTCOUNT,
-  S_TOTAL64, S_VIEWPAIRS,
+  S_TOTAL64, S_VIEWPAIRS, S_WCOUNT, S_WSLOT, S_WSUMS, S_WSTART,
   S_COUNT_SLOTS
 };
 
@@ -76,6 +76,9 @@ struct gsct_ctx_s {
   bool saved_valid = false;
   std::string saved_key;
   bool fgsc_table_ready = false;  // S_FGSC_LOG holds the binary16 log table
+  // the saved forward's walk-order buckets (S_WCOUNT / S_WSLOT, all views of the call)
+  bool walk_valid = false;
+  gsct_dev::WalkLayout walk_L;
 };
 
 namespace gsct_dev {
@@ -514,6 +517,38 @@ std::vector<int> bin_ranges(const unsigned long long* view_pairs, int n_views) {
   return cut;
 }
 
+// Walk order of the lane-per-item backward over views [0, n_views) of `rec`: the chain kernel
+// (32 B-aligned rows) uses the hand-written spatial counting sort (order.cu: buckets from the
+// records here; the forward's set-up produces them directly when it saves its records); the
+// other row widths keep the shape keys + radix sort of the lane kernel.
+#ifndef GSCT_BWD_COUNTSORT
+#define GSCT_BWD_COUNTSORT 1
+#endif
+const uint32_t* walk_order(gsct_ctx c, const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v, int vec,
+                           uint32_t* k1, uint32_t* v1, uint32_t* k2, uint32_t* v2) {
+  const int64_t items = n * n_views;
+  if (GSCT_BWD_COUNTSORT && bwd_chain_applies(vec)) {
+    c->walk_valid = false;  // S_WCOUNT / S_WSLOT reused below
+    const WalkLayout L = walk_layout(n_views, n_u, n_v);
+    const int64_t nb = walk_buckets(L, n_views);
+    uint32_t* counts = ws<uint32_t>(c, S_WCOUNT, static_cast<size_t>(nb));
+    uint32_t* starts = ws<uint32_t>(c, S_WSTART, static_cast<size_t>(nb));
+    uint2* slots = ws<uint2>(c, S_WSLOT, static_cast<size_t>(items));
+    uint32_t* sums = ws<uint32_t>(c, S_WSUMS, static_cast<size_t>(scan_workspace_u32(nb)));
+    CK(cudaMemsetAsync(counts, 0, static_cast<size_t>(nb) * sizeof(uint32_t), c->stream));
+    launch_walk_count(rec, n, n_views, L, counts, slots, c->stream);
+    launch_walk_scatter(counts, starts, nb, slots, items, sums, v1, c->stream);
+    return v1;
+  }
+  const int kbits = launch_bwd_shape_keys(rec, n, n_views, n_u, n_v, vec, k1, v1, c->stream);
+  cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
+  void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
+  return vb.Current();
+}
+
 // Identity of a rasterizer call for save-for-backward: cloud buffers and size, geometry,
 // angles and settings, field by field (no struct padding).
 std::string raster_call_key(const gsct_cloud* cl, const gsct_geometry* g, const double* angles, int n_views,
@@ -795,6 +830,17 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     // bin + forward 42.2 ms vs 43.2 capped)
     const BinPlan plan = fwd_bin_plan(n, n_tiles);
     int chunk = views_per_chunk(n, n_views, GSCT_FWD_TILECAP && !plan.packed ? n_tiles : 0);
+    // saved records: the set-up also files every item into the backward's walk-order buckets
+    c->walk_valid = false;
+    WalkOut walk;
+    const bool walk_out = GSCT_BWD_COUNTSORT && saved != nullptr && geom->n_u % 8 == 0;
+    if (walk_out) {
+      walk.L = walk_layout(n_views, geom->n_u, geom->n_v);
+      const int64_t nb = walk_buckets(walk.L, n_views);
+      walk.count = ws<uint32_t>(c, S_WCOUNT, static_cast<size_t>(nb));
+      walk.slot = ws<uint2>(c, S_WSLOT, static_cast<size_t>(n) * n_views);
+      CK(cudaMemsetAsync(walk.count, 0, static_cast<size_t>(nb) * sizeof(uint32_t), c->stream));
+    }
     unsigned long long* dpairs = ws<unsigned long long>(c, S_VIEWPAIRS, static_cast<size_t>(chunk) + 1);
     std::vector<unsigned long long> hpairs(static_cast<size_t>(chunk));
     for (int v0 = 0; v0 < n_views; v0 += chunk) {
@@ -819,14 +865,18 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
             const int64_t i0 = n * k / cloud_pieces, i1 = n * (k + 1) / cloud_pieces;
             CK(cudaStreamWaitEvent(c->stream, piece_up[static_cast<size_t>(k)], 0));
             launch_splat_prepare(d, pre, pre_aos, c->dstats, c->stream, i0, i1);
+            WalkOut wk = walk;
+            if (walk_out) wk.slot = walk.slot + static_cast<int64_t>(v0) * n, wk.view_base = v0;
             launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream, i0,
-                                     i1, dpairs);
+                                     i1, dpairs, walk_out ? &wk : nullptr);
           }
           for (cudaEvent_t e : piece_up) c->event_pool.push_back(e);
           piece_up.clear();
         } else {
+          WalkOut wk = walk;
+          if (walk_out) wk.slot = walk.slot + static_cast<int64_t>(v0) * n, wk.view_base = v0;
           launch_raster_preprocess(pre, n, dframes + v0, cv, g, r, kBinTile, rec, cnt, c->dstats, c->stream, 0, -1,
-                                   dpairs);
+                                   dpairs, walk_out ? &wk : nullptr);
         }
       }
       CK(cudaGetLastError());
@@ -900,6 +950,8 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (saved) {
       c->saved_key = raster_call_key(cloud, geom, angles, n_views, rs);
       c->saved_valid = true;
+      c->walk_valid = walk_out;
+      c->walk_L = walk.L;
     }
   });
 }
@@ -1051,7 +1103,9 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     // with the forward's records of every view at hand (save-for-backward) and several chunks,
     // the walk order of all views is sorted once up front (view-major keys: each chunk is a
     // contiguous range) instead of once per chunk
-    const bool one_sort = reuse && n > 0 && cb.size() > 2 && bwd_view_major(geom->n_u, geom->n_v);
+    const float* gbase_ = gdev ? gdev : grad_images;
+    const bool saved_walk = reuse && n > 0 && c->walk_valid && bwd_chain_applies(bwd_vec(geom->n_u, gbase_));
+    const bool one_sort = saved_walk || (reuse && n > 0 && cb.size() > 2 && bwd_view_major(geom->n_u, geom->n_v));
 #ifndef GSCT_BWD_DUAL
 #define GSCT_BWD_DUAL 1  // chunk walks alternate between two streams
 #endif
@@ -1064,14 +1118,17 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, static_cast<size_t>(items));
       uint32_t* v2 = ws<uint32_t>(c, S_VALS2, static_cast<size_t>(items));
       const float* gbase = gdev ? gdev : grad_images;
-      const int kbits = launch_bwd_shape_keys(saved, n, n_views, geom->n_u, geom->n_v, bwd_vec(geom->n_u, gbase), k1, v1,
-                                              c->stream);
-      cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
-      size_t tmp_bytes = 0;
-      CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
-      void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
-      CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
-      all_order = vb.Current();
+      if (saved_walk) {  // the forward's set-up filed every item: scan the bucket counts, scatter
+        const int64_t nb = walk_buckets(c->walk_L, n_views);
+        uint32_t* starts = ws<uint32_t>(c, S_WSTART, static_cast<size_t>(nb));
+        uint32_t* sums = ws<uint32_t>(c, S_WSUMS, static_cast<size_t>(scan_workspace_u32(nb)));
+        launch_walk_scatter(ws<uint32_t>(c, S_WCOUNT, static_cast<size_t>(nb)), starts, nb,
+                            ws<uint2>(c, S_WSLOT, static_cast<size_t>(items)), items, sums, v1, c->stream);
+        all_order = v1;
+      } else {
+        all_order =
+            walk_order(c, saved, n, n_views, geom->n_u, geom->n_v, bwd_vec(geom->n_u, gbase), k1, v1, k2, v2);
+      }
       if (GSCT_BWD_DUAL) stream_after(c, c->aux_stream, c->stream);  // after the sort
     }
     for (int ci = 0; ci + 1 < static_cast<int>(cb.size()) && n > 0; ++ci) {
@@ -1100,23 +1157,17 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         uint32_t* v1 = ws<uint32_t>(c, S_VALS, static_cast<size_t>(items));
         uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, static_cast<size_t>(items));
         uint32_t* v2 = ws<uint32_t>(c, S_VALS2, static_cast<size_t>(items));
-        cub::DoubleBuffer<uint32_t> kb(k1, k2), vb(v1, v2);
+        const uint32_t* order = nullptr;
         {
           Phase po(c, GSCT_PH_RASTER_ORDER);
-          const int kbits =
-              launch_bwd_shape_keys(rec, n, cv, geom->n_u, geom->n_v, bwd_vec(geom->n_u, gimg), k1, v1, c->stream);
-          size_t tmp_bytes = 0;
-          CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits,
-                                             c->stream));
-          void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
-          CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, static_cast<int>(items), 0, kbits, c->stream));
+          order = walk_order(c, rec, n, cv, geom->n_u, geom->n_v, bwd_vec(geom->n_u, gimg), k1, v1, k2, v2);
         }
         if (gdev) {
           CK(cudaStreamWaitEvent(c->stream, up_done[static_cast<size_t>(ci)], 0));
           c->event_pool.push_back(up_done[static_cast<size_t>(ci)]);
         }
         Phase ph(c, GSCT_PH_RASTER_BWD);
-        launch_raster_bwd_lanes(rec, vb.Current(), n, cv, geom->n_u, geom->n_v, gimg, mom, v0, c->stream);
+        launch_raster_bwd_lanes(rec, order, n, cv, geom->n_u, geom->n_v, gimg, mom, v0, c->stream);
       }
       CK(cudaGetLastError());
     }

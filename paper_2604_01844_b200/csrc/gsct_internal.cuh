@@ -67,6 +67,39 @@ __device__ __forceinline__ bool raster_chain_safe(float A, float B, float C, flo
   return emin > -100.f && dmax < 100.f && A > -25.f;
 }
 
+// Walk-order buckets of the raster backward (K4a, order.cu): view-major over a call's views,
+// then a coarse bbox shape class (chunks per row 1..4+ x rows / 4; near-uniform loop trip
+// counts in a warp), the exact top row (>> vs) and a column band (>> us): the lanes of a warp
+// then walk coinciding rows with 32 B chunks in shared 128 B lines. Empty items: the last
+// class of their view.
+struct WalkLayout {
+  int shapes = 65;  // 64 shape classes + the empty class
+  int vs = 0, us = 0;
+  int nv = 1, nu = 1;  // row / column bands
+};
+__device__ __forceinline__ uint32_t walk_bucket(uint32_t urange, uint32_t vrange, int view, const WalkLayout& L) {
+  const int u0 = urange & 0xFFFF, u1 = urange >> 16;
+  const int v0 = vrange & 0xFFFF, v1 = vrange >> 16;
+  const int W = u1 - u0 + 1, H = v1 - v0 + 1;
+  int shape = L.shapes - 1, pv = 0, pu = 0;
+  if (W > 0 && H > 0) {
+    const int nch = ((u0 & 7) + W + 7) >> 3;
+    shape = ((min(nch, 4) - 1) << 4) | min(H >> 2, 15);
+    pv = min(v0 >> L.vs, L.nv - 1);
+    pu = min(u0 >> L.us, L.nu - 1);
+  }
+  return (static_cast<uint32_t>(view * L.shapes + shape) * static_cast<uint32_t>(L.nv) + static_cast<uint32_t>(pv)) *
+             static_cast<uint32_t>(L.nu) +
+         static_cast<uint32_t>(pu);
+}
+// optional output of the set-up kernel: per item its walk bucket and rank in it
+struct WalkOut {
+  uint32_t* count = nullptr;  // [buckets], zeroed by the caller
+  uint2* slot = nullptr;      // [items of the launch]: (bucket, rank)
+  int view_base = 0;          // global view index of the launch's view 0
+  WalkLayout L;
+};
+
 struct Cloud {
   int64_t n;
   const double* pos;
@@ -87,7 +120,22 @@ void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevS
 void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views,
                               const Geo& g, const RSet& rs, int bin_ts, RasterRec* rec,
                               uint32_t* tile_count, DevStats* stats, cudaStream_t st, int64_t i0 = 0,
-                              int64_t i1 = -1, unsigned long long* view_pairs = nullptr);
+                              int64_t i1 = -1, unsigned long long* view_pairs = nullptr,
+                              const WalkOut* walk = nullptr);
+// order.cu: exclusive scan of u32 (in == out allowed); block_sums needs scan_workspace_u32(n) words
+int64_t scan_workspace_u32(int64_t n);
+void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* block_sums, cudaStream_t st);
+// raster backward walk order by a counting sort into spatial buckets (shape class, top row,
+// column band): counts[walk_order_buckets(...)], slots[items], block_sums[scan_workspace_u32(buckets)]
+WalkLayout walk_layout(int n_views, int n_u, int n_v);
+int64_t walk_buckets(const WalkLayout& L, int n_views);
+// buckets + ranks from records (when the set-up did not produce them)
+void launch_walk_count(const RasterRec* rec, int64_t n, int n_views, const WalkLayout& L, uint32_t* counts,
+                       uint2* slots, cudaStream_t st);
+// counts -> bucket starts, then order[start[b] + rank] = item (counts kept: the order can be
+// rebuilt from the same slots)
+void launch_walk_scatter(const uint32_t* counts, uint32_t* starts, int64_t n_buckets, const uint2* slots,
+                         int64_t items, uint32_t* block_sums, uint32_t* order, cudaStream_t st);
 // *total += sum of counts[0, n) (64-bit)
 void launch_sum_u32(const uint32_t* counts, int64_t n, unsigned long long* total, cudaStream_t st);
 // (tail.cu) acc: fp64 [11][N] view sum (g_pos 3, g_sigma 6, g_raw, sum |dL/dmean2d|);
@@ -145,6 +193,8 @@ int bwd_vec(int n_u, const float* grad_images);  // 8, 4 or 1 floats per row loa
 // true when the walk-order keys of an n_u x n_v detector are view-major (each view a
 // contiguous range of the order)
 bool bwd_view_major(int n_u, int n_v);
+// the chain backward (k_raster_bwd_chain + spatial walk order) runs for this row-load width
+bool bwd_chain_applies(int vec);
 // returns the number of key bits to sort on
 int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v, int vec,
                           uint32_t* keys, uint32_t* vals, cudaStream_t st);

@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const 
                                                            RasterRec* __restrict__ rec,
                                                            uint32_t* __restrict__ tile_count,
                                                            DevStats* __restrict__ st,
-                                                           unsigned long long* __restrict__ view_pairs) {
+                                                           unsigned long long* __restrict__ view_pairs,
+                                                           WalkOut walk) {
   const int64_t i = i0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   unsigned long long n_culled = 0, n_degen = 0, n_tp = 0, n_pp = 0;
   PreSplat s;
@@ -113,6 +114,10 @@ __global__ void __launch_bounds__(128, GSCT_PRE_MINB) k_raster_preprocess(const 
     const int64_t item = static_cast<int64_t>(v) * n + i;
     rec[item] = r;
     if (tile_count) tile_count[item] = cnt;
+    if (walk.count) {  // the backward's walk-order bucket and rank (order.cu)
+      const uint32_t b = walk_bucket(r.urange, r.vrange, walk.view_base + v, walk.L);
+      walk.slot[item] = make_uint2(b, atomicAdd(walk.count + b, 1u));
+    }
   }
   // per-view pair totals (every lane of the warp shares the view: blockIdx.y)
   if (view_pairs && v < n_views) {
@@ -307,12 +312,12 @@ void launch_splat_prepare(const Cloud& c, PreSplat* pre, PreSplat* pre_aos, DevS
 void launch_raster_preprocess(const PreSplat* pre, int64_t n, const Frame* frames_dev, int n_views, const Geo& g,
                               const RSet& rs, int bin_ts, RasterRec* rec, uint32_t* tile_count,
                               DevStats* stats, cudaStream_t st, int64_t i0, int64_t i1,
-                              unsigned long long* view_pairs) {
+                              unsigned long long* view_pairs, const WalkOut* walk) {
   if (i1 < 0) i1 = n;
   if (i1 <= i0 || n_views == 0) return;
   dim3 grid(blocks_for(i1 - i0, 128), static_cast<unsigned>((n_views + kPreViews - 1) / kPreViews));
   k_raster_preprocess<<<grid, 128, 0, st>>>(pre, n, i0, i1, n_views, frames_dev, g, rs, bin_ts, rec, tile_count,
-                                            stats, tile_count ? view_pairs : nullptr);
+                                            stats, tile_count ? view_pairs : nullptr, walk ? *walk : WalkOut{});
   count_launch();
 }
 

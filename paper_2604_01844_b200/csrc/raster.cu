@@ -969,6 +969,9 @@ void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint3
   count_launch();
 }
 
+#ifndef GSCT_BWD_CHAIN
+#define GSCT_BWD_CHAIN 1  // chain backward + spatial walk order for 32 B-aligned rows
+#endif
 #ifndef GSCT_BWD_VEC
 #define GSCT_BWD_VEC 8  // widest grad-image row load of the lane-per-item backward (8: 32 B)
 #endif
@@ -984,6 +987,8 @@ int bwd_vec(int n_u, const float* grad_images) {
 #endif
 bool bwd_view_major(int n_u, int n_v) { return static_cast<int64_t>(n_u) * n_v <= GSCT_VIEW_MAJOR_MAX_PX; }
 
+bool bwd_chain_applies(int vec) { return GSCT_BWD_CHAIN && vec == 8; }
+
 int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u, int n_v, int vec,
                           uint32_t* keys, uint32_t* vals, cudaStream_t st) {
   const int64_t n_items = n * n_views;
@@ -995,9 +1000,6 @@ int launch_bwd_shape_keys(const RasterRec* rec, int64_t n, int n_views, int n_u,
   // key within 24 bits (three radix passes). A/B (shape-major): C2 (512^2, 75 views) 6 bits
   // 3.54 ms vs 8 bits 3.60; C5 (2048^2, 8 views) 6 bits 73.5 ms, 10 bits 67.7, 12 bits 66.4;
   // (view-major, C2) 2 / 4 / 6 / 8 bits: 3.63 / 3.55 / 3.44 / 3.53 ms
-#ifndef GSCT_BWD_CHAIN
-#define GSCT_BWD_CHAIN 1  // chain backward + spatial walk order for 32 B-aligned rows
-#endif
   if (GSCT_BWD_CHAIN && vec == 8) {
     auto bits_of = [](int x) {
       int b = 0;
