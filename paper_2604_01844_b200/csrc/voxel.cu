@@ -9,6 +9,8 @@
 // walks its own box sequentially, so gradients are bit-stable without atomics.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "gsct_internal.cuh"
 #include "packed_f32.cuh"
 
@@ -388,6 +390,197 @@ __global__ void __launch_bounds__(256, GSCT_VBWD_MINB) k_voxel_bwd_lanes(const V
   }
 }
 
+// Voxel backward, chain variant (the default for 32 B-aligned rows): the ownership of
+// k_voxel_bwd_lanes (kVoxLanes lanes per splat over interleaved z-slices, x-rows as 32 B chunks,
+// a fixed xor tree at the end) with the raster chain backward's arithmetic: along an x-row the
+// exponent e(k) = A' k^2 + B' k + C' (k = x - round(centre x)) is a multiplicative chain over
+// voxel PAIRS, g(k+2) = g(k) r(k), r(k+2) = r(k) c with r(k) = 2^(e(k+2) - e(k)),
+// c = 2^(8 A') -- 4 MUFU per row instead of one per voxel -- and per-chunk sums with
+// compile-time column offsets. Edge voxels of the first / last chunk are zeroed by 0/1 pairs
+// computed once per splat. A splat whose chain could leave the normal fp32 range over its
+// walked box (quadratic minimum and step extremes at the box corners) takes the direct path.
+__device__ __forceinline__ float vox_q(const VoxelRec& r, float dx, float dy, float dz) {
+  return fmaf(dx, fmaf(r.Q00, dx, fmaf(r.Q01, dy, r.Q02 * dz)), fmaf(dy, fmaf(r.Q11, dy, r.Q12 * dz), r.Q22 * dz * dz));
+}
+
+#ifndef GSCT_VCHAIN_MINB
+#define GSCT_VCHAIN_MINB 3
+#endif
+__global__ void __launch_bounds__(256, GSCT_VCHAIN_MINB) k_voxel_bwd_chain(const VoxelRec* __restrict__ rec,
+                                                                           const uint32_t* __restrict__ order,
+                                                                           int64_t n, Window win, float sp,
+                                                                           const float* __restrict__ grad,
+                                                                           float* __restrict__ mom) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t t = tid / kVoxLanes;
+  const int q = static_cast<int>(tid % kVoxLanes);
+  const bool live = t < n;
+  const int64_t i = live ? (order ? static_cast<int64_t>(__ldg(order + t)) : t) : 0;
+  const VoxelRec r = rec[i];
+  const int x0 = max(static_cast<int>(r.lox), win.lo[0]), y0 = max(static_cast<int>(r.loy), win.lo[1]),
+            z0 = max(static_cast<int>(r.loz), win.lo[2]);
+  const int W = min(static_cast<int>(r.hix), win.hi[0] - 1) - x0 + 1,
+            H = min(static_cast<int>(r.hiy), win.hi[1] - 1) - y0 + 1,
+            D = live ? min(static_cast<int>(r.hiz), win.hi[2] - 1) - z0 + 1 : 0;
+  const bool empty = W <= 0 || H <= 0 || D <= 0;  // moments were zero-filled
+  const int wx = win.hi[0] - win.lo[0], wy = win.hi[1] - win.lo[1];
+  const int xa = x0 - ((x0 - win.lo[0]) & 7);  // aligned first column
+  const int lead = x0 - xa, ncol = lead + W, nch = (ncol + 7) >> 3;
+  const float cxf = r.lox + r.offx / sp;
+  const float xc = rintf(cxf);
+  const float delta = fmaf(r.lox - xc, sp, r.offx);  // dx = sp k - delta
+  const float fk0 = static_cast<float>(xa) - xc;      // k of the first walked column
+  const float sp2 = sp * sp;
+  const float Ap = r.Q00 * sp2;  // e(k) = Ap k^2 + B' k + C'
+  // chain safety over the walked box: k in [fk0, fk0 + 8 nch + 1], the box's y / z offsets
+  bool safe = false;
+  if (!empty) {
+    const float dxa = fmaf(sp, fk0, -delta), dxb = fmaf(sp, fk0 + static_cast<float>(8 * nch + 1), -delta);
+    const float dya = fmaf(static_cast<float>(y0) - r.loy, sp, -r.offy), dyb = dya + sp * static_cast<float>(H - 1);
+    const float dza = fmaf(static_cast<float>(z0) - r.loz, sp, -r.offz), dzb = dza + sp * static_cast<float>(D - 1);
+    float emin = 0.f, dmax = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float dx = (c & 1) ? dxb : dxa, dy = (c & 2) ? dyb : dya, dz = (c & 4) ? dzb : dza;
+      emin = fminf(emin, vox_q(r, dx, dy, dz));
+      // e(k+2) - e(k) in dx units: Q00 (4 sp dx + 4 sp^2) + 2 sp (Q01 dy + Q02 dz)
+      const float d2 = fmaf(r.Q00, fmaf(4.f * sp, dx, 4.f * sp2), 2.f * sp * fmaf(r.Q01, dy, r.Q02 * dz));
+      dmax = fmaxf(dmax, fabsf(d2));
+    }
+    safe = emin > -100.f && dmax < 100.f && Ap > -12.f;
+  }
+  const f2_t c2 = f2_bc(ex2_approx(8.f * Ap));
+  const f2_t KO0 = f2_pack(0.f, 1.f);
+  f2_t MF[4], ML[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const int a = 2 * h, b = 2 * h + 1, last = 8 * (nch - 1);
+    const bool f0 = a >= lead && (nch > 1 || a < ncol), f1 = b >= lead && (nch > 1 || b < ncol);
+    MF[h] = f2_pack(f0 ? 1.f : 0.f, f1 ? 1.f : 0.f);
+    ML[h] = f2_pack(last + a < ncol ? 1.f : 0.f, last + b < ncol ? 1.f : 0.f);
+  }
+  const float* __restrict__ gz = grad + (static_cast<int64_t>(z0 - win.lo[2]) * wy + (y0 - win.lo[1])) * wx +
+                                 (xa - win.lo[0]);
+  float m[10];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) m[k] = 0.f;
+  for (int zz = q; zz < (empty ? 0 : D); zz += kVoxLanes) {
+    const float dz = fmaf(static_cast<float>(z0 + zz) - r.loz, sp, -r.offz);
+    const float* __restrict__ prow = gz + static_cast<int64_t>(zz) * wy * wx;
+    for (int yy = 0; yy < H; ++yy, prow += wx) {
+      const float dy = fmaf(static_cast<float>(y0 + yy) - r.loy, sp, -r.offy);
+      const float L = fmaf(r.Q01, dy, r.Q02 * dz);
+      const float K = fmaf(dy, fmaf(r.Q11, dy, r.Q12 * dz), r.Q22 * dz * dz);
+      const float bp = sp * fmaf(-2.f * r.Q00, delta, L);
+      const float cp = fmaf(delta, fmaf(r.Q00, delta, -L), K);
+      f2_t X0 = f2_bc(0.f), X1 = X0, X2 = X0;
+      f2_t BE = f2_add(f2_bc(fk0), KO0);  // (k of the chunk's column 0, column 1)
+      if (safe) {
+        const float e0 = fmaf(fmaf(Ap, fk0, bp), fk0, cp);
+        const float e1 = fmaf(fmaf(Ap, fk0 + 1.f, bp), fk0 + 1.f, cp);
+        const float d0 = fmaf(Ap, fmaf(4.f, fk0, 4.f), 2.f * bp);
+        const float d1 = fmaf(4.f, Ap, d0);
+        f2_t g = f2_pack(ex2_approx(e0), ex2_approx(e1));
+        f2_t rr = f2_pack(ex2_approx(d0), ex2_approx(d1));
+        auto chunk = [&](const float* __restrict__ p, const f2_t* M, auto masked) {
+          float w[8];
+          ldg_v8(p, w);
+          f2_t W0 = f2_pack(w[0], w[1]), W1 = f2_pack(w[2], w[3]), W2 = f2_pack(w[4], w[5]),
+               W3 = f2_pack(w[6], w[7]);
+          if constexpr (decltype(masked)::value) {
+            W0 = f2_mul(W0, M[0]), W1 = f2_mul(W1, M[1]), W2 = f2_mul(W2, M[2]), W3 = f2_mul(W3, M[3]);
+          }
+          const f2_t t0 = f2_mul(g, W0);
+          g = f2_mul(g, rr);
+          rr = f2_mul(rr, c2);
+          const f2_t t1 = f2_mul(g, W1);
+          g = f2_mul(g, rr);
+          rr = f2_mul(rr, c2);
+          const f2_t t2 = f2_mul(g, W2);
+          g = f2_mul(g, rr);
+          rr = f2_mul(rr, c2);
+          const f2_t t3 = f2_mul(g, W3);
+          g = f2_mul(g, rr);
+          rr = f2_mul(rr, c2);
+          const f2_t Y0 = f2_add(f2_add(t0, t1), f2_add(t2, t3));
+          const f2_t Z = f2_fma(t3, f2_bc(3.f), f2_fma(t2, f2_bc(2.f), t1));
+          const f2_t Q = f2_fma(t3, f2_bc(9.f), f2_fma(t2, f2_bc(4.f), t1));
+          X0 = f2_add(X0, Y0);
+          X1 = f2_fma(BE, Y0, f2_fma(Z, f2_bc(2.f), X1));
+          X2 = f2_fma(BE, f2_fma(Z, f2_bc(4.f), f2_mul(BE, Y0)), f2_fma(Q, f2_bc(4.f), X2));
+          BE = f2_add(BE, f2_bc(8.f));
+        };
+        using yes = std::integral_constant<bool, true>;
+        using no = std::integral_constant<bool, false>;
+        chunk(prow, MF, yes{});
+#pragma unroll 1
+        for (int j = 1; j < nch - 1; ++j) chunk(prow + 8 * j, nullptr, no{});
+        if (nch > 1) chunk(prow + 8 * (nch - 1), ML, yes{});
+      } else {
+        const f2_t A2 = f2_bc(Ap), BP2 = f2_bc(bp), CP2 = f2_bc(cp);
+#pragma unroll 1
+        for (int j = 0; j < nch; ++j) {
+          float w[8];
+          ldg_v8(prow + 8 * j, w);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const f2_t e = f2_fma(f2_fma(A2, BE, BP2), BE, CP2);
+            float e0, e1;
+            f2_unpack(e, e0, e1);
+            f2_t wp = f2_pack(w[2 * h], w[2 * h + 1]);
+            if (j == 0)
+              wp = f2_mul(wp, MF[h]);
+            else if (j == nch - 1)
+              wp = f2_mul(wp, ML[h]);
+            const f2_t tt = f2_mul(f2_pack(ex2_approx(e0), ex2_approx(e1)), wp);
+            X0 = f2_add(X0, tt);
+            const f2_t tk = f2_mul(tt, BE);
+            X1 = f2_add(X1, tk);
+            X2 = f2_fma(tk, BE, X2);
+            BE = f2_add(BE, f2_bc(2.f));
+          }
+        }
+      }
+      float t0, t1, t2;
+      {
+        float a, b;
+        f2_unpack(X0, a, b);
+        t0 = a + b;
+        f2_unpack(X1, a, b);
+        t1 = a + b;
+        f2_unpack(X2, a, b);
+        t2 = a + b;
+      }
+      // sum t dx = sp t1 - delta t0;  sum t dx^2 = sp^2 t2 - 2 sp delta t1 + delta^2 t0
+      const float sx = fmaf(sp, t1, -delta * t0);
+      const float sxx = fmaf(sp2, t2, delta * fmaf(delta, t0, -2.f * sp * t1));
+      m[0] += t0;
+      m[1] += sx;
+      m[2] = fmaf(dy, t0, m[2]);
+      m[3] = fmaf(dz, t0, m[3]);
+      m[4] += sxx;
+      m[5] = fmaf(dy * dy, t0, m[5]);
+      m[6] = fmaf(dz * dz, t0, m[6]);
+      m[7] = fmaf(dy, sx, m[7]);
+      m[8] = fmaf(dz, sx, m[8]);
+      m[9] = fmaf(dy * dz, t0, m[9]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+#pragma unroll
+    for (int o = 1; o < kVoxLanes; o <<= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
+  }
+  if (live && !empty && q == 0) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) mom[static_cast<int64_t>(k) * n + i] = m[k];
+  }
+}
+
+#ifndef GSCT_VREGION_SHIFT
+#define GSCT_VREGION_SHIFT 6  // walk-order regions of 2^6 = 64 voxels per side
+#endif
+constexpr int kVRegionShift = GSCT_VREGION_SHIFT;
 // Walk order for the lane-per-splat backward: 64^3 region of the box corner (L2 locality of
 // the grad volume), then box shape (chunks per row, y-z rows / 16) for uniform warp trip
 // counts. Returns the key bits through *bits.
@@ -407,8 +600,9 @@ __global__ void k_voxel_lane_keys(const VoxelRec* __restrict__ rec, int64_t n, W
     const int lead = vec > 1 ? ((x0 - win.lo[0]) & (vec - 1)) : 0;
     const uint32_t nch = min((lead + W + cw - 1) / cw, 7);
     const uint32_t rows = min((H * D) >> 4, 63);
-    const uint32_t region = static_cast<uint32_t>((((z0 - win.lo[2]) >> 6) * nry + ((y0 - win.lo[1]) >> 6)) * nrx +
-                                                  ((x0 - win.lo[0]) >> 6));
+    const uint32_t region = static_cast<uint32_t>(
+        (((z0 - win.lo[2]) >> kVRegionShift) * nry + ((y0 - win.lo[1]) >> kVRegionShift)) * nrx +
+        ((x0 - win.lo[0]) >> kVRegionShift));
     key = (region << 9) | (nch << 6) | rows;
   }
   keys[i] = key;
@@ -446,8 +640,9 @@ int voxel_bwd_vec(const Window& win, const float* grad_volume) {
 
 int launch_voxel_lane_keys(const VoxelRec* rec, int64_t n, const Window& win, int vec, uint32_t* keys,
                            uint32_t* vals, cudaStream_t st) {
-  const int nrx = (win.hi[0] - win.lo[0] + 63) >> 6, nry = (win.hi[1] - win.lo[1] + 63) >> 6,
-            nrz = (win.hi[2] - win.lo[2] + 63) >> 6;
+  const int rs = kVRegionShift, rm = (1 << kVRegionShift) - 1;
+  const int nrx = (win.hi[0] - win.lo[0] + rm) >> rs, nry = (win.hi[1] - win.lo[1] + rm) >> rs,
+            nrz = (win.hi[2] - win.lo[2] + rm) >> rs;
   int rb = 0;
   while ((int64_t(1) << rb) < int64_t(nrx) * nry * nrz) ++rb;
   if (n > 0) {
@@ -460,7 +655,13 @@ int launch_voxel_lane_keys(const VoxelRec* rec, int64_t n, const Window& win, in
 void launch_voxel_bwd_lanes(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
                             float spacing, const float* grad_volume, float* moments, cudaStream_t st) {
   if (n == 0) return;
-  if (voxel_bwd_vec(win, grad_volume) == 8)
+#ifndef GSCT_VBWD_CHAIN
+#define GSCT_VBWD_CHAIN 1
+#endif
+  if (GSCT_VBWD_CHAIN && voxel_bwd_vec(win, grad_volume) == 8)
+    k_voxel_bwd_chain<<<blocks_for(n * kVoxLanes, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume,
+                                                                     moments);
+  else if (voxel_bwd_vec(win, grad_volume) == 8)
     k_voxel_bwd_lanes<8><<<blocks_for(n * kVoxLanes, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume,
                                                                         moments);
   else
