@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define GSCT_ABI_VERSION 1
+#define GSCT_ABI_VERSION 2
 
 enum gsct_status {
   GSCT_OK = 0,
@@ -57,6 +57,7 @@ enum gsct_status {
 enum gsct_location { GSCT_HOST = 0, GSCT_DEVICE = 1 };
 
 typedef struct gsct_ctx_s* gsct_ctx;
+typedef struct gsct_group_s* gsct_group;
 
 /* ScanGeometry minus the angle list (core.hpp:203-222). */
 typedef struct {
@@ -190,16 +191,48 @@ int gsct_voxelize_bwd(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_grid* gr
                       const float* grad_volume, int grad_location, gsct_grads* out,
                       gsct_stats* stats);
 
-/* Split backward for z-slab sharding: per-splat partial sums over the window
- * (moments: device fp32 [10][N]: sum t, sum t*d (3), sum t*d_i*d_j (6; xx,yy,zz,xy,xz,yz),
- * t = exp(-q/2) * w, d in world units), reduced across ranks by the caller (NCCL
- * all-reduce sum), then finished per splat in fp64. */
+/* Split backward for z-slab sharding by a caller with its own collectives: per-splat
+ * partial sums over the window (moments: device fp64 [10][N]: sum t, sum t*d (3),
+ * sum t*d_i*d_j (6; xx,yy,zz,xy,xz,yz), t = exp(-q/2) * w, d in world units; each splat's
+ * window sum is formed in fp32, then widened), reduced across ranks by the caller (fp64
+ * all-reduce sum), then finished per splat in fp64. With a group attached to the context
+ * (gsct_ctx_set_group) gsct_voxelize_bwd does this reduction itself. */
 int gsct_voxelize_bwd_moments(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_grid* grid,
                               const gsct_window* window, const gsct_voxel_settings* vs,
-                              const float* grad_volume, int grad_location, float* moments_dev);
+                              const float* grad_volume, int grad_location, double* moments_dev);
 int gsct_voxelize_bwd_finish(gsct_ctx ctx, const gsct_cloud* cloud, const gsct_grid* grid,
-                             const gsct_voxel_settings* vs, const float* moments_dev,
+                             const gsct_voxel_settings* vs, const double* moments_dev,
                              gsct_grads* out);
+
+/* ---- multi-GPU: one NCCL communicator per context -------------------
+ * Rank 0 makes an id (gsct_group_new_id), the caller distributes its 128 bytes to every
+ * rank over its own channel (MPI, torch.distributed, a file), and every rank creates its
+ * group on its context's device (collective: all ranks must call) and attaches it. With a
+ * group attached:
+ *   gsct_rasterize_bwd  -- each rank passes ITS views (e.g. round-robin view shards); the
+ *       fp64 per-splat view sums are all-reduced on the context stream before the final
+ *       chain rule, so every rank gets (bit-identical) gradients summed over ALL ranks'
+ *       views = ParamGradients::add over every view (core.hpp:152-162). A rank with no views
+ *       (n_views == 0) still takes part. gsct_rasterize_fwd is unchanged (images stay
+ *       rank-local).
+ *   gsct_voxelize_fwd   -- window NULL: rank r computes z-slab [r nz/P, (r+1) nz/P) of the
+ *       full grid and the slabs are all-gathered, so every rank holds voxelize_full's
+ *       volume (slabs tile it bit for bit); window given: that window only, no exchange.
+ *   gsct_voxelize_bwd   -- window NULL: rank r walks its z-slab of the (full-grid) grad
+ *       volume; window given: that window (ranks pass disjoint windows). The per-splat
+ *       moments are all-reduced in fp64 before the fp64 finish; pos_grad_norm is formed
+ *       after the reduction (voxelizer.hpp:250-255).
+ * All collectives are enqueued on the context stream (no host synchronisation beyond the
+ * call's own). NCCL (libnccl.so.2) is loaded at the first gsct_group_* call. */
+typedef struct {
+  unsigned char bytes[128]; /* ncclUniqueId */
+} gsct_group_id;
+int gsct_group_new_id(gsct_ctx ctx, gsct_group_id* out);
+int gsct_group_create(gsct_ctx ctx, const gsct_group_id* id, int n_ranks, int rank, gsct_group* out);
+/* Attach (g != NULL) or detach (NULL) a group; the group's device must be the context's. */
+int gsct_ctx_set_group(gsct_ctx ctx, gsct_group g);
+int gsct_group_info(gsct_group g, int* rank, int* n_ranks);
+void gsct_group_destroy(gsct_group g);
 
 /* ---- next-row operators ----------------------------------------------- */
 /* Image loss of the reconstruction loop: total_loss_recon (losses.hpp:613-637) with

@@ -24,7 +24,7 @@ NVFLAGS = ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xpt
 # preprocess.cu holds the fp64 set-up whose operation order must match the reference
 # exactly (no FMA contraction) so integer boxes / keys are bit-exact.
 PER_FILE = {"preprocess.cu": ["--fmad=false"], "control.cu": ["--fmad=false"], "codec.cu": ["--fmad=false"]}
-CU_SOURCES = ["api.cu", "preprocess.cu", "tail.cu", "raster.cu", "order.cu", "voxel.cu", "loss.cu", "control.cu", "codec.cu", "microbench.cu"]
+CU_SOURCES = ["api.cu", "preprocess.cu", "tail.cu", "raster.cu", "order.cu", "voxel.cu", "loss.cu", "control.cu", "codec.cu", "microbench.cu", "group.cu"]
 CXX_SOURCES = ["host.cpp"]
 
 
@@ -62,13 +62,13 @@ def build_variant(tag: str, defines: list[str]) -> Path:
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         list(ex.map(lambda j: _run(*j), jobs))
     lib = ROOT / "build" / "variants" / f"libgsct_{tag}.so"
-    _run([NVCC] + ARCH + ["-shared", "-o", str(lib)] + [str(o) for o in objs], vdir / "link.log")
+    _run([NVCC] + ARCH + ["-shared", "-o", str(lib)] + [str(o) for o in objs] + ["-ldl"], vdir / "link.log")
     return lib
 
 
 def build(force: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
-    headers = sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "gsct_cuda.h"]
+    headers = sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "gsct_cuda.h"]
     jobs = []
     objs = []
     for src in CU_SOURCES:
@@ -86,7 +86,7 @@ def build(force: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
         list(ex.map(lambda j: _run(*j), jobs))
     if force or jobs or _stale(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", str(LIB)] + [str(o) for o in objs], OBJ / "link.log")
+        _run([NVCC] + ARCH + ["-shared", "-o", str(LIB)] + [str(o) for o in objs] + ["-ldl"], OBJ / "link.log")
     return LIB
 
 

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/gsct_cuda.h"
+#include "group.h"
 #include "gsct_internal.cuh"
 
 using namespace gsct_dev;
@@ -26,7 +27,7 @@ enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
   S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG, S_FGSC, S_FGSC_LOG, S_FGSC_CNT, S_VTCOUNT,
-  S_TOTAL64, S_VIEWPAIRS, S_WCOUNT, S_WSLOT, S_WSUMS, S_WSTART,
+  S_TOTAL64, S_VIEWPAIRS, S_WCOUNT, S_WSLOT, S_WSUMS, S_WSTART, S_MOMENTS64,
   S_COUNT_SLOTS
 };
 
@@ -79,6 +80,8 @@ struct gsct_ctx_s {
   // the saved forward's walk-order buckets (S_WCOUNT / S_WSLOT, all views of the call)
   bool walk_valid = false;
   gsct_dev::WalkLayout walk_L;
+  // multi-GPU group (gsct_ctx_set_group): collectives of the backward / voxel calls
+  gsct_group group = nullptr;
 };
 
 namespace gsct_dev {
@@ -102,6 +105,11 @@ void throw_cuda(cudaError_t e, const char* what) {
 
 void contract(bool ok, const std::string& msg) {
   if (!ok) throw CallError{GSCT_ERR_CONTRACT, msg};
+}
+
+// group.cu calls: empty string = success
+void GK(const std::string& err) {
+  if (!err.empty()) throw CallError{GSCT_ERR_CUDA, err};
 }
 
 template <class T>
@@ -753,6 +761,43 @@ int gsct_microbench(gsct_ctx c, int kind, double* ops_per_second) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Multi-GPU group (group.cu)
+// ---------------------------------------------------------------------------------------
+
+int gsct_group_new_id(gsct_ctx c, gsct_group_id* out) {
+  return run(c, [&] {
+    contract(out != nullptr, "gsct_group_new_id: null output");
+    GK(group_new_id(out->bytes));
+  });
+}
+
+int gsct_group_create(gsct_ctx c, const gsct_group_id* id, int n_ranks, int rank, gsct_group* out) {
+  return run(c, [&] {
+    contract(id != nullptr && out != nullptr, "gsct_group_create: null argument");
+    contract(n_ranks >= 1 && rank >= 0 && rank < n_ranks, "gsct_group_create: rank outside [0, n_ranks)");
+    *out = nullptr;
+    CK(cudaStreamSynchronize(c->stream));
+    GK(group_create(c->device, id->bytes, n_ranks, rank, out));
+  });
+}
+
+int gsct_ctx_set_group(gsct_ctx c, gsct_group g) {
+  return run(c, [&] {
+    contract(g == nullptr || group_device(g) == c->device, "gsct_ctx_set_group: group made on another device");
+    c->group = g;
+  });
+}
+
+int gsct_group_info(gsct_group g, int* rank, int* n_ranks) {
+  if (!g) return GSCT_ERR_CONTRACT;
+  if (rank) *rank = group_rank(g);
+  if (n_ranks) *n_ranks = group_size(g);
+  return GSCT_OK;
+}
+
+void gsct_group_destroy(gsct_group g) { group_destroy(g); }
+
+// ---------------------------------------------------------------------------------------
 // Rasterizer
 // ---------------------------------------------------------------------------------------
 
@@ -1008,7 +1053,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       }
       gv = ws<uint8_t>(c, S_GVIS, un);  // visibility bytes always staged (N bytes)
     }
-    if (n > 0 && n_views == 0) {
+    if (n > 0 && n_views == 0 && !c->group) {
       CK(cudaMemsetAsync(gp, 0, 3 * un * sizeof(double), c->stream));
       CK(cudaMemsetAsync(gl, 0, 3 * un * sizeof(double), c->stream));
       CK(cudaMemsetAsync(gq, 0, 4 * un * sizeof(double), c->stream));
@@ -1180,7 +1225,21 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     const bool stage_grads = out->location == GSCT_HOST && n > 0 && !zc_grads;
     const int pieces = (stage_grads || zc_grads) && n_views > 0 && n >= 4096 ? GSCT_TAIL_PIECES : 1;
     bool grads_down = false;
-    if (n > 0 && n_views > 0) {
+    if (n > 0 && c->group) {
+      // multi-GPU: this rank's view sums, one fp64 all-reduce of the [11][N] accumulators
+      // (+ max of the visibility bytes) on the stream, then the chain rule on the total
+      Phase ph(c, GSCT_PH_RASTER_TAIL);
+      if (cloud_up) CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));
+      if (n_views > 0) {
+        launch_raster_tail(pre_aos, n, 0, n, dframes, n_views, g, r, mom, acc, gv, c->stream);
+      } else {
+        CK(cudaMemsetAsync(acc, 0, 11 * un * sizeof(double), c->stream));
+        CK(cudaMemsetAsync(gv, 0, un, c->stream));
+      }
+      GK(group_allreduce_sum_f64(c->group, acc, 11 * un, c->stream));
+      GK(group_allreduce_max_u8(c->group, gv, un, c->stream));
+      launch_raster_finalize(d, 0, n, acc, gp, gl, gq, gr, gn, c->stream, zc_grads ? 1 : 0);
+    } else if (n > 0 && n_views > 0) {
       Phase ph(c, GSCT_PH_RASTER_TAIL);
       if (cloud_up) CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));
 #ifndef GSCT_TAIL_DUAL
@@ -1331,6 +1390,52 @@ void grads_to_host(gsct_ctx c, gsct_grads* out, const GradPtrs& p, size_t un) {
 
 }  // namespace
 
+namespace {
+
+// first slice of rank r's z-slab of nz slices over p ranks (the first nz % p slabs one
+// slice thicker; sharding.zslab_windows)
+int slab_lo(int nz, int r, int p) { return r * (nz / p) + std::min(r, nz % p); }
+
+// Forward of one window into outv (device, window dims).
+void voxel_fwd_window(gsct_ctx c, const Cloud& d, const VoxGrid& vg, const Window& win,
+                      const gsct_voxel_settings* vs, float* outv) {
+  const int64_t n = d.n;
+  const int64_t nvox = window_count(win);
+  const int nbx = (win.hi[0] - win.lo[0] + kBrick - 1) / kBrick;
+  const int nby = (win.hi[1] - win.lo[1] + kBrick - 1) / kBrick;
+  const int nbz = (win.hi[2] - win.lo[2] + kBrickZ - 1) / kBrickZ;
+  const uint64_t n_bricks = static_cast<uint64_t>(nbx) * nby * nbz;
+  contract(n_bricks < (uint64_t(1) << 31), "voxelize: grid too large");
+  if (n == 0) {
+    CK(cudaMemsetAsync(outv, 0, static_cast<size_t>(nvox) * sizeof(float), c->stream));
+    return;
+  }
+  VoxelRec* rec = ws<VoxelRec>(c, S_VREC, static_cast<size_t>(n));
+  uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n));
+  {
+    Phase ph(c, GSCT_PH_VOXEL_SETUP);
+    launch_voxel_preprocess(d, vg, win, vs->tau_cut, vs->sigma_cap, rec, cnt, nullptr, nullptr, nullptr,
+                            c->dstats, c->stream);
+  }
+  uint32_t *keys, *vals, *start, *end;
+  {
+    Phase ph(c, GSCT_PH_VOXEL_BIN);
+    bin_and_sort(
+        c, cnt, n, static_cast<uint32_t>(n_bricks),
+        [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
+          launch_emit_brick_pairs(rec, offsets, cnt, n, win, nbx, nby, k, v, c->stream);
+        },
+        &keys, &vals, &start, &end);
+  }
+  {
+    Phase ph(c, GSCT_PH_VOXEL_FWD);
+    launch_voxel_fwd(rec, vals, start, end, win, nbx, nby, nbz, static_cast<float>(vg.spacing), outv, c->stream);
+  }
+  CK(cudaGetLastError());
+}
+
+}  // namespace
+
 int gsct_voxelize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid,
                       const gsct_window* window, const gsct_voxel_settings* vs, float* volume,
                       int volume_location, gsct_stats* stats) {
@@ -1342,41 +1447,22 @@ int gsct_voxelize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
     if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
     reset_stats(c);
     const Cloud d = upload_cloud(c, cloud);
-    const int64_t n = d.n;
     const int64_t nvox = window_count(win);
     float* outv = volume;
     if (volume_location == GSCT_HOST) outv = ws<float>(c, S_VOLUME, static_cast<size_t>(nvox));
-    const int nbx = (win.hi[0] - win.lo[0] + kBrick - 1) / kBrick;
-    const int nby = (win.hi[1] - win.lo[1] + kBrick - 1) / kBrick;
-    const int nbz = (win.hi[2] - win.lo[2] + kBrickZ - 1) / kBrickZ;
-    const uint64_t n_bricks = static_cast<uint64_t>(nbx) * nby * nbz;
-    contract(n_bricks < (uint64_t(1) << 31), "voxelize: grid too large");
-    if (n == 0) {
-      CK(cudaMemsetAsync(outv, 0, static_cast<size_t>(nvox) * sizeof(float), c->stream));
+    if (c->group && window == nullptr) {
+      // multi-GPU voxelize_full: this rank's z-slab, then every slab broadcast to all ranks
+      const int P = group_size(c->group), rk = group_rank(c->group), nz = grid->dims[2];
+      const int64_t plane = static_cast<int64_t>(grid->dims[0]) * grid->dims[1];
+      std::vector<size_t> off(static_cast<size_t>(P) + 1);
+      for (int k = 0; k <= P; ++k) off[static_cast<size_t>(k)] = static_cast<size_t>(plane * slab_lo(nz, k, P));
+      Window sw = win;
+      sw.lo[2] = slab_lo(nz, rk, P);
+      sw.hi[2] = slab_lo(nz, rk + 1, P);
+      if (sw.hi[2] > sw.lo[2]) voxel_fwd_window(c, d, vg, sw, vs, outv + plane * sw.lo[2]);
+      GK(group_allgather_slabs_f32(c->group, outv, off.data(), c->stream));
     } else {
-      VoxelRec* rec = ws<VoxelRec>(c, S_VREC, static_cast<size_t>(n));
-      uint32_t* cnt = ws<uint32_t>(c, S_COUNT, static_cast<size_t>(n));
-      {
-        Phase ph(c, GSCT_PH_VOXEL_SETUP);
-        launch_voxel_preprocess(d, vg, win, vs->tau_cut, vs->sigma_cap, rec, cnt, nullptr, nullptr, nullptr,
-                                c->dstats, c->stream);
-      }
-      uint32_t *keys, *vals, *start, *end;
-      {
-        Phase ph(c, GSCT_PH_VOXEL_BIN);
-        bin_and_sort(
-            c, cnt, n, static_cast<uint32_t>(n_bricks),
-            [&](const uint32_t* offsets, uint32_t* k, uint32_t* v) {
-              launch_emit_brick_pairs(rec, offsets, cnt, n, win, nbx, nby, k, v, c->stream);
-            },
-            &keys, &vals, &start, &end);
-      }
-      {
-        Phase ph(c, GSCT_PH_VOXEL_FWD);
-        launch_voxel_fwd(rec, vals, start, end, win, nbx, nby, nbz, static_cast<float>(vg.spacing), outv,
-                         c->stream);
-      }
-      CK(cudaGetLastError());
+      voxel_fwd_window(c, d, vg, win, vs, outv);
     }
     if (volume_location == GSCT_HOST)
       CK(cudaMemcpyAsync(volume, outv, static_cast<size_t>(nvox) * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
@@ -1384,13 +1470,56 @@ int gsct_voxelize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
   });
 }
 
+namespace {
+
+// This call's window (or, with a group and no window, this rank's z-slab of the full grid)
+// walked into fp32 moments; with a group the moments are widened to fp64 and all-reduced.
+// Returns the moments the finish reads: float* (single GPU) or double* (group).
+struct VoxMoments {
+  const float* f32 = nullptr;
+  const double* f64 = nullptr;
+};
+VoxMoments voxel_bwd_moments(gsct_ctx c, const Cloud& d, const VoxGrid& vg, const gsct_grid* grid,
+                             const gsct_window* window, const gsct_voxel_settings* vs, const float* grad_volume,
+                             int grad_location, bool want_f64) {
+  const size_t un = static_cast<size_t>(d.n);
+  float* mom = ws<float>(c, S_MOMENTS, un * 10 + 1);
+  Window win = make_window(grid, window);
+  const float* gvol = grad_volume;
+  bool empty = false;
+  if (c->group && window == nullptr) {
+    const int P = group_size(c->group), rk = group_rank(c->group), nz = grid->dims[2];
+    const int64_t plane = static_cast<int64_t>(grid->dims[0]) * grid->dims[1];
+    win.lo[2] = slab_lo(nz, rk, P);
+    win.hi[2] = slab_lo(nz, rk + 1, P);
+    gvol = grad_volume + plane * win.lo[2];
+    empty = win.hi[2] <= win.lo[2];
+  }
+  if (empty)
+    CK(cudaMemsetAsync(mom, 0, un * 10 * sizeof(float), c->stream));
+  else
+    voxel_moments(c, d, vg, win, vs, gvol, grad_location, mom);
+  VoxMoments m;
+  if (!want_f64 && !c->group) {
+    m.f32 = mom;
+    return m;
+  }
+  double* m64 = ws<double>(c, S_MOMENTS64, un * 10 + 1);
+  launch_widen_f32(mom, m64, static_cast<int64_t>(un) * 10, c->stream);
+  if (c->group) GK(group_allreduce_sum_f64(c->group, m64, un * 10, c->stream));
+  m.f64 = m64;
+  return m;
+}
+
+}  // namespace
+
 int gsct_voxelize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid,
                       const gsct_window* window, const gsct_voxel_settings* vs,
                       const float* grad_volume, int grad_location, gsct_grads* out,
                       gsct_stats* stats) {
   return run(c, [&] {
     const VoxGrid vg = make_grid(grid);
-    const Window win = make_window(grid, window);
+    make_window(grid, window);
     contract(vs != nullptr, "VoxelSettings: null");
     contract(out != nullptr, "voxelize_backward: null gradient output");
     contract(grad_volume != nullptr, "voxelize_backward: grad dims must match region");
@@ -1398,13 +1527,16 @@ int gsct_voxelize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
     reset_stats(c);
     const Cloud d = upload_cloud(c, cloud);
     const size_t un = static_cast<size_t>(d.n);
-    float* mom = ws<float>(c, S_MOMENTS, un * 10 + 1);
-    voxel_moments(c, d, vg, win, vs, grad_volume, grad_location, mom);
+    const VoxMoments m = voxel_bwd_moments(c, d, vg, grid, window, vs, grad_volume, grad_location, false);
     const GradPtrs p = grad_targets(c, out, un);
     {
       Phase ph(c, GSCT_PH_VOXEL_TAIL);
-      launch_voxel_tail(d, vg, vs->tau_cut, vs->sigma_cap, mom, p.gp, p.gl, p.gq, p.gr, p.gn, p.gv, c->dstats,
-                        c->stream);
+      if (m.f64)
+        launch_voxel_tail(d, vg, vs->tau_cut, vs->sigma_cap, m.f64, p.gp, p.gl, p.gq, p.gr, p.gn, p.gv, c->dstats,
+                          c->stream);
+      else
+        launch_voxel_tail(d, vg, vs->tau_cut, vs->sigma_cap, m.f32, p.gp, p.gl, p.gq, p.gr, p.gn, p.gv, c->dstats,
+                          c->stream);
     }
     CK(cudaGetLastError());
     grads_to_host(c, out, p, un);
@@ -1414,20 +1546,23 @@ int gsct_voxelize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
 
 int gsct_voxelize_bwd_moments(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid,
                               const gsct_window* window, const gsct_voxel_settings* vs,
-                              const float* grad_volume, int grad_location, float* moments_dev) {
+                              const float* grad_volume, int grad_location, double* moments_dev) {
   return run(c, [&] {
     const VoxGrid vg = make_grid(grid);
     const Window win = make_window(grid, window);
     contract(vs != nullptr && moments_dev != nullptr && grad_volume != nullptr, "voxelize_backward: null buffer");
     reset_stats(c);
     const Cloud d = upload_cloud(c, cloud);
-    voxel_moments(c, d, vg, win, vs, grad_volume, grad_location, moments_dev);
+    const size_t un = static_cast<size_t>(d.n);
+    float* mom = ws<float>(c, S_MOMENTS, un * 10 + 1);
+    voxel_moments(c, d, vg, win, vs, grad_volume, grad_location, mom);
+    launch_widen_f32(mom, moments_dev, static_cast<int64_t>(un) * 10, c->stream);
     finish_sync(c, nullptr, false, nullptr);
   });
 }
 
 int gsct_voxelize_bwd_finish(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid,
-                             const gsct_voxel_settings* vs, const float* moments_dev,
+                             const gsct_voxel_settings* vs, const double* moments_dev,
                              gsct_grads* out) {
   return run(c, [&] {
     const VoxGrid vg = make_grid(grid);

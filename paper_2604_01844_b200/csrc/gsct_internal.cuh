@@ -154,10 +154,13 @@ void launch_voxel_preprocess(const Cloud& c, const VoxGrid& grid, const Window& 
                              double tau_cut, double sigma_cap, VoxelRec* rec,
                              uint32_t* brick_count, int32_t* lo_out, int32_t* hi_out,
                              uint8_t* skip_out, DevStats* stats, cudaStream_t st);
+template <class T>
 void launch_voxel_tail(const Cloud& c, const VoxGrid& grid, double tau_cut, double sigma_cap,
-                       const float* moments, double* g_pos, double* g_ls, double* g_q,
+                       const T* moments, double* g_pos, double* g_ls, double* g_q,
                        double* g_raw, double* g_pgn, uint8_t* visible, DevStats* stats,
                        cudaStream_t st);
+// b[i] = (double)a[i]
+void launch_widen_f32(const float* a, double* b, int64_t n, cudaStream_t st);
 
 void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets,
                             const uint32_t* counts, int64_t n, int n_views, int ts, int tiles_u,

@@ -240,8 +240,10 @@ __global__ void __launch_bounds__(256) k_voxel_preprocess(Cloud c, VoxGrid grid,
 
 // K8b: one thread per splat: from the fp32 voxel-loop moments (summed over all windows)
 // to dL/d(raw parameters) in fp64, voxelizer.hpp:250-255 + covariance_backward.
+// T: float (this call's own moments) or double (moments all-reduced across ranks in fp64).
+template <class T>
 __global__ void __launch_bounds__(128) k_voxel_tail(Cloud c, VoxGrid grid, double tau_cut,
-                                                    double sigma_cap, const float* __restrict__ m,
+                                                    double sigma_cap, const T* __restrict__ m,
                                                     double* __restrict__ g_pos,
                                                     double* __restrict__ g_ls, double* __restrict__ g_q,
                                                     double* __restrict__ g_raw,
@@ -357,13 +359,29 @@ void launch_voxel_preprocess(const Cloud& c, const VoxGrid& grid, const Window& 
   count_launch();
 }
 
+template <class T>
 void launch_voxel_tail(const Cloud& c, const VoxGrid& grid, double tau_cut, double sigma_cap,
-                       const float* moments, double* g_pos, double* g_ls, double* g_q,
+                       const T* moments, double* g_pos, double* g_ls, double* g_q,
                        double* g_raw, double* g_pgn, uint8_t* visible, DevStats* stats,
                        cudaStream_t st) {
   if (c.n == 0) return;
-  k_voxel_tail<<<blocks_for(c.n, 128), 128, 0, st>>>(c, grid, tau_cut, sigma_cap, moments, g_pos,
-                                                     g_ls, g_q, g_raw, g_pgn, visible, stats);
+  k_voxel_tail<T><<<blocks_for(c.n, 128), 128, 0, st>>>(c, grid, tau_cut, sigma_cap, moments, g_pos,
+                                                        g_ls, g_q, g_raw, g_pgn, visible, stats);
+  count_launch();
+}
+template void launch_voxel_tail<float>(const Cloud&, const VoxGrid&, double, double, const float*, double*, double*,
+                                       double*, double*, double*, uint8_t*, DevStats*, cudaStream_t);
+template void launch_voxel_tail<double>(const Cloud&, const VoxGrid&, double, double, const double*, double*,
+                                        double*, double*, double*, double*, uint8_t*, DevStats*, cudaStream_t);
+
+__global__ void k_widen_f32(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = static_cast<double>(a[i]);
+}
+
+void launch_widen_f32(const float* a, double* b, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_widen_f32<<<blocks_for(n, 256), 256, 0, st>>>(a, b, n);
   count_launch();
 }
 

@@ -130,6 +130,10 @@ class c_grads(C.Structure):
                 ("location", C.c_int)]
 
 
+class c_group_id(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 128)]
+
+
 _P = C.POINTER
 _SIGS = {
     "gsct_abi_version": (C.c_int, []),
@@ -146,6 +150,11 @@ _SIGS = {
     "gsct_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "gsct_ctx_phase_times": (C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_int64)]),
     "gsct_microbench": (C.c_int, [C.c_void_p, C.c_int, _P(C.c_double)]),
+    "gsct_group_new_id": (C.c_int, [C.c_void_p, _P(c_group_id)]),
+    "gsct_group_create": (C.c_int, [C.c_void_p, _P(c_group_id), C.c_int, C.c_int, _P(C.c_void_p)]),
+    "gsct_ctx_set_group": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gsct_group_info": (C.c_int, [C.c_void_p, _P(C.c_int), _P(C.c_int)]),
+    "gsct_group_destroy": (None, [C.c_void_p]),
     "gsct_rasterize_fwd": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), _P(C.c_double), C.c_int,
                                      _P(c_raster_settings), C.c_void_p, C.c_int, _P(c_stats)]),
     "gsct_rasterize_bwd": (C.c_int, [C.c_void_p, _P(c_cloud), _P(c_geometry), _P(C.c_double), C.c_int,
@@ -506,11 +515,52 @@ class Context:
         self.check(self._lib.gsct_ctx_phase_times(self.handle, ms, cnt))
         return {name: (ms[i], cnt[i]) for i, name in enumerate(PHASES)}
 
+    def group_new_id(self) -> bytes:
+        """A fresh 128-byte group id (ncclUniqueId); rank 0 makes it, every rank gets a copy."""
+        gid = c_group_id()
+        self.check(self._lib.gsct_group_new_id(self.handle, C.byref(gid)))
+        return bytes(gid.bytes)
+
+    def create_group(self, group_id: bytes, n_ranks: int, rank: int, attach: bool = True) -> "Group":
+        """Collective over all ranks: the NCCL communicator of this context's device. With
+        attach, the backward / voxel calls of this context run their cross-rank reductions
+        (include/gsct_cuda.h, multi-GPU)."""
+        if len(group_id) != 128:
+            raise ContractError("gsct_group_create: the group id is 128 bytes")
+        gid = c_group_id()
+        C.memmove(gid.bytes, group_id, 128)
+        h = C.c_void_p()
+        self.check(self._lib.gsct_group_create(self.handle, C.byref(gid), int(n_ranks), int(rank), C.byref(h)))
+        g = Group(self._lib, h)
+        if attach:
+            self.set_group(g)
+        return g
+
+    def set_group(self, group: Optional["Group"]) -> None:
+        self.check(self._lib.gsct_ctx_set_group(self.handle, group.handle if group is not None else None))
+        self._group = group
+
     def microbench(self, kind: str) -> float:
         """Device-wide ops/s: "ex2" (MUFU ex2.approx.f32) or "ffma" (FP32 FFMA)."""
         out = C.c_double(0.0)
         self.check(self._lib.gsct_microbench(self.handle, {"ex2": 0, "ffma": 1}[kind], C.byref(out)))
         return out.value
+
+
+class Group:
+    """A gsct_group (one NCCL communicator per context)."""
+
+    def __init__(self, lib_, handle):
+        self._lib = lib_
+        self.handle = handle
+        r, n = C.c_int(0), C.c_int(0)
+        lib_.gsct_group_info(handle, C.byref(r), C.byref(n))
+        self.rank, self.size = r.value, n.value
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.gsct_group_destroy(self.handle)
+            self.handle = None
 
 
 _contexts: dict[int, Context] = {}
@@ -710,14 +760,15 @@ def voxelize_backward(cloud: GaussianCloud, region, grad_volume, settings: Voxel
 
 def voxelize_backward_moments(cloud: GaussianCloud, region, grad_window, window, moments,
                               settings: VoxelSettings = VoxelSettings(), ctx: Optional[Context] = None):
-    """Per-splat partial sums over one window (z-slab) into device moments [10, N] float32."""
+    """Per-splat partial sums over one window (z-slab) into device moments [10, N] float64
+    (each splat's window sum formed in fp32, then widened; reduced across ranks in fp64)."""
     ctx = _ctx_for(cloud, ctx)
     keep: list = []
     cc = cloud._c(keep)
     gptr, gloc = _ptr(grad_window, keep)
     mptr, mloc = _ptr(moments, keep)
-    if mloc != GSCT_DEVICE:
-        raise ContractError("voxelize_backward_moments: moments must be a CUDA tensor")
+    if mloc != GSCT_DEVICE or str(moments.dtype) != "torch.float64" or tuple(moments.shape) != (10, cloud.size()):
+        raise ContractError("voxelize_backward_moments: moments must be a [10, N] float64 CUDA tensor")
     gr = _grid_c(region)
     win = _window_c(window)
     vs = settings.c()

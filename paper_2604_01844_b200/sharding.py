@@ -5,14 +5,17 @@
   sum), then one all-reduce (sum) of the packed gradient buffer and one (max) of the
   visibility bytes. Images stay rank-local. Oracle: sum over all views of
   rasterize_backward via ParamGradients::add (core.hpp:152-162).
-* Voxelizer — z-slab sharding: rank r owns z slices [r*nz/P, (r+1)*nz/P). Forward needs no
+* Voxelizer — z-slab sharding: rank r owns the r-th of P contiguous z-slabs. Forward needs no
   communication (each rank writes its slab; boxes are computed in full-grid coordinates,
-  so slabs tile the full-grid volume bit for bit). Backward: per-splat fp32 moment partial
-  sums over the slab, all-reduce (sum) of the [10, N] moments, then the fp64 finish.
+  so slabs tile the full-grid volume bit for bit). Backward: per-splat moment partial
+  sums over the slab, fp64 all-reduce (sum) of the [10, N] moments, then the fp64 finish.
   pos_grad_norm is formed after the reduction (the norm is nonlinear).
 
 The functions take a `torch.distributed` process group (NCCL on GPUs; gloo in the CPU
-tests) and only move data that the path must exchange.
+tests) and only move data that the path must exchange. `native_group` instead builds the
+library's own group (include/gsct_cuda.h, multi-GPU): one NCCL communicator per context,
+whose reductions the C-ABI calls enqueue themselves -- the path a C++ caller of the
+reference API takes.
 """
 from __future__ import annotations
 
@@ -63,8 +66,19 @@ def allreduce_grads(flat, visible, group=None) -> None:
     dist.all_reduce(visible, op=dist.ReduceOp.MAX, group=group)
 
 
+def native_group(ctx, pg=None):
+    """The library's NCCL group over the ranks of `pg` (default: the world), attached to
+    `ctx`: rank 0 makes the id, a torch.distributed broadcast hands it to every rank."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(pg), dist.get_world_size(pg)
+    box = [ctx.group_new_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(pg, 0) if pg is not None else 0, group=pg)
+    return ctx.create_group(box[0], world, rank, attach=True)
+
+
 def allreduce_moments(moments, group=None) -> None:
-    """Sum the [10, N] fp32 voxel-backward partial moments over the z-slabs."""
+    """Sum the [10, N] fp64 voxel-backward partial moments over the z-slabs."""
     import torch.distributed as dist
 
     dist.all_reduce(moments, op=dist.ReduceOp.SUM, group=group)

@@ -29,7 +29,7 @@ def test_header_symbols_are_exported_and_bound():
     for name in sorted(names):
         assert hasattr(lib, name), f"{name} declared in gsct_cuda.h but not exported"
     assert names == set(gsct.exported_symbols()), names ^ set(gsct.exported_symbols())
-    assert lib.gsct_abi_version() == 1
+    assert lib.gsct_abi_version() == 2
 
 
 def test_library_is_sm100a_and_has_no_host_fallback():

@@ -203,7 +203,7 @@ def test_c3_voxel_backward_slab(ctx, ref):
     # the z-slab sharded path: moments over the window of the full grid, then the finish
     d = cloud.to_device(0)
     full = gsct.GridRegion.covering(grid)
-    mom = torch.zeros((10, n), dtype=torch.float32, device="cuda")
+    mom = torch.zeros((10, n), dtype=torch.float64, device="cuda")
     gsct.voxelize_backward_moments(d, full, torch.from_numpy(gv).cuda(), ((0, 0, z0), (side, side, z0 + dz)), mom,
                                    vs, ctx=ctx)
     gm = gsct.voxelize_backward_finish(d, full, mom, vs, ctx=ctx)

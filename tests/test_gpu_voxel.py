@@ -123,7 +123,7 @@ def test_z_slab_backward_moments_sum(ctx, orc):
     region = gsct.GridRegion.covering(grid)
     gv = np.random.default_rng(3).uniform(-1, 1, size=(24, 24, 24)).astype(np.float32)
     full = gsct.voxelize_backward(cloud, region, gv, ctx=ctx)
-    total = torch.zeros((10, cloud.size()), dtype=torch.float32, device="cuda")
+    total = torch.zeros((10, cloud.size()), dtype=torch.float64, device="cuda")
     for a, b in ((0, 7), (7, 16), (16, 24)):
         m = torch.zeros_like(total)
         gsct.voxelize_backward_moments(cloud, region, torch.from_numpy(gv[a:b].copy()).cuda(),
