@@ -497,10 +497,13 @@ def _voxel_line(ctx, peaks, ref, side: int, n: int, seed: int, k: int, ncu_tag: 
 
 
 def secondary_train(ctx, k: int = 5) -> dict:
-    """BASELINE configs[1] as a device-resident training iteration: render the 75 C2 views,
-    fused L1 + 0.25 SSIM2D image loss against measured projections (rendered from the
-    unperturbed cloud), backward to the Gaussians, one Adam step (batched-gradient data
-    parallelism: one optimiser step per 75-view batch)."""
+    """BASELINE configs[1] as a device-resident training iteration (the loop body of
+    train_reconstruction, optim.hpp:456-492, batched over the 75 C2 views): render, fused
+    L1 + 0.25 SSIM2D image loss against measured projections (rendered from the unperturbed
+    cloud), backward to the Gaussians, the TV term on a 32^3 sub-volume drawn by
+    sample_subvolume (voxelize -> tv3d -> voxelize_backward, weight 0.05, added to the
+    gradients), lr_schedule for the position rate, one Adam step (batched-gradient data
+    parallelism: one optimiser step and one TV sub-volume per 75-view batch)."""
     import torch
     from paper_2604_01844_b200 import gsct
 
@@ -516,11 +519,23 @@ def secondary_train(ctx, k: int = 5) -> dict:
     adam = gsct.AdamState(pert.size(), ctx.device)
     lrs = gsct.LearningRates()
     losses = []
+    side = WORKLOADS["c2"][0]
+    grid = gsct.GridSpec.centered((side, side, side), 1.0)
+    rng_sub = gsct.Rng(11)
+    extent = gsct.scene_extent(pert)
+    horizon = 300 * len(views)  # TrainConfig iterations x views (optim.hpp:435-438)
+    vs = gsct.VoxelSettings()
 
     def it():
         gsct.rasterize_views(st.dcloud, geom, views, st.rs, out=st.images, ctx=ctx)
         lv, _ = gsct.image_loss(st.images, measured, 0.25, grad_out=st.grad_images, ctx=ctx)
         gsct.rasterize_backward_views(st.dcloud, geom, views, st.grad_images, st.rs, out=st.grads, ctx=ctx)
+        region = gsct.sample_subvolume(grid, (32, 32, 32), rng_sub)
+        sub = gsct.voxelize(st.dcloud, region, vs, ctx=ctx)
+        _, tv_grad = gsct.tv3d(sub, ctx=ctx)
+        tvg = gsct.voxelize_backward(st.dcloud, region, tv_grad.mul_(0.05), vs, ctx=ctx)
+        st.grads.add(tvg)
+        lrs.position = gsct.lr_schedule(2e-4 * extent, 1e-6 * extent, adam.step, horizon)
         gsct.adam_step(st.dcloud, adam, st.grads, lrs, ctx=ctx)
         losses.append(float(lv[:, 2].mean()))
 
@@ -528,9 +543,39 @@ def secondary_train(ctx, k: int = 5) -> dict:
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     ts = timed_steps(it, st.stream, k, lambda: flush.zero_())
     ms = float(np.mean(ts))
-    return {"workload": "C2 training iteration: 75 views render + L1/SSIM2D loss + backward + Adam (device-resident)",
+    return {"workload": "C2 training iteration: 75 views render + L1/SSIM2D loss + backward + 32^3 TV sub-volume "
+                        "(voxelize, tv3d, voxelize_backward) + lr_schedule + Adam (device-resident)",
             "ms_per_iteration": ms, "proj_per_s": len(views) / (ms / 1e3),
             "mean_view_loss_first_last": [losses[0], losses[-1]], "iterations": len(losses)}
+
+
+def run_dropin(timeout_s: float = 240.0) -> dict:
+    """The UNCHANGED reference loop train_reconstruction (optim.hpp:397-538), one epoch at C2
+    (75 views at 512^2, 200k Gaussians; per view-step: render, 32^3 TV voxelize, L1+SSIM2D+TV
+    loss, backward, voxelize_backward, Adam -- one fwd+bwd projection each), through the C++
+    drop-in (oracle/_ref/dropin_train_b200: gsct_b200_dropin.hpp over libgsct_b200.so,
+    pageable std::vector buffers) and as the plain reference on the host cores
+    (dropin_train_cpu). tests/cpp/dropin_train.cpp."""
+    import subprocess
+
+    root = Path(__file__).resolve().parent / "oracle" / "_ref"
+    out: dict = {"unit": "view-steps/s (one fwd+bwd projection each) through train_reconstruction",
+                 "config": "C2: 200000 Gaussians, 75 cone views at 512^2, 1 epoch, TrainConfig defaults"}
+    for tag, exe in (("b200", root / "dropin_train_b200"), ("cpu", root / "dropin_train_cpu")):
+        if not exe.exists():
+            out[tag] = {"unavailable": f"{exe.name} not built (needs /root/reference at build time)"}
+            continue
+        r = subprocess.run([str(exe), "200000", "256", "75", "512", "1"], capture_output=True, text=True,
+                           timeout=timeout_s)
+        line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        out[tag] = json.loads(line[-1]) if line else {"error": (r.stderr or r.stdout)[-300:]}
+    b = out.get("b200", {})
+    if "view_steps_per_s" in b:
+        out["value"] = b["view_steps_per_s"]
+        c = out.get("cpu", {})
+        if "view_steps_per_s" in c:
+            out["speedup_vs_reference_loop"] = round(b["view_steps_per_s"] / c["view_steps_per_s"], 3)
+    return out
 
 
 def run_ours(args, rank: int, world: int, local_rank: int) -> None:
@@ -613,6 +658,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     }
     if e2e is not None:
         out["e2e"] = e2e
+    if not args.no_secondary and world == 1:
+        try:
+            out["dropin"] = run_dropin()
+        except Exception as exc:
+            out["dropin"] = {"error": repr(exc)}
     ref = None
     if not args.no_cpu_baseline and world == 1:
         try:

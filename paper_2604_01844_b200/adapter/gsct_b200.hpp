@@ -23,9 +23,14 @@
 // these under the original names).
 #pragma once
 
+#include <malloc.h>
+
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/gsct_cuda.h"
@@ -33,10 +38,29 @@
 namespace gsct {
 namespace b200 {
 
+// The reference API returns fresh multi-MB containers from every call (ParamGradients:
+// 96 B/splat, 19 MB at 200k splats, twice per view-step of train_reconstruction). glibc
+// serves blocks that large with fresh mmaps by default, so every call pays first-touch page
+// faults (measured: ~4 ms per 19 MB result, more than the GPU work of a one-view call). The
+// first use of the adapter keeps such blocks in the heap instead (reused, already mapped);
+// GSCT_B200_NO_MALLOC_TUNE=1 leaves the process's allocator settings alone.
+inline void tune_host_allocator() {
+  static const bool done = [] {
+    const char* e = std::getenv("GSCT_B200_NO_MALLOC_TUNE");
+    if (!(e && e[0] == '1')) {
+      mallopt(M_MMAP_THRESHOLD, 32 << 20);    // glibc's upper limit on 64-bit
+      mallopt(M_TRIM_THRESHOLD, 1024 << 20);  // keep freed heap for the next call's result
+    }
+    return true;
+  }();
+  (void)done;
+}
+
 // One context per thread and device (the C ABI context is single-threaded).
 class Device {
  public:
   static gsct_ctx ctx(int device = -1) {
+    tune_host_allocator();
     thread_local Device d;
     if (device >= 0 && device != d.device_) d.reset(device);
     if (!d.ctx_) d.reset(d.device_ < 0 ? 0 : d.device_);
@@ -58,7 +82,31 @@ class Device {
   int device_ = -1;
 };
 
+// Wall time spent inside the B200 operators of this thread (drop-in accounting: the
+// reference loop's own CPU work = its wall time minus this).
+struct OpTimes {
+  double seconds = 0.0;
+  std::int64_t calls = 0;
+  double kind_seconds[4] = {0, 0, 0, 0};  // rasterize fwd, rasterize bwd, voxelize, voxelize bwd
+};
+inline OpTimes& op_times() {
+  static thread_local OpTimes t;
+  return t;
+}
+
 namespace detail {
+
+struct OpTimer {
+  int kind;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit OpTimer(int k) : kind(k) {}
+  ~OpTimer() {
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    op_times().seconds += s;
+    op_times().kind_seconds[kind] += s;
+    op_times().calls += 1;
+  }
+};
 
 inline void check_status(gsct_ctx c, int status) {
   if (status == GSCT_OK) return;
@@ -145,7 +193,14 @@ struct GradBuffers {
   ParamGradients g;
   gsct_grads c;
   explicit GradBuffers(std::size_t n) {
-    g.resize(n);
+    // every element is overwritten by the call: default-insert (no ParamGradients::resize
+    // zero pass over the 96 B/splat; Eigen's fixed-size vectors are left uninitialised)
+    g.positions.resize(n);
+    g.log_scales.resize(n);
+    g.rotations.resize(n);
+    g.raw_densities.resize(n);
+    g.pos_grad_norm.resize(n);
+    g.visible.resize(n);
     c.pos = reinterpret_cast<double*>(g.positions.data());
     c.log_scale = reinterpret_cast<double*>(g.log_scales.data());
     c.quat = reinterpret_cast<double*>(g.rotations.data());
@@ -163,6 +218,7 @@ inline std::vector<Image> rasterize_views(const GaussianCloud& cloud, const Scan
                                           const std::vector<std::size_t>& angle_indices,
                                           const RasterSettings& settings = {}, RenderStats* stats = nullptr) {
   geometry.validate();
+  detail::OpTimer timer_(0);
   std::vector<double> angles;
   for (std::size_t v : angle_indices) {
     check(v < geometry.angles.size(), "view_frame: angle index out of range");
@@ -198,6 +254,7 @@ inline ParamGradients rasterize_backward_views(const GaussianCloud& cloud, const
                                                const std::vector<const Image*>& grad_images,
                                                const RasterSettings& settings = {}, RenderStats* stats = nullptr) {
   check(grad_images.size() == angle_indices.size(), "rasterize_backward: one grad image per view");
+  detail::OpTimer timer_(1);
   std::vector<double> angles;
   const std::size_t npx = static_cast<std::size_t>(geometry.n_u) * geometry.n_v;
   std::vector<float> gi(npx * angle_indices.size());
@@ -217,7 +274,7 @@ inline ParamGradients rasterize_backward_views(const GaussianCloud& cloud, const
   detail::check_status(c, gsct_rasterize_bwd(c, &cc, &cg, angles.data(), static_cast<int>(angles.size()), &rs,
                                               gi.data(), GSCT_HOST, &gb.c, stats ? &st : nullptr));
   detail::take_stats(st, stats);
-  return gb.g;
+  return std::move(gb.g);  // a member: no implicit move, so move explicitly (19 MB at 200k)
 }
 
 // gsct::rasterize_backward (projector.hpp:371-482)
@@ -232,6 +289,7 @@ inline ParamGradients rasterize_backward(const GaussianCloud& cloud, const ScanG
 // gsct::voxelize (voxelizer.hpp:162-199)
 inline Volume voxelize(const GaussianCloud& cloud, const GridRegion& region, const VoxelSettings& settings = {},
                        RenderStats* stats = nullptr) {
+  detail::OpTimer timer_(2);
   gsct_ctx c = Device::ctx();
   const gsct_cloud cc = detail::c_cloud(cloud);
   const gsct_grid g = detail::c_grid(region.dims, region.spacing, region.origin);
@@ -256,6 +314,7 @@ inline ParamGradients voxelize_backward(const GaussianCloud& cloud, const GridRe
                                         const Volume& grad_volume, const VoxelSettings& settings = {},
                                         RenderStats* stats = nullptr) {
   check(grad_volume.dims == region.dims, "voxelize_backward: grad dims must match region");
+  detail::OpTimer timer_(3);
   gsct_ctx c = Device::ctx();
   const gsct_cloud cc = detail::c_cloud(cloud);
   const gsct_grid g = detail::c_grid(region.dims, region.spacing, region.origin);
@@ -267,7 +326,7 @@ inline ParamGradients voxelize_backward(const GaussianCloud& cloud, const GridRe
   detail::check_status(c, gsct_voxelize_bwd(c, &cc, &g, nullptr, &vs, gv.data(), GSCT_HOST, &gb.c,
                                              stats ? &st : nullptr));
   detail::take_stats(st, stats);
-  return gb.g;
+  return std::move(gb.g);  // a member: no implicit move, so move explicitly (19 MB at 200k)
 }
 
 }  // namespace b200

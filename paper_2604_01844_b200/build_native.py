@@ -24,7 +24,7 @@ NVFLAGS = ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xpt
 # preprocess.cu holds the fp64 set-up whose operation order must match the reference
 # exactly (no FMA contraction) so integer boxes / keys are bit-exact.
 PER_FILE = {"preprocess.cu": ["--fmad=false"], "control.cu": ["--fmad=false"], "codec.cu": ["--fmad=false"]}
-CU_SOURCES = ["api.cu", "preprocess.cu", "tail.cu", "raster.cu", "order.cu", "voxel.cu", "loss.cu", "control.cu", "codec.cu", "microbench.cu", "group.cu"]
+CU_SOURCES = ["api.cu", "preprocess.cu", "tail.cu", "raster.cu", "order.cu", "voxel.cu", "loss.cu", "control.cu", "codec.cu", "microbench.cu", "group.cu", "hostio.cu"]
 CXX_SOURCES = ["host.cpp"]
 
 

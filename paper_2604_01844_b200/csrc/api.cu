@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -13,6 +14,7 @@
 
 #include "../../include/gsct_cuda.h"
 #include "group.h"
+#include "hostio.h"
 #include "gsct_internal.cuh"
 
 using namespace gsct_dev;
@@ -82,6 +84,8 @@ struct gsct_ctx_s {
   gsct_dev::WalkLayout walk_L;
   // multi-GPU group (gsct_ctx_set_group): collectives of the backward / voxel calls
   gsct_group group = nullptr;
+  // staged transfers of pageable host buffers + the pageable host-cloud replica (hostio.cu)
+  gsct_dev::HostIO hio;
 };
 
 namespace gsct_dev {
@@ -107,9 +111,28 @@ void contract(bool ok, const std::string& msg) {
   if (!ok) throw CallError{GSCT_ERR_CONTRACT, msg};
 }
 
+// Host <-> device copies of caller buffers: pageable memory is staged (hostio.cu) in
+// synchronous mode; async calls (whose completion the caller owns) use plain copies.
+void h2d(gsct_ctx c, void* dst, const void* src, size_t bytes, cudaStream_t st);
+void d2h(gsct_ctx c, void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 // group.cu calls: empty string = success
 void GK(const std::string& err) {
   if (!err.empty()) throw CallError{GSCT_ERR_CUDA, err};
+}
+
+void h2d(gsct_ctx c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (c->async)
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+  else
+    CK(c->hio.h2d(dst, src, bytes, st));
+}
+
+void d2h(gsct_ctx c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (c->async)
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+  else
+    CK(c->hio.d2h(dst, src, bytes, st));
 }
 
 template <class T>
@@ -189,6 +212,17 @@ struct Guard {  // sets the launch counter for the duration of an API call
   ~Guard() { g_launch_counter = nullptr; }
 };
 
+// error path: in-flight DMAs may still target the staging arena (and the cloud replica
+// is suspect), so wait for them before the arena is reused
+void drop_staged(gsct_ctx c) {
+  cudaStreamSynchronize(c->copy_stream);
+  cudaStreamSynchronize(c->aux_stream);
+  cudaStreamSynchronize(c->stream);
+  cudaGetLastError();
+  c->hio.discard();
+  c->hio.invalidate_cloud();
+}
+
 template <class F>
 int run(gsct_ctx c, F&& f) {
   if (!c) return GSCT_ERR_CONTRACT;
@@ -199,9 +233,11 @@ int run(gsct_ctx c, F&& f) {
     return GSCT_OK;
   } catch (const CallError& e) {
     c->err = e.msg;
+    drop_staged(c);
     return e.code;
   } catch (const std::exception& e) {
     c->err = e.what();
+    drop_staged(c);
     return GSCT_ERR_CUDA;
   }
 }
@@ -240,11 +276,19 @@ RSet make_rs(const gsct_raster_settings* r) {
 }
 
 // Device view of a cloud; host arrays get device copies (allocated here; the copy is
-// enqueued on `st` unless `copy` is false -- then copy_cloud() does it later).
+// enqueued on `st` unless `copy` is false -- then copy_cloud() does it later). A pageable
+// host cloud in synchronous mode is kept as a device replica refreshed chunk-wise
+// (hostio.cu), whatever `copy` says.
 Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl, cudaStream_t st = nullptr, bool copy = true);
+
+bool replica_applies(gsct_ctx c, const gsct_cloud* cl) {
+  return !c->async && cl->location == GSCT_HOST && cl->n > 0 && host_pageable(cl->pos) &&
+         host_pageable(cl->log_scale) && host_pageable(cl->quat) && host_pageable(cl->raw_density);
+}
 
 void copy_cloud(gsct_ctx c, const gsct_cloud* cl, const Cloud& d, cudaStream_t st) {
   const size_t n = static_cast<size_t>(cl->n);
+  c->hio.invalidate_cloud();  // the device buffers no longer hold the pageable replica
   if (st != c->stream) stream_after(c, st, c->stream);  // after the (re)allocation and prior readers
   CK(cudaMemcpyAsync(const_cast<double*>(d.pos), cl->pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(const_cast<double*>(d.ls), cl->log_scale, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -266,7 +310,15 @@ Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl, cudaStream_t st, bool copy)
     d.ls = ws<double>(c, S_LS, 3 * n);
     d.q = ws<double>(c, S_Q, 4 * n);
     d.raw = ws<double>(c, S_RAW, n);
-    if (copy) copy_cloud(c, cl, d, st);
+    if (replica_applies(c, cl)) {
+      // pageable host cloud (the C++ drop-in): chunks changed since the last call only
+      const CloudArrays h{{cl->pos, cl->log_scale, cl->quat, cl->raw_density}};
+      const CloudArrays dv{{d.pos, d.ls, d.q, d.raw}};
+      if (st != c->stream) stream_after(c, st, c->stream);
+      CK(c->hio.cloud_to_device(h, dv, cl->n, c->device, st, nullptr));
+    } else if (copy) {
+      copy_cloud(c, cl, d, st);
+    }
   }
   return d;
 }
@@ -303,8 +355,13 @@ void finish_sync(gsct_ctx c, gsct_stats* stats, bool counters, double* ms_slot) 
   if (c->async) return;
   CK(cudaMemcpyAsync(c->hstats, c->dstats, sizeof(DevStats), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaEventRecord(c->ev1, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaStreamSynchronize(c->stream));
+    c->hio.ms_sync += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
   CK(cudaGetLastError());
+  c->hio.finish();  // deferred copy-outs of staged D2H into pageable caller buffers
   const DevStats& h = *c->hstats;
   if (h.error_key != ~0ull) {
     const unsigned long long idx = h.error_key >> 2;
@@ -816,13 +873,15 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
                              // as soon as its bytes are in (single view chunk only)
 #endif
     const int64_t n_in = cloud ? cloud->n : 0;
-    const int cloud_pieces = cloud && cloud->location == GSCT_HOST && n_in >= 16384 && n_views > 0 &&
+    const int cloud_pieces = cloud && cloud->location == GSCT_HOST && !replica_applies(c, cloud) && n_in >= 16384 &&
+                                     n_views > 0 &&
                                      views_per_chunk(n_in, n_views, 0) >= n_views
                                  ? GSCT_CLOUD_PIECES
                                  : 1;
     const Cloud d = upload_cloud(c, cloud, c->stream, cloud_pieces == 1);
     std::vector<cudaEvent_t> piece_up;
     if (cloud_pieces > 1) {
+      c->hio.invalidate_cloud();
       stream_after(c, c->copy_stream, c->stream);  // after the (re)allocation and prior readers
       for (int k = 0; k < cloud_pieces; ++k) {
         const size_t a = static_cast<size_t>(n_in * k / cloud_pieces), b = static_cast<size_t>(n_in * (k + 1) / cloud_pieces);
@@ -895,8 +954,8 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         CK(cudaMemsetAsync(img, 0, static_cast<size_t>(npx) * cv * sizeof(float), c->stream));
         if (images_location == GSCT_HOST) {
           stream_after(c, c->copy_stream, c->stream);
-          CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0) * npx, img, static_cast<size_t>(npx) * cv * sizeof(float),
-                             cudaMemcpyDeviceToHost, c->copy_stream));
+          d2h(c, images + static_cast<int64_t>(v0) * npx, img, static_cast<size_t>(npx) * cv * sizeof(float),
+              c->copy_stream);
         }
         continue;
       }
@@ -983,9 +1042,8 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
           CK(cudaGetLastError());
           if (stage_images) {
             stream_after(c, c->copy_stream, fs);
-            CK(cudaMemcpyAsync(images + static_cast<int64_t>(v0 + b0 + vs) * npx,
-                               bimg + static_cast<int64_t>(vs) * npx, static_cast<size_t>(npx) * nvs * sizeof(float),
-                               cudaMemcpyDeviceToHost, c->copy_stream));
+            d2h(c, images + static_cast<int64_t>(v0 + b0 + vs) * npx, bimg + static_cast<int64_t>(vs) * npx,
+                static_cast<size_t>(npx) * nvs * sizeof(float), c->copy_stream);
           }
         }
         if (dual) stream_after(c, c->stream, c->aux_stream);
@@ -1018,7 +1076,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     // goes up on the copy stream, overlapped with the pixel walk
     const bool reuse = c->save_fb && c->saved_valid && cloud != nullptr && cloud->n > 0 &&
                        c->saved_key == raster_call_key(cloud, geom, angles, n_views, rs);
-    const bool late_cloud = reuse && cloud->location == GSCT_HOST;
+    const bool late_cloud = reuse && cloud->location == GSCT_HOST && !replica_applies(c, cloud);
     const Cloud d = upload_cloud(c, cloud, c->stream, !late_cloud);
     cudaEvent_t cloud_up = nullptr;
     const int64_t n = d.n;
@@ -1134,8 +1192,8 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       stream_after(c, c->copy_stream, c->stream);
       for (size_t k = 0; k + 1 < cb.size(); ++k) {
         const int v0 = cb[k], cv = cb[k + 1] - cb[k];
-        CK(cudaMemcpyAsync(gdev + static_cast<int64_t>(v0) * npx, grad_images + static_cast<int64_t>(v0) * npx,
-                           static_cast<size_t>(npx) * cv * sizeof(float), cudaMemcpyHostToDevice, c->copy_stream));
+        h2d(c, gdev + static_cast<int64_t>(v0) * npx, grad_images + static_cast<int64_t>(v0) * npx,
+            static_cast<size_t>(npx) * cv * sizeof(float), c->copy_stream);
         up_done.push_back(pooled_event(c));
         CK(cudaEventRecord(up_done.back(), c->copy_stream));
       }
@@ -1255,16 +1313,12 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         if (pieces > 1 && stage_grads) {
           const size_t a = static_cast<size_t>(i0), m = static_cast<size_t>(i1 - i0);
           stream_after(c, c->copy_stream, ts);
-          CK(cudaMemcpyAsync(out->pos + 3 * a, gp + 3 * a, 3 * m * sizeof(double), cudaMemcpyDeviceToHost,
-                             c->copy_stream));
-          CK(cudaMemcpyAsync(out->log_scale + 3 * a, gl + 3 * a, 3 * m * sizeof(double), cudaMemcpyDeviceToHost,
-                             c->copy_stream));
-          CK(cudaMemcpyAsync(out->quat + 4 * a, gq + 4 * a, 4 * m * sizeof(double), cudaMemcpyDeviceToHost,
-                             c->copy_stream));
-          CK(cudaMemcpyAsync(out->raw_density + a, gr + a, m * sizeof(double), cudaMemcpyDeviceToHost, c->copy_stream));
-          CK(cudaMemcpyAsync(out->pos_grad_norm + a, gn + a, m * sizeof(double), cudaMemcpyDeviceToHost,
-                             c->copy_stream));
-          CK(cudaMemcpyAsync(out->visible + a, gv + a, m, cudaMemcpyDeviceToHost, c->copy_stream));
+          d2h(c, out->pos + 3 * a, gp + 3 * a, 3 * m * sizeof(double), c->copy_stream);
+          d2h(c, out->log_scale + 3 * a, gl + 3 * a, 3 * m * sizeof(double), c->copy_stream);
+          d2h(c, out->quat + 4 * a, gq + 4 * a, 4 * m * sizeof(double), c->copy_stream);
+          d2h(c, out->raw_density + a, gr + a, m * sizeof(double), c->copy_stream);
+          d2h(c, out->pos_grad_norm + a, gn + a, m * sizeof(double), c->copy_stream);
+          d2h(c, out->visible + a, gv + a, m, c->copy_stream);
         }
       }
       if (tdual) stream_after(c, c->stream, c->aux_stream);
@@ -1277,14 +1331,14 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       CK(cudaStreamWaitEvent(c->stream, cloud_up, 0));  // also when n_views == 0
       c->event_pool.push_back(cloud_up);
     }
-    if (zc_grads) CK(cudaMemcpyAsync(out->visible, gv, un, cudaMemcpyDeviceToHost, c->stream));
+    if (zc_grads) d2h(c, out->visible, gv, un, c->stream);
     if (stage_grads && !grads_down) {
-      CK(cudaMemcpyAsync(out->pos, gp, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(out->log_scale, gl, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(out->quat, gq, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(out->raw_density, gr, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(out->pos_grad_norm, gn, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(out->visible, gv, un, cudaMemcpyDeviceToHost, c->stream));
+      d2h(c, out->pos, gp, 3 * un * sizeof(double), c->stream);
+      d2h(c, out->log_scale, gl, 3 * un * sizeof(double), c->stream);
+      d2h(c, out->quat, gq, 4 * un * sizeof(double), c->stream);
+      d2h(c, out->raw_density, gr, un * sizeof(double), c->stream);
+      d2h(c, out->pos_grad_norm, gn, un * sizeof(double), c->stream);
+      d2h(c, out->visible, gv, un, c->stream);
     }
     finish_sync(c, stats, false, stats ? &stats->backward_ms : nullptr);
   });
@@ -1331,7 +1385,7 @@ void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window
   const int64_t nvox = window_count(win);
   if (grad_location == GSCT_HOST) {
     float* dst = ws<float>(c, S_GRADVOL, static_cast<size_t>(nvox));
-    CK(cudaMemcpyAsync(dst, grad, static_cast<size_t>(nvox) * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    h2d(c, dst, grad, static_cast<size_t>(nvox) * sizeof(float), c->stream);
     grad = dst;
   }
   CK(cudaMemsetAsync(mom, 0, static_cast<size_t>(n) * 10 * sizeof(float), c->stream));
@@ -1380,12 +1434,12 @@ GradPtrs grad_targets(gsct_ctx c, gsct_grads* out, size_t un) {
 
 void grads_to_host(gsct_ctx c, gsct_grads* out, const GradPtrs& p, size_t un) {
   if (out->location != GSCT_HOST || un == 0) return;
-  CK(cudaMemcpyAsync(out->pos, p.gp, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(out->log_scale, p.gl, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(out->quat, p.gq, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(out->raw_density, p.gr, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(out->pos_grad_norm, p.gn, un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(out->visible, p.gv, un, cudaMemcpyDeviceToHost, c->stream));
+  d2h(c, out->pos, p.gp, 3 * un * sizeof(double), c->stream);
+  d2h(c, out->log_scale, p.gl, 3 * un * sizeof(double), c->stream);
+  d2h(c, out->quat, p.gq, 4 * un * sizeof(double), c->stream);
+  d2h(c, out->raw_density, p.gr, un * sizeof(double), c->stream);
+  d2h(c, out->pos_grad_norm, p.gn, un * sizeof(double), c->stream);
+  d2h(c, out->visible, p.gv, un, c->stream);
 }
 
 }  // namespace
@@ -1465,7 +1519,7 @@ int gsct_voxelize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
       voxel_fwd_window(c, d, vg, win, vs, outv);
     }
     if (volume_location == GSCT_HOST)
-      CK(cudaMemcpyAsync(volume, outv, static_cast<size_t>(nvox) * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+      d2h(c, volume, outv, static_cast<size_t>(nvox) * sizeof(float), c->stream);
     finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
   });
 }
@@ -2116,6 +2170,7 @@ int gsct_decompress_model(gsct_ctx c, const uint8_t* bytes, int64_t n_bytes, int
       q = const_cast<double*>(out->quat);
       r = const_cast<double*>(out->raw_density);
     } else {
+      c->hio.invalidate_cloud();  // decoded into the host-cloud replica's buffers
       p = ws<double>(c, S_POS, 3 * un);
       l = ws<double>(c, S_LS, 3 * un);
       q = ws<double>(c, S_Q, 4 * un);
@@ -2124,14 +2179,13 @@ int gsct_decompress_model(gsct_ctx c, const uint8_t* bytes, int64_t n_bytes, int
     launch_fgsc_decode(body, n, table, p, l, q, r, c->stream);
     CK(cudaGetLastError());
     if (out->location == GSCT_HOST) {
-      CK(cudaMemcpyAsync(const_cast<double*>(out->pos), p, 3 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(const_cast<double*>(out->log_scale), l, 3 * un * sizeof(double), cudaMemcpyDeviceToHost,
-                         c->stream));
-      CK(cudaMemcpyAsync(const_cast<double*>(out->quat), q, 4 * un * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(const_cast<double*>(out->raw_density), r, un * sizeof(double), cudaMemcpyDeviceToHost,
-                         c->stream));
+      d2h(c, const_cast<double*>(out->pos), p, 3 * un * sizeof(double), c->stream);
+      d2h(c, const_cast<double*>(out->log_scale), l, 3 * un * sizeof(double), c->stream);
+      d2h(c, const_cast<double*>(out->quat), q, 4 * un * sizeof(double), c->stream);
+      d2h(c, const_cast<double*>(out->raw_density), r, un * sizeof(double), c->stream);
     }
     CK(cudaStreamSynchronize(c->stream));
+    c->hio.finish();
   });
 }
 

@@ -1108,6 +1108,26 @@ class LearningRates:
     density: float = 1e-2
 
 
+def lr_schedule(base: float, final_lr: float, step: int, horizon: int) -> float:
+    """lr_schedule (optim.hpp:71-78): log-linear decay from base to final over [0, horizon],
+    clamped at final (host scalar, the reference's std::pow)."""
+    if not (base > 0.0 and final_lr > 0.0):
+        raise ContractError("lr_schedule: rates must be positive")
+    if step <= 0:
+        return float(base)
+    if horizon <= 0 or step >= horizon:
+        return float(final_lr)
+    return float(base * (final_lr / base) ** (float(step) / float(horizon)))
+
+
+def scene_extent(cloud: GaussianCloud) -> float:
+    """scene_extent (core.hpp:120-129): half the diagonal of the positions' bounding box."""
+    if cloud.size() == 0:
+        raise ContractError("scene_extent: empty model")
+    p = cloud.positions.cpu().numpy() if _is_torch(cloud.positions) else np.asarray(cloud.positions)
+    return float(0.5 * np.linalg.norm(p.max(axis=0) - p.min(axis=0)))
+
+
 class AdamState:
     """OptimState's Adam moments (optim.hpp:84-114) as device fp64 tensors."""
 
