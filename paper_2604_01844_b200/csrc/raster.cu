@@ -674,36 +674,31 @@ __device__ __forceinline__ bool raster_chain2_safe(float A, float B, float C, fl
 #ifndef GSCT_CHAIN_UNROLL
 #define GSCT_CHAIN_UNROLL 1
 #endif
+#ifndef GSCT_CHAIN_MINB4_MAX_PX
+#define GSCT_CHAIN_MINB4_MAX_PX (1 << 20)  // images up to 1M pixels: the 64-register walk
+#endif
 constexpr int kChainUnroll = GSCT_CHAIN_UNROLL;
-__global__ void __launch_bounds__(256, GSCT_CHAIN_MINB) k_raster_bwd_chain(const RasterRec* __restrict__ rec,
-                                                                           const uint32_t* __restrict__ order,
-                                                                           int64_t n_items, int64_t n, int n_u,
-                                                                           int n_v, const float* __restrict__ grad,
-                                                                           float* __restrict__ moments, double inv_n,
-                                                                           int view_offset) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= n_items) return;
-  const int64_t item = order ? static_cast<int64_t>(__ldg(order + t)) : t;
-  const RasterRec r = rec[item];
-  const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
-  const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
-  const int W = u1 - u0 + 1, H = v1 - v0 + 1;
-  float4* dst = reinterpret_cast<float4*>(moments + (static_cast<int64_t>(view_offset) * n + item) * 8);
-  if (W <= 0 || H <= 0) {
-    dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    return;
-  }
-  const int view = static_cast<int>((static_cast<double>(item) + 0.5) * inv_n);
-  const int ua = u0 & ~7;
-  const int lead = u0 - ua;
+
+// Row source of the chain walk: a grad-image row in global memory (32 B-aligned chunks,
+// ld.global.nc.v8). (A shared-memory tile source -- one CTA per 64x64 region staging its grad
+// tile -- was slower: lane-per-item gathers from shared memory bank-conflict.)
+struct GlobalRows {
+  const float* p;
+  int stride;
+  __device__ __forceinline__ void load(int off, float (&w)[8]) const { ldg_v8(p + off, w); }
+  __device__ __forceinline__ void next() { p += stride; }
+};
+
+// One (view, splat) item's pixel walk (K4a arithmetic, see above): rows of `row` starting at
+// the walked column ua = u0 - lead; writes the 6 moments + visibility to dst.
+template <class Rows>
+__device__ __forceinline__ void bwd_walk(const RasterRec& r, int lead, int W, int H, Rows row, float4* dst) {
   const int ncol = lead + W;
   const int nch = (ncol + 7) >> 3;
   // walked column k = 0 .. 8 nch - 1 (absolute ua + k); du = k - kap
   const float kap = static_cast<float>(lead) + r.mo_u;
   const float kr = rintf(kap);
   const float dl = kap - kr;  // du = k' - dl, k' = k - kr
-  const float* __restrict__ prow = grad + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(v0) * n_u + ua;
   const float A = r.A, B = r.B, C = r.C;
   const bool safe = raster_chain2_safe(A, B, C, -kap, static_cast<float>(8 * nch + 1) - kap, -r.mo_v,
                                        static_cast<float>(H - 1) - r.mo_v);
@@ -720,7 +715,7 @@ __global__ void __launch_bounds__(256, GSCT_CHAIN_MINB) k_raster_bwd_chain(const
     MF[h] = f2_pack(f0 ? 1.f : 0.f, f1 ? 1.f : 0.f);
     ML[h] = f2_pack(last + q0 < ncol ? 1.f : 0.f, last + q1 < ncol ? 1.f : 0.f);
   }
-  for (int row = 0; row < H; ++row, prow += n_u, dv += 1.f) {
+  for (int rw = 0; rw < H; ++rw, row.next(), dv += 1.f) {
     f2_t X0 = f2_bc(0.f), X1 = X0, X2 = X0;
     if (safe) {
       const float du0 = -kap;
@@ -736,9 +731,9 @@ __global__ void __launch_bounds__(256, GSCT_CHAIN_MINB) k_raster_bwd_chain(const
       //   sum t k' = BE Y0 + 2 Z,  sum t k'^2 = BE (BE Y0 + 4 Z) + 4 Q
       f2_t BE = f2_add(f2_bc(-kr), KO0);
       // one 8-column chunk; kMask: first / last chunk (edge columns zeroed by the 0/1 pairs)
-      auto chunk = [&](const float* __restrict__ p, const f2_t* M, auto masked) {
+      auto chunk = [&](int off, const f2_t* M, auto masked) {
         float w[8];
-        ldg_v8(p, w);
+        row.load(off, w);
         f2_t W0 = f2_pack(w[0], w[1]), W1 = f2_pack(w[2], w[3]), W2 = f2_pack(w[4], w[5]),
              W3 = f2_pack(w[6], w[7]);
         if constexpr (decltype(masked)::value) {
@@ -766,10 +761,10 @@ __global__ void __launch_bounds__(256, GSCT_CHAIN_MINB) k_raster_bwd_chain(const
       };
       using yes = std::integral_constant<bool, true>;
       using no = std::integral_constant<bool, false>;
-      chunk(prow, MF, yes{});
+      chunk(0, MF, yes{});
 #pragma unroll kChainUnroll
-      for (int j = 1; j < nch - 1; ++j) chunk(prow + 8 * j, nullptr, no{});
-      if (nch > 1) chunk(prow + 8 * (nch - 1), ML, yes{});
+      for (int j = 1; j < nch - 1; ++j) chunk(8 * j, nullptr, no{});
+      if (nch > 1) chunk(8 * (nch - 1), ML, yes{});
     } else {
       // direct path: one exp2 per pixel (the quadratic in k' evaluated per column pair)
       float b = -kr;
@@ -779,7 +774,7 @@ __global__ void __launch_bounds__(256, GSCT_CHAIN_MINB) k_raster_bwd_chain(const
 #pragma unroll 1
       for (int j = 0; j < nch; ++j, b += 8.f) {
         float w[8];
-        ldg_v8(prow + 8 * j, w);
+        row.load(8 * j, w);
         f2_t kA = f2_add(f2_bc(b), KO0);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -823,6 +818,34 @@ __global__ void __launch_bounds__(256, GSCT_CHAIN_MINB) k_raster_bwd_chain(const
   }
   dst[0] = make_float4(m0, mu, mv, muu);
   dst[1] = make_float4(muv, mvv, 1.f, 0.f);
+}
+
+// MINB: resident CTAs per SM the registers are capped for (3: 80 registers, 4: 64 with a few
+// spilled bytes -- A/B: C2 (512^2) 2.365 vs 2.418 ms, C5 (2048^2) 56.1 vs 55.7 ms).
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_raster_bwd_chain(const RasterRec* __restrict__ rec,
+                                                                           const uint32_t* __restrict__ order,
+                                                                           int64_t n_items, int64_t n, int n_u,
+                                                                           int n_v, const float* __restrict__ grad,
+                                                                           float* __restrict__ moments, double inv_n,
+                                                                           int view_offset) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n_items) return;
+  const int64_t item = order ? static_cast<int64_t>(__ldg(order + t)) : t;
+  const RasterRec r = rec[item];
+  const int u0 = r.urange & 0xFFFF, u1 = r.urange >> 16;
+  const int v0 = r.vrange & 0xFFFF, v1 = r.vrange >> 16;
+  const int W = u1 - u0 + 1, H = v1 - v0 + 1;
+  float4* dst = reinterpret_cast<float4*>(moments + (static_cast<int64_t>(view_offset) * n + item) * 8);
+  if (W <= 0 || H <= 0) {
+    dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int view = static_cast<int>((static_cast<double>(item) + 0.5) * inv_n);
+  const int ua = u0 & ~7;
+  const GlobalRows rows{grad + static_cast<int64_t>(view) * n_u * n_v + static_cast<int64_t>(v0) * n_u + ua, n_u};
+  bwd_walk(r, u0 - ua, W, H, rows, dst);
 }
 
 // Spatial walk-order keys for the chain backward: a coarse shape class (chunks per row
@@ -1042,8 +1065,12 @@ void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_
   if (items == 0) return;
   const int vec = bwd_vec(n_u, grad_images);
   if (GSCT_BWD_CHAIN && vec == 8)
-    k_raster_bwd_chain<<<blocks_for(items, 256), 256, 0, st>>>(rec, order, items, n, n_u, n_v, grad_images, moments,
-                                                               1.0 / static_cast<double>(n), view_offset);
+    if (static_cast<int64_t>(n_u) * n_v <= GSCT_CHAIN_MINB4_MAX_PX)
+      k_raster_bwd_chain<4><<<blocks_for(items, 256), 256, 0, st>>>(rec, order, items, n, n_u, n_v, grad_images,
+                                                                     moments, 1.0 / static_cast<double>(n), view_offset);
+    else
+      k_raster_bwd_chain<GSCT_CHAIN_MINB><<<blocks_for(items, 256), 256, 0, st>>>(
+          rec, order, items, n, n_u, n_v, grad_images, moments, 1.0 / static_cast<double>(n), view_offset);
   else if (vec == 8)
     k_raster_bwd_lanes<8><<<blocks_for(items, 256), 256, 0, st>>>(rec, order, items, n, n_u, n_v, grad_images,
                                                                   moments, 1.0 / static_cast<double>(n), view_offset);
