@@ -120,17 +120,19 @@ class ClockSampler:
         self._thr = None
         self._nv = None
 
-    def _poll(self):
+    def _sample(self):
         nv, h = self._nv, self._h
-        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+            self.rows.append((int(sm), int(self._smax), int(rs), float(pw)))
+        except Exception:
+            pass
+
+    def _poll(self):
         while not self._stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
-                self.rows.append((int(sm), int(smax), int(rs), float(pw)))
-            except Exception:
-                pass
+            self._sample()
             time.sleep(self.period)
 
     def __enter__(self):
@@ -139,6 +141,10 @@ class ClockSampler:
 
             nv.nvmlInit()
             self._nv, self._h = nv, nv.nvmlDeviceGetHandleByIndex(self.device)
+            self._smax = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._sample()  # at the start of the timed region (the GPU is busy with the warm-up)
+            self._switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.0005)  # let the sampling thread in between launches
             self._thr = threading.Thread(target=self._poll, daemon=True)
             self._thr.start()
             time.sleep(0.01)
@@ -147,6 +153,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        if self._nv is not None:
+            self._sample()  # the end of the timed region
+            sys.setswitchinterval(self._switch)
         self._stop.set()
         if self._thr is not None:
             self._thr.join(timeout=2)

@@ -29,7 +29,7 @@ enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
   S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG, S_FGSC, S_FGSC_LOG, S_FGSC_CNT, S_VTCOUNT,
-  S_TOTAL64, S_VIEWPAIRS, S_WCOUNT, S_WSLOT, S_WSUMS, S_WSTART, S_MOMENTS64,
+  S_TOTAL64, S_VIEWPAIRS, S_WCOUNT, S_WSLOT, S_WSUMS, S_WSTART, S_MOMENTS64, S_BSUMS,
   S_COUNT_SLOTS
 };
 
@@ -510,24 +510,26 @@ void bin_packed(gsct_ctx c, const BinPlan& pl, const RasterRec* rec, const uint3
     return;
   }
   uint32_t* offsets = ws<uint32_t>(c, S_OFFSET, static_cast<size_t>(n_items));
-  size_t tmp_bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
-  void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
-  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offsets, static_cast<int>(n_items), c->stream));
   uint32_t* k1 = ws<uint32_t>(c, S_KEYS, static_cast<size_t>(total));
   uint32_t* k2 = ws<uint32_t>(c, S_KEYS2, static_cast<size_t>(total));
   uint32_t* vt = ws<uint32_t>(c, S_VTCOUNT, static_cast<size_t>(n_views) * n_tiles);
   CK(cudaMemsetAsync(vt, 0, static_cast<size_t>(n_views) * n_tiles * sizeof(uint32_t), c->stream));
-  if (pl.wide)
+  // item offsets: the hand-written u32 scan (order.cu)
+  launch_exclusive_scan_u32(counts, offsets, n_items,
+                            ws<uint32_t>(c, S_BSUMS, static_cast<size_t>(scan_workspace_u32(n_items))), c->stream);
+#ifndef GSCT_EMIT_WIDE_ALL
+#define GSCT_EMIT_WIDE_ALL 1  // 4096-item emitting CTAs for the narrow layout too (A/B C2 emit 0.234 -> 0.176 ms)
+#endif
+  if (pl.wide || (GSCT_EMIT_WIDE_ALL && n >= kWideItems))
     launch_emit_tile_keys_wide(rec, offsets, counts, n, n_views, kBinTile, tiles_u, n_tiles, pl.shift, k1, vt,
                                c->stream);
   else
     launch_emit_tile_keys(rec, offsets, counts, n, n_views, kBinTile, tiles_u, n_tiles, k1, vt, c->stream);
   cub::DoubleBuffer<uint32_t> kb(k1, k2);
-  tmp_bytes = 0;
+  size_t tmp_bytes = 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, kb, static_cast<int>(total), pl.shift,
                                     pl.shift + pl.tile_bits, c->stream));
-  tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
+  void* tmp = ws<uint8_t>(c, S_CUB, tmp_bytes);
   CK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, kb, static_cast<int>(total), pl.shift, pl.shift + pl.tile_bits,
                                     c->stream));
   *keys_out = kb.Current();

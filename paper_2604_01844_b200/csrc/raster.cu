@@ -966,8 +966,8 @@ void launch_emit_tile_keys_wide(const RasterRec* rec, const uint32_t* offsets, c
   const int64_t items = n * n_views;
   if (items == 0) return;
   const size_t smem = 2 * static_cast<size_t>(n_tiles) * sizeof(uint32_t);
-  k_emit_tile_keys_wide<<<blocks_for(items, kWideItems), 256, smem, st>>>(rec, offsets, counts, n, n_views, tiles_u,
-                                                                          n_tiles, ts, shift, keys, vt_count);
+  k_emit_tile_keys_wide<<<blocks_for(items, kWideItems), 256, smem, st>>>(
+      rec, offsets, counts, n, n_views, tiles_u, n_tiles, ts, shift, keys, vt_count);
   count_launch();
 }
 
