@@ -290,6 +290,8 @@ struct Proj {
   bool culled, degenerate;
   double ad[3], beta, mu, k, cov_px[4], d_ray[3];
   double t_cam[3], jac[6], dist;
+  // backward tail only (project_full<false>): reciprocals shared with raster_chain_rule
+  double itz, inv_dist, rb;  // 1 / t_cam.z, 1 / dist, 1 / sqrt(beta)
 };
 
 // detail::project_full (projector.hpp:143-236)
@@ -346,7 +348,13 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
     double rel[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) rel[k] = position[k] - fr.src[k];
-    p.dist = sqrt(dot3(rel, rel));
+    if (kBox) {
+      p.dist = sqrt(dot3(rel, rel));
+    } else {  // one rsqrt for the distance and its reciprocal
+      const double d2 = dot3(rel, rel);
+      p.inv_dist = rsqrt(d2);
+      p.dist = d2 * p.inv_dist;
+    }
     p.t_cam[0] = dot3(rel, fr.u);
     p.t_cam[1] = dot3(rel, fr.v);
     p.t_cam[2] = dot3(rel, fr.d);
@@ -367,10 +375,12 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
       J[4] = f / (g.s_v * tz);
       J[5] = -f * p.t_cam[1] / (g.s_v * tz * tz);
     } else {  // backward tail: tolerance-level arithmetic, reciprocals instead of divisions
-      const double inv_dist = 1.0 / p.dist;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) p.d_ray[k] = rel[k] * inv_dist;
-      const double fu = f / (g.s_u * tz), fv = f / (g.s_v * tz), itz = 1.0 / tz;
+      for (int k = 0; k < 3; ++k) p.d_ray[k] = rel[k] * p.inv_dist;
+      const double itz = 1.0 / tz;
+      p.itz = itz;
+      // 1 / s_u, 1 / s_v depend on kernel parameters only (hoisted out of the view loop)
+      const double fu = f * (1.0 / g.s_u) * itz, fv = f * (1.0 / g.s_v) * itz;
       J[0] = fu;
       J[2] = -fu * p.t_cam[0] * itz;
       J[4] = fv;
@@ -412,16 +422,25 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
     p.degenerate = true;
     return;
   }
-  p.mu = sqrt(2.0 * 3.14159265358979323846 / p.beta);
+  if (kBox) {
+    p.mu = sqrt(2.0 * 3.14159265358979323846 / p.beta);
+  } else {
+    p.rb = rsqrt(p.beta);
+    p.mu = 2.5066282746310002 * p.rb;  // sqrt(2 pi / beta)
+  }
 
   double cr[4] = {p.cov_px[0], p.cov_px[1], p.cov_px[2], p.cov_px[3]};
   if (rs.dilate) {
     cr[0] += rs.dilation_px2;
     cr[3] += rs.dilation_px2;
-    const double det_raw = dmax_(det2(p.cov_px), 0.0);
-    p.k = sqrt(det_raw / det2(cr));
   }
   const double dt2 = det2(cr);
+  double rdt = 0.0;  // tail: 1 / sqrt(dt2) (the visible item has dt2 > 0)
+  if (!kBox) rdt = rsqrt(dt2);
+  if (rs.dilate) {
+    const double det_raw = dmax_(det2(p.cov_px), 0.0);
+    p.k = kBox ? sqrt(det_raw / dt2) : sqrt(det_raw) * rdt;
+  }
   if (kBox) {
     const double lam_max = max_eig2(cr);
     const double lam_min = dt2 / dmax_(lam_max, DBL_MIN);
@@ -435,7 +454,7 @@ __device__ __forceinline__ void project_full(const Frame& fr, const Geo& g, cons
   {
     // the conic feeds only the fp32 record and the gradients (never the integer box), so one
     // reciprocal replaces the reference's four divisions (<= 1 ulp apart)
-    const double idt = 1.0 / dt2;
+    const double idt = kBox ? 1.0 / dt2 : rdt * rdt;
     p.conic[0] = cr[3] * idt;
     p.conic[1] = -cr[1] * idt;
     p.conic[2] = -cr[2] * idt;
@@ -484,7 +503,7 @@ __device__ __forceinline__ void raster_chain_rule(const Frame& fr, const Geo& g,
       for (int k = 0; k < 4; ++k) gcov[k] += sc * (ci[k] - p.conic[k]);
     }
   }
-  const double g_beta = -g_mu * p.mu / (2.0 * p.beta);
+  const double g_beta = -g_mu * p.mu * (0.5 * p.rb * p.rb);  // -g_mu mu / (2 beta)
   double gsig[9];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
@@ -582,8 +601,8 @@ __device__ __forceinline__ void raster_chain_rule(const Frame& fr, const Geo& g,
 #pragma unroll
     for (int k = 0; k < 3; ++k) gt[k] = J[0 * 3 + k] * gm[0] + J[1 * 3 + k] * gm[1];
     // (tail-only code, tolerance-level: reciprocals instead of divisions)
-    const double itz = 1.0 / tz;
-    const double fu2 = -f / (su * tz * tz), fv2 = -f / (sv * tz * tz);
+    const double itz = p.itz;
+    const double fu2 = -f * (1.0 / su) * itz * itz, fv2 = -f * (1.0 / sv) * itz * itz;
     gt[0] += gJ[0 * 3 + 2] * fu2;
     gt[1] += gJ[1 * 3 + 2] * fv2;
     gt[2] += gJ[0 * 3 + 0] * fu2 + gJ[0 * 3 + 2] * (-2.0 * fu2 * p.t_cam[0] * itz) + gJ[1 * 3 + 1] * fv2 +
@@ -599,7 +618,7 @@ __device__ __forceinline__ void raster_chain_rule(const Frame& fr, const Geo& g,
 #pragma unroll
     for (int k = 0; k < 3; ++k) gd[k] = 2.0 * g_beta * p.ad[k];
     const double dd = dot3(p.d_ray, gd);
-    const double inv_dist = 1.0 / p.dist;
+    const double inv_dist = p.inv_dist;
 #pragma unroll
     for (int k = 0; k < 3; ++k) gp[k] += (gd[k] - p.d_ray[k] * dd) * inv_dist;
   }
