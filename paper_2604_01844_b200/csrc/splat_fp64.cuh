@@ -512,10 +512,11 @@ __device__ __forceinline__ void raster_chain_rule(const Frame& fr, const Geo& g,
   double gp[3];
   if (!g.cone) {
     double mc[6];
+    const double isu = 1.0 / g.s_u, isv = 1.0 / g.s_v;  // kernel-parameter reciprocals (hoisted)
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      mc[k * 2 + 0] = fr.u[k] / g.s_u;
-      mc[k * 2 + 1] = fr.v[k] / g.s_v;
+      mc[k * 2 + 0] = fr.u[k] * isu;
+      mc[k * 2 + 1] = fr.v[k] * isv;
     }
     double A[6];
 #pragma unroll
@@ -595,7 +596,7 @@ __device__ __forceinline__ void raster_chain_rule(const Frame& fr, const Geo& g,
         acc += gT[r * 3 + 2] * rows[j][2];
         gJ[r * 3 + j] = acc;
       }
-    const double f = fr.focal, tz = p.t_cam[2];
+    const double f = fr.focal;
     const double su = g.s_u, sv = g.s_v;
     double gt[3];
 #pragma unroll
