@@ -178,12 +178,15 @@ class ClockSampler:
 class DeviceStep:
     """One fwd+bwd pass over this rank's views with device-resident inputs/outputs."""
 
-    def __init__(self, ctx, cloud, geom, views, world: int):
+    def __init__(self, ctx, cloud, geom, views, world: int, native_group: bool = False):
         import torch
         from paper_2604_01844_b200 import gsct
 
         self.gsct, self.torch, self.ctx = gsct, torch, ctx
         self.geom, self.views, self.world = geom, views, world
+        # native_group: the context carries the library's NCCL group, so gsct_rasterize_bwd
+        # itself all-reduces the per-splat view sums on its stream (include/gsct_cuda.h)
+        self.native_group = native_group
         self.dev = torch.device(f"cuda:{ctx.device}")
         self.dcloud = cloud.to_device(ctx.device)
         n = cloud.size()
@@ -205,7 +208,7 @@ class DeviceStep:
         g.rasterize_views(self.dcloud, self.geom, self.views, self.rs, out=self.images, ctx=self.ctx)
         g.rasterize_backward_views(self.dcloud, self.geom, self.views, self.grad_images, self.rs, out=self.grads,
                                    ctx=self.ctx)
-        if self.world > 1:
+        if self.world > 1 and not self.native_group:
             from paper_2604_01844_b200.sharding import allreduce_grads
 
             with self.torch.cuda.stream(self.stream):  # NCCL on the library's stream, no host sync
@@ -229,7 +232,7 @@ def timed_steps(step, stream, k: int, flush) -> list[float]:
     return times
 
 
-def run_e2e(ctx, cloud, geom, views, k: int, w: int, world: int = 1) -> dict:
+def run_e2e(ctx, cloud, geom, views, k: int, w: int, world: int = 1, native_group: bool = False) -> dict:
     """Same step through the C ABI with pinned host buffers; copies inside the timed region.
     With several ranks each rank runs its view shard and the summed gradients are formed by
     an all-reduce of the packed fp64 gradient buffer (host -> device -> all-reduce -> host,
@@ -252,12 +255,13 @@ def run_e2e(ctx, cloud, geom, views, k: int, w: int, world: int = 1) -> dict:
                                 f[10 * n:11 * n], f[11 * n:], torch.zeros(n, dtype=torch.uint8).pin_memory().numpy())
     rs = gsct.RasterSettings()
     dev = torch.device(f"cuda:{ctx.device}")
-    flat_d = torch.empty(12 * n, dtype=torch.float64, device=dev) if world > 1 else None
+    torch_reduce = world > 1 and not native_group  # with the native group the call reduces itself
+    flat_d = torch.empty(12 * n, dtype=torch.float64, device=dev) if torch_reduce else None
 
     def step():
         gsct.rasterize_views(hcloud, geom, views, rs, out=images, ctx=ctx)
         gsct.rasterize_backward_views(hcloud, geom, views, gimg, rs, out=grads, ctx=ctx)
-        if world > 1:
+        if torch_reduce:
             import torch.distributed as dist
 
             flat_d.copy_(flat_h, non_blocking=True)
@@ -283,8 +287,8 @@ def run_e2e(ctx, cloud, geom, views, k: int, w: int, world: int = 1) -> dict:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ts = t.cpu().tolist()
     cloud_bytes = n * 11 * 8
-    h2d = 2 * cloud_bytes + gimg.nbytes + (flat_h.numel() * 8 if world > 1 else 0)  # cloud up in both calls
-    d2h = images.nbytes + n * (12 * 8 + 1) + (flat_h.numel() * 8 if world > 1 else 0)
+    h2d = 2 * cloud_bytes + gimg.nbytes + (flat_h.numel() * 8 if torch_reduce else 0)  # cloud up in both calls
+    d2h = images.nbytes + n * (12 * 8 + 1) + (flat_h.numel() * 8 if torch_reduce else 0)
     return {"ms": ts, "h2d": h2d, "d2h": d2h}
 
 
@@ -597,7 +601,15 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     ctx = gsct.context(local_rank)
     cloud, geom = make_workload(args.config)
     views = shard_views(len(geom.angles), rank, world)
-    step = DeviceStep(ctx, cloud, geom, views, world)
+    # N > 1 over NCCL: the library's own group (one NCCL communicator per context) carries
+    # the gradient all-reduce inside gsct_rasterize_bwd; over gloo (ranks sharing one GPU,
+    # where NCCL refuses duplicate devices) the packed buffers are reduced by torch
+    native = (world > 1 or os.environ.get("GSCT_BENCH_NATIVE_GROUP") == "1") and args.dist_backend == "nccl"
+    if native:
+        from paper_2604_01844_b200.sharding import native_group
+
+        native_group(ctx)
+    step = DeviceStep(ctx, cloud, geom, views, world, native_group=native)
     flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=step.dev)
 
     # exact work counters of one step (RenderStats), untimed
@@ -633,12 +645,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     # e2e through the C ABI with pinned host buffers (every rank: its shard + the all-reduce)
     e2e = None
     if not args.no_e2e:
-        e = run_e2e(ctx, cloud, geom, views, max(3, min(args.steps, 5)), 2, world)
+        e = run_e2e(ctx, cloud, geom, views, max(3, min(args.steps, 5)), 2, world, native_group=native)
         e_ms = float(np.mean(e["ms"]))
         e2e = {"value": round(n_views_total / (e_ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": e["h2d"],
                "d2h_bytes_per_step": e["d2h"], "ms_per_step": round(e_ms, 3),
                "path": "gsct_rasterize_fwd + gsct_rasterize_bwd (C ABI, GSCT_HOST pinned buffers, sync)"
-                       + (" + all-reduce of the packed gradients, max over ranks" if world > 1 else "")}
+                       + (" with the library's NCCL group (all-reduce inside the backward), max over ranks" if native
+                          else " + all-reduce of the packed gradients, max over ranks" if world > 1 else "")}
         ctx.set_async(True)
 
     if rank != 0:
@@ -788,7 +801,10 @@ def main() -> None:
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    # GSCT_BENCH_NATIVE_GROUP=1 (under torchrun): the library's NCCL group even at one rank,
+    # to exercise the multi-GPU wiring on a one-GPU box
+    use_dist = world > 1 or os.environ.get("GSCT_BENCH_NATIVE_GROUP") == "1"
+    if use_dist:
         import torch
         import torch.distributed as dist
 
@@ -800,7 +816,7 @@ def main() -> None:
     try:
         run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if use_dist:
             import torch.distributed as dist
 
             dist.destroy_process_group()
