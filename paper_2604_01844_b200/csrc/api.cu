@@ -29,7 +29,7 @@ enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
   S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG, S_FGSC, S_FGSC_LOG, S_FGSC_CNT, S_VTCOUNT,
-  S_TOTAL64, S_VIEWPAIRS, S_WCOUNT, S_WSLOT, S_WSUMS, S_WSTART, S_MOMENTS64, S_BSUMS,
+  S_TOTAL64, S_VIEWPAIRS, S_WCOUNT, S_WSLOT, S_WSUMS, S_WSTART, S_MOMENTS64, S_BSUMS, S_FSCHED,
   S_COUNT_SLOTS
 };
 
@@ -1035,11 +1035,15 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
           cudaStream_t fs = dual && (k & 1) ? c->aux_stream : c->stream;
           {
             Phase ph(c, GSCT_PH_RASTER_FWD);
+            // warp schedule scratch: a disjoint slice per view sub-range (they may run concurrently)
+            uint32_t* fsched = ws<uint32_t>(c, S_FSCHED, static_cast<size_t>(bv) * (2 * n_tiles + 32)) +
+                               static_cast<int64_t>(vs) * (2 * n_tiles + 32);
             launch_raster_fwd_super(brec + static_cast<int64_t>(vs) * n, bins.vals,
                                     bins.start + static_cast<int64_t>(vs) * stride,
                                     bins.end + static_cast<int64_t>(vs) * stride, n, nvs, geom->n_u, geom->n_v,
                                     tiles_u, tiles_v, stride, bimg + static_cast<int64_t>(vs) * npx, fs,
-                                    (zc_images || GSCT_FWD_BULK_DEVICE) && GSCT_FWD_BULKSTORE ? 1 : 0, plan.vmask);
+                                    (zc_images || GSCT_FWD_BULK_DEVICE) && GSCT_FWD_BULKSTORE ? 1 : 0, plan.vmask,
+                                    fsched);
           }
           CK(cudaGetLastError());
           if (stage_images) {
@@ -1485,7 +1489,8 @@ void voxel_fwd_window(gsct_ctx c, const Cloud& d, const VoxGrid& vg, const Windo
   }
   {
     Phase ph(c, GSCT_PH_VOXEL_FWD);
-    launch_voxel_fwd(rec, vals, start, end, win, nbx, nby, nbz, static_cast<float>(vg.spacing), outv, c->stream);
+    launch_voxel_fwd(rec, vals, start, end, win, nbx, nby, nbz, static_cast<float>(vg.spacing), outv, c->stream,
+                     ws<uint32_t>(c, S_FSCHED, 2 * static_cast<size_t>(n_bricks) + 32));
   }
   CK(cudaGetLastError());
 }

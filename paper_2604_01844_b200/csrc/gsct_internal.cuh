@@ -85,6 +85,10 @@ __device__ __forceinline__ uint32_t walk_bucket(uint32_t urange, uint32_t vrange
   if (W > 0 && H > 0) {
     const int nch = ((u0 & 7) + W + 7) >> 3;
     shape = ((min(nch, 4) - 1) << 4) | min(H >> 2, 15);
+#ifndef GSCT_WALK_BIG_FIRST
+#define GSCT_WALK_BIG_FIRST 1  // largest shape classes first in each view (no long items in the last wave)
+#endif
+    if (GSCT_WALK_BIG_FIRST) shape = L.shapes - 2 - shape;
     pv = min(v0 >> L.vs, L.nv - 1);
     pu = min(u0 >> L.us, L.nu - 1);
   }
@@ -171,11 +175,14 @@ void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint3
 void launch_ranges_swapped(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, int tile_bits,
                            uint32_t* start, uint32_t* end, cudaStream_t st);
 // forward over 32x32 super-tile lists (keys = view * n_stiles + super-tile)
+// Longest-first order of n_views x n_lists lists [start, end) (list (v, t) at key v * key_stride + t):
+// ws needs 32 + 2 * items words; the order (item = v * n_lists + t) lands at ws + 32 + items.
+void launch_fwd_schedule(const uint32_t* start, const uint32_t* end, int n_views, int n_lists, int key_stride,
+                         uint32_t* ws, cudaStream_t st);
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
-                             int stiles_v, int key_stride, float* images, cudaStream_t st,
-                             int bulk_out = 0,             // 1: images are host-mapped (TMA bulk row stores)
-                             uint32_t vmask = 0xFFFFFFFFu);  // splat = vals[k] & vmask (packed keys)
+                             int stiles_v, int key_stride, float* images, cudaStream_t st, int bulk_out,
+                             uint32_t vmask, uint32_t* sched_ws = nullptr);  // 32 + 2 * views * super-tiles words  // splat = vals[k] & vmask (packed keys)
 // packed keys-only binning (tile << 24 | splat) with (view, tile) counts, and its ranges
 void launch_emit_tile_keys(const RasterRec* rec, const uint32_t* offsets, const uint32_t* counts, int64_t n,
                            int n_views, int ts, int tiles_u, int n_tiles, uint32_t* keys, uint32_t* vt_count,
@@ -210,7 +217,7 @@ void launch_emit_brick_pairs(const VoxelRec* rec, const uint32_t* offsets,
                              int nby, uint32_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t* start,
                       const uint32_t* end, const Window& win, int nbx, int nby, int nbz,
-                      float spacing, float* volume, cudaStream_t st);
+                      float spacing, float* volume, cudaStream_t st, uint32_t* sched_ws = nullptr);
 // lane-per-splat voxel backward: row-load width (8 or 1), walk-order keys (returns key
 // bits), the pixel walk
 int voxel_bwd_vec(const Window& win, const float* grad_volume);

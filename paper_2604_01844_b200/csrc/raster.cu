@@ -328,14 +328,26 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
                                                      const uint32_t* __restrict__ start,
                                                      const uint32_t* __restrict__ end, int64_t n, int n_u,
                                                      int n_v, int stiles_u, int n_stiles, int key_stride,
-                                                     float* __restrict__ images, int bulk_out, uint32_t vmask) {
+                                                     float* __restrict__ images, int bulk_out, uint32_t vmask, const uint32_t* __restrict__ sched,
+    int n_views) {
   constexpr int kHH = kTile;  // half-tile: 32 wide, 16 tall
   constexpr int kBatch = 32 * kFwdGroups;
   __shared__ StagedRec2 s_rec[4][kBatch];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = blockIdx.x * 4 + warp;  // 2 halves per super-tile
-  if (half >= 2 * n_stiles) return;
-  const int st = half >> 1, view = blockIdx.y;
+  int half, st, view;
+  if (sched) {  // longest lists first (k_fwd_sched_*): 1-D grid over (view, super-tile, half)
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * 4 + warp;
+    if (w >= 2 * static_cast<int64_t>(n_views) * n_stiles) return;
+    const uint32_t it = __ldg(sched + (w >> 1));
+    view = static_cast<int>(it / static_cast<uint32_t>(n_stiles));
+    st = static_cast<int>(it - static_cast<uint32_t>(view) * n_stiles);
+    half = 2 * st + static_cast<int>(w & 1);
+  } else {
+    half = blockIdx.x * 4 + warp;  // 2 halves per super-tile
+    if (half >= 2 * n_stiles) return;
+    st = half >> 1;
+    view = blockIdx.y;
+  }
   const int tx0 = (st % stiles_u) * kBinTile;
   const int ty0 = (st / stiles_u) * kBinTile + (half & 1) * kHH;
   if (ty0 >= n_v) return;
@@ -496,6 +508,42 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
         if (px0 + k < n_u) rowp[px0 + k] = v[k];
     }
   }
+}
+
+// Longest-first schedule of the forward's warps: (view, super-tile) pairs ordered by
+// descending list length class (floor(log2(length)); an integer-atomic counting sort, the
+// order inside a class is arbitrary -- it only decides which warp starts when, never what a
+// warp computes). Without it the few longest lists (the phantom's centre, in every view) can
+// start in the last wave and set the kernel's end.
+__global__ void k_fwd_sched_count(const uint32_t* __restrict__ start, const uint32_t* __restrict__ end, int n_views,
+                                  int n_stiles, int key_stride, uint32_t* __restrict__ cls_cnt,
+                                  uint32_t* __restrict__ slot) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(n_views) * n_stiles) return;
+  const int v = static_cast<int>(i / n_stiles), t = static_cast<int>(i - static_cast<int64_t>(v) * n_stiles);
+  const uint32_t key = static_cast<uint32_t>(v) * key_stride + t;
+  const uint32_t len = end[key] - start[key];
+  const uint32_t cls = static_cast<uint32_t>(__clz(len | 1u));  // 0 = longest class
+  slot[i] = (cls << 26) | atomicAdd(cls_cnt + cls, 1u);
+}
+__global__ void k_fwd_sched_scatter(const uint32_t* __restrict__ cls_cnt, const uint32_t* __restrict__ slot,
+                                    int64_t n, uint32_t* __restrict__ sched) {
+  __shared__ uint32_t off[32];
+  if (threadIdx.x < 32) {
+    const uint32_t c = cls_cnt[threadIdx.x];
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (static_cast<int>(threadIdx.x) >= o) x += y;
+    }
+    off[threadIdx.x] = x - c;
+  }
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t s = slot[i];
+  sched[off[s >> 26] + (s & 0x03FFFFFFu)] = static_cast<uint32_t>(i);
 }
 
 // Lane-per-item backward (K4a). The per-(view, splat) pixel loop is small (hundreds of
@@ -1083,20 +1131,44 @@ void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_
   count_launch();
 }
 
+#ifndef GSCT_FWD_LPT
+#define GSCT_FWD_LPT 1  // longest lists first (k_fwd_sched_*; A/B C2 forward 2.52 -> 2.26 ms)
+#endif
+void launch_fwd_schedule(const uint32_t* start, const uint32_t* end, int n_views, int n_lists, int key_stride,
+                         uint32_t* ws, cudaStream_t st) {
+  const int64_t items = static_cast<int64_t>(n_views) * n_lists;
+  if (items == 0) return;
+  uint32_t* cnt = ws;
+  uint32_t* slot = ws + 32;
+  cudaMemsetAsync(cnt, 0, 32 * sizeof(uint32_t), st);
+  k_fwd_sched_count<<<blocks_for(items, 256), 256, 0, st>>>(start, end, n_views, n_lists, key_stride, cnt, slot);
+  count_launch();
+  k_fwd_sched_scatter<<<blocks_for(items, 256), 256, 0, st>>>(cnt, slot, items, slot + items);
+  count_launch();
+}
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
                              int stiles_v, int key_stride, float* images, cudaStream_t st, int bulk_out,
-                             uint32_t vmask) {
+                             uint32_t vmask, uint32_t* sched_ws) {
   if (n_views == 0) return;
   const int n_stiles = stiles_u * stiles_v;
+  const int64_t items = static_cast<int64_t>(n_views) * n_stiles;
+  uint32_t* sched = nullptr;
+  if (GSCT_FWD_LPT && sched_ws) {  // sched_ws: 32 + 2 * items words
+    launch_fwd_schedule(start, end, n_views, n_stiles, key_stride, sched_ws, st);
+    sched = sched_ws + 32 + items;
+  }
   // one warp per 32x16 half-super-tile (A/B at C2: 2x4-px lane blocks 3.65 ms, 2x8 2.96 ms,
   // 4x8 3.34 ms; CTA-shared staging with block barriers was slower still)
-  dim3 g4(static_cast<unsigned>((2 * n_stiles + 3) / 4), static_cast<unsigned>(n_views));
-  k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, key_stride, images,
-                                    bulk_out, vmask);
+  if (sched) {
+    k_raster_fwd4<<<blocks_for(2 * items, 4), 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles,
+                                                           key_stride, images, bulk_out, vmask, sched, n_views);
+  } else {
+    dim3 g4(static_cast<unsigned>((2 * n_stiles + 3) / 4), static_cast<unsigned>(n_views));
+    k_raster_fwd4<<<g4, 128, 0, st>>>(rec, vals, start, end, n, n_u, n_v, stiles_u, n_stiles, key_stride, images,
+                                      bulk_out, vmask, nullptr, n_views);
+  }
   count_launch();
 }
-
-
 
 }  // namespace gsct_dev

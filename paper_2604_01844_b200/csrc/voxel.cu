@@ -81,11 +81,12 @@ __global__ void __launch_bounds__(128, GSCT_VFWD_MINB) k_voxel_fwd2(const VoxelR
                                                    const uint32_t* __restrict__ start,
                                                    const uint32_t* __restrict__ end, Window win,
                                                    int nbx, int nby, int n_bricks, float sp,
-                                                   float* __restrict__ volume) {
+                                                   float* __restrict__ volume, const uint32_t* __restrict__ sched) {
   __shared__ StagedVox s_rec[4][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int brick = blockIdx.x * 4 + warp;
-  if (brick >= n_bricks) return;
+  const int w = blockIdx.x * 4 + warp;
+  if (w >= n_bricks) return;
+  const int brick = sched ? static_cast<int>(__ldg(sched + w)) : w;  // longest lists first
   const int bx = brick % nbx, by = (brick / nbx) % nby, bz = brick / (nbx * nby);
   const int gx0 = win.lo[0] + bx * kBrick, gy0 = win.lo[1] + by * kBrick, gz0 = win.lo[2] + bz * kBrickZ;
   const int yp = lane & 3, zp = lane >> 2;
@@ -622,13 +623,21 @@ void launch_emit_brick_pairs(const VoxelRec* rec, const uint32_t* offsets, const
   count_launch();
 }
 
+#ifndef GSCT_VFWD_LPT
+#define GSCT_VFWD_LPT 0  // 1: longest brick lists first (A/B 512^3: 1.08 vs 0.98 ms -- the z-major brick order keeps records L2-resident)
+#endif
 void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t* start,
                       const uint32_t* end, const Window& win, int nbx, int nby, int nbz,
-                      float spacing, float* volume, cudaStream_t st) {
+                      float spacing, float* volume, cudaStream_t st, uint32_t* sched_ws) {
   const int64_t bricks = static_cast<int64_t>(nbx) * nby * nbz;
   if (bricks == 0) return;
-  k_voxel_fwd2<<<static_cast<unsigned>((bricks + 3) / 4), 128, 0, st>>>(rec, vals, start, end, win, nbx, nby,
-                                                                        static_cast<int>(bricks), spacing, volume);
+  const uint32_t* sched = nullptr;
+  if (GSCT_VFWD_LPT && sched_ws) {  // the forward raster's longest-first schedule over the brick lists
+    launch_fwd_schedule(start, end, 1, static_cast<int>(bricks), static_cast<int>(bricks), sched_ws, st);
+    sched = sched_ws + 32 + bricks;
+  }
+  k_voxel_fwd2<<<static_cast<unsigned>((bricks + 3) / 4), 128, 0, st>>>(
+      rec, vals, start, end, win, nbx, nby, static_cast<int>(bricks), spacing, volume, sched);
   count_launch();
 }
 
