@@ -1036,8 +1036,8 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
           {
             Phase ph(c, GSCT_PH_RASTER_FWD);
             // warp schedule scratch: a disjoint slice per view sub-range (they may run concurrently)
-            uint32_t* fsched = ws<uint32_t>(c, S_FSCHED, static_cast<size_t>(bv) * (2 * n_tiles + 32)) +
-                               static_cast<int64_t>(vs) * (2 * n_tiles + 32);
+            uint32_t* fsched = ws<uint32_t>(c, S_FSCHED, static_cast<size_t>(bv) * (2 * n_tiles + 2048)) +
+                               static_cast<int64_t>(vs) * (2 * n_tiles + 2048);
             launch_raster_fwd_super(brec + static_cast<int64_t>(vs) * n, bins.vals,
                                     bins.start + static_cast<int64_t>(vs) * stride,
                                     bins.end + static_cast<int64_t>(vs) * stride, n, nvs, geom->n_u, geom->n_v,
@@ -1490,7 +1490,7 @@ void voxel_fwd_window(gsct_ctx c, const Cloud& d, const VoxGrid& vg, const Windo
   {
     Phase ph(c, GSCT_PH_VOXEL_FWD);
     launch_voxel_fwd(rec, vals, start, end, win, nbx, nby, nbz, static_cast<float>(vg.spacing), outv, c->stream,
-                     ws<uint32_t>(c, S_FSCHED, 2 * static_cast<size_t>(n_bricks) + 32));
+                     ws<uint32_t>(c, S_FSCHED, 2 * static_cast<size_t>(n_bricks) + 2048));
   }
   CK(cudaGetLastError());
 }

@@ -175,14 +175,15 @@ void launch_ranges(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, uint3
 void launch_ranges_swapped(const uint32_t* keys, int64_t n_pairs, uint32_t n_keys, int tile_bits,
                            uint32_t* start, uint32_t* end, cudaStream_t st);
 // forward over 32x32 super-tile lists (keys = view * n_stiles + super-tile)
-// Longest-first order of n_views x n_lists lists [start, end) (list (v, t) at key v * key_stride + t):
-// ws needs 32 + 2 * items words; the order (item = v * n_lists + t) lands at ws + 32 + items.
+// Longest-first order of n_views x n_lists lists [start, end) (list (v, t) at key v * key_stride + t)
+// inside groups of view_group consecutive views (ceil(n_views / view_group) <= 64): ws needs
+// 2048 + 2 * items words; the order (item = v * n_lists + t) lands at ws + 2048 + items.
 void launch_fwd_schedule(const uint32_t* start, const uint32_t* end, int n_views, int n_lists, int key_stride,
-                         uint32_t* ws, cudaStream_t st);
+                         int view_group, uint32_t* ws, cudaStream_t st);
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
                              int stiles_v, int key_stride, float* images, cudaStream_t st, int bulk_out,
-                             uint32_t vmask, uint32_t* sched_ws = nullptr);  // 32 + 2 * views * super-tiles words  // splat = vals[k] & vmask (packed keys)
+                             uint32_t vmask, uint32_t* sched_ws = nullptr);  // 2048 + 2 * views * super-tiles words  // splat = vals[k] & vmask (packed keys)
 // packed keys-only binning (tile << 24 | splat) with (view, tile) counts, and its ranges
 void launch_emit_tile_keys(const RasterRec* rec, const uint32_t* offsets, const uint32_t* counts, int64_t n,
                            int n_views, int ts, int tiles_u, int n_tiles, uint32_t* keys, uint32_t* vt_count,

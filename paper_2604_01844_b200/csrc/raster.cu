@@ -14,6 +14,7 @@
 // with shape-sorted work in the backward). See DESIGN.md section 4.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "gsct_internal.cuh"
@@ -510,40 +511,67 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
   }
 }
 
-// Longest-first schedule of the forward's warps: (view, super-tile) pairs ordered by
-// descending list length class (floor(log2(length)); an integer-atomic counting sort, the
-// order inside a class is arbitrary -- it only decides which warp starts when, never what a
-// warp computes). Without it the few longest lists (the phantom's centre, in every view) can
-// start in the last wave and set the kernel's end.
+// Longest-first schedule of the forward's warps: (view, super-tile) pairs ordered by view
+// group (groups of `vg` consecutive views), then by descending list length class
+// (floor(log2(length))) inside the group -- an integer-atomic counting sort; the order inside
+// a class is arbitrary: it only decides which warp starts when, never what a warp computes.
+// Without it the longest lists (the phantom's centre, in every view) can start in the last
+// wave and set the kernel's end. Across all views at once the records of every view are
+// re-read from DRAM by tiles spread over the whole kernel (C2: 2.9 GB of DRAM reads instead
+// of 1.2), which still costs less than the tail.
 __global__ void k_fwd_sched_count(const uint32_t* __restrict__ start, const uint32_t* __restrict__ end, int n_views,
-                                  int n_stiles, int key_stride, uint32_t* __restrict__ cls_cnt,
+                                  int n_stiles, int key_stride, int vg, uint32_t* __restrict__ cls_cnt,
                                   uint32_t* __restrict__ slot) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= static_cast<int64_t>(n_views) * n_stiles) return;
   const int v = static_cast<int>(i / n_stiles), t = static_cast<int>(i - static_cast<int64_t>(v) * n_stiles);
   const uint32_t key = static_cast<uint32_t>(v) * key_stride + t;
   const uint32_t len = end[key] - start[key];
-  const uint32_t cls = static_cast<uint32_t>(__clz(len | 1u));  // 0 = longest class
-  slot[i] = (cls << 26) | atomicAdd(cls_cnt + cls, 1u);
+  const uint32_t b = static_cast<uint32_t>(v / vg) * 32u + static_cast<uint32_t>(__clz(len | 1u));
+  slot[i] = (b << 21) | atomicAdd(cls_cnt + b, 1u);  // ranks < 2^21, buckets < 2^11
 }
-__global__ void k_fwd_sched_scatter(const uint32_t* __restrict__ cls_cnt, const uint32_t* __restrict__ slot,
-                                    int64_t n, uint32_t* __restrict__ sched) {
-  __shared__ uint32_t off[32];
-  if (threadIdx.x < 32) {
-    const uint32_t c = cls_cnt[threadIdx.x];
-    uint32_t x = c;
+__global__ void k_fwd_sched_scatter(const uint32_t* __restrict__ cls_cnt, int n_buckets,
+                                    const uint32_t* __restrict__ slot, int64_t n, uint32_t* __restrict__ sched) {
+  __shared__ uint32_t off[2048];
+  __shared__ uint32_t wsum[32];
+  // exclusive scan of the bucket counts (<= 2048), 256 threads x 8
+  uint32_t v[8], run = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (static_cast<int>(threadIdx.x) >= o) x += y;
+  for (int k = 0; k < 8; ++k) {
+    const int bi = threadIdx.x * 8 + k;
+    v[k] = bi < n_buckets ? cls_cnt[bi] : 0u;
+    run += v[k];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < 8 ? wsum[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
     }
-    off[threadIdx.x] = x - c;
+    if (lane < 8) wsum[lane] = w;
+  }
+  __syncthreads();
+  uint32_t base = (warp ? wsum[warp - 1] : 0u) + x - run;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    off[threadIdx.x * 8 + k] = base;
+    base += v[k];
   }
   __syncthreads();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t s = slot[i];
-  sched[off[s >> 26] + (s & 0x03FFFFFFu)] = static_cast<uint32_t>(i);
+  sched[off[s >> 21] + (s & 0x001FFFFFu)] = static_cast<uint32_t>(i);
 }
 
 // Lane-per-item backward (K4a). The per-(view, splat) pixel loop is small (hundreds of
@@ -1135,17 +1163,20 @@ void launch_raster_bwd_lanes(const RasterRec* rec, const uint32_t* order, int64_
 #define GSCT_FWD_LPT 1  // longest lists first (k_fwd_sched_*; A/B C2 forward 2.52 -> 2.26 ms)
 #endif
 void launch_fwd_schedule(const uint32_t* start, const uint32_t* end, int n_views, int n_lists, int key_stride,
-                         uint32_t* ws, cudaStream_t st) {
+                         int view_group, uint32_t* ws, cudaStream_t st) {
   const int64_t items = static_cast<int64_t>(n_views) * n_lists;
   if (items == 0) return;
+  const int vg = view_group < 1 ? 1 : view_group;
+  const int n_buckets = ((n_views + vg - 1) / vg) * 32;  // <= 2048 (callers keep n_views / vg <= 64)
   uint32_t* cnt = ws;
-  uint32_t* slot = ws + 32;
-  cudaMemsetAsync(cnt, 0, 32 * sizeof(uint32_t), st);
-  k_fwd_sched_count<<<blocks_for(items, 256), 256, 0, st>>>(start, end, n_views, n_lists, key_stride, cnt, slot);
+  uint32_t* slot = ws + 2048;
+  cudaMemsetAsync(cnt, 0, static_cast<size_t>(n_buckets) * sizeof(uint32_t), st);
+  k_fwd_sched_count<<<blocks_for(items, 256), 256, 0, st>>>(start, end, n_views, n_lists, key_stride, vg, cnt, slot);
   count_launch();
-  k_fwd_sched_scatter<<<blocks_for(items, 256), 256, 0, st>>>(cnt, slot, items, slot + items);
+  k_fwd_sched_scatter<<<blocks_for(items, 256), 256, 0, st>>>(cnt, n_buckets, slot, items, slot + items);
   count_launch();
 }
+
 void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const uint32_t* start,
                              const uint32_t* end, int64_t n, int n_views, int n_u, int n_v, int stiles_u,
                              int stiles_v, int key_stride, float* images, cudaStream_t st, int bulk_out,
@@ -1154,9 +1185,12 @@ void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const u
   const int n_stiles = stiles_u * stiles_v;
   const int64_t items = static_cast<int64_t>(n_views) * n_stiles;
   uint32_t* sched = nullptr;
-  if (GSCT_FWD_LPT && sched_ws) {  // sched_ws: 32 + 2 * items words
-    launch_fwd_schedule(start, end, n_views, n_stiles, key_stride, sched_ws, st);
-    sched = sched_ws + 32 + items;
+  // over all views of the launch (A/B C2: 2.25 ms; per 7-view groups that keep the records
+  // L2-resident 2.49; none 2.52). Not for host-mapped images: there the kernel's PCIe stores
+  // follow the schedule and scattered host writes cost more than the tail (C2 e2e 8.36 vs 7.87 ms)
+  if (GSCT_FWD_LPT && sched_ws && !bulk_out) {  // sched_ws: 2048 + 2 * items words
+    launch_fwd_schedule(start, end, n_views, n_stiles, key_stride, n_views, sched_ws, st);
+    sched = sched_ws + 2048 + items;
   }
   // one warp per 32x16 half-super-tile (A/B at C2: 2x4-px lane blocks 3.65 ms, 2x8 2.96 ms,
   // 4x8 3.34 ms; CTA-shared staging with block barriers was slower still)

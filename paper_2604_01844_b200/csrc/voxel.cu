@@ -633,8 +633,8 @@ void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t*
   if (bricks == 0) return;
   const uint32_t* sched = nullptr;
   if (GSCT_VFWD_LPT && sched_ws) {  // the forward raster's longest-first schedule over the brick lists
-    launch_fwd_schedule(start, end, 1, static_cast<int>(bricks), static_cast<int>(bricks), sched_ws, st);
-    sched = sched_ws + 32 + bricks;
+    launch_fwd_schedule(start, end, 1, static_cast<int>(bricks), static_cast<int>(bricks), 1, sched_ws, st);
+    sched = sched_ws + 2048 + bricks;
   }
   k_voxel_fwd2<<<static_cast<unsigned>((bricks + 3) / 4), 128, 0, st>>>(
       rec, vals, start, end, win, nbx, nby, static_cast<int>(bricks), spacing, volume, sched);
