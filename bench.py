@@ -608,7 +608,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if native:
         from paper_2604_01844_b200.sharding import native_group
 
-        native_group(ctx)
+        try:
+            native_group(ctx)
+        except Exception as exc:  # e.g. NCCL unavailable: the torch reduction carries the sum
+            log(f"native group unavailable ({exc}); reducing with torch.distributed")
+            native = False
     step = DeviceStep(ctx, cloud, geom, views, world, native_group=native)
     flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=step.dev)
 
