@@ -185,3 +185,25 @@ def test_raymarch_matches_reference(ref, ctx, cone):
     assert np.max(np.abs(got - want)) <= 1e-6 * np.max(np.abs(want))
     gd = gsct.raymarch_project(torch.from_numpy(vol).cuda(), grid, geom, ctx=ctx).cpu().numpy()
     assert np.array_equal(gd, got)
+
+
+def test_lr_schedule_and_scene_extent():
+    """lr_schedule (optim.hpp:71-78) and scene_extent (core.hpp:120-129) of the host mirror:
+    log-linear decay clamped at the ends, contract on non-positive rates; half the diagonal
+    of the positions' bounding box."""
+    base, final, horizon = 2e-4 * 7.5, 1e-6 * 7.5, 22500
+    assert gsct.lr_schedule(base, final, 0, horizon) == base
+    assert gsct.lr_schedule(base, final, -3, horizon) == base
+    assert gsct.lr_schedule(base, final, horizon, horizon) == final
+    assert gsct.lr_schedule(base, final, 10 * horizon, horizon) == final
+    assert gsct.lr_schedule(base, final, 5, 0) == final
+    mid = gsct.lr_schedule(base, final, horizon // 2, horizon)
+    assert mid == pytest.approx(base * (final / base) ** ((horizon // 2) / horizon), rel=1e-15)
+    assert final < mid < base
+    with pytest.raises(gsct.ContractError):
+        gsct.lr_schedule(0.0, final, 1, horizon)
+    cloud = gsct.make_cloud("random", 500, seed=4, pos_range=3.0)
+    p = np.asarray(cloud.positions)
+    assert gsct.scene_extent(cloud) == pytest.approx(0.5 * np.linalg.norm(p.max(0) - p.min(0)), rel=1e-15)
+    with pytest.raises(gsct.ContractError):
+        gsct.scene_extent(gsct.GaussianCloud.empty())
