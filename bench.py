@@ -567,14 +567,17 @@ def run_dropin(timeout_s: float = 240.0) -> dict:
     (75 views at 512^2, 200k Gaussians; per view-step: render, 32^3 TV voxelize, L1+SSIM2D+TV
     loss, backward, voxelize_backward, Adam -- one fwd+bwd projection each), through the C++
     drop-in (oracle/_ref/dropin_train_b200: gsct_b200_dropin.hpp over libgsct_b200.so,
-    pageable std::vector buffers) and as the plain reference on the host cores
-    (dropin_train_cpu). tests/cpp/dropin_train.cpp."""
+    pageable std::vector buffers; the loop's total_loss_recon on the device too), the same with
+    the reference's CPU loss (dropin_train_b200_cpuloss: only the five hot-path operators on
+    the GPU), and as the plain reference on the host cores (dropin_train_cpu).
+    tests/cpp/dropin_train.cpp."""
     import subprocess
 
     root = Path(__file__).resolve().parent / "oracle" / "_ref"
     out: dict = {"unit": "view-steps/s (one fwd+bwd projection each) through train_reconstruction",
                  "config": "C2: 200000 Gaussians, 75 cone views at 512^2, 1 epoch, TrainConfig defaults"}
-    for tag, exe in (("b200", root / "dropin_train_b200"), ("cpu", root / "dropin_train_cpu")):
+    for tag, exe in (("b200", root / "dropin_train_b200"), ("b200_cpu_loss", root / "dropin_train_b200_cpuloss"),
+                     ("cpu", root / "dropin_train_cpu")):
         if not exe.exists():
             out[tag] = {"unavailable": f"{exe.name} not built (needs /root/reference at build time)"}
             continue

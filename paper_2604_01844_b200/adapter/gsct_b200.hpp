@@ -87,7 +87,7 @@ class Device {
 struct OpTimes {
   double seconds = 0.0;
   std::int64_t calls = 0;
-  double kind_seconds[4] = {0, 0, 0, 0};  // rasterize fwd, rasterize bwd, voxelize, voxelize bwd
+  double kind_seconds[5] = {0, 0, 0, 0, 0};  // rasterize fwd, rasterize bwd, voxelize, voxelize bwd, loss
 };
 inline OpTimes& op_times() {
   static thread_local OpTimes t;

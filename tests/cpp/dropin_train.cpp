@@ -104,9 +104,9 @@ int main(int argc, char** argv) {
   long long op_calls = 0;
 #ifdef GSCT_DROPIN
   op_s = b200::op_times().seconds;
-  std::fprintf(stderr, "operator seconds by kind: fwd %.3f bwd %.3f vox %.3f voxbwd %.3f\n",
+  std::fprintf(stderr, "operator seconds by kind: fwd %.3f bwd %.3f vox %.3f voxbwd %.3f loss %.3f\n",
                b200::op_times().kind_seconds[0], b200::op_times().kind_seconds[1], b200::op_times().kind_seconds[2],
-               b200::op_times().kind_seconds[3]);
+               b200::op_times().kind_seconds[3], b200::op_times().kind_seconds[4]);
   op_calls = static_cast<long long>(b200::op_times().calls);
   const char* impl = "b200_dropin";
 #else
