@@ -72,8 +72,17 @@ __device__ __forceinline__ bool raster_chain_safe(float A, float B, float C, flo
 // counts in a warp), the exact top row (>> vs) and a column band (>> us): the lanes of a warp
 // then walk coinciding rows with 32 B chunks in shared 128 B lines. Empty items: the last
 // class of their view.
+#ifndef GSCT_WALK_HCLASSES
+#define GSCT_WALK_HCLASSES 16  // row-count classes per chunk count (H >> GSCT_WALK_HSHIFT, clamped)
+#endif
+#ifndef GSCT_WALK_HSHIFT
+#define GSCT_WALK_HSHIFT 2
+#endif
+#ifndef GSCT_WALK_BANDS
+#define GSCT_WALK_BANDS 8  // at most this many column bands per row
+#endif
 struct WalkLayout {
-  int shapes = 65;  // 64 shape classes + the empty class
+  int shapes = 4 * GSCT_WALK_HCLASSES + 1;  // shape classes + the empty class
   int vs = 0, us = 0;
   int nv = 1, nu = 1;  // row / column bands
 };
@@ -84,7 +93,7 @@ __device__ __forceinline__ uint32_t walk_bucket(uint32_t urange, uint32_t vrange
   int shape = L.shapes - 1, pv = 0, pu = 0;
   if (W > 0 && H > 0) {
     const int nch = ((u0 & 7) + W + 7) >> 3;
-    shape = ((min(nch, 4) - 1) << 4) | min(H >> 2, 15);
+    shape = (min(nch, 4) - 1) * GSCT_WALK_HCLASSES + min(H >> GSCT_WALK_HSHIFT, GSCT_WALK_HCLASSES - 1);
 #ifndef GSCT_WALK_BIG_FIRST
 #define GSCT_WALK_BIG_FIRST 1  // largest shape classes first in each view (no long items in the last wave)
 #endif

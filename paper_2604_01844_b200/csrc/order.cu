@@ -179,7 +179,7 @@ WalkLayout walk_layout(int n_views, int n_u, int n_v) {
   WalkLayout L;
   // column bands: at most 8 per row (the top row must be exact for shared lines, the column
   // can be coarse); rows exact while the bucket table stays <= 2^25 words
-  while (((n_u - 1) >> L.us) + 1 > 8) ++L.us;
+  while (((n_u - 1) >> L.us) + 1 > GSCT_WALK_BANDS) ++L.us;
   L.nu = ((n_u - 1) >> L.us) + 1;
   auto total = [&]() { return static_cast<int64_t>(n_views) * L.shapes * (((n_v - 1) >> L.vs) + 1) * L.nu; };
   while (total() > (int64_t(1) << 25) && L.vs < 16) ++L.vs;
