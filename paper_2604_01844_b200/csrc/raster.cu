@@ -266,6 +266,12 @@ struct __align__(16) StagedRec2 {
   uint4 m;   // column mask (32 columns), row mask (16 rows), lane mask, -
 };
 
+#ifndef GSCT_FWD_SAFE_BATCH
+#define GSCT_FWD_SAFE_BATCH 1  // all-chain-safe batches skip the per-record safety branch
+#endif
+#ifndef GSCT_FWD_STAGE_A1E
+#define GSCT_FWD_STAGE_A1E 1  // the staging lane pre-computes the chain step's record terms
+#endif
 #ifndef GSCT_FWD_PREFLAG
 #define GSCT_FWD_PREFLAG 1  // chain-safety flag from the set-up instead of per staged record
 #endif
@@ -313,7 +319,12 @@ __device__ __forceinline__ uint32_t stage_record(const RasterRec& r, int tx0, in
 #endif
   s.p = make_float4(du_t, dv_t, r.A, r.B);
   s.q = make_float4(r.C, fabsf(r.amp), ex2_approx(2.f * r.A), safe ? 1.f : 0.f);
+#if GSCT_FWD_STAGE_A1E
+  // the chain's column-step term A (2 du + 1) at du = du_t + lc is K1 + K2 lc (one FFMA per lane)
+  s.m = make_uint4(cm, rm, __float_as_uint(r.A * fmaf(2.f, du_t, 1.f)), __float_as_uint(2.f * r.A));
+#else
   s.m = make_uint4(cm, rm, lanes_rel, 0u);
+#endif
   *slot = s;
   return lanes_rel;
 }
@@ -374,9 +385,11 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
   }
   for (uint32_t base = b; base < e; base += kBatch) {
     uint32_t todo[kFwdGroups];
+    bool my_safe = true;  // every record this lane staged (and some lane walks) is chain-safe
 #pragma unroll
     for (int g = 0; g < kFwdGroups; ++g) {
       const uint32_t rel = base + 32 * g + lane < e ? stage_record(recs[g], tx0, ty0, sw + 32 * g + lane) : 0u;
+      if (rel) my_safe = my_safe && sw[32 * g + lane].q.w != 0.f;  // the staged flag (this lane's own write)
       todo[g] = warp_transpose32(rel, lane);
     }
     __syncwarp();
@@ -387,7 +400,9 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
       idx_next[g] = k + kBatch < e ? __ldg(vals + k + kBatch) & vmask : 0u;
     }
     // one flat loop over the lane's records of the whole batch, so lanes do not wait for
-    // each other at group boundaries
+    // each other at group boundaries; a batch whose records are all chain-safe (the common
+    // case) runs a copy of the loop without the per-record safety branch
+    auto walk = [&](auto all_safe) {
 #if GSCT_FWD_GROUPS == 1
     uint32_t cur = todo[0];
 #pragma unroll kFwdUnroll
@@ -421,7 +436,11 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
 #endif
       const float4 p = sw[j].p;
       const float4 q = sw[j].q;
+#if GSCT_FWD_STAGE_A1E
+      const uint4 mm = sw[j].m;
+#else
       const uint2 mm = make_uint2(sw[j].m.x, sw[j].m.y);
+#endif
       const uint32_t mask = (mm.x >> lc) & 0xFFu;  // this lane's 8 columns
       const uint32_t rows = (mm.y >> lr) & 3u;     // this lane's 2 rows
       const float a0 = (rows & 1u) ? q.y : 0.f, a1 = (rows & 2u) ? q.y : 0.f;
@@ -432,10 +451,14 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
       const float2 DV2 = make_float2(dv0, dv0 + 1.f);
       // accumulation inside each branch: no merge of the h registers after the branch
       // (a merged h[8] cost ~10 register-pair MOVs per record)
-      if (q.w != 0.f) {
+      if (decltype(all_safe)::value || q.w != 0.f) {
         const float2 E0 = __ffma2_rn(DV2, __ffma2_rn(make_float2(q.x, q.x), DV2, make_float2(bdu, bdu)),
                                      make_float2(au2, au2));
+#if GSCT_FWD_STAGE_A1E
+        const float a1e = fmaf(__uint_as_float(mm.w), flc, __uint_as_float(mm.z));
+#else
         const float a1e = p.z * fmaf(2.f, du0, 1.f);
+#endif
         const float2 D = __ffma2_rn(make_float2(p.w, p.w), DV2, make_float2(a1e, a1e));
         float2 h = make_float2(ex2_approx(E0.x), ex2_approx(E0.y));
         float2 rr = make_float2(ex2_approx(D.x), ex2_approx(D.y));
@@ -458,6 +481,13 @@ __global__ void __launch_bounds__(128, GSCT_FWD_MINB) k_raster_fwd4(const Raster
         }
       }
     }
+    };
+#if GSCT_FWD_SAFE_BATCH
+    if (__all_sync(0xffffffffu, my_safe))
+      walk(std::integral_constant<bool, true>{});
+    else
+#endif
+      walk(std::integral_constant<bool, false>{});
     __syncwarp();
   }
   const int px0 = tx0 + lc;
