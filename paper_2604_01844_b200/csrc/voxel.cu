@@ -69,6 +69,9 @@ struct __align__(16) StagedVox {
 // fp32 under/overflow anywhere in the brick window) falling back to direct exp2; the rows
 // holding an exactly-on-lattice centre also use the direct path so the peak voxel is
 // rho * exp2(0) = rho exactly (test_voxelizer.cpp:16-22).
+#ifndef GSCT_VFWD_PLAIN_BATCH
+#define GSCT_VFWD_PLAIN_BATCH 1
+#endif
 #ifndef GSCT_VFWD_MINB
 #define GSCT_VFWD_MINB 6  // 80 registers, 6 CTAs/SM (A/B 512^3: 5 CTAs 1.011 ms, 6 0.976, 7 1.001, 8 1.096)
 #endif
@@ -99,6 +102,7 @@ __global__ void __launch_bounds__(128, GSCT_VFWD_MINB) k_voxel_fwd2(const VoxelR
   for (uint32_t base = b; base < e; base += 32) {
     const int cnt = min(32u, e - base);
     uint32_t lanes_rel = 0u;
+    bool my_plain = true;  // the staged record is chain-safe and has no lattice-exact peak here
     if (lane < cnt) {
       const VoxelRec r = rec[vals[base + lane]];
       StagedVox s;
@@ -151,9 +155,12 @@ __global__ void __launch_bounds__(128, GSCT_VFWD_MINB) k_voxel_fwd2(const VoxelR
       s.r = make_float4(r.Q02, r.Q12, ex2_approx(c2e), safe ? 1.f : 0.f);
       s.m = make_uint4(xm | (ym << 8) | (zm << 16), lanes_rel, peak, __float_as_uint(r.offz));
       sw[lane] = s;
+      my_plain = safe && peak == 0xFFFFFFFFu;
     }
     __syncwarp();
     uint32_t todo = warp_transpose32(lanes_rel, lane);
+    // a batch of only plain records (the common case) walks without the direct-path branch
+    auto walk = [&](auto plain) {
 #pragma unroll kVfwdUnroll
     while (todo) {
       const int j = __ffs(todo) - 1;
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(128, GSCT_VFWD_MINB) k_voxel_fwd2(const VoxelR
       const f2_t RHO = f2_pack((rows & 1u) ? p.w : 0.f, (rows & 2u) ? p.w : 0.f);
       const float dy0 = p.y + fy, dx0 = p.x;
       const f2_t DY = f2_pack(dy0, dy0 + sp);
-      const bool direct = rr4.w == 0.f || m.z == static_cast<uint32_t>(lane);
+      const bool direct = !decltype(plain)::value && (rr4.w == 0.f || m.z == static_cast<uint32_t>(lane));
       // the exponent / chain arithmetic stays in inline-asm packed ops (never contracted, so a
       // voxel's value does not depend on which lane or unrolled z step computes it: z-slab
       // windows stay bit-identical); only the accumulation uses the __fadd2_rn builtin, which
@@ -213,6 +220,13 @@ __global__ void __launch_bounds__(128, GSCT_VFWD_MINB) k_voxel_fwd2(const VoxelR
         }
       }
     }
+    };
+#if GSCT_VFWD_PLAIN_BATCH
+    if (__all_sync(0xffffffffu, my_plain))
+      walk(std::integral_constant<bool, true>{});
+    else
+#endif
+      walk(std::integral_constant<bool, false>{});
     __syncwarp();
   }
   const int wx = win.hi[0] - win.lo[0], wy = win.hi[1] - win.lo[1];
