@@ -383,6 +383,11 @@ int gsct_host_sample_subvolume(const int parent_dims[3], const int sub_dims[3], 
  *           p1=spacing; positions uniform in the outer ellipsoid, 1-NN-like scales. */
 int gsct_host_make_cloud(int kind, int64_t count, uint64_t seed, const double* params,
                          double* pos, double* log_scale, double* quat, double* raw);
+/* Element conversions of host arrays on the library's host worker pool (the C++ adapter's
+ * fp64 <-> fp32 image / volume conversions; GSCT_HOSTIO_THREADS threads, serial below 64k
+ * elements): dst[i] = (float)src[i];  dst[i] = scale * (double)src[i]. */
+void gsct_host_f64_to_f32(const double* src, float* dst, int64_t n);
+void gsct_host_f32_to_f64(const float* src, double* dst, int64_t n, double scale);
 
 #ifdef __cplusplus
 }

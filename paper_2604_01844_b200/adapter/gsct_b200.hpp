@@ -26,10 +26,13 @@
 #include <malloc.h>
 
 #include <chrono>
+#include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -88,6 +91,10 @@ struct OpTimes {
   double seconds = 0.0;
   std::int64_t calls = 0;
   double kind_seconds[5] = {0, 0, 0, 0, 0};  // rasterize fwd, rasterize bwd, voxelize, voxelize bwd, loss
+  double api_seconds = 0.0;                   // of which inside the C ABI calls (the rest: host-side conversions)
+  double pre_seconds[5] = {0, 0, 0, 0, 0};    // per kind: operator entry -> first C ABI call
+  double post_seconds[5] = {0, 0, 0, 0, 0};   // per kind: last C ABI call -> operator return
+  double api_kind_seconds[5] = {0, 0, 0, 0, 0};
 };
 inline OpTimes& op_times() {
   static thread_local OpTimes t;
@@ -96,15 +103,30 @@ inline OpTimes& op_times() {
 
 namespace detail {
 
+struct OpTimer;
+inline OpTimer*& active_timer() {
+  static thread_local OpTimer* t = nullptr;
+  return t;
+}
+
 struct OpTimer {
   int kind;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  explicit OpTimer(int k) : kind(k) {}
+  std::chrono::steady_clock::time_point first_api{}, last_api{};
+  OpTimer* outer;
+  explicit OpTimer(int k) : kind(k), outer(active_timer()) { active_timer() = this; }
   ~OpTimer() {
-    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    using sec = std::chrono::duration<double>;
+    const auto t1 = std::chrono::steady_clock::now();
+    const double s = sec(t1 - t0).count();
     op_times().seconds += s;
     op_times().kind_seconds[kind] += s;
     op_times().calls += 1;
+    if (first_api != std::chrono::steady_clock::time_point{}) {
+      op_times().pre_seconds[kind] += sec(first_api - t0).count();
+      op_times().post_seconds[kind] += sec(t1 - last_api).count();
+    }
+    active_timer() = outer;
   }
 };
 
@@ -113,6 +135,22 @@ inline void check_status(gsct_ctx c, int status) {
   const std::string msg = gsct_ctx_last_error(c);
   if (status == GSCT_ERR_CONTRACT) throw contract_error(msg);
   throw error("gsct::b200: " + msg);
+}
+
+// C ABI call timed into op_times().api_seconds
+template <class F>
+inline void call_api(gsct_ctx c, F&& f) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int status = f();
+  const auto t1 = std::chrono::steady_clock::now();
+  const double s = std::chrono::duration<double>(t1 - t0).count();
+  op_times().api_seconds += s;
+  if (OpTimer* t = active_timer()) {
+    op_times().api_kind_seconds[t->kind] += s;
+    if (t->first_api == std::chrono::steady_clock::time_point{}) t->first_api = t0;
+    t->last_api = t1;
+  }
+  check_status(c, status);
 }
 
 // GaussianCloud stores std::vector<Vec3/Vec4>: fixed-size Eigen vectors are dense doubles
@@ -189,18 +227,93 @@ inline gsct_stats put_stats(const RenderStats* stats) {
   return s;
 }
 
+// every element is overwritten by the call: default-insert (no ParamGradients::resize
+// zero pass over the 96 B/splat; Eigen's fixed-size vectors are left uninitialised)
+inline void build_grads(ParamGradients& g, std::size_t n) {
+  g.positions.resize(n);
+  g.log_scales.resize(n);
+  g.rotations.resize(n);
+  g.raw_densities.resize(n);
+  g.pos_grad_norm.resize(n);
+  g.visible.resize(n);
+}
+
+// The reference API returns a fresh ParamGradients (19 MB at 200k splats) from every backward
+// call; constructing its six vectors is single-threaded host work on the call's critical path
+// (measured in the unchanged train_reconstruction: 1.4-1.9 ms per call, two calls per
+// view-step). A per-thread worker builds the NEXT result's containers while the caller works
+// with the current one, so a call finds them ready (same size) and only moves them out.
+// GSCT_B200_NO_PREBUILD=1 builds them inline.
+class GradPrebuild {
+ public:
+  static GradPrebuild& get() {
+    static thread_local GradPrebuild p;
+    return p;
+  }
+  ParamGradients take(std::size_t n) {
+    ParamGradients g;
+    if (!enabled_) {
+      build_grads(g, n);
+      return g;
+    }
+    std::unique_lock<std::mutex> lk(mu_);
+    if (!worker_.joinable()) worker_ = std::thread([this] { loop(); });
+    done_cv_.wait(lk, [&] { return !want_; });
+    if (ready_ && n_ == n) {
+      g = std::move(next_);
+    } else {
+      lk.unlock();
+      build_grads(g, n);
+      lk.lock();
+    }
+    ready_ = false;
+    n_ = n;
+    want_ = true;  // build the next one
+    cv_.notify_one();
+    return g;
+  }
+  ~GradPrebuild() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_one();
+    if (worker_.joinable()) worker_.join();
+  }
+
+ private:
+  GradPrebuild() {
+    const char* e = std::getenv("GSCT_B200_NO_PREBUILD");
+    enabled_ = !(e && e[0] == '1');
+  }
+  void loop() {
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || want_; });
+      if (stop_) return;
+      const std::size_t n = n_;
+      lk.unlock();
+      ParamGradients g;
+      build_grads(g, n);
+      lk.lock();
+      next_ = std::move(g);
+      ready_ = true;
+      want_ = false;
+      done_cv_.notify_all();
+    }
+  }
+  bool enabled_ = true, want_ = false, ready_ = false, stop_ = false;
+  std::size_t n_ = 0;
+  ParamGradients next_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::thread worker_;
+};
+
 struct GradBuffers {
   ParamGradients g;
   gsct_grads c;
-  explicit GradBuffers(std::size_t n) {
-    // every element is overwritten by the call: default-insert (no ParamGradients::resize
-    // zero pass over the 96 B/splat; Eigen's fixed-size vectors are left uninitialised)
-    g.positions.resize(n);
-    g.log_scales.resize(n);
-    g.rotations.resize(n);
-    g.raw_densities.resize(n);
-    g.pos_grad_norm.resize(n);
-    g.visible.resize(n);
+  explicit GradBuffers(std::size_t n) : g(GradPrebuild::get().take(n)) {
     c.pos = reinterpret_cast<double*>(g.positions.data());
     c.log_scale = reinterpret_cast<double*>(g.log_scales.data());
     c.quat = reinterpret_cast<double*>(g.rotations.data());
@@ -231,13 +344,13 @@ inline std::vector<Image> rasterize_views(const GaussianCloud& cloud, const Scan
   const std::size_t npx = static_cast<std::size_t>(geometry.n_u) * geometry.n_v;
   std::vector<float> buf(npx * angles.size());
   gsct_stats st = detail::put_stats(stats);
-  detail::check_status(c, gsct_rasterize_fwd(c, &cc, &cg, angles.data(), static_cast<int>(angles.size()), &rs,
-                                              buf.data(), GSCT_HOST, stats ? &st : nullptr));
+  detail::call_api(c, [&] { return gsct_rasterize_fwd(c, &cc, &cg, angles.data(), static_cast<int>(angles.size()), &rs,
+                                              buf.data(), GSCT_HOST, stats ? &st : nullptr); });
   detail::take_stats(st, stats);
   std::vector<Image> out(angles.size());
   for (std::size_t v = 0; v < angles.size(); ++v) {
     out[v] = Image::zeros(geometry.n_u, geometry.n_v);
-    for (std::size_t k = 0; k < npx; ++k) out[v].values[k] = buf[v * npx + k];
+    gsct_host_f32_to_f64(buf.data() + v * npx, out[v].values.data(), static_cast<int64_t>(npx), 1.0);
   }
   return out;
 }
@@ -263,7 +376,7 @@ inline ParamGradients rasterize_backward_views(const GaussianCloud& cloud, const
           "rasterize_backward: grad image dims must match detector");
     check(angle_indices[k] < geometry.angles.size(), "view_frame: angle index out of range");
     angles.push_back(geometry.angles[angle_indices[k]]);
-    for (std::size_t p = 0; p < npx; ++p) gi[k * npx + p] = static_cast<float>(grad_images[k]->values[p]);
+    gsct_host_f64_to_f32(grad_images[k]->values.data(), gi.data() + k * npx, static_cast<int64_t>(npx));
   }
   gsct_ctx c = Device::ctx();
   const gsct_cloud cc = detail::c_cloud(cloud);
@@ -271,8 +384,8 @@ inline ParamGradients rasterize_backward_views(const GaussianCloud& cloud, const
   const gsct_raster_settings rs = detail::c_raster(settings);
   detail::GradBuffers gb(cloud.size());
   gsct_stats st = detail::put_stats(stats);
-  detail::check_status(c, gsct_rasterize_bwd(c, &cc, &cg, angles.data(), static_cast<int>(angles.size()), &rs,
-                                              gi.data(), GSCT_HOST, &gb.c, stats ? &st : nullptr));
+  detail::call_api(c, [&] { return gsct_rasterize_bwd(c, &cc, &cg, angles.data(), static_cast<int>(angles.size()), &rs,
+                                              gi.data(), GSCT_HOST, &gb.c, stats ? &st : nullptr); });
   detail::take_stats(st, stats);
   return std::move(gb.g);  // a member: no implicit move, so move explicitly (19 MB at 200k)
 }
@@ -297,9 +410,9 @@ inline Volume voxelize(const GaussianCloud& cloud, const GridRegion& region, con
   Volume out = Volume::zeros(region.dims, region.spacing, region.origin);
   std::vector<float> buf(out.values.size());
   gsct_stats st = detail::put_stats(stats);
-  detail::check_status(c, gsct_voxelize_fwd(c, &cc, &g, nullptr, &vs, buf.data(), GSCT_HOST, stats ? &st : nullptr));
+  detail::call_api(c, [&] { return gsct_voxelize_fwd(c, &cc, &g, nullptr, &vs, buf.data(), GSCT_HOST, stats ? &st : nullptr); });
   detail::take_stats(st, stats);
-  for (std::size_t k = 0; k < buf.size(); ++k) out.values[k] = buf[k];
+  gsct_host_f32_to_f64(buf.data(), out.values.data(), static_cast<int64_t>(buf.size()), 1.0);
   return out;
 }
 
@@ -320,11 +433,11 @@ inline ParamGradients voxelize_backward(const GaussianCloud& cloud, const GridRe
   const gsct_grid g = detail::c_grid(region.dims, region.spacing, region.origin);
   const gsct_voxel_settings vs = detail::c_voxel(settings);
   std::vector<float> gv(grad_volume.values.size());
-  for (std::size_t k = 0; k < gv.size(); ++k) gv[k] = static_cast<float>(grad_volume.values[k]);
+  gsct_host_f64_to_f32(grad_volume.values.data(), gv.data(), static_cast<int64_t>(gv.size()));
   detail::GradBuffers gb(cloud.size());
   gsct_stats st = detail::put_stats(stats);
-  detail::check_status(c, gsct_voxelize_bwd(c, &cc, &g, nullptr, &vs, gv.data(), GSCT_HOST, &gb.c,
-                                             stats ? &st : nullptr));
+  detail::call_api(c, [&] { return gsct_voxelize_bwd(c, &cc, &g, nullptr, &vs, gv.data(), GSCT_HOST, &gb.c,
+                                             stats ? &st : nullptr); });
   detail::take_stats(st, stats);
   return std::move(gb.g);  // a member: no implicit move, so move explicitly (19 MB at 200k)
 }

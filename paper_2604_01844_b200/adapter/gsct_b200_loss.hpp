@@ -25,28 +25,26 @@ inline ReconLoss total_loss_recon(const Image& rendered, const Image& measured, 
   gsct_ctx c = Device::ctx();
   const std::size_t npx = rendered.values.size();
   std::vector<float> r(npx), m(npx), g(npx);
-  for (std::size_t k = 0; k < npx; ++k) {
-    r[k] = static_cast<float>(rendered.values[k]);
-    m[k] = static_cast<float>(measured.values[k]);
-  }
+  gsct_host_f64_to_f32(rendered.values.data(), r.data(), static_cast<int64_t>(npx));
+  gsct_host_f64_to_f32(measured.values.data(), m.data(), static_cast<int64_t>(npx));
   double lv[3] = {0.0, 0.0, 0.0};
-  detail::check_status(c, gsct_image_loss(c, r.data(), m.data(), 1, rendered.n_u, rendered.n_v, weights.alpha_ssim,
-                                          g.data(), GSCT_HOST, lv));
+  detail::call_api(c, [&] { return gsct_image_loss(c, r.data(), m.data(), 1, rendered.n_u, rendered.n_v, weights.alpha_ssim,
+                                          g.data(), GSCT_HOST, lv); });
   ReconLoss out;
   out.l1 = lv[0];
   out.ssim = weights.alpha_ssim > 0.0 ? lv[1] : 0.0;
   out.grad_image = Image::zeros(rendered.n_u, rendered.n_v);
-  for (std::size_t k = 0; k < npx; ++k) out.grad_image.values[k] = g[k];
+  gsct_host_f32_to_f64(g.data(), out.grad_image.values.data(), static_cast<int64_t>(npx), 1.0);
   if (weights.alpha_tv > 0.0) {
     const std::size_t nvox = subvolume.values.size();
     std::vector<float> v(nvox), gv(nvox);
-    for (std::size_t k = 0; k < nvox; ++k) v[k] = static_cast<float>(subvolume.values[k]);
+    gsct_host_f64_to_f32(subvolume.values.data(), v.data(), static_cast<int64_t>(nvox));
     const int dims[3] = {subvolume.dims[0], subvolume.dims[1], subvolume.dims[2]};
     double tv = 0.0;
-    detail::check_status(c, gsct_tv3d(c, v.data(), dims, gv.data(), GSCT_HOST, &tv));
+    detail::call_api(c, [&] { return gsct_tv3d(c, v.data(), dims, gv.data(), GSCT_HOST, &tv); });
     out.tv = tv;
     out.grad_subvolume = Volume::zeros(subvolume.dims, subvolume.spacing, subvolume.origin);
-    for (std::size_t k = 0; k < nvox; ++k) out.grad_subvolume.values[k] = weights.alpha_tv * gv[k];
+    gsct_host_f32_to_f64(gv.data(), out.grad_subvolume.values.data(), static_cast<int64_t>(nvox), weights.alpha_tv);
   } else {
     out.grad_subvolume = Volume::zeros(subvolume.dims, subvolume.spacing, subvolume.origin);
   }

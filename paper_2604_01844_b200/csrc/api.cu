@@ -227,8 +227,11 @@ template <class F>
 int run(gsct_ctx c, F&& f) {
   if (!c) return GSCT_ERR_CONTRACT;
   Guard guard(c);
+  const auto t0 = std::chrono::steady_clock::now();
   try {
     f();
+    c->hio.ms_api += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    ++c->hio.n_api;
     c->err.clear();
     return GSCT_OK;
   } catch (const CallError& e) {
@@ -355,13 +358,15 @@ void finish_sync(gsct_ctx c, gsct_stats* stats, bool counters, double* ms_slot) 
   if (c->async) return;
   CK(cudaMemcpyAsync(c->hstats, c->dstats, sizeof(DevStats), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaEventRecord(c->ev1, c->stream));
+  // deferred copy-outs of staged D2H into pageable caller buffers, each piece as it lands
+  const cudaError_t landed = c->hio.finish();
   {
     const auto t0 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(c->stream));
     c->hio.ms_sync += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
+  CK(landed);
   CK(cudaGetLastError());
-  c->hio.finish();  // deferred copy-outs of staged D2H into pageable caller buffers
   const DevStats& h = *c->hstats;
   if (h.error_key != ~0ull) {
     const unsigned long long idx = h.error_key >> 2;
@@ -2192,7 +2197,7 @@ int gsct_decompress_model(gsct_ctx c, const uint8_t* bytes, int64_t n_bytes, int
       d2h(c, const_cast<double*>(out->raw_density), r, un * sizeof(double), c->stream);
     }
     CK(cudaStreamSynchronize(c->stream));
-    c->hio.finish();
+    CK(c->hio.finish());
   });
 }
 

@@ -32,8 +32,6 @@
 
 namespace gsct_dev {
 
-namespace {
-
 // Process-wide worker pool for the host-side copies (parallel_for over chunk indices).
 class Pool {
  public:
@@ -118,7 +116,19 @@ class Pool {
   bool stop_ = false;
 };
 
-constexpr size_t kChunk = size_t(1) << 20;  // bytes per pool task
+namespace {
+
+constexpr size_t kChunk = size_t(1) << 20;      // bytes per pool task
+// bytes per staged D2H piece (one event each); GSCT_HOSTIO_PIECE_MB=0: one piece per copy
+size_t len_step(size_t piece, size_t left) { return std::min(piece, left); }
+size_t land_piece() {
+  static const size_t v = [] {
+    const char* e = std::getenv("GSCT_HOSTIO_PIECE_MB");
+    const long mb = e ? std::atol(e) : 4;
+    return mb > 0 ? static_cast<size_t>(mb) << 20 : ~size_t(0);
+  }();
+  return v;
+}
 
 void parallel_copy(void* dst, const void* src, size_t bytes) {
   const int64_t tasks = static_cast<int64_t>((bytes + kChunk - 1) / kChunk);
@@ -150,11 +160,26 @@ HostIO::~HostIO() {
   if (const char* e = std::getenv("GSCT_HOSTIO_STATS"))
     if (e[0] == '1')
       std::fprintf(stderr,
-                   "hostio: replica %.1f ms (%lld calls, %.1f MB up), staged h2d %.1f ms, copy-out %.1f ms, "
-                   "stream sync %.1f ms\n",
-                   ms_replica, static_cast<long long>(n_replica), bytes_replica_up / 1e6, ms_h2d, ms_copyout, ms_sync);
+                   "hostio: replica %.1f ms (%lld calls, %.1f MB up; %lld calls with changes %.1f ms), staged h2d "
+                   "%.1f ms, copy-out %.1f ms, stream sync %.1f ms; API calls %lld, %.1f ms inside\n",
+                   ms_replica, static_cast<long long>(n_replica), bytes_replica_up / 1e6,
+                   static_cast<long long>(n_replica_dirty), ms_replica_dirty, ms_h2d, ms_copyout, ms_sync,
+                   static_cast<long long>(n_api), ms_api);
   for (auto& b : blocks_) cudaFreeHost(b.p);
   if (shadow_) cudaFreeHost(shadow_);
+  for (cudaEvent_t e : events_) cudaEventDestroy(e);
+}
+
+cudaEvent_t HostIO::next_event() {
+  if (n_events_used_ == events_.size()) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    events_.push_back(e);
+  }
+  return events_[n_events_used_++];
 }
 
 void* HostIO::stage(size_t bytes) {
@@ -189,31 +214,59 @@ cudaError_t HostIO::d2h(void* dst, const void* src, size_t bytes, cudaStream_t s
   if (bytes < kMinStaged || !host_pageable(dst)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
   void* s = stage(bytes);
   if (!s) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
-  pending_.push_back(Pending{dst, s, bytes});
-  return cudaMemcpyAsync(s, src, bytes, cudaMemcpyDeviceToHost, st);
+  cudaGetDevice(&device_);
+  // pieces of <= kLandPiece bytes, each with an event behind its DMA
+  const size_t piece = land_piece();
+  for (size_t a = 0; a < bytes; a += len_step(piece, bytes - a)) {
+    const size_t len = std::min(piece, bytes - a);
+    const cudaError_t r = cudaMemcpyAsync(static_cast<char*>(s) + a, static_cast<const char*>(src) + a, len,
+                                          cudaMemcpyDeviceToHost, st);
+    if (r != cudaSuccess) return r;
+    cudaEvent_t e = next_event();
+    if (e && cudaEventRecord(e, st) != cudaSuccess) {
+      cudaGetLastError();
+      e = nullptr;
+    }
+    pending_.push_back(Pending{static_cast<char*>(dst) + a, static_cast<char*>(s) + a, len, e});
+  }
+  return cudaSuccess;
 }
 
-void HostIO::finish() {
+cudaError_t HostIO::finish() {
+  std::atomic<int> err{static_cast<int>(cudaSuccess)};
   if (!pending_.empty()) {
     const auto t0 = std::chrono::steady_clock::now();
-    // one pool job over all pending copies' 1 MB pieces
-    std::vector<std::pair<size_t, size_t>> pieces;  // (pending index, offset)
+    // one pool job over all pending pieces' 1 MB chunks, in enqueue order: a task waits for
+    // its piece's DMA, so chunks of landed pieces are copied while later DMAs are in flight
+    std::vector<std::pair<size_t, size_t>> chunks;  // (pending index, offset)
     for (size_t i = 0; i < pending_.size(); ++i)
-      for (size_t a = 0; a < pending_[i].bytes; a += kChunk) pieces.emplace_back(i, a);
-    Pool::get().run(static_cast<int64_t>(pieces.size()), [&](int64_t k) {
-      const Pending& p = pending_[pieces[static_cast<size_t>(k)].first];
-      const size_t a = pieces[static_cast<size_t>(k)].second, b = std::min(p.bytes, a + kChunk);
+      for (size_t a = 0; a < pending_[i].bytes; a += kChunk) chunks.emplace_back(i, a);
+    const int dev = device_;
+    Pool::get().run(static_cast<int64_t>(chunks.size()), [&](int64_t k) {
+      const Pending& p = pending_[chunks[static_cast<size_t>(k)].first];
+      if (p.landed) {
+        cudaSetDevice(dev);
+        const cudaError_t r = cudaEventSynchronize(p.landed);
+        if (r != cudaSuccess) {
+          err.store(static_cast<int>(r));
+          return;
+        }
+      }
+      const size_t a = chunks[static_cast<size_t>(k)].second, b = std::min(p.bytes, a + kChunk);
       memcpy(static_cast<char*>(p.dst) + a, static_cast<const char*>(p.staged) + a, b - a);
     });
     pending_.clear();
     ms_copyout += ms_since(t0);
   }
+  n_events_used_ = 0;
   for (auto& b : blocks_) b.used = 0;
   cur_ = 0;
+  return static_cast<cudaError_t>(err.load());
 }
 
 void HostIO::discard() {
   pending_.clear();
+  n_events_used_ = 0;
   for (auto& b : blocks_) b.used = 0;
   cur_ = 0;
 }
@@ -277,7 +330,12 @@ cudaError_t HostIO::cloud_to_device(const CloudArrays& host, const CloudArrays& 
   key_n_ = n;
   key_valid_ = true;
   bytes_replica_up += up;
-  ms_replica += ms_since(t0);
+  const double ms = ms_since(t0);
+  ms_replica += ms;
+  if (up > 0) {
+    ms_replica_dirty += ms;
+    ++n_replica_dirty;
+  }
   if (bytes_uploaded) *bytes_uploaded = up;
   return cudaSuccess;
 }
@@ -285,3 +343,36 @@ cudaError_t HostIO::cloud_to_device(const CloudArrays& host, const CloudArrays& 
 void HostIO::invalidate_cloud() { key_valid_ = false; }
 
 }  // namespace gsct_dev
+
+// include/gsct_cuda.h host conversions: 64k-element pieces over the pool
+namespace {
+constexpr int64_t kConvPiece = int64_t(1) << 16;
+template <class F>
+void conv_pieces(int64_t n, F&& f) {
+  if (n <= kConvPiece) {
+    f(int64_t(0), n);
+    return;
+  }
+  gsct_dev::Pool::get().run((n + kConvPiece - 1) / kConvPiece, [&](int64_t k) {
+    const int64_t a = k * kConvPiece;
+    f(a, std::min(n, a + kConvPiece));
+  });
+}
+}  // namespace
+
+extern "C" void gsct_host_f64_to_f32(const double* src, float* dst, int64_t n) {
+  if (!src || !dst || n <= 0) return;
+  conv_pieces(n, [&](int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) dst[i] = static_cast<float>(src[i]);
+  });
+}
+
+extern "C" void gsct_host_f32_to_f64(const float* src, double* dst, int64_t n, double scale) {
+  if (!src || !dst || n <= 0) return;
+  conv_pieces(n, [&](int64_t a, int64_t b) {
+    if (scale == 1.0)
+      for (int64_t i = a; i < b; ++i) dst[i] = static_cast<double>(src[i]);
+    else
+      for (int64_t i = a; i < b; ++i) dst[i] = scale * static_cast<double>(src[i]);
+  });
+}

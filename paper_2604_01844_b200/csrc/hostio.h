@@ -23,8 +23,10 @@ class HostIO {
   // cudaMemcpyAsync.
   cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
   cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
-  // After the stream(s) of the call are synchronised: deferred D2H copy-outs, arena reset.
-  void finish();
+  // Deferred D2H copy-outs (each piece as soon as its DMA has landed, so the copy-out of one
+  // piece overlaps the DMA of the next), then the arena reset. Called before the call's
+  // stream synchronisation; returns the first error an awaited DMA reported.
+  cudaError_t finish();
   // Drop deferred copies (error path; the arena is reset).
   void discard();
   bool has_pending() const { return !pending_.empty(); }
@@ -36,8 +38,8 @@ class HostIO {
 
   static constexpr size_t kMinStaged = size_t(256) << 10;
   // GSCT_HOSTIO_STATS=1: host-side milliseconds per activity, printed when the context dies
-  double ms_replica = 0, ms_h2d = 0, ms_copyout = 0, ms_sync = 0;
-  int64_t n_replica = 0, bytes_replica_up = 0;
+  double ms_replica = 0, ms_h2d = 0, ms_copyout = 0, ms_sync = 0, ms_api = 0, ms_replica_dirty = 0;
+  int64_t n_replica = 0, bytes_replica_up = 0, n_api = 0, n_replica_dirty = 0;
 
  private:
   void* stage(size_t bytes);
@@ -49,7 +51,12 @@ class HostIO {
     void* dst;
     const void* staged;
     size_t bytes;
+    cudaEvent_t landed;  // recorded behind the piece's DMA
   };
+  cudaEvent_t next_event();
+  std::vector<cudaEvent_t> events_;
+  size_t n_events_used_ = 0;
+  int device_ = 0;
   std::vector<Block> blocks_;
   size_t cur_ = 0;
   std::vector<Pending> pending_;

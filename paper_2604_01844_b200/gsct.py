@@ -201,6 +201,8 @@ _SIGS = {
     "gsct_host_rng_get_state": (None, [C.c_void_p, _P(c_rng_state)]),
     "gsct_host_rng_set_state": (None, [C.c_void_p, _P(c_rng_state)]),
     "gsct_host_sample_subvolume": (C.c_int, [_P(C.c_int), _P(C.c_int), C.c_void_p, _P(C.c_int), _P(C.c_int)]),
+    "gsct_host_f64_to_f32": (None, [C.c_void_p, C.c_void_p, C.c_int64]),
+    "gsct_host_f32_to_f64": (None, [C.c_void_p, C.c_void_p, C.c_int64, C.c_double]),
     "gsct_host_make_cloud": (C.c_int, [C.c_int, C.c_int64, C.c_uint64, _P(C.c_double), C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p]),
 }

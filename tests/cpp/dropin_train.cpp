@@ -18,6 +18,8 @@
 #include "gsct_b200_dropin.hpp"
 #endif
 
+#include <sys/resource.h>
+
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -104,6 +106,11 @@ int main(int argc, char** argv) {
   long long op_calls = 0;
 #ifdef GSCT_DROPIN
   op_s = b200::op_times().seconds;
+  std::fprintf(stderr, "operator seconds inside the C ABI: %.3f\n", b200::op_times().api_seconds);
+  for (int k = 0; k < 5; ++k)
+    std::fprintf(stderr, "  kind %d: total %.3f api %.3f pre %.3f post %.3f\n", k, b200::op_times().kind_seconds[k],
+                 b200::op_times().api_kind_seconds[k], b200::op_times().pre_seconds[k],
+                 b200::op_times().post_seconds[k]);
   std::fprintf(stderr, "operator seconds by kind: fwd %.3f bwd %.3f vox %.3f voxbwd %.3f loss %.3f\n",
                b200::op_times().kind_seconds[0], b200::op_times().kind_seconds[1], b200::op_times().kind_seconds[2],
                b200::op_times().kind_seconds[3], b200::op_times().kind_seconds[4]);
@@ -141,7 +148,7 @@ int main(int argc, char** argv) {
   const double t_adam = ms_of([&] { adam_step(cl, st, grads, lrs); });
   // the loop body of train_reconstruction (optim.hpp:456-492) restated with a timer per
   // piece, over 20 view-steps: where a view-step's wall time goes
-  double piece[8] = {};
+  double piece[8] = {}, faults[8] = {};
   const char* piece_name[8] = {"sample_subvolume", "rasterize_view", "voxelize", "total_loss_recon",
                                "rasterize_backward", "accumulate_control_stats", "voxelize_backward+add",
                                "adam_step"};
@@ -149,9 +156,18 @@ int main(int argc, char** argv) {
     OptimState s2;
     s2.init(cl.size(), 0);
     auto now = [] { return std::chrono::steady_clock::now(); };
+    auto minflt = [] {
+      rusage u{};
+      getrusage(RUSAGE_SELF, &u);
+      return static_cast<long long>(u.ru_minflt);
+    };
+    long long flt_mark = minflt();
     auto tick = [&](int k, std::chrono::steady_clock::time_point& t) {
       const auto t2 = now();
       piece[k] += std::chrono::duration<double, std::milli>(t2 - t).count();
+      const long long f = minflt();
+      faults[k] += static_cast<double>(f - flt_mark);
+      flt_mark = f;
       t = t2;
     };
     const int n_steps = 20;
@@ -177,6 +193,10 @@ int main(int argc, char** argv) {
       tick(7, t);
     }
     for (double& p : piece) p /= n_steps;
+    // minor page faults per piece (first touches of fresh heap / mmap pages)
+    std::fprintf(stderr, "minor faults per view-step piece:");
+    for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s %.0f", piece_name[k], faults[k] / n_steps);
+    std::fprintf(stderr, "\n");
   }
   std::printf(
       "{\"impl\": \"%s\", \"gaussians\": %lld, \"views\": %d, \"detector\": %d, \"epochs\": %d, "

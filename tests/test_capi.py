@@ -134,3 +134,21 @@ def test_cloud_lockstep_and_param_gradients_add():
     assert np.array_equal(a.positions[1], [1, 2, 3]) and a.visible.tolist() == [0, 0, 1]
     with pytest.raises(gsct.ContractError):
         a.add(gsct.ParamGradients.zeros(4))
+
+
+def test_host_conversions_match_numpy():
+    """gsct_host_f64_to_f32 / gsct_host_f32_to_f64 (the C++ adapter's image and volume
+    conversions, run on the library's host pool): element-wise IEEE conversions, bit-equal
+    to numpy's, serial and pooled sizes, with the scaled widening the TV gradient uses."""
+    lib = gsct.lib()
+    rng = np.random.default_rng(3)
+    for n in (1, 1000, (1 << 16) + 7, 300_001):
+        d = rng.standard_normal(n) * 10.0 ** rng.integers(-30, 30, n)
+        f = np.empty(n, np.float32)
+        lib.gsct_host_f64_to_f32(d.ctypes.data, f.ctypes.data, n)
+        assert np.array_equal(f.view(np.uint32), d.astype(np.float32).view(np.uint32))
+        w = np.empty(n, np.float64)
+        lib.gsct_host_f32_to_f64(f.ctypes.data, w.ctypes.data, n, 1.0)
+        assert np.array_equal(w, f.astype(np.float64))
+        lib.gsct_host_f32_to_f64(f.ctypes.data, w.ctypes.data, n, 0.05)
+        assert np.array_equal(w, 0.05 * f.astype(np.float64))
