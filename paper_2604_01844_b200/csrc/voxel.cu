@@ -262,8 +262,13 @@ constexpr int kVoxLanes = GSCT_VOX_LANES;
 #ifndef GSCT_VLD_NA
 #define GSCT_VLD_NA 1  // grad-volume row loads bypass L1 allocation (A/B: 2.36 vs 2.54 ms at 512^3)
 #endif
+#ifndef GSCT_VLD_L2PF
+#define GSCT_VLD_L2PF 0  // 1: L2::256B prefetch-size hint on the grad-volume row loads
+#endif
 __device__ __forceinline__ void ldg_v8(const float* p, float (&w)[8]) {
-#if GSCT_VLD_NA
+#if GSCT_VLD_NA && GSCT_VLD_L2PF
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#elif GSCT_VLD_NA
   asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
 #else
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -421,6 +426,12 @@ __device__ __forceinline__ float vox_q(const VoxelRec& r, float dx, float dy, fl
 #ifndef GSCT_VCHAIN_MINB
 #define GSCT_VCHAIN_MINB 3
 #endif
+#ifndef GSCT_VCHAIN_PIPE
+#define GSCT_VCHAIN_PIPE 0
+#endif
+#ifndef GSCT_VBWD_YLANES
+#define GSCT_VBWD_YLANES 1  // lanes interleave y-rows of a slice (A/B: 1024^3 25.5 -> 11.8 ms, 512^3 1.774 vs 1.786)
+#endif
 __global__ void __launch_bounds__(256, GSCT_VCHAIN_MINB) k_voxel_bwd_chain(const VoxelRec* __restrict__ rec,
                                                                            const uint32_t* __restrict__ order,
                                                                            int64_t n, Window win, float sp,
@@ -479,10 +490,19 @@ __global__ void __launch_bounds__(256, GSCT_VCHAIN_MINB) k_voxel_bwd_chain(const
   float m[10];
 #pragma unroll
   for (int k = 0; k < 10; ++k) m[k] = 0.f;
+#if GSCT_VBWD_YLANES
+  // lane q walks rows q, q+4, ... of every z-slice: the lanes of a splat read neighbouring rows
+  // of one slice (one 2 MB page) instead of four slices megabytes apart
+  for (int zz = 0; zz < (empty ? 0 : D); ++zz) {
+    const float dz = fmaf(static_cast<float>(z0 + zz) - r.loz, sp, -r.offz);
+    const float* __restrict__ prow = gz + static_cast<int64_t>(zz) * wy * wx + static_cast<int64_t>(q) * wx;
+    for (int yy = q; yy < H; yy += kVoxLanes, prow += kVoxLanes * wx) {
+#else
   for (int zz = q; zz < (empty ? 0 : D); zz += kVoxLanes) {
     const float dz = fmaf(static_cast<float>(z0 + zz) - r.loz, sp, -r.offz);
     const float* __restrict__ prow = gz + static_cast<int64_t>(zz) * wy * wx;
     for (int yy = 0; yy < H; ++yy, prow += wx) {
+#endif
       const float dy = fmaf(static_cast<float>(y0 + yy) - r.loy, sp, -r.offy);
       const float L = fmaf(r.Q01, dy, r.Q02 * dz);
       const float K = fmaf(dy, fmaf(r.Q11, dy, r.Q12 * dz), r.Q22 * dz * dz);
@@ -497,9 +517,7 @@ __global__ void __launch_bounds__(256, GSCT_VCHAIN_MINB) k_voxel_bwd_chain(const
         const float d1 = fmaf(4.f, Ap, d0);
         f2_t g = f2_pack(ex2_approx(e0), ex2_approx(e1));
         f2_t rr = f2_pack(ex2_approx(d0), ex2_approx(d1));
-        auto chunk = [&](const float* __restrict__ p, const f2_t* M, auto masked) {
-          float w[8];
-          ldg_v8(p, w);
+        auto chunk = [&](const float (&w)[8], const f2_t* M, auto masked) {
           f2_t W0 = f2_pack(w[0], w[1]), W1 = f2_pack(w[2], w[3]), W2 = f2_pack(w[4], w[5]),
                W3 = f2_pack(w[6], w[7]);
           if constexpr (decltype(masked)::value) {
@@ -527,10 +545,39 @@ __global__ void __launch_bounds__(256, GSCT_VCHAIN_MINB) k_voxel_bwd_chain(const
         };
         using yes = std::integral_constant<bool, true>;
         using no = std::integral_constant<bool, false>;
-        chunk(prow, MF, yes{});
+#if GSCT_VCHAIN_PIPE
+        // the next chunk's load is issued before the current chunk's arithmetic: two 32 B
+        // loads in flight per lane (the walk at 1024^3 is L2 / DRAM latency-bound)
+        float wa[8], wb[8];
+        ldg_v8(prow, wa);
+        if (nch > 1) ldg_v8(prow + 8, wb);
+        chunk(wa, MF, yes{});
+#pragma unroll 2
+        for (int j = 1; j < nch - 1; ++j) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) wa[k] = wb[k];
+          ldg_v8(prow + 8 * (j + 1), wb);
+          chunk(wa, nullptr, no{});
+        }
+        if (nch > 1) chunk(wb, ML, yes{});
+#else
+        {
+          float w[8];
+          ldg_v8(prow, w);
+          chunk(w, MF, yes{});
+        }
 #pragma unroll 1
-        for (int j = 1; j < nch - 1; ++j) chunk(prow + 8 * j, nullptr, no{});
-        if (nch > 1) chunk(prow + 8 * (nch - 1), ML, yes{});
+        for (int j = 1; j < nch - 1; ++j) {
+          float w[8];
+          ldg_v8(prow + 8 * j, w);
+          chunk(w, nullptr, no{});
+        }
+        if (nch > 1) {
+          float w[8];
+          ldg_v8(prow + 8 * (nch - 1), w);
+          chunk(w, ML, yes{});
+        }
+#endif
       } else {
         const f2_t A2 = f2_bc(Ap), BP2 = f2_bc(bp), CP2 = f2_bc(cp);
 #pragma unroll 1

@@ -69,7 +69,7 @@ def main() -> None:
         for _ in range(reps):
             step()
     else:
-        side, n = (512, 500_000) if cfg == "c3" else (128, 50_000)
+        side, n = {"c3": (512, 500_000), "c5": (1024, 1_000_000)}.get(cfg, (128, 50_000))
         cloud = gsct.make_cloud("shepp_logan", n, seed=1, side=side, spacing=1.0).to_device(0)
         region = gsct.GridRegion.covering(gsct.GridSpec.centered((side, side, side), 1.0))
         vol = torch.empty((side, side, side), dtype=torch.float32, device="cuda")
