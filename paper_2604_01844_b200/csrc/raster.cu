@@ -1218,11 +1218,15 @@ void launch_raster_fwd_super(const RasterRec* rec, const uint32_t* vals, const u
   // over all views of the launch (A/B C2: 2.25 ms; per 7-view groups that keep the records
   // L2-resident 2.49; none 2.52). Not for host-mapped images: there the kernel's PCIe stores
   // follow the schedule and scattered host writes cost more than the tail (C2 e2e 8.36 vs 7.87 ms)
+#ifndef GSCT_FWD_LPT_DEV_VG
+#define GSCT_FWD_LPT_DEV_VG 0  // > 0: device images scheduled longest-first within groups of this many views
+#endif
 #ifndef GSCT_FWD_LPT_HOST_VG
 #define GSCT_FWD_LPT_HOST_VG 0  // > 0: host-mapped images scheduled longest-first within groups of this many views
 #endif
   if (GSCT_FWD_LPT && sched_ws && (!bulk_out || GSCT_FWD_LPT_HOST_VG > 0)) {  // sched_ws: 2048 + 2 * items words
-    const int vg = bulk_out ? std::min(GSCT_FWD_LPT_HOST_VG, n_views) : n_views;
+    const int vg = bulk_out ? std::min(GSCT_FWD_LPT_HOST_VG, n_views)
+                            : (GSCT_FWD_LPT_DEV_VG > 0 ? std::min(GSCT_FWD_LPT_DEV_VG, n_views) : n_views);
     if ((n_views + vg - 1) / vg <= 64) {
       launch_fwd_schedule(start, end, n_views, n_stiles, key_stride, vg, sched_ws, st);
       sched = sched_ws + 2048 + items;
