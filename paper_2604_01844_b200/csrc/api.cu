@@ -1426,7 +1426,8 @@ void voxel_moments(gsct_ctx c, const Cloud& d, const VoxGrid& grid, const Window
   }
   {
     Phase ph(c, GSCT_PH_VOXEL_BWD);
-    launch_voxel_bwd_lanes(rec, order, n, win, static_cast<float>(grid.spacing), grad, mom, c->stream);
+    const double vps = static_cast<double>(grid.dims[0]) * grid.dims[1] * grid.dims[2] / static_cast<double>(n);
+    launch_voxel_bwd_lanes(rec, order, n, win, static_cast<float>(grid.spacing), grad, mom, c->stream, vps);
   }
   CK(cudaGetLastError());
 }

@@ -233,8 +233,10 @@ void launch_voxel_fwd(const VoxelRec* rec, const uint32_t* vals, const uint32_t*
 int voxel_bwd_vec(const Window& win, const float* grad_volume);
 int launch_voxel_lane_keys(const VoxelRec* rec, int64_t n, const Window& win, int vec, uint32_t* keys,
                            uint32_t* vals, cudaStream_t st);
+// voxels_per_splat: full-grid voxels / splats (stands in for the box size: lanes per splat)
 void launch_voxel_bwd_lanes(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
-                            float spacing, const float* grad_volume, float* moments, cudaStream_t st);
+                            float spacing, const float* grad_volume, float* moments, cudaStream_t st,
+                            double voxels_per_splat);
 // (loss.cu) fused L1 + SSIM2D image loss: coef = 3 * n_views * n_out fp32 scratch,
 // part_s / part_l1 = per-tile partials (image_loss_partials total), out3[3 * n_views] =
 // {l1, ssim loss, total} per view (device), grad = d total / d pred (fp32, device)

@@ -432,14 +432,15 @@ __device__ __forceinline__ float vox_q(const VoxelRec& r, float dx, float dy, fl
 #ifndef GSCT_VBWD_YLANES
 #define GSCT_VBWD_YLANES 1  // lanes interleave y-rows of a slice (A/B: 1024^3 25.5 -> 11.8 ms, 512^3 1.774 vs 1.786)
 #endif
+template <int LANES>
 __global__ void __launch_bounds__(256, GSCT_VCHAIN_MINB) k_voxel_bwd_chain(const VoxelRec* __restrict__ rec,
                                                                            const uint32_t* __restrict__ order,
                                                                            int64_t n, Window win, float sp,
                                                                            const float* __restrict__ grad,
                                                                            float* __restrict__ mom) {
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t t = tid / kVoxLanes;
-  const int q = static_cast<int>(tid % kVoxLanes);
+  const int64_t t = tid / LANES;
+  const int q = static_cast<int>(tid % LANES);
   const bool live = t < n;
   const int64_t i = live ? (order ? static_cast<int64_t>(__ldg(order + t)) : t) : 0;
   const VoxelRec r = rec[i];
@@ -496,9 +497,9 @@ __global__ void __launch_bounds__(256, GSCT_VCHAIN_MINB) k_voxel_bwd_chain(const
   for (int zz = 0; zz < (empty ? 0 : D); ++zz) {
     const float dz = fmaf(static_cast<float>(z0 + zz) - r.loz, sp, -r.offz);
     const float* __restrict__ prow = gz + static_cast<int64_t>(zz) * wy * wx + static_cast<int64_t>(q) * wx;
-    for (int yy = q; yy < H; yy += kVoxLanes, prow += kVoxLanes * wx) {
+    for (int yy = q; yy < H; yy += LANES, prow += LANES * wx) {
 #else
-  for (int zz = q; zz < (empty ? 0 : D); zz += kVoxLanes) {
+  for (int zz = q; zz < (empty ? 0 : D); zz += LANES) {
     const float dz = fmaf(static_cast<float>(z0 + zz) - r.loz, sp, -r.offz);
     const float* __restrict__ prow = gz + static_cast<int64_t>(zz) * wy * wx;
     for (int yy = 0; yy < H; ++yy, prow += wx) {
@@ -631,7 +632,7 @@ __global__ void __launch_bounds__(256, GSCT_VCHAIN_MINB) k_voxel_bwd_chain(const
 #pragma unroll
   for (int k = 0; k < 10; ++k) {
 #pragma unroll
-    for (int o = 1; o < kVoxLanes; o <<= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
+    for (int o = 1; o < LANES; o <<= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
   }
   if (live && !empty && q == 0) {
 #pragma unroll
@@ -723,14 +724,24 @@ int launch_voxel_lane_keys(const VoxelRec* rec, int64_t n, const Window& win, in
 }
 
 void launch_voxel_bwd_lanes(const VoxelRec* rec, const uint32_t* order, int64_t n, const Window& win,
-                            float spacing, const float* grad_volume, float* moments, cudaStream_t st) {
+                            float spacing, const float* grad_volume, float* moments, cudaStream_t st,
+                            double vps) {
   if (n == 0) return;
 #ifndef GSCT_VBWD_CHAIN
 #define GSCT_VBWD_CHAIN 1
 #endif
-  if (GSCT_VBWD_CHAIN && voxel_bwd_vec(win, grad_volume) == 8)
-    k_voxel_bwd_chain<<<blocks_for(n * kVoxLanes, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume,
-                                                                     moments);
+#ifndef GSCT_VBWD_WIDE_VPS
+#define GSCT_VBWD_WIDE_VPS 768  // grid voxels per splat above which 8 lanes share a splat
+#endif
+  // Large boxes (coarse clouds in big grids: 1024^3 / 1M splats ~ 1074 voxels per splat) walk
+  // faster with 8 lanes per splat (A/B: 10.9 vs 11.8 ms at 1024^3), small ones with 4 (512^3 /
+  // 500k ~ 268: 1.78 vs 1.90 ms); the full grid's voxels per splat stand in for the box size
+  // (a z-slab window of the same grid takes the same choice).
+  if (GSCT_VBWD_CHAIN && voxel_bwd_vec(win, grad_volume) == 8 && vps > GSCT_VBWD_WIDE_VPS)
+    k_voxel_bwd_chain<8><<<blocks_for(n * 8, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume, moments);
+  else if (GSCT_VBWD_CHAIN && voxel_bwd_vec(win, grad_volume) == 8)
+    k_voxel_bwd_chain<kVoxLanes><<<blocks_for(n * kVoxLanes, 256), 256, 0, st>>>(rec, order, n, win, spacing,
+                                                                                grad_volume, moments);
   else if (voxel_bwd_vec(win, grad_volume) == 8)
     k_voxel_bwd_lanes<8><<<blocks_for(n * kVoxLanes, 256), 256, 0, st>>>(rec, order, n, win, spacing, grad_volume,
                                                                         moments);
