@@ -46,6 +46,70 @@ __global__ void k_emit_brick_pairs(const VoxelRec* __restrict__ rec,
 
 
 
+// Warp-cooperative form of k_emit_brick_pairs: the 32 splats of a warp hold a contiguous run
+// of the pair array (offsets are the exclusive scan of the counts in splat order), so the
+// warp writes that run with coalesced stores -- pair p of the run goes to the lane whose
+// prefix covers p, decoded into its (bz, by, bx) in the same bz-by-bx order -- instead of
+// every lane storing its own run (32 scattered runs per store instruction).
+__global__ void __launch_bounds__(256) k_emit_brick_pairs_warp(const VoxelRec* __restrict__ rec,
+                                                               const uint32_t* __restrict__ offsets,
+                                                               const uint32_t* __restrict__ counts, int64_t n,
+                                                               Window win, int nbx, int nby,
+                                                               uint32_t* __restrict__ keys,
+                                                               uint32_t* __restrict__ vals) {
+  __shared__ int s_box[8][32][4];  // per warp, per lane: run start (in the warp's run), bx0, by0 | nx, bz0 | ny
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t c = 0;
+  int bx0 = 0, by0 = 0, bz0 = 0, nx = 1, ny = 1;
+  if (i < n) {
+    c = counts[i];
+    if (c) {
+      const VoxelRec r = rec[i];
+      // record boxes are grid-clipped; bin only the part inside the window
+      const int x0 = max(static_cast<int>(r.lox), win.lo[0]), x1 = min(static_cast<int>(r.hix), win.hi[0] - 1);
+      const int y0 = max(static_cast<int>(r.loy), win.lo[1]), y1 = min(static_cast<int>(r.hiy), win.hi[1] - 1);
+      const int z0 = max(static_cast<int>(r.loz), win.lo[2]);
+      bx0 = (x0 - win.lo[0]) / kBrick;
+      by0 = (y0 - win.lo[1]) / kBrick;
+      bz0 = (z0 - win.lo[2]) / kBrickZ;
+      nx = (x1 - win.lo[0]) / kBrick - bx0 + 1;
+      ny = (y1 - win.lo[1]) / kBrick - by0 + 1;
+    }
+  }
+  uint32_t ex = c;  // inclusive warp scan, then exclusive
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, ex, o);
+    if (lane >= o) ex += y;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, ex, 31);
+  ex -= c;
+  const uint32_t base = __shfl_sync(0xffffffffu, i < n ? offsets[i] : 0u, 0);
+  s_box[w][lane][0] = static_cast<int>(ex);
+  s_box[w][lane][1] = bx0;
+  s_box[w][lane][2] = by0 | (nx << 16);
+  s_box[w][lane][3] = bz0 | (ny << 16);
+  __syncwarp();
+  const int64_t i0 = i - lane;
+  for (uint32_t p = lane; p < total; p += 32) {
+    // owner: the last lane whose run starts at or before p (lanes with empty runs share
+    // their start with the next lane and are skipped by taking the last such lane)
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+      if (static_cast<uint32_t>(s_box[w][lo + step][0]) <= p) lo += step;
+    const int j = static_cast<int>(p - static_cast<uint32_t>(s_box[w][lo][0]));
+    const int b1 = s_box[w][lo][1], b2 = s_box[w][lo][2], b3 = s_box[w][lo][3];
+    const int onx = b2 >> 16, ony = b3 >> 16;
+    const int nxy = onx * ony;
+    const int bz = j / nxy, rem = j - bz * nxy;
+    const int by = rem / onx, bx = rem - by * onx;
+    keys[base + p] = static_cast<uint32_t>(((bz + (b3 & 0xFFFF)) * nby + by + (b2 & 0xFFFF)) * nbx + bx + b1);
+    vals[base + p] = static_cast<uint32_t>(i0 + lo);
+  }
+}
+
 __device__ __forceinline__ float vox_e(const VoxelRec& r, float dx, float dy, float dz) {
   // Q00 dx^2 + Q11 dy^2 + Q22 dz^2 + Q01 dx dy + Q02 dx dz + Q12 dy dz
   return fmaf(dx, fmaf(r.Q00, dx, fmaf(r.Q01, dy, r.Q02 * dz)), fmaf(dy, fmaf(r.Q11, dy, r.Q12 * dz), r.Q22 * dz * dz));
@@ -680,8 +744,13 @@ void launch_emit_brick_pairs(const VoxelRec* rec, const uint32_t* offsets, const
                              int64_t n, const Window& win, int nbx, int nby, uint32_t* keys,
                              uint32_t* vals, cudaStream_t st) {
   if (n == 0) return;
-  k_emit_brick_pairs<<<blocks_for(n, 256), 256, 0, st>>>(rec, offsets, counts, n, win, nbx, nby,
-                                                         keys, vals);
+#ifndef GSCT_VEMIT_WARP
+#define GSCT_VEMIT_WARP 1  // coalesced warp-cooperative brick-pair emission
+#endif
+  if (GSCT_VEMIT_WARP)
+    k_emit_brick_pairs_warp<<<blocks_for(n, 256), 256, 0, st>>>(rec, offsets, counts, n, win, nbx, nby, keys, vals);
+  else
+    k_emit_brick_pairs<<<blocks_for(n, 256), 256, 0, st>>>(rec, offsets, counts, n, win, nbx, nby, keys, vals);
   count_launch();
 }
 
