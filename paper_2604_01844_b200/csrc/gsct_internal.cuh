@@ -79,7 +79,13 @@ __device__ __forceinline__ bool raster_chain_safe(float A, float B, float C, flo
 #define GSCT_WALK_HSHIFT 2
 #endif
 #ifndef GSCT_WALK_BANDS
-#define GSCT_WALK_BANDS 8  // at most this many column bands per row
+#define GSCT_WALK_BANDS 64  // at most this many column bands per row
+#endif
+#ifndef GSCT_WALK_BAND_PX
+#define GSCT_WALK_BAND_PX 64  // column band width (pixels, power of two), detectors <= 512 wide
+#endif
+#ifndef GSCT_WALK_BAND_PX_WIDE
+#define GSCT_WALK_BAND_PX_WIDE 32  // ... wider detectors (their top rows are coarsened by the 2^25 cap)
 #endif
 struct WalkLayout {
   int shapes = 4 * GSCT_WALK_HCLASSES + 1;  // shape classes + the empty class

@@ -177,9 +177,12 @@ void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uin
 
 WalkLayout walk_layout(int n_views, int n_u, int n_v) {
   WalkLayout L;
-  // column bands: at most 8 per row (the top row must be exact for shared lines, the column
-  // can be coarse); rows exact while the bucket table stays <= 2^25 words
-  while (((n_u - 1) >> L.us) + 1 > GSCT_WALK_BANDS) ++L.us;
+  // column bands (the top row must be exact for shared lines, the column can be coarse); rows
+  // exact while the bucket table stays <= 2^25 words. Band width A/B (backward ms): 512^2
+  // 64 px 2.348 / 32 px 2.369 / 128 px 2.416; 1024^2 256 px (8 bands) 10.95 / 64 px 11.00 /
+  // 32 px 10.88; 2048^2 256 px 55.70 / 128 px 54.99 / 64 px 53.79 / 32 px 52.52
+  const int band_px = n_u > 512 ? GSCT_WALK_BAND_PX_WIDE : GSCT_WALK_BAND_PX;
+  while ((1 << L.us) < band_px || ((n_u - 1) >> L.us) + 1 > GSCT_WALK_BANDS) ++L.us;
   L.nu = ((n_u - 1) >> L.us) + 1;
   auto total = [&]() { return static_cast<int64_t>(n_views) * L.shapes * (((n_v - 1) >> L.vs) + 1) * L.nu; };
   while (total() > (int64_t(1) << 25) && L.vs < 16) ++L.vs;
