@@ -175,6 +175,11 @@ void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uin
   count_launch();
 }
 
+#ifndef GSCT_WALK_CAP_LOG2
+#define GSCT_WALK_CAP_LOG2 25  // bucket table of at most 2^this words (rows coarsened beyond; A/B
+                               // 2^26 / 2^27: C5 backward 52.8 / 53.2 ms vs 52.5, 1024^2 set-up +
+                               // order + backward within +-0.05 ms -- finer rows buy nothing)
+#endif
 WalkLayout walk_layout(int n_views, int n_u, int n_v) {
   WalkLayout L;
   // column bands (the top row must be exact for shared lines, the column can be coarse); rows
@@ -185,7 +190,7 @@ WalkLayout walk_layout(int n_views, int n_u, int n_v) {
   while ((1 << L.us) < band_px || ((n_u - 1) >> L.us) + 1 > GSCT_WALK_BANDS) ++L.us;
   L.nu = ((n_u - 1) >> L.us) + 1;
   auto total = [&]() { return static_cast<int64_t>(n_views) * L.shapes * (((n_v - 1) >> L.vs) + 1) * L.nu; };
-  while (total() > (int64_t(1) << 25) && L.vs < 16) ++L.vs;
+  while (total() > (int64_t(1) << GSCT_WALK_CAP_LOG2) && L.vs < 16) ++L.vs;
   L.nv = ((n_v - 1) >> L.vs) + 1;
   return L;
 }
