@@ -294,10 +294,15 @@ class GradPrebuild {
       const std::size_t n = n_;
       lk.unlock();
       ParamGradients g;
-      build_grads(g, n);
+      bool ok = true;
+      try {
+        build_grads(g, n);
+      } catch (...) {  // e.g. bad_alloc: the next take() builds inline and reports it there
+        ok = false;
+      }
       lk.lock();
-      next_ = std::move(g);
-      ready_ = true;
+      if (ok) next_ = std::move(g);
+      ready_ = ok;
       want_ = false;
       done_cv_.notify_all();
     }
