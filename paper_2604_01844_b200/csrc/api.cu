@@ -1149,11 +1149,15 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
 #ifndef GSCT_BWD_ONECHUNK
 #define GSCT_BWD_ONECHUNK 1  // the lane backward has no tile keys: chunk by the item budget only
 #endif
+#ifndef GSCT_BWD_L2_MB
+#define GSCT_BWD_L2_MB 96  // grad-image MB per walked view chunk (A/B C5: 48 / 64 / 96 / 128 / 192 MB
+                           // within 0.1%)
+#endif
     int chunk = views_per_chunk(n, n_views, GSCT_BWD_ONECHUNK ? 0 : static_cast<int64_t>(tiles_u) * tiles_v);
     {
       // keep one chunk's grad images L2-resident (126 MB L2): C2's 75 x 1 MB in one chunk,
       // C5's 16 MB images 6 at a time (A/B at C5: 8-view chunk 77.7 ms vs 4-view 74.2)
-      const int64_t l2_views = std::max<int64_t>(1, (int64_t(96) << 20) / (static_cast<int64_t>(npx) * 4));
+      const int64_t l2_views = std::max<int64_t>(1, (int64_t(GSCT_BWD_L2_MB) << 20) / (static_cast<int64_t>(npx) * 4));
       if (chunk > l2_views) {
         const int64_t nc = (n_views + l2_views - 1) / l2_views;
         chunk = static_cast<int>((n_views + nc - 1) / nc);
