@@ -332,12 +332,20 @@ def roofline_objects(peaks: dict, phase: str, kernel: str, ms_total: float, laun
             "launches_per_step": launches_per_step,
             "algorithmic_bytes_def": "SURVEY.md 8(d): 44 B params read + 49 B grads written (bwd) per (view, splat), "
                                      "4 B per pixel/voxel written (fwd) or read (bwd)",
-            "note": "compulsory HBM bytes are a few % of peak by design; the binding units are MUFU/FMA "
-                    "(roofline_sfu) -- see profiles/ for the pipe utilisation"}
+            "note": "compulsory HBM bytes are a few % of peak by design (neither path is bandwidth-bound); "
+                    "the binding unit is named in 'binding' from the committed ncu capture, the pair rate "
+                    "against the on-box MUFU / FFMA peaks is in roofline_sfu"}
     if meas:
         roof["ncu"] = {k: meas[k] for k in ("issue_active_pct", "fma_pipe_pct", "xu_pipe_pct", "l1tex_throughput_pct",
                                              "warps_active_pct", "duration_ms") if k in meas}
         roof["ncu"]["source"] = f"profiles/{ncu_tag}/summary.json"
+        util = {"L1TEX (data pipe / wavefronts)": meas.get("l1tex_throughput_pct"),
+                "FMA pipe": meas.get("fma_pipe_pct"), "issue": meas.get("issue_active_pct"),
+                "XU (MUFU)": meas.get("xu_pipe_pct")}
+        util = {k: v for k, v in util.items() if v is not None}
+        if util:
+            top = max(util, key=util.get)
+            roof["binding"] = {"unit": top, "pct_of_peak": round(util[top], 1), "source": roof["ncu"]["source"]}
     fma = FMA_PER_PAIR[phase]
     sfu = {"bound": "sfu_ex2", "kernel": kernel, "achieved": rate, "peak": peaks["ex2"],
            "unit": "splat-pairs/s (one exp per pair in the reference, projector.hpp:341,410 / voxelizer.hpp:184,242)",
