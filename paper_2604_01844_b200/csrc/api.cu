@@ -885,7 +885,14 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
                                      views_per_chunk(n_in, n_views, 0) >= n_views
                                  ? GSCT_CLOUD_PIECES
                                  : 1;
+    auto fwd_t = std::chrono::steady_clock::now();
+    auto fwd_mark = [&](int k) {
+      const auto t = std::chrono::steady_clock::now();
+      c->hio.ms_fwd[k] += std::chrono::duration<double, std::milli>(t - fwd_t).count();
+      fwd_t = t;
+    };
     const Cloud d = upload_cloud(c, cloud, c->stream, cloud_pieces == 1);
+    fwd_mark(0);
     std::vector<cudaEvent_t> piece_up;
     if (cloud_pieces > 1) {
       c->hio.invalidate_cloud();
@@ -995,6 +1002,7 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
       CK(cudaMemcpyAsync(hpairs.data(), dpairs, static_cast<size_t>(cv) * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
+      fwd_mark(1);
       const std::vector<int> cut = bin_ranges(hpairs.data(), cv);
       for (size_t bi = 0; bi + 1 < cut.size(); ++bi) {
         const int b0 = cut[bi], bv = cut[bi + 1] - cut[bi];  // views [v0 + b0, v0 + b0 + bv)
@@ -1060,7 +1068,10 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
         if (dual) stream_after(c, c->stream, c->aux_stream);
       }
     }
-    if (stage_images && n_views) stream_after(c, c->stream, c->copy_stream);    finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
+    if (stage_images && n_views) stream_after(c, c->stream, c->copy_stream);
+    fwd_mark(2);
+    finish_sync(c, stats, true, stats ? &stats->forward_ms : nullptr);
+    fwd_mark(3);
     if (saved) {
       c->saved_key = raster_call_key(cloud, geom, angles, n_views, rs);
       c->saved_valid = true;

@@ -165,6 +165,10 @@ HostIO::~HostIO() {
                    ms_replica, static_cast<long long>(n_replica), bytes_replica_up / 1e6,
                    static_cast<long long>(n_replica_dirty), ms_replica_dirty, ms_h2d, ms_copyout, ms_sync,
                    static_cast<long long>(n_api), ms_api);
+  if (const char* e = std::getenv("GSCT_HOSTIO_STATS"))
+    if (e[0] == '1')
+      std::fprintf(stderr, "hostio: forward calls: upload %.1f ms, set-up + count wait %.1f ms, bin + raster enqueue %.1f ms, "
+                           "sync + copy-out %.1f ms\n", ms_fwd[0], ms_fwd[1], ms_fwd[2], ms_fwd[3]);
   for (auto& b : blocks_) cudaFreeHost(b.p);
   if (shadow_) cudaFreeHost(shadow_);
   for (cudaEvent_t e : events_) cudaEventDestroy(e);

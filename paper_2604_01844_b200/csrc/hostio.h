@@ -40,6 +40,9 @@ class HostIO {
   // GSCT_HOSTIO_STATS=1: host-side milliseconds per activity, printed when the context dies
   double ms_replica = 0, ms_h2d = 0, ms_copyout = 0, ms_sync = 0, ms_api = 0, ms_replica_dirty = 0;
   int64_t n_replica = 0, bytes_replica_up = 0, n_api = 0, n_replica_dirty = 0;
+  // host-side split of the forward call (GSCT_HOSTIO_STATS): cloud upload, set-up enqueue +
+  // pair-count wait, binning + raster enqueue, final sync + copy-out
+  double ms_fwd[4] = {0, 0, 0, 0};
 
  private:
   void* stage(size_t bytes);
