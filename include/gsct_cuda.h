@@ -54,7 +54,10 @@ enum gsct_status {
   GSCT_ERR_PARSE = 4     /* maps to gsct::parse_error; the message ends "(byte offset N)" */
 };
 
-enum gsct_location { GSCT_HOST = 0, GSCT_DEVICE = 1 };
+/* GSCT_HOST_ZEROED (gradient outputs only): host buffers the caller has zero-filled, so a call
+ * whose gradients are sparse (gsct_voxelize_bwd over a sub-region: only the splats whose box
+ * meets it have entries) transfers and writes only those splats' rows; elsewhere = GSCT_HOST. */
+enum gsct_location { GSCT_HOST = 0, GSCT_DEVICE = 1, GSCT_HOST_ZEROED = 2 };
 
 typedef struct gsct_ctx_s* gsct_ctx;
 typedef struct gsct_group_s* gsct_group;

@@ -227,9 +227,14 @@ inline gsct_stats put_stats(const RenderStats* stats) {
   return s;
 }
 
-// every element is overwritten by the call: default-insert (no ParamGradients::resize
-// zero pass over the 96 B/splat; Eigen's fixed-size vectors are left uninitialised)
-inline void build_grads(ParamGradients& g, std::size_t n) {
+// zero = false: every element is overwritten by the call, so default-insert (no
+// ParamGradients::resize zero pass; Eigen's fixed-size vectors are left uninitialised);
+// zero = true: zero-filled, for calls that write only the rows they touch (GSCT_HOST_ZEROED)
+inline void build_grads(ParamGradients& g, std::size_t n, bool zero) {
+  if (zero) {
+    g.resize(n);
+    return;
+  }
   g.positions.resize(n);
   g.log_scales.resize(n);
   g.rotations.resize(n);
@@ -250,10 +255,11 @@ class GradPrebuild {
     static thread_local GradPrebuild p;
     return p;
   }
-  ParamGradients take(std::size_t n) {
+  // zero: the caller needs zero-filled containers (the prebuilt ones always are)
+  ParamGradients take(std::size_t n, bool zero) {
     ParamGradients g;
     if (!enabled_) {
-      build_grads(g, n);
+      build_grads(g, n, zero);
       return g;
     }
     std::unique_lock<std::mutex> lk(mu_);
@@ -263,7 +269,7 @@ class GradPrebuild {
       g = std::move(next_);
     } else {
       lk.unlock();
-      build_grads(g, n);
+      build_grads(g, n, zero);
       lk.lock();
     }
     ready_ = false;
@@ -296,7 +302,7 @@ class GradPrebuild {
       ParamGradients g;
       bool ok = true;
       try {
-        build_grads(g, n);
+        build_grads(g, n, true);  // off the critical path: zero-filled, usable by every call
       } catch (...) {  // e.g. bad_alloc: the next take() builds inline and reports it there
         ok = false;
       }
@@ -318,14 +324,16 @@ class GradPrebuild {
 struct GradBuffers {
   ParamGradients g;
   gsct_grads c;
-  explicit GradBuffers(std::size_t n) : g(GradPrebuild::get().take(n)) {
+  // sparse = true: zero-filled containers, so a sparse call (voxelize_backward of a sub-region)
+  // brings down and writes only the rows of the splats it touched
+  explicit GradBuffers(std::size_t n, bool sparse = false) : g(GradPrebuild::get().take(n, sparse)) {
     c.pos = reinterpret_cast<double*>(g.positions.data());
     c.log_scale = reinterpret_cast<double*>(g.log_scales.data());
     c.quat = reinterpret_cast<double*>(g.rotations.data());
     c.raw_density = g.raw_densities.data();
     c.pos_grad_norm = g.pos_grad_norm.data();
     c.visible = g.visible.data();
-    c.location = GSCT_HOST;
+    c.location = sparse ? GSCT_HOST_ZEROED : GSCT_HOST;
   }
 };
 
@@ -439,7 +447,7 @@ inline ParamGradients voxelize_backward(const GaussianCloud& cloud, const GridRe
   const gsct_voxel_settings vs = detail::c_voxel(settings);
   std::vector<float> gv(grad_volume.values.size());
   gsct_host_f64_to_f32(grad_volume.values.data(), gv.data(), static_cast<int64_t>(gv.size()));
-  detail::GradBuffers gb(cloud.size());
+  detail::GradBuffers gb(cloud.size(), /*sparse=*/true);
   gsct_stats st = detail::put_stats(stats);
   detail::call_api(c, [&] { return gsct_voxelize_bwd(c, &cc, &g, nullptr, &vs, gv.data(), GSCT_HOST, &gb.c,
                                              stats ? &st : nullptr); });

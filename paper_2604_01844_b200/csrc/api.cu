@@ -29,7 +29,7 @@ enum Slot {
   S_POS, S_LS, S_Q, S_RAW, S_FRAMES, S_REC, S_COUNT, S_OFFSET, S_KEYS, S_VALS, S_KEYS2, S_VALS2,
   S_CUB, S_START, S_END, S_IMAGES, S_GRADIMG, S_MOMENTS, S_GPOS, S_GLS, S_GQ, S_GRAW, S_GPGN,
   S_GVIS, S_VREC, S_VOLUME, S_GRADVOL, S_DBG0, S_DBG1, S_DBG2, S_DBG3, S_DBG4, S_PRE, S_PRE_AOS, S_ACC, S_SAVED, S_LOSS_IN, S_LOSS_TGT, S_LOSS_GRAD, S_LOSS_COEF, S_LOSS_PART, S_ADAM_SKIP, S_VLOSS_SCR, S_CTRL, S_CTRL_RNG, S_FGSC, S_FGSC_LOG, S_FGSC_CNT, S_VTCOUNT,
-  S_TOTAL64, S_VIEWPAIRS, S_WCOUNT, S_WSLOT, S_WSUMS, S_WSTART, S_MOMENTS64, S_BSUMS, S_FSCHED,
+  S_TOTAL64, S_VIEWPAIRS, S_WCOUNT, S_WSLOT, S_WSUMS, S_WSTART, S_MOMENTS64, S_BSUMS, S_FSCHED, S_GFLAG, S_GPOSN, S_GSUMS, S_GROWS, S_GIDX, S_GCNT,
   S_COUNT_SLOTS
 };
 
@@ -283,6 +283,15 @@ RSet make_rs(const gsct_raster_settings* r) {
 // host cloud in synchronous mode is kept as a device replica refreshed chunk-wise
 // (hostio.cu), whatever `copy` says.
 Cloud upload_cloud(gsct_ctx c, const gsct_cloud* cl, cudaStream_t st = nullptr, bool copy = true);
+
+// GSCT_HOST_ZEROED outputs have host semantics; *zeroed tells a sparse-capable call that the
+// caller's buffers are already zero-filled
+gsct_grads host_norm(const gsct_grads* g, bool* zeroed) {
+  gsct_grads o = *g;
+  *zeroed = o.location == GSCT_HOST_ZEROED;
+  if (*zeroed) o.location = GSCT_HOST;
+  return o;
+}
 
 bool replica_applies(gsct_ctx c, const gsct_cloud* cl) {
   return !c->async && cl->location == GSCT_HOST && cl->n > 0 && host_pageable(cl->pos) &&
@@ -1091,6 +1100,9 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     contract(rs->tile_size >= 1, "bin_tiles: tile size must be at least 1");
     contract(out != nullptr, "rasterize_backward: null gradient output");
     contract(grad_images != nullptr || n_views == 0, "rasterize_backward: grad image dims must match detector");
+    bool zeroed = false;  // dense output: written in full either way
+    gsct_grads out_n = host_norm(out, &zeroed);
+    out = &out_n;
     if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
     reset_stats(c);
     // reuse the forward's set-up (PreSplat + records) when save-for-backward matched; then
@@ -1459,6 +1471,55 @@ GradPtrs grad_targets(gsct_ctx c, gsct_grads* out, size_t un) {
   return GradPtrs{out->pos, out->log_scale, out->quat, out->raw_density, out->pos_grad_norm, out->visible};
 }
 
+// Sparse transfer of the gradients (zero-filled host outputs): rows of the splats that are
+// visible or have a non-zero entry, compacted on the device in splat order, brought down
+// and scattered into the caller's arrays after the call's sync (scatter_sparse_grads).
+struct SparseGrads {
+  std::vector<double> rows;  // 13 per row
+  std::vector<uint32_t> idx;
+};
+void stage_sparse_grads(gsct_ctx c, const GradPtrs& p, size_t un, SparseGrads& sg) {
+  if (un == 0) return;
+  const int64_t n = static_cast<int64_t>(un);
+  uint32_t* flag = ws<uint32_t>(c, S_GFLAG, un);
+  uint32_t* pos = ws<uint32_t>(c, S_GPOSN, un);
+  uint32_t* sums = ws<uint32_t>(c, S_GSUMS, static_cast<size_t>(scan_workspace_u32(n)));
+  double* rows = ws<double>(c, S_GROWS, un * 13);
+  uint32_t* idx = ws<uint32_t>(c, S_GIDX, un);
+  uint32_t* cnt = ws<uint32_t>(c, S_GCNT, 1);
+  launch_grad_row_flags(p.gp, p.gl, p.gq, p.gr, p.gn, p.gv, n, flag, c->stream);
+  launch_exclusive_scan_u32(flag, pos, n, sums, c->stream);
+  launch_grad_rows(p.gp, p.gl, p.gq, p.gr, p.gn, p.gv, n, flag, pos, rows, idx, cnt, c->stream);
+  CK(cudaMemcpyAsync(c->hscratch, cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  uint32_t m = 0;
+  std::memcpy(&m, c->hscratch, sizeof m);
+  sg.rows.resize(static_cast<size_t>(m) * 13);
+  sg.idx.resize(m);
+  if (m == 0) return;
+  d2h(c, sg.rows.data(), rows, sg.rows.size() * sizeof(double), c->stream);
+  d2h(c, sg.idx.data(), idx, sg.idx.size() * sizeof(uint32_t), c->stream);
+}
+void scatter_sparse_grads(const SparseGrads& sg, gsct_grads* out) {
+  const int64_t m = static_cast<int64_t>(sg.idx.size());
+  constexpr int64_t kRows = 4096;
+  host_parallel_for((m + kRows - 1) / kRows, [&](int64_t t) {
+    const int64_t a = t * kRows, b = std::min(m, a + kRows);
+    for (int64_t r = a; r < b; ++r) {
+      const int64_t i = sg.idx[static_cast<size_t>(r)];
+      const double* o = sg.rows.data() + r * 13;
+      for (int k = 0; k < 3; ++k) {
+        out->pos[3 * i + k] = o[k];
+        out->log_scale[3 * i + k] = o[3 + k];
+      }
+      for (int k = 0; k < 4; ++k) out->quat[4 * i + k] = o[6 + k];
+      out->raw_density[i] = o[10];
+      out->pos_grad_norm[i] = o[11];
+      out->visible[i] = o[12] != 0.0 ? 1 : 0;
+    }
+  });
+}
+
 void grads_to_host(gsct_ctx c, gsct_grads* out, const GradPtrs& p, size_t un) {
   if (out->location != GSCT_HOST || un == 0) return;
   d2h(c, out->pos, p.gp, 3 * un * sizeof(double), c->stream);
@@ -1605,6 +1666,9 @@ int gsct_voxelize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
     contract(vs != nullptr, "VoxelSettings: null");
     contract(out != nullptr, "voxelize_backward: null gradient output");
     contract(grad_volume != nullptr, "voxelize_backward: grad dims must match region");
+    bool zeroed = false;
+    gsct_grads out_n = host_norm(out, &zeroed);
+    out = &out_n;
     if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
     reset_stats(c);
     const Cloud d = upload_cloud(c, cloud);
@@ -1621,6 +1685,13 @@ int gsct_voxelize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_grid* grid
                           c->stream);
     }
     CK(cudaGetLastError());
+    if (zeroed && !c->async && out->location == GSCT_HOST) {  // sparse rows into the zero-filled buffers
+      SparseGrads sg;
+      stage_sparse_grads(c, p, un, sg);
+      finish_sync(c, stats, false, stats ? &stats->backward_ms : nullptr);
+      scatter_sparse_grads(sg, out);
+      return;
+    }
     grads_to_host(c, out, p, un);
     finish_sync(c, stats, false, stats ? &stats->backward_ms : nullptr);
   });
@@ -1649,6 +1720,9 @@ int gsct_voxelize_bwd_finish(gsct_ctx c, const gsct_cloud* cloud, const gsct_gri
   return run(c, [&] {
     const VoxGrid vg = make_grid(grid);
     contract(vs != nullptr && moments_dev != nullptr && out != nullptr, "voxelize_backward: null buffer");
+    bool zeroed = false;
+    gsct_grads out_n = host_norm(out, &zeroed);
+    out = &out_n;
     reset_stats(c);
     const Cloud d = upload_cloud(c, cloud);
     const size_t un = static_cast<size_t>(d.n);

@@ -180,6 +180,12 @@ void launch_voxel_tail(const Cloud& c, const VoxGrid& grid, double tau_cut, doub
                        cudaStream_t st);
 // b[i] = (double)a[i]
 void launch_widen_f32(const float* a, double* b, int64_t n, cudaStream_t st);
+// sparse gradient rows (GSCT_HOST_ZEROED outputs)
+void launch_grad_row_flags(const double* gp, const double* gl, const double* gq, const double* gr, const double* gn,
+                           const uint8_t* gv, int64_t n, uint32_t* flag, cudaStream_t st);
+void launch_grad_rows(const double* gp, const double* gl, const double* gq, const double* gr, const double* gn,
+                      const uint8_t* gv, int64_t n, const uint32_t* flag, const uint32_t* pos, double* rows,
+                      uint32_t* idx, uint32_t* count, cudaStream_t st);  // rows: 13 doubles
 
 void launch_emit_tile_pairs(const RasterRec* rec, const uint32_t* offsets,
                             const uint32_t* counts, int64_t n, int n_views, int ts, int tiles_u,

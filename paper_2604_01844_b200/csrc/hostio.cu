@@ -140,6 +140,8 @@ void parallel_copy(void* dst, const void* src, size_t bytes) {
 
 }  // namespace
 
+void host_parallel_for(int64_t n_tasks, const std::function<void(int64_t)>& fn) { Pool::get().run(n_tasks, fn); }
+
 bool host_pageable(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a{};

@@ -4,12 +4,15 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 namespace gsct_dev {
 
 // true when p is ordinary (pageable) host memory, not page-locked / device memory
 bool host_pageable(const void* p);
+// fn(k) for k in [0, n_tasks) on the process-wide host worker pool (the caller helps)
+void host_parallel_for(int64_t n_tasks, const std::function<void(int64_t)>& fn);
 
 struct CloudArrays {
   const void* p[4];  // pos, log_scale, quat, raw_density

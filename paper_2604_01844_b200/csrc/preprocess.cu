@@ -379,6 +379,61 @@ __global__ void k_widen_f32(const float* __restrict__ a, double* __restrict__ b,
   if (i < n) b[i] = static_cast<double>(a[i]);
 }
 
+// Sparse gradient rows (GSCT_HOST_ZEROED): a splat's row is kept when it is visible or has
+// any non-zero entry (so the zero-filled host buffers end up equal to the dense output).
+__global__ void k_grad_row_flags(const double* __restrict__ gp, const double* __restrict__ gl,
+                                 const double* __restrict__ gq, const double* __restrict__ gr,
+                                 const double* __restrict__ gn, const uint8_t* __restrict__ gv, int64_t n,
+                                 uint32_t* __restrict__ flag) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool keep = gv[i] != 0 || gr[i] != 0.0 || gn[i] != 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) keep = keep || gp[3 * i + k] != 0.0 || gl[3 * i + k] != 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) keep = keep || gq[4 * i + k] != 0.0;
+  flag[i] = keep ? 1u : 0u;
+}
+// rows[r] = {pos 3, log_scale 3, quat 4, raw, pos_grad_norm, visible}, idx[r] = splat (ascending)
+__global__ void k_grad_rows(const double* __restrict__ gp, const double* __restrict__ gl,
+                            const double* __restrict__ gq, const double* __restrict__ gr,
+                            const double* __restrict__ gn, const uint8_t* __restrict__ gv, int64_t n,
+                            const uint32_t* __restrict__ flag,
+                            const uint32_t* __restrict__ pos, double* __restrict__ rows, uint32_t* __restrict__ idx,
+                            uint32_t* __restrict__ count) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == n - 1) *count = pos[i] + flag[i];
+  if (!flag[i]) return;
+  const uint32_t r = pos[i];
+  double* o = rows + static_cast<int64_t>(r) * 13;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    o[k] = gp[3 * i + k];
+    o[3 + k] = gl[3 * i + k];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) o[6 + k] = gq[4 * i + k];
+  o[10] = gr[i];
+  o[11] = gn[i];
+  o[12] = gv[i] ? 1.0 : 0.0;
+  idx[r] = static_cast<uint32_t>(i);
+}
+
+void launch_grad_row_flags(const double* gp, const double* gl, const double* gq, const double* gr, const double* gn,
+                           const uint8_t* gv, int64_t n, uint32_t* flag, cudaStream_t st) {
+  if (n <= 0) return;
+  k_grad_row_flags<<<blocks_for(n, 256), 256, 0, st>>>(gp, gl, gq, gr, gn, gv, n, flag);
+  count_launch();
+}
+void launch_grad_rows(const double* gp, const double* gl, const double* gq, const double* gr, const double* gn,
+                      const uint8_t* gv, int64_t n, const uint32_t* flag, const uint32_t* pos, double* rows,
+                      uint32_t* idx, uint32_t* count, cudaStream_t st) {
+  if (n <= 0) return;
+  k_grad_rows<<<blocks_for(n, 256), 256, 0, st>>>(gp, gl, gq, gr, gn, gv, n, flag, pos, rows, idx, count);
+  count_launch();
+}
+
 void launch_widen_f32(const float* a, double* b, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   k_widen_f32<<<blocks_for(n, 256), 256, 0, st>>>(a, b, n);

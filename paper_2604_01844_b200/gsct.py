@@ -33,7 +33,7 @@ GSCT_OK, GSCT_ERR_CONTRACT, GSCT_ERR_CUDA, GSCT_ERR_OOM, GSCT_ERR_PARSE = 0, 1, 
 # enum gsct_phase (include/gsct_cuda.h)
 PHASES = ("raster_setup", "raster_bin", "raster_fwd", "raster_bwd", "raster_tail",
           "voxel_setup", "voxel_bin", "voxel_fwd", "voxel_bwd", "voxel_tail", "raster_order")
-GSCT_HOST, GSCT_DEVICE = 0, 1
+GSCT_HOST, GSCT_DEVICE, GSCT_HOST_ZEROED = 0, 1, 2
 
 
 class GsctError(RuntimeError):
@@ -439,11 +439,12 @@ class ParamGradients:
         self.pos_grad_norm = self.pos_grad_norm + other.pos_grad_norm
         self.visible = self.visible | other.visible
 
-    def _c(self) -> c_grads:
+    def _c(self, zeroed: bool = False) -> c_grads:
+        """zeroed: host arrays known to be zero-filled (GSCT_HOST_ZEROED: sparse outputs may skip rows)."""
         arrs = [self.positions, self.log_scales, self.rotations, self.raw_densities, self.pos_grad_norm, self.visible]
         if _is_torch(self.positions):
             return c_grads(*[a.data_ptr() for a in arrs], GSCT_DEVICE)
-        return c_grads(*[a.ctypes.data if a.size else None for a in arrs], GSCT_HOST)
+        return c_grads(*[a.ctypes.data if a.size else None for a in arrs], GSCT_HOST_ZEROED if zeroed else GSCT_HOST)
 
 
 # ---------------------------------------------------------------------------------------
@@ -747,9 +748,10 @@ def voxelize_backward(cloud: GaussianCloud, region, grad_volume, settings: Voxel
     else:
         grad_volume = np.ascontiguousarray(grad_volume, dtype=np.float32)
     gptr, gloc = _ptr(grad_volume, keep)
+    fresh = out is None  # zero-filled here: the library may transfer only the touched splats' rows
     if out is None:
         out = ParamGradients.zeros(cloud.size(), cloud.positions.device.index if cloud.on_device else None)
-    cg = out._c()
+    cg = out._c(zeroed=fresh)
     s = stats._c() if stats is not None else c_stats()
     gr = _grid_c(region)
     vs = settings.c()

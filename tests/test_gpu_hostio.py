@@ -67,3 +67,23 @@ def test_pageable_cloud_replica_new_arrays_and_sizes(ctx):
         a = gsct.rasterize_views(cloud, geom, None, ctx=ctx)
         b = gsct.rasterize_views(cloud.to_device(0), geom, None, ctx=ctx).cpu().numpy()
         assert np.array_equal(a, b), (seed, n)
+
+
+def test_sparse_voxel_gradients_into_zero_filled_host_buffers(ctx):
+    """GSCT_HOST_ZEROED: voxelize_backward of a 32^3 sub-region (the training loop's TV term)
+    brings down only the touched splats' rows; the zero-filled host output must equal the
+    dense host output and the device-resident result bit for bit (every splat, visible flags
+    included), also for a region no splat touches and for the full grid."""
+    cloud = gsct.make_cloud("shepp_logan", 40_000, seed=3, side=128, spacing=1.0)
+    grid = gsct.GridSpec.centered((128, 128, 128), 1.0)
+    dcloud = cloud.to_device(0)
+    rng = np.random.default_rng(5)
+    for region in (gsct.GridRegion.of_parent(grid, (40, 50, 60), (32, 32, 32)),
+                   gsct.GridRegion.of_parent(grid, (0, 0, 0), (4, 4, 4)),
+                   gsct.GridRegion.covering(grid)):
+        gv = rng.uniform(-1, 1, size=(region.dims[2], region.dims[1], region.dims[0])).astype(np.float32)
+        sparse = gsct.voxelize_backward(cloud, region, gv, ctx=ctx)  # library-allocated zeros: sparse rows
+        dense = gsct.voxelize_backward(cloud, region, gv, out=gsct.ParamGradients.zeros(cloud.size()), ctx=ctx)
+        dev = gsct.voxelize_backward(dcloud, region, gv, ctx=ctx)
+        _same_grads(sparse, dense)
+        _same_grads(sparse, dev)
