@@ -44,15 +44,16 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 
 
 def build_variant(tag: str, defines: list[str]) -> Path:
-    """Builds build/variants/libgsct_<tag>.so with extra -D flags (A/B experiments; the
-    product library is always the default build)."""
+    """Builds build/variants/libgsct_<tag>.so with extra -D flags (entries starting with '-'
+    are passed to nvcc as they are; A/B experiments -- the product library is always the
+    default build)."""
     vdir = ROOT / "build" / "variants" / tag
     vdir.mkdir(parents=True, exist_ok=True)
     jobs, objs = [], []
     for src in CU_SOURCES:
         o = vdir / (src + ".o")
         objs.append(o)
-        jobs.append(([NVCC] + NVFLAGS + PER_FILE.get(src, []) + [f"-D{d}" for d in defines] +
+        jobs.append(([NVCC] + NVFLAGS + PER_FILE.get(src, []) + [d if d.startswith("-") else f"-D{d}" for d in defines] +
                      ["-c", str(CSRC / src), "-o", str(o)], vdir / (src + ".log")))
     for src in CXX_SOURCES:
         o = vdir / (src + ".o")
