@@ -233,3 +233,25 @@ def test_c4_three_views(ctx, ref):
             assert all(e <= TOL for e in errs.values()), (v, errs)
     finally:
         ref.free_cloud(h)
+
+
+@pytest.mark.parametrize("det,n,bounding,dilate", [(600, 5000, "square_circumscribed", False),
+                                                   (256, 20000, "rect_density_aware", True)])
+def test_parallel_beam_bins_images_gradients(ctx, ref, orc, det, n, bounding, dilate):
+    """Parallel-beam geometry through the packed binning the forward ships (wide layout at
+    600^2 with > 256 super-tiles, narrow at 256^2, n >= 4096), with square bounding /
+    no dilation: lists bit-exact vs bin_tiles, images and gradients vs the oracle."""
+    cloud = gsct.make_cloud("random", n, seed=9, pos_range=30.0, scale_lo=0.3, scale_hi=2.0)
+    geom = gsct.ScanGeometry("parallel", det, det, 0.12, 0.12, [0.2, 1.7, 4.1], 0.0, 0.0)
+    rs = gsct.RasterSettings(bounding=bounding, dilate=dilate)
+    views = [0, 1, 2]
+    _check_bins(ref, cloud, geom, views, rs=rs, ctx=ctx)
+    imgs = gsct.rasterize_views(cloud, geom, views, rs, ctx=ctx)
+    gi = np.random.default_rng(4).uniform(-1, 1, size=imgs.shape).astype(np.float32)
+    g = gsct.rasterize_backward_views(cloud, geom, [1], gi[1:2], rs, ctx=ctx)
+    for v in views:
+        rimg, _ = orc.rasterize_view(cloud, geom, v, rs)
+        assert max_err_rel_peak(imgs[v], rimg) <= TOL
+    r = orc.rasterize_backward(cloud, geom, 1, gi[1].astype(np.float64), rs)
+    errs = grad_class_errors(g, r)
+    assert all(e <= TOL for e in errs.values()), errs
