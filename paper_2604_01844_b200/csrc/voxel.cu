@@ -133,6 +133,9 @@ struct __align__(16) StagedVox {
 // fp32 under/overflow anywhere in the brick window) falling back to direct exp2; the rows
 // holding an exactly-on-lattice centre also use the direct path so the peak voxel is
 // rho * exp2(0) = rho exactly (test_voxelizer.cpp:16-22).
+#ifndef GSCT_VFWD_PACK
+#define GSCT_VFWD_PACK 1  // staged record fields ordered so the walk loads 56 of its 64 bytes
+#endif
 #ifndef GSCT_VFWD_PLAIN_BATCH
 #define GSCT_VFWD_PLAIN_BATCH 1
 #endif
@@ -216,8 +219,14 @@ __global__ void __launch_bounds__(128, GSCT_VFWD_MINB) k_voxel_fwd2(const VoxelR
       }
       s.p = make_float4(dxb, dyb, fgz, r.rho);
       s.q = make_float4(r.Q00, r.Q11, r.Q22, r.Q01);
+#if GSCT_VFWD_PACK
+      // the walk reads p, q, r and the first half of m (masks, peak): 56 of the 64 bytes
+      s.r = make_float4(r.Q02, r.Q12, ex2_approx(c2e), r.offz);
+      s.m = make_uint4(xm | (ym << 8) | (zm << 16), peak, safe ? 1u : 0u, lanes_rel);
+#else
       s.r = make_float4(r.Q02, r.Q12, ex2_approx(c2e), safe ? 1.f : 0.f);
       s.m = make_uint4(xm | (ym << 8) | (zm << 16), lanes_rel, peak, __float_as_uint(r.offz));
+#endif
       sw[lane] = s;
       my_plain = safe && peak == 0xFFFFFFFFu;
     }
@@ -232,13 +241,23 @@ __global__ void __launch_bounds__(128, GSCT_VFWD_MINB) k_voxel_fwd2(const VoxelR
       const float4 p = sw[j].p;
       const float4 q = sw[j].q;
       const float4 rr4 = sw[j].r;
+#if GSCT_VFWD_PACK
+      const uint2 m = *reinterpret_cast<const uint2*>(&sw[j].m);  // masks, peak lane
+      const float offz = rr4.w;
+#else
       const uint4 m = sw[j].m;
+      const float offz = __uint_as_float(m.w);
+#endif
       const uint32_t xm = m.x & 0xFFu;
       const uint32_t rows = (m.x >> (8 + 2 * yp)) & 3u;
       const f2_t RHO = f2_pack((rows & 1u) ? p.w : 0.f, (rows & 2u) ? p.w : 0.f);
       const float dy0 = p.y + fy, dx0 = p.x;
       const f2_t DY = f2_pack(dy0, dy0 + sp);
+#if GSCT_VFWD_PACK
+      const bool direct = !decltype(plain)::value && (sw[j].m.z == 0u || m.y == static_cast<uint32_t>(lane));
+#else
       const bool direct = !decltype(plain)::value && (rr4.w == 0.f || m.z == static_cast<uint32_t>(lane));
+#endif
       // the exponent / chain arithmetic stays in inline-asm packed ops (never contracted, so a
       // voxel's value does not depend on which lane or unrolled z step computes it: z-slab
       // windows stay bit-identical); only the accumulation uses the __fadd2_rn builtin, which
@@ -252,7 +271,7 @@ __global__ void __launch_bounds__(128, GSCT_VFWD_MINB) k_voxel_fwd2(const VoxelR
 #pragma unroll
       for (int zz = 0; zz < 2; ++zz) {
         if (!((m.x >> (16 + 2 * zp + zz)) & 1u)) continue;
-        const float dz = fmaf(p.z + static_cast<float>(2 * zp + zz), sp, -__uint_as_float(m.w));
+        const float dz = fmaf(p.z + static_cast<float>(2 * zp + zz), sp, -offz);
         // e(dx) = Q00 dx^2 + L dx + K,  L = Q01 dy + Q02 dz,  K = Q11 dy^2 + Q12 dy dz + Q22 dz^2
         const f2_t L = f2_fma(f2_bc(q.w), DY, f2_bc(rr4.x * dz));
         const f2_t K = f2_fma(DY, f2_fma(f2_bc(q.y), DY, f2_bc(rr4.y * dz)), f2_bc(q.z * dz * dz));
