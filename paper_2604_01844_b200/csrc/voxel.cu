@@ -140,7 +140,8 @@ struct __align__(16) StagedVox {
 #define GSCT_VFWD_PLAIN_BATCH 1
 #endif
 #ifndef GSCT_VFWD_MINB
-#define GSCT_VFWD_MINB 6  // 80 registers, 6 CTAs/SM (A/B 512^3: 5 CTAs 1.011 ms, 6 0.976, 7 1.001, 8 1.096)
+#define GSCT_VFWD_MINB 7  // 72 registers, 7 CTAs/SM (A/B 512^3 before the packed staging: 5 CTAs 1.011 ms,
+                          // 6 0.976, 7 1.001, 8 1.096; with it: 6 0.945, 7 0.936 -- 1024^3 5.67 / 5.61)
 #endif
 #ifndef GSCT_VFWD_UNROLL
 #define GSCT_VFWD_UNROLL 1  // (2: 0.985 ms with 6 CTAs)
