@@ -885,8 +885,9 @@ int gsct_rasterize_fwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (!c->async) CK(cudaEventRecord(c->ev0, c->stream));
     reset_stats(c);
 #ifndef GSCT_CLOUD_PIECES
-#define GSCT_CLOUD_PIECES 4  // host cloud uploaded in splat ranges, each range's set-up starting
-                             // as soon as its bytes are in (single view chunk only)
+#define GSCT_CLOUD_PIECES 2  // host cloud uploaded in splat ranges, each range's set-up starting
+                             // as soon as its bytes are in (single view chunk only; A/B C2 e2e:
+                             // 1 / 2 / 3 / 4 / 8 pieces -> 7.63 / 7.55 / 7.63 / 7.74 / 7.82 ms)
 #endif
     const int64_t n_in = cloud ? cloud->n : 0;
     const int cloud_pieces = cloud && cloud->location == GSCT_HOST && !replica_applies(c, cloud) && n_in >= 16384 &&
@@ -1193,7 +1194,8 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
 #define GSCT_BWD_GROW 1
 #endif
 #ifndef GSCT_BWD_GROW_X10
-#define GSCT_BWD_GROW_X10 14  // next chunk = 1.4 x the views so far
+#define GSCT_BWD_GROW_X10 12  // next chunk = 1.2 x the views so far (A/B C2 e2e with the other two
+                              // pipelining knobs: 1.1 / 1.2 / 1.4 / 1.7 -> 7.58 / 7.55 / 7.74 / 7.89 ms)
 #endif
     std::vector<int> cb{0};
 #ifndef GSCT_BWD_HOST_CHUNKS
@@ -1314,9 +1316,10 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     }
     if (one_sort && GSCT_BWD_DUAL) stream_after(c, c->stream, c->aux_stream);
 #ifndef GSCT_TAIL_PIECES
-#define GSCT_TAIL_PIECES 6  // staged host gradients: tail + finalize in splat ranges, each range's
+#define GSCT_TAIL_PIECES 8  // staged host gradients: tail + finalize in splat ranges, each range's
                             // D2H overlapping the next range's tail (A/B e2e with two streams: 2 / 4 / 6
-                            // pieces 8.85 / 8.69 / 8.63 ms)
+                            // pieces 8.85 / 8.69 / 8.63 ms; current kernels 2 / 6 / 8: 7.98 / 7.74 / 7.74,
+                            // with 2 cloud pieces and 1.2x chunk growth 6 / 8: 7.57 / 7.54)
 #endif
     const bool stage_grads = out->location == GSCT_HOST && n > 0 && !zc_grads;
     const int pieces = (stage_grads || zc_grads) && n_views > 0 && n >= 4096 ? GSCT_TAIL_PIECES : 1;
