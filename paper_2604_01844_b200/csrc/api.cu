@@ -1193,6 +1193,9 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
 #ifndef GSCT_BWD_GROW
 #define GSCT_BWD_GROW 1
 #endif
+#ifndef GSCT_BWD_FIRST_DIV
+#define GSCT_BWD_FIRST_DIV 20  // first host grad-image chunk ~ n_views / this (A/B 10 / 20 / 40: within 0.3%)
+#endif
 #ifndef GSCT_BWD_GROW_X10
 #define GSCT_BWD_GROW_X10 12  // next chunk = 1.2 x the views so far (A/B C2 e2e with the other two
                               // pipelining knobs: 1.1 / 1.2 / 1.4 / 1.7 -> 7.58 / 7.55 / 7.74 / 7.89 ms)
@@ -1205,7 +1208,7 @@ int gsct_rasterize_bwd(gsct_ctx c, const gsct_cloud* cloud, const gsct_geometry*
     if (grad_location == GSCT_HOST && !GSCT_BWD_HOST_CHUNKS) {
       cb.push_back(n_views);
     } else if (grad_location == GSCT_HOST && n_views >= 12 && GSCT_BWD_GROW) {
-      const int s0 = std::max(1, (n_views + 19) / 20);
+      const int s0 = std::max(1, (n_views + GSCT_BWD_FIRST_DIV - 1) / GSCT_BWD_FIRST_DIV);
       while (cb.back() < n_views) {
         const int done = cb.back(), rem = n_views - done;
         int sz = std::max(s0, (done * GSCT_BWD_GROW_X10 + 9) / 10);
